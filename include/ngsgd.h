@@ -1,0 +1,200 @@
+/*
+ * ngsgd.h -- C ABI of libngsgd.so: the data-parallel hot path of arXiv 1410.7455
+ * (Povey, Zhang & Khudanpur, "Parallel training of DNNs with natural gradient and
+ * parameter averaging") on NVIDIA B200 (sm_100a).
+ *
+ * Citations: "P:n" = line n of the paper's PAPER.md, with the section / equation label.
+ *
+ * Conventions (all entry points)
+ *  - Every call returns ng_status and never throws across the ABI.  On failure,
+ *    ng_last_error() returns a thread-local, human-readable message.
+ *  - Plain pointers only.  "device" pointers are CUDA global-memory addresses on the
+ *    device that was current when the handle was created; "host" pointers are ordinary
+ *    CPU memory.  No pointer is retained after the call returns unless stated.
+ *  - Matrices are row-major, one frame (minibatch element) per row, with an
+ *    explicit leading dimension `ld` (elements between consecutive rows, ld >= cols).
+ *  - Work is enqueued on the CUDA stream given at create time and is asynchronous unless
+ *    stated; the caller keeps argument buffers alive until that stream has consumed them.
+ *  - Argument/shape errors are detected on the host before anything is enqueued.
+ *    Device-detected conditions (non-finite data, label out of range, a failed Cholesky
+ *    in the re-orthogonalisation) raise a sticky device flag that is reported by the next
+ *    synchronising call (ngsgd_get_state, nnet_get_params, nnet_average, or
+ *    nnet_forward_backward with objective_out != NULL).
+ *  - One stream owns a handle; handles are not thread-safe (the paper's try-lock of
+ *    B.3.4, is a CPU-Hogwild device and has no counterpart here).
+ */
+#ifndef NGSGD_H_
+#define NGSGD_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ common ---- */
+
+typedef enum {
+  NG_OK = 0,
+  NG_EINVAL = 1,      /* bad argument (NULL handle, negative size, bad enum)          */
+  NG_ESHAPE = 2,      /* inconsistent dimensions / leading dimension / n > max rows    */
+  NG_ENONFINITE = 3,  /* NaN/Inf seen in device data (sticky flag)                     */
+  NG_ELABEL = 4,      /* label outside [0, num_classes) (sticky flag)                  */
+  NG_ECUDA = 5,       /* CUDA runtime error                                            */
+  NG_ENCCL = 6,       /* NCCL error / communicator not initialised                     */
+  NG_ENOTPD = 7,      /* Cholesky of O_t failed in B.3.1 repair: corrupted NG state    */
+  NG_ESTATE = 8,      /* operation not valid in the handle's current state             */
+  NG_ENOMEM = 9       /* device allocation failed                                      */
+} ng_status;
+
+/* Thread-local message describing the last failure on this thread ("" if none). */
+const char* ng_last_error(void);
+/* Library version / build string (static storage). */
+const char* ng_version(void);
+
+/* ------------------------------------ online NG-SGD preconditioner (Appendix B) ---- */
+
+/* Configuration of one preconditioner ("one Kronecker side of one weight matrix",
+ * P:913-919).  Defaults per B.4/B.5 are filled in by
+ * ngsgd_config_default(). */
+typedef struct {
+  int32_t rank;                /* R, rank of the non-identity part; 20 input /
+                                  80 output side.  Clipped to dim-1.  <= 112. */
+  float alpha;                 /* identity smoothing, 4               */
+  float s_samples;             /* S; forgetting factor eta = 1-exp(-N/S), 2000*/
+  int32_t update_period;       /* J = 4                             */
+  int32_t always_update_first; /* 10: always update on the first 10 minibatches  */
+  float epsilon;               /* floor of rho and d, 1e-10      */
+} ngsgd_config;
+
+void ngsgd_config_default(ngsgd_config* cfg, int32_t rank);
+
+typedef struct ngsgd_ctx* ngsgd_t;
+
+/* Create one online NG-SGD state for vectors of logical dimension `dim` (D; on the input
+ * side of a weight matrix D includes the appended 1 of the bias, e.g. 301).
+ * `max_rows` bounds the minibatch size N of later calls (workspaces are sized here so
+ * the hot path never allocates).  `cuda_stream` is a cudaStream_t (NULL = legacy default
+ * stream).  The state is uninitialised until the first minibatch with tr(X^T X) > 0
+ * (B.3.2; reading R7).  Owns all its device memory. */
+ng_status ngsgd_create(int32_t dim, int32_t max_rows, const ngsgd_config* cfg,
+                       void* cuda_stream, ngsgd_t* out);
+ng_status ngsgd_destroy(ngsgd_t h);
+
+/* Precondition one minibatch X (B.5 summary), in place.
+ *   x          device float, n rows x dim columns, leading dimension ld (ld >= dim).
+ *              On return holds X_hat = X - X W_t^T W_t (eqn:hatxt:compute),
+ *              NOT multiplied by gamma: "we actually output gamma_t and let the user do the
+ *              scaling later on".  Columns dim..ld-1 are not touched.
+ *   gamma_out  device float[1] or NULL: gamma_t = sqrt(tr(X X^T)/tr(X_hat X_hat^T))
+ *              (eqn:gammat), 1 if the denominator is 0.
+ *   p_out      device float[n] or NULL: p_i = ||x_hat_i||^2 (eqn:pi), the
+ *              UNSCALED row products; gamma^2 p_i = ||x_bar_i||^2.
+ *   update     -1: internal policy "t < always_update_first or J divides t";
+ *              0 / 1: force the non-update / update branch.
+ * The first call with non-zero X initialises the state from that X (t = 0) and, unlike
+ * every other call, synchronises the stream once (to test tr(X^T X) > 0).
+ * Errors: NG_ESHAPE if n < 1, n > max_rows or ld < dim. */
+ng_status ngsgd_precondition(ngsgd_t h, int32_t n, float* x, int64_t ld,
+                             float* gamma_out, float* p_out, int32_t update);
+
+/* Host snapshot of a state (B.5: the stored variables are rho_t, D_t, W_t). */
+typedef struct {
+  int32_t dim, rank, t, initialized;
+  double rho;        /* rho_t                                                      */
+  double* d;         /* host double[rank]  caller-allocated: diag(D_t), descending */
+  float* w;          /* host float[rank*dim] caller-allocated: W_t row-major        */
+  int32_t last_updated, last_floored, last_reorth_checked, last_reorthogonalized;
+} ngsgd_state_host;
+
+/* Copy the state to the host (synchronises the handle's stream).  d / w may be NULL to
+ * query only the scalar fields.  Also reports sticky device errors (NG_ENONFINITE,
+ * NG_ENOTPD). */
+ng_status ngsgd_get_state(ngsgd_t h, ngsgd_state_host* out);
+/* Overwrite the state from the host (e.g. to inject an oracle state for parity tests).
+ * rank must equal the handle's effective rank; initialized != 0 marks it initialised. */
+ng_status ngsgd_set_state(ngsgd_t h, const ngsgd_state_host* in);
+
+/* ---------------------------------------- p-norm / softmax DNN training step ---- */
+
+typedef enum { NG_FP32 = 0, NG_BF16 = 1 } ng_precision;
+
+/* Network: input_dim -> num_hidden x [affine hidden_dim -> p-norm /pnorm_group] ->
+ * affine num_classes -> softmax (p = 2, R19). */
+typedef struct {
+  int32_t input_dim, num_hidden, hidden_dim, pnorm_group, num_classes;
+  int32_t max_minibatch;        /* N bound; 512 on GPU              */
+  int32_t precond;              /* 0: plain SGD, 1: online NG-SGD (Appendix B)            */
+  ngsgd_config ng_in, ng_out;   /* R_in = 20, R_out = 80                    */
+  int32_t precision;            /* ng_precision of the DNN GEMMs                          */
+  uint64_t seed;                /* weight-init seed (C.6)                    */
+} nnet_config;
+
+typedef struct nnet_ctx* nnet_t;
+
+/* Create a network with C.6 initialisation: N(0, 1/fan-in) with the bias
+ * column counted in the fan-in (R20), softmax layer zero.  Parameters live in
+ * one contiguous FP32 device arena (for nnet_average). */
+ng_status nnet_create(const nnet_config* cfg, void* cuda_stream, nnet_t* out);
+ng_status nnet_destroy(nnet_t h);
+
+/* Forward + backward for one minibatch with the current weights: fills, for
+ * every weight matrix, X_i (derivative of sum_i log p(y_i|x_i) w.r.t. its output) and Y_i
+ * (its input with the appended 1), kept inside the handle for nnet_update.
+ *   frames       device float, n x input_dim, leading dimension ld.
+ *   labels       device int32[n] in [0, num_classes).
+ *   objective_out host double* or NULL. If non-NULL the call synchronises and returns
+ *                sum_i log p(y_i | x_i) (a sum, not a mean). */
+ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld,
+                                const int32_t* labels, int32_t n, double* objective_out);
+
+typedef struct {
+  float alpha_t[16];      /* max-change scale per weight matrix (C.3)        */
+  float gamma_in[16];     /* gamma of the input side (eqn:gammat)                        */
+  float gamma_out[16];    /* gamma of the output side                                    */
+  int32_t updated_in[16], updated_out[16];  /* Fisher factor refreshed this step         */
+} nnet_update_stats;
+
+/* Precondition both sides of every weight matrix (2I calls), compute the
+ * max-change scale alpha_t from the preconditioned row norms, and apply
+ * W_i += alpha_t * lr * gamma_x * gamma_y * X_hat_i^T Y_hat_i (eqn:add:w).
+ *   lr   per-job learning rate = n_jobs x effective rate.
+ *   max_change_per_sample  0.075.
+ *   stats_or_null  host; if non-NULL the call synchronises and fills it. */
+ng_status nnet_update(nnet_t h, float lr, float max_change_per_sample,
+                      nnet_update_stats* stats_or_null);
+
+/* Number of weight matrices I and the shape (rows = D_out, cols = D_in + 1) of each. */
+ng_status nnet_num_layers(nnet_t h, int32_t* out);
+ng_status nnet_layer_shape(nnet_t h, int32_t layer, int32_t* rows, int32_t* cols);
+
+/* Copy weight matrix `layer` (rows x cols, row-major, bias last column) to / from the
+ * host.  count must equal rows*cols.  get_params synchronises. */
+ng_status nnet_get_params(nnet_t h, int32_t layer, float* host, int64_t count);
+ng_status nnet_set_params(nnet_t h, int32_t layer, const float* host, int64_t count);
+/* Borrowed handle of the input-side (side = 0) or output-side (side = 1) preconditioner
+ * of weight matrix `layer`; valid while the network lives; NULL-equivalent error if
+ * precond == 0. */
+ng_status nnet_get_ngsgd(nnet_t h, int32_t layer, int32_t side, ngsgd_t* out);
+
+/* ----------------------------------------------- parameter averaging (3.1) ---- */
+
+/* Size in bytes of the NCCL unique id expected by nnet_comm_init (128). */
+int32_t nnet_comm_id_bytes(void);
+/* Create an NCCL unique id into host buffer `id_out` (nnet_comm_id_bytes() bytes), to
+ * be broadcast by the caller (e.g. torch.distributed) to all ranks. */
+ng_status nnet_comm_get_unique_id(void* id_out);
+/* Join the communicator of `nranks` jobs as `rank` (one process per GPU). */
+ng_status nnet_comm_init(nnet_t h, const void* nccl_unique_id, int32_t rank, int32_t nranks);
+/* In-place average of all parameters over the ranks (3.1): W <- (sum_r W^r)/n
+ * with the sum taken in a fixed pairwise-tree order over rank index (R18), so
+ * every rank ends with bit-identical parameters equal to the host tree sum.  NG states
+ * are per-job and untouched.  mode 0: deterministic
+ * (all-to-all of shards, fixed-order sum kernel, all-gather); mode 1: ncclAllReduce(sum)
+ * then scale (speed reference; order not fixed).  Synchronises the stream. */
+ng_status nnet_average(nnet_t h, int32_t mode);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NGSGD_H_ */

@@ -1,0 +1,205 @@
+"""Python binding of libngsgd.so: same names as include/ngsgd.h, argument marshalling only.
+
+torch supplies device memory and the CUDA stream; every arithmetic step runs in the
+library's kernels.  Tensors passed in must be CUDA float32 / int32, row-major with unit
+column stride.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import NgError, check, lib
+
+library_path = _lib.LIB_PATH
+
+
+def version() -> str:
+    return lib.ng_version().decode()
+
+
+def _stream_handle(stream: Optional[torch.cuda.Stream]) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else int(t.data_ptr())
+
+
+def _check_matrix(x: torch.Tensor, dtype=torch.float32) -> int:
+    if not x.is_cuda or x.dtype != dtype or x.dim() != 2 or x.stride(1) != 1:
+        raise ValueError("expected a CUDA %s matrix with unit column stride" % dtype)
+    return x.stride(0)
+
+
+def default_ng_config(rank: int, **overrides) -> _lib.NgsgdConfig:
+    """B.4/B.5 defaults: alpha=4, S=2000, J=4, first 10, eps=1e-10."""
+    cfg = _lib.NgsgdConfig()
+    lib.ngsgd_config_default(ctypes.byref(cfg), int(rank))
+    for k, v in overrides.items():
+        setattr(cfg, k, v)
+    return cfg
+
+
+class OnlinePreconditioner:
+    """One online NG-SGD state (Appendix B; ngsgd_create / ngsgd_precondition)."""
+
+    def __init__(self, dim: int, max_rows: int, rank: int = 20, stream: Optional[torch.cuda.Stream] = None,
+                 _borrowed: Optional[int] = None, **cfg_overrides):
+        self._owned = _borrowed is None
+        if _borrowed is not None:
+            self._h = ctypes.c_void_p(_borrowed)
+            return
+        cfg = default_ng_config(rank, **cfg_overrides)
+        h = ctypes.c_void_p()
+        check(lib.ngsgd_create(int(dim), int(max_rows), ctypes.byref(cfg), _stream_handle(stream), ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_owned", False) and self._h:
+            lib.ngsgd_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def precondition(self, x: torch.Tensor, gamma: Optional[torch.Tensor] = None, p: Optional[torch.Tensor] = None,
+                     update: int = -1) -> None:
+        """In place: x <- X_hat; gamma[0] <- gamma_t; p[:n] <- p_i (unscaled)."""
+        ld = _check_matrix(x)
+        check(lib.ngsgd_precondition(self._h, x.shape[0], _ptr(x), ld, _ptr(gamma), _ptr(p), int(update)))
+
+    def get_state(self) -> dict:
+        st = _lib.NgsgdStateHost()
+        check_q = lib.ngsgd_get_state(self._h, ctypes.byref(st))
+        R, D = st.rank, st.dim
+        d = np.zeros(max(R, 1), dtype=np.float64)
+        w = np.zeros((max(R, 1), D), dtype=np.float32)
+        st.d = d.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        st.w = w.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+        code = lib.ngsgd_get_state(self._h, ctypes.byref(st))
+        check(check_q)
+        check(code)
+        return dict(dim=D, rank=R, t=st.t, initialized=bool(st.initialized), rho=st.rho, d=d[:R].copy(),
+                    W=w[:R].copy(), updated=bool(st.last_updated), floored=bool(st.last_floored),
+                    reorth_checked=bool(st.last_reorth_checked), reorthogonalized=bool(st.last_reorthogonalized))
+
+    def set_state(self, rho: float, d: np.ndarray, W: np.ndarray, t: int, initialized: bool = True) -> None:
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        W = np.ascontiguousarray(W, dtype=np.float32)
+        st = _lib.NgsgdStateHost()
+        st.dim = W.shape[1] if W.ndim == 2 and W.shape[0] > 0 else self.get_state()["dim"]
+        st.rank = W.shape[0]
+        st.t = int(t)
+        st.initialized = 1 if initialized else 0
+        st.rho = float(rho)
+        st.d = d.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        st.w = W.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+        check(lib.ngsgd_set_state(self._h, ctypes.byref(st)))
+
+
+@dataclasses.dataclass
+class NnetStats:
+    alpha_t: np.ndarray
+    gamma_in: np.ndarray
+    gamma_out: np.ndarray
+    updated_in: np.ndarray
+    updated_out: np.ndarray
+
+
+class Nnet:
+    """p-norm/softmax DNN with online NG-SGD (nnet_create ... nnet_average)."""
+
+    def __init__(self, input_dim: int, num_hidden: int, hidden_dim: int, pnorm_group: int, num_classes: int,
+                 max_minibatch: int = 512, precond: bool = True, rank_in: int = 20, rank_out: int = 80,
+                 precision: str = "fp32", seed: int = 0, stream: Optional[torch.cuda.Stream] = None,
+                 ng_overrides: Optional[dict] = None):
+        cfg = _lib.NnetConfig()
+        cfg.input_dim, cfg.num_hidden, cfg.hidden_dim = input_dim, num_hidden, hidden_dim
+        cfg.pnorm_group, cfg.num_classes, cfg.max_minibatch = pnorm_group, num_classes, max_minibatch
+        cfg.precond = 1 if precond else 0
+        cfg.ng_in = default_ng_config(rank_in, **(ng_overrides or {}))
+        cfg.ng_out = default_ng_config(rank_out, **(ng_overrides or {}))
+        cfg.precision = {"fp32": 0, "bf16": 1}[precision]
+        cfg.seed = int(seed)
+        h = ctypes.c_void_p()
+        check(lib.nnet_create(ctypes.byref(cfg), _stream_handle(stream), ctypes.byref(h)))
+        self._h = h
+        self.cfg = cfg
+        n = ctypes.c_int32()
+        check(lib.nnet_num_layers(h, ctypes.byref(n)))
+        self.num_layers = n.value
+        self.shapes = []
+        for l in range(self.num_layers):
+            r, c = ctypes.c_int32(), ctypes.c_int32()
+            check(lib.nnet_layer_shape(h, l, ctypes.byref(r), ctypes.byref(c)))
+            self.shapes.append((r.value, c.value))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.nnet_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def forward_backward(self, frames: torch.Tensor, labels: torch.Tensor, objective: bool = False):
+        ld = _check_matrix(frames)
+        if not labels.is_cuda or labels.dtype != torch.int32:
+            raise ValueError("labels must be a CUDA int32 vector")
+        out = ctypes.c_double() if objective else None
+        check(lib.nnet_forward_backward(self._h, _ptr(frames), ld, _ptr(labels), frames.shape[0],
+                                        ctypes.byref(out) if objective else None))
+        return out.value if objective else None
+
+    def update(self, lr: float, max_change_per_sample: float = 0.075, stats: bool = False):
+        st = _lib.NnetUpdateStats() if stats else None
+        check(lib.nnet_update(self._h, float(lr), float(max_change_per_sample), ctypes.byref(st) if stats else None))
+        if not stats:
+            return None
+        L = self.num_layers
+        return NnetStats(np.array(st.alpha_t[:L]), np.array(st.gamma_in[:L]), np.array(st.gamma_out[:L]),
+                         np.array(st.updated_in[:L]), np.array(st.updated_out[:L]))
+
+    def get_params(self, layer: int) -> np.ndarray:
+        r, c = self.shapes[layer]
+        out = np.empty((r, c), dtype=np.float32)
+        check(lib.nnet_get_params(self._h, layer, out.ctypes.data, r * c))
+        return out
+
+    def set_params(self, layer: int, w: np.ndarray) -> None:
+        r, c = self.shapes[layer]
+        w = np.ascontiguousarray(w, dtype=np.float32)
+        assert w.shape == (r, c)
+        check(lib.nnet_set_params(self._h, layer, w.ctypes.data, r * c))
+
+    def ngsgd(self, layer: int, side: str) -> OnlinePreconditioner:
+        h = ctypes.c_void_p()
+        check(lib.nnet_get_ngsgd(self._h, layer, {"in": 0, "out": 1}[side], ctypes.byref(h)))
+        return OnlinePreconditioner(0, 0, _borrowed=h.value)
+
+    def comm_init(self, unique_id: bytes, rank: int, nranks: int) -> None:
+        buf = ctypes.create_string_buffer(bytes(unique_id), len(unique_id))
+        check(lib.nnet_comm_init(self._h, buf, int(rank), int(nranks)))
+
+    def average(self, mode: int = 0) -> None:
+        check(lib.nnet_average(self._h, int(mode)))
+
+
+def comm_unique_id() -> bytes:
+    n = lib.nnet_comm_id_bytes()
+    buf = ctypes.create_string_buffer(n)
+    check(lib.nnet_comm_get_unique_id(buf))
+    return buf.raw

@@ -1,0 +1,158 @@
+// eig_jacobi.cuh -- one-CTA symmetric eigensolver (cyclic parallel Jacobi, FP64).
+//
+// Used for Z_t = U_t C_t U_t^T (eqn:zt:eig, P:990-993 / P:1121-1124), which the paper
+// ran on the CPU "in O(R^2)" plus an eigendecomposition; here
+// it runs on the device in one CTA so the step never crosses to the host.  Also used
+// once per state for the initial top-R eigenpairs of S_0 (B.3.2).
+//
+// Algorithm: Jacobi rotations in round-robin ("circle") ordering: each round applies
+// floor(n/2) disjoint plane rotations simultaneously.  A' = J^T A J is done as
+// independent 2x2 block updates  A'[P,Q] = G_P^T A[P,Q] G_Q  (P, Q index rotation
+// pairs), so one round costs one barrier after computing the rotations and one after
+// the update.  Eigenvectors are accumulated as ROWS of Vt (Vt = U^T).  Sweeps stop when
+// a full sweep performs no rotation (|a_pq| <= 1e-15 sqrt(|a_pp a_qq|) or below an
+// absolute floor), or after max_sweeps.
+//
+// A and Vt may live in shared or global memory (generic addressing).
+#pragma once
+
+#include "ng_common.cuh"
+
+namespace ng {
+
+struct JacobiScratch {  // shared memory, sized for m = ceil(n/2) pairs
+  int* pp;
+  int* qq;
+  double* c;
+  double* s;
+  double* t;
+  int* nrot;
+};
+
+__device__ __forceinline__ void jacobi_pair(int round, int k, int npad, int& p, int& q) {
+  // circle method: player npad-1 fixed; the other npad-1 rotate.
+  const int m1 = npad - 1;
+  if (k == 0) { p = m1; q = round % m1; }
+  else { p = (round + k) % m1; q = (round - k + m1) % m1; }
+  if (p > q) { int tmp = p; p = q; q = tmp; }
+}
+
+// Eigen-decompose the symmetric n x n matrix A (row-major, lda) in place: on return
+// the diagonal of A holds the eigenvalues (unsorted), Vt (n x n, ldv) holds the
+// eigenvectors as rows.  Must be called by all threads of the CTA.
+__device__ void jacobi_eig(double* A, int lda, double* Vt, int ldv, int n, JacobiScratch sc,
+                           int max_sweeps, double abs_floor) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int npad = n + (n & 1);
+  const int m = npad / 2;
+  for (int idx = tid; idx < n * n; idx += nt) {
+    const int i = idx / n, j = idx % n;
+    Vt[(int64_t)i * ldv + j] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  if (n <= 1) return;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) *sc.nrot = 0;
+    __syncthreads();
+    for (int round = 0; round < npad - 1; ++round) {
+      // ---- rotation parameters for the m disjoint pairs of this round
+      for (int k = tid; k < m; k += nt) {
+        int p, q;
+        jacobi_pair(round, k, npad, p, q);
+        double c = 1.0, s = 0.0, t = 0.0;
+        if (q < n) {
+          const double app = A[(int64_t)p * lda + p], aqq = A[(int64_t)q * lda + q];
+          const double apq = A[(int64_t)p * lda + q];
+          const double thr = fmax(1e-15 * sqrt(fabs(app * aqq)), abs_floor);
+          if (fabs(apq) > thr) {
+            const double theta = (aqq - app) / (2.0 * apq);
+            t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+            c = 1.0 / sqrt(t * t + 1.0);
+            s = t * c;
+            atomicAdd(sc.nrot, 1);
+          }
+        }
+        sc.pp[k] = p; sc.qq[k] = q; sc.c[k] = c; sc.s[k] = s; sc.t[k] = t;
+      }
+      __syncthreads();
+      // ---- A' = J^T A J as 2x2 block updates over pairs (k1 <= k2), mirrored.
+      const int nblk = m * (m + 1) / 2;
+      for (int idx = tid; idx < nblk; idx += nt) {
+        // map idx -> (k1, k2) with k1 <= k2
+        int k1 = (int)((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
+        while ((k1 + 1) * (k1 + 2) / 2 <= idx) ++k1;
+        while (k1 * (k1 + 1) / 2 > idx) --k1;
+        const int k2r = idx - k1 * (k1 + 1) / 2;  // 0..k1
+        const int ka = k2r, kb = k1;              // ka <= kb
+        const int p1 = sc.pp[ka], q1 = sc.qq[ka], p2 = sc.pp[kb], q2 = sc.qq[kb];
+        const double c1 = sc.c[ka], s1 = sc.s[ka], c2 = sc.c[kb], s2 = sc.s[kb];
+        if (s1 == 0.0 && s2 == 0.0) continue;
+        const bool v1 = q1 < n, v2 = q2 < n;
+        if (ka == kb) {
+          // diagonal block: closed form a' = a - t apq, d' = d + t apq, off-diagonal 0
+          const double tt = sc.t[ka];
+          const double apq = A[(int64_t)p1 * lda + q1];
+          A[(int64_t)p1 * lda + p1] -= tt * apq;
+          A[(int64_t)q1 * lda + q1] += tt * apq;
+          A[(int64_t)p1 * lda + q1] = 0.0;
+          A[(int64_t)q1 * lda + p1] = 0.0;
+          continue;
+        }
+        const double m00 = A[(int64_t)p1 * lda + p2];
+        const double m01 = v2 ? A[(int64_t)p1 * lda + q2] : 0.0;
+        const double m10 = v1 ? A[(int64_t)q1 * lda + p2] : 0.0;
+        const double m11 = (v1 && v2) ? A[(int64_t)q1 * lda + q2] : 0.0;
+        // T = G1^T M   (G = [[c, s], [-s, c]])
+        const double t00 = c1 * m00 - s1 * m10, t01 = c1 * m01 - s1 * m11;
+        const double t10 = s1 * m00 + c1 * m10, t11 = s1 * m01 + c1 * m11;
+        // T G2
+        const double r00 = c2 * t00 - s2 * t01, r01 = s2 * t00 + c2 * t01;
+        const double r10 = c2 * t10 - s2 * t11, r11 = s2 * t10 + c2 * t11;
+        A[(int64_t)p1 * lda + p2] = r00; A[(int64_t)p2 * lda + p1] = r00;
+        if (v2) { A[(int64_t)p1 * lda + q2] = r01; A[(int64_t)q2 * lda + p1] = r01; }
+        if (v1) { A[(int64_t)q1 * lda + p2] = r10; A[(int64_t)p2 * lda + q1] = r10; }
+        if (v1 && v2) { A[(int64_t)q1 * lda + q2] = r11; A[(int64_t)q2 * lda + q1] = r11; }
+      }
+      // ---- Vt rows: row'_p = c row_p - s row_q, row'_q = s row_p + c row_q
+      for (int idx = tid; idx < m * n; idx += nt) {
+        const int k = idx / n, j = idx % n;
+        const double s = sc.s[k];
+        if (s == 0.0) continue;
+        const double c = sc.c[k];
+        const int p = sc.pp[k], q = sc.qq[k];
+        const double vp = Vt[(int64_t)p * ldv + j], vq = Vt[(int64_t)q * ldv + j];
+        Vt[(int64_t)p * ldv + j] = c * vp - s * vq;
+        Vt[(int64_t)q * ldv + j] = s * vp + c * vq;
+      }
+      __syncthreads();
+    }
+    const int rot = *sc.nrot;
+    __syncthreads();
+    if (rot == 0) break;
+  }
+}
+
+// Sort eigenpairs descending: writes eigenvalues to lam_out[n] and the permuted rows of
+// Vt into Vt_out (n x n, ldo).  Ties keep ascending original index (reading R7/R12).
+__device__ void eig_sort_desc(const double* A, int lda, const double* Vt, int ldv, int n,
+                              double* lam_out, double* Vt_out, int ldo, int* rank_scratch) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < n; i += nt) {
+    const double li = A[(int64_t)i * lda + i];
+    int r = 0;
+    for (int j = 0; j < n; ++j) {
+      const double lj = A[(int64_t)j * lda + j];
+      r += (lj > li) || (lj == li && j < i);
+    }
+    rank_scratch[i] = r;
+    lam_out[r] = li;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < n * n; idx += nt) {
+    const int i = idx / n, j = idx % n;
+    Vt_out[(int64_t)rank_scratch[i] * ldo + j] = Vt[(int64_t)i * ldv + j];
+  }
+  __syncthreads();
+}
+
+}  // namespace ng

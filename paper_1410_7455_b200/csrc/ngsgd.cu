@@ -1,0 +1,821 @@
+// ngsgd.cu -- online natural-gradient preconditioner (Appendix B of arXiv 1410.7455)
+// on sm_100a.  Every step of B.5 runs in the kernels below; the paper's
+// CPU part (Z_t, its eigendecomposition, rho/D/E/A_t) runs
+// in ONE CTA on the device (refresh_kernel), so a step never crosses to the host.
+//
+// Per call (non-update):  proj (H partials) -> reduce H -> apply (X_hat, partial row
+//   norms) -> finalize (p_i, tr(X X^T), sum p, gamma)
+// Per call (update):      proj -> reduce H -> J = H^T X -> K = J J^T, L -> apply ->
+//   finalize -> refresh (Z, Jacobi eig, floors, rho', D', E', A_t) -> B_t = J + s.W ->
+//   W' = A_t B_t -> [gated] W'W'^T -> [gated] check/Cholesky -> [gated] M W'.
+#include <math.h>
+
+#include <cmath>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "eig_jacobi.cuh"
+#include "gemm_simt.cuh"
+#include "ngsgd_impl.cuh"
+
+namespace ng {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error() { return g_last_error.c_str(); }
+
+ng_status status_from_flags(uint32_t f, const char* where) {
+  if (f & kErrNotPD) { set_error(std::string(where) + ": Cholesky of O_t failed (corrupted NG state, B.3.1)"); return NG_ENOTPD; }
+  if (f & kErrLabel) { set_error(std::string(where) + ": label out of range"); return NG_ELABEL; }
+  if (f & kErrNonFinite) { set_error(std::string(where) + ": non-finite value in device data"); return NG_ENONFINITE; }
+  return NG_OK;
+}
+
+constexpr int kApplyRows = 16, kApplyCols = 128;
+constexpr int kMaxRank = 112;
+
+// ------------------------------------------------------------------------------------
+// kernels: apply / finalize / reductions
+// ------------------------------------------------------------------------------------
+
+// X_hat = X - H W (eqn:hatxt:compute:2), in place; partial row sums of
+// x_i^2 (for tr(X X^T)) and x_hat_i^2 (p_i, eqn:pi) over this column tile.
+__global__ void __launch_bounds__(256)
+apply_kernel(int n, int D, int R, float* __restrict__ X, int64_t ldx, const float* __restrict__ H,
+             const float* __restrict__ W, int64_t ldw, float* __restrict__ xxpart,
+             float* __restrict__ ppart, int64_t part_ld) {
+  extern __shared__ __align__(16) unsigned char ng_smem[];
+  float* sm = reinterpret_cast<float*>(ng_smem);
+  float* Hs = sm;                          // kApplyRows x R
+  float* Ws = sm + kApplyRows * R;         // R x kApplyCols
+  const int r0 = blockIdx.x * kApplyRows, c0 = blockIdx.y * kApplyCols;
+  for (int i = threadIdx.x; i < kApplyRows * R; i += blockDim.x) {
+    const int rr = i / R, k = i % R;
+    Hs[i] = (r0 + rr < n) ? H[(int64_t)(r0 + rr) * R + k] : 0.f;
+  }
+  for (int i = threadIdx.x; i < R * kApplyCols; i += blockDim.x) {
+    const int k = i / kApplyCols, cc = i % kApplyCols;
+    Ws[i] = (c0 + cc < D) ? W[(int64_t)k * ldw + c0 + cc] : 0.f;
+  }
+  __syncthreads();
+  const int row = threadIdx.x >> 4, l16 = threadIdx.x & 15;
+  const int gr = r0 + row;
+  float xx = 0.f, pp = 0.f;
+#pragma unroll
+  for (int j = 0; j < kApplyCols / 16; ++j) {
+    const int cc = l16 + 16 * j, gc = c0 + cc;
+    float acc = 0.f;
+    for (int k = 0; k < R; ++k) acc = fmaf(Hs[row * R + k], Ws[k * kApplyCols + cc], acc);
+    if (gr < n && gc < D) {
+      float* px = X + (int64_t)gr * ldx + gc;
+      const float x = *px;
+      xx = fmaf(x, x, xx);
+      const float xn = x - acc;
+      *px = xn;
+      pp = fmaf(xn, xn, pp);
+    }
+  }
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) {
+    xx += __shfl_xor_sync(0xffffffffu, xx, o);
+    pp += __shfl_xor_sync(0xffffffffu, pp, o);
+  }
+  if (l16 == 0 && gr < n) {
+    xxpart[(int64_t)blockIdx.y * part_ld + gr] = xx;
+    ppart[(int64_t)blockIdx.y * part_ld + gr] = pp;
+  }
+}
+
+// R == 0: X_hat = X; partial row norms only.
+__global__ void rownorm_part_kernel(int n, int D, const float* __restrict__ X, int64_t ldx,
+                                    float* __restrict__ xxpart, float* __restrict__ ppart) {
+  const int row = blockIdx.x;
+  float s = 0.f;
+  for (int j = threadIdx.x; j < D; j += blockDim.x) { const float x = X[(int64_t)row * ldx + j]; s = fmaf(x, x, s); }
+  __shared__ float sc[32];
+  s = block_sum(s, sc);
+  if (threadIdx.x == 0) { xxpart[row] = s; ppart[row] = s; }
+}
+
+// p_i = sum over tiles (fixed order); tr(X X^T) and sum p_i with the same tree (reading
+// R27); gamma = sqrt(tr(X X^T)/sum p) or 1 (eqn:gammat).
+__global__ void __launch_bounds__(512)
+finalize_kernel(int n, int tiles, const float* __restrict__ xxpart, const float* __restrict__ ppart,
+                int64_t part_ld, float* __restrict__ p_int, float* __restrict__ p_out,
+                double* __restrict__ sums, float* __restrict__ gamma_int,
+                float* __restrict__ gamma_out, int* __restrict__ flags) {
+  __shared__ double sc[32];
+  double sxx = 0.0, spp = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    float xx = 0.f, pp = 0.f;
+    for (int t = 0; t < tiles; ++t) { xx += xxpart[(int64_t)t * part_ld + i]; pp += ppart[(int64_t)t * part_ld + i]; }
+    p_int[i] = pp;
+    if (p_out) p_out[i] = pp;
+    sxx += (double)xx;
+    spp += (double)pp;
+  }
+  sxx = block_sum(sxx, sc);
+  spp = block_sum(spp, sc);
+  if (threadIdx.x == 0) {
+    sums[0] = sxx;
+    sums[1] = spp;
+    const float g = (spp > 0.0) ? (float)sqrt(sxx / spp) : 1.0f;
+    *gamma_int = g;
+    if (gamma_out) *gamma_out = g;
+    if (!isfinite(sxx) || !isfinite(spp)) atomicOr(reinterpret_cast<unsigned*>(flags + 3), kErrNonFinite);
+  }
+}
+
+// out[i] = sum_z part[z * zstride + i], fixed order.
+__global__ void reduce_splits_kernel(float* __restrict__ out, const float* __restrict__ part, int64_t count,
+                                     int splits, int64_t zstride, const int* gate) {
+  if (gate && *gate == 0) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += part[(int64_t)z * zstride + i];
+    out[i] = s;
+  }
+}
+
+// B_t = J_t + (N(1-eta)/eta)(D_t + rho_t I) W_t, in J's buffer.
+__global__ void bscale_kernel(int R, int D, float* __restrict__ J, const float* __restrict__ W,
+                              int64_t ldw, const float* __restrict__ s) {
+  const int64_t total = (int64_t)R * D;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / D), j = (int)(i % D);
+    J[(int64_t)r * ldw + j] = fmaf(s[r], W[(int64_t)r * ldw + j], J[(int64_t)r * ldw + j]);
+  }
+}
+
+__global__ void copy_gated_kernel(int R, int D, float* __restrict__ dst, const float* __restrict__ src,
+                                  int64_t ld, const int* gate) {
+  if (gate && *gate == 0) return;
+  const int64_t total = (int64_t)R * D;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / D), j = (int)(i % D);
+    dst[(int64_t)r * ld + j] = src[(int64_t)r * ld + j];
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// refresh: the R x R part of the update, one CTA, FP64
+// ------------------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(512)
+refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
+               const float* __restrict__ KL, double* __restrict__ dstate,
+               const double* __restrict__ sums, float* __restrict__ Amat,
+               float* __restrict__ svec, int* __restrict__ flags) {
+  extern __shared__ __align__(16) unsigned char ng_smem[];
+  double* sm = reinterpret_cast<double*>(ng_smem);
+  double* Z = sm;                 // R*R
+  double* Vt = Z + R * R;         // R*R
+  double* d = Vt + R * R;         // R   old d
+  double* emh = d + R;            // R   E_t^{-1/2}
+  double* dr = emh + R;           // R   d + rho
+  double* c = dr + R;             // R   sorted eigenvalues
+  double* dn = c + R;             // R   new d
+  double* jc = dn + R;            // R/2+1 rotation c
+  double* js = jc + (R / 2 + 1);  // s
+  double* jt = js + (R / 2 + 1);  // t
+  double* red = jt + (R / 2 + 1); // 32 reduction scratch
+  int* ip = reinterpret_cast<int*>(red + 32);
+  int* jp = ip;                   // R/2+1
+  int* jq = jp + (R / 2 + 1);     // R/2+1
+  int* perm = jq + (R / 2 + 1);   // R
+  int* nrot = perm + R;           // 1
+  int* iflag = nrot + 1;          // 1 (floored)
+  const int tid = threadIdx.x, nt = blockDim.x;
+
+  const double rho = dstate[0];
+  for (int i = tid; i < R; i += nt) d[i] = dstate[1 + i];
+  __syncthreads();
+  // beta_t (eqn:beta2) and e_tii (eqn:etii)
+  double sd = 0.0;
+  for (int i = tid; i < R; i += nt) sd += d[i];
+  sd = block_sum(sd, red);
+  const double beta = rho * (1.0 + alpha) + (alpha / D) * sd;
+  for (int i = tid; i < R; i += nt) {
+    const double e = 1.0 / (beta / d[i] + 1.0);
+    emh[i] = 1.0 / sqrt(e);
+    dr[i] = d[i] + rho;
+  }
+  if (tid == 0) *iflag = 0;
+  __syncthreads();
+  // Z_t by eqn:zt:compute, symmetrised
+  const float* K = KL;
+  const float* L = KL + R * R;
+  const double a1 = eta * eta / ((double)N * N), a2 = (1.0 - eta) * (1.0 - eta), a3 = eta * (1.0 - eta) / N;
+  for (int idx = tid; idx < R * R; idx += nt) {
+    const int i = idx / R, j = idx % R;
+    const double ks = 0.5 * ((double)K[i * R + j] + (double)K[j * R + i]);
+    const double ls = 0.5 * ((double)L[i * R + j] + (double)L[j * R + i]);
+    double z = a1 * emh[i] * ks * emh[j] + a3 * emh[i] * ls * emh[j] * (dr[i] + dr[j]);
+    if (i == j) z += a2 * dr[i] * dr[i];
+    Z[idx] = z;
+  }
+  __syncthreads();
+  double zmax = 0.0;
+  for (int i = tid; i < R; i += nt) zmax = fmax(zmax, fabs(Z[i * R + i]));
+  zmax = block_max(zmax, red);
+  // Z = U C U^T (eqn:zt:eig:repeat)
+  JacobiScratch scr{jp, jq, jc, js, jt, nrot};
+  jacobi_eig(Z, R, Vt, R, R, scr, 40, 1e-18 * zmax);
+  // descending order
+  for (int i = tid; i < R; i += nt) {
+    const double li = Z[i * R + i];
+    int r = 0;
+    for (int j = 0; j < R; ++j) { const double lj = Z[j * R + j]; r += (lj > li) || (lj == li && j < i); }
+    perm[r] = i;
+  }
+  __syncthreads();
+  // floor C at (1-eta)^2 rho_t^2 (reading R13)
+  const double cf = a2 * rho * rho;
+  for (int r = tid; r < R; r += nt) {
+    double cr = Z[perm[r] * R + perm[r]];
+    if (cr < cf) { cr = cf; atomicOr(iflag, 1); }
+    c[r] = cr;
+  }
+  __syncthreads();
+  // rho'_{t+1} (eqn:rhodash2), D_{t+1} (eqn:dt1), rho_{t+1} (eqn:rhot1)
+  const double trX = sums[0];
+  double ssc = 0.0;
+  for (int r = tid; r < R; r += nt) ssc += sqrt(c[r]);
+  ssc = block_sum(ssc, red);
+  const double rho_dash = ((eta / N) * trX + (1.0 - eta) * (D * rho + sd) - ssc) / (double)(D - R);
+  const double rho_new = fmax(eps, rho_dash);
+  for (int r = tid; r < R; r += nt) dn[r] = fmax(sqrt(c[r]) - rho_dash, eps);
+  __syncthreads();
+  double sdn = 0.0;
+  for (int r = tid; r < R; r += nt) sdn += dn[r];
+  sdn = block_sum(sdn, red);
+  const double beta_new = rho_new * (1.0 + alpha) + (alpha / D) * sdn;
+  // A_t = (eta/N) E_{t+1}^{1/2} C^{-1/2} U^T E_t^{-1/2}
+  for (int idx = tid; idx < R * R; idx += nt) {
+    const int r = idx / R, j = idx % R;
+    const double en = 1.0 / (beta_new / dn[r] + 1.0);
+    Amat[idx] = (float)((eta / N) * sqrt(en) / sqrt(c[r]) * Vt[perm[r] * R + j] * emh[j]);
+  }
+  // row scale of B_t with the OLD d, rho
+  for (int k = tid; k < R; k += nt) svec[k] = (float)((N * (1.0 - eta) / eta) * dr[k]);
+  double cmax = 0.0, cmin = 1e300;
+  for (int r = tid; r < R; r += nt) { cmax = fmax(cmax, c[r]); cmin = fmin(cmin, c[r]); }
+  cmax = block_max(cmax, red);
+  cmin = -block_max(-cmin, red);
+  __syncthreads();
+  // commit the new state
+  if (tid == 0) dstate[0] = rho_new;
+  for (int r = tid; r < R; r += nt) {
+    dstate[1 + r] = dn[r];
+    dstate[1 + R + r] = 1.0 / (beta_new / dn[r] + 1.0);
+  }
+  if (tid == 0) {
+    const int fl = *iflag;
+    flags[0] = fl;
+    flags[1] = (fl || cmax / cmin > 1e6) ? 1 : 0;     // B.3.1 trigger
+    flags[2] = 0;
+    if (!isfinite(rho_new) || !isfinite(sdn)) atomicOr(reinterpret_cast<unsigned*>(flags + 3), kErrNonFinite);
+  }
+}
+
+// B.3.1 (reading R5): O = E^{-1/2} (W W^T) E^{-1/2} for the NEW state; if
+// max |O - I| > 1e-3: O = C C^T, M = E^{1/2} C^{-1} E^{-1/2} (flags[2] = 1).
+__global__ void __launch_bounds__(256)
+reorth_check_kernel(int R, const float* __restrict__ WW, const double* __restrict__ dstate,
+                    float* __restrict__ Mmat, int* __restrict__ flags) {
+  if (flags[1] == 0) return;
+  extern __shared__ __align__(16) unsigned char ng_smem[];
+  double* sm = reinterpret_cast<double*>(ng_smem);
+  double* O = sm;             // R*R
+  double* Li = O + R * R;     // R*R  (C^{-1})
+  double* eh = Li + R * R;    // R    e^{1/2}
+  double* red = eh + R;       // 32
+  __shared__ int fail;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) fail = 0;
+  for (int i = tid; i < R; i += nt) eh[i] = sqrt(dstate[1 + R + i]);
+  __syncthreads();
+  double dev = 0.0;
+  for (int idx = tid; idx < R * R; idx += nt) {
+    const int i = idx / R, j = idx % R;
+    const double w = 0.5 * ((double)WW[i * R + j] + (double)WW[j * R + i]);
+    const double o = w / (eh[i] * eh[j]);
+    O[idx] = o;
+    dev = fmax(dev, fabs(o - (i == j ? 1.0 : 0.0)));
+  }
+  dev = block_max(dev, red);
+  if (dev <= 1e-3) { if (tid == 0) flags[2] = 0; return; }
+  // Cholesky (lower), right-looking
+  for (int k = 0; k < R; ++k) {
+    if (tid == 0) {
+      const double okk = O[k * R + k];
+      if (!(okk > 0.0)) fail = 1; else O[k * R + k] = sqrt(okk);
+    }
+    __syncthreads();
+    if (fail) break;
+    const double ckk = O[k * R + k];
+    for (int i = k + 1 + tid; i < R; i += nt) O[i * R + k] /= ckk;
+    __syncthreads();
+    const int m = R - k - 1;
+    for (int idx = tid; idx < m * m; idx += nt) {
+      const int i = k + 1 + idx / m, j = k + 1 + idx % m;
+      if (j <= i) O[i * R + j] -= O[i * R + k] * O[j * R + k];
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (tid == 0) { flags[2] = 0; atomicOr(reinterpret_cast<unsigned*>(flags + 3), kErrNotPD); }
+    return;
+  }
+  // C^{-1} by forward substitution, one column per thread
+  for (int j = tid; j < R; j += nt) {
+    for (int i = 0; i < R; ++i) {
+      if (i < j) { Li[i * R + j] = 0.0; continue; }
+      double s = (i == j) ? 1.0 : 0.0;
+      for (int k = j; k < i; ++k) s -= O[i * R + k] * Li[k * R + j];
+      Li[i * R + j] = s / O[i * R + i];
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < R * R; idx += nt) {
+    const int i = idx / R, j = idx % R;
+    Mmat[idx] = (float)(eh[i] * Li[idx] / eh[j]);
+  }
+  if (tid == 0) flags[2] = 1;
+}
+
+// ------------------------------------------------------------------------------------
+// initialisation kernels (B.3.2): once per state, host-synchronising
+// ------------------------------------------------------------------------------------
+
+__global__ void sumsq_kernel(int n, int D, const float* __restrict__ X, int64_t ldx, double* out) {
+  __shared__ double sc[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < (int64_t)n * D; i += blockDim.x) {
+    const float x = X[(i / D) * ldx + (i % D)];
+    s += (double)x * x;
+  }
+  s = block_sum(s, sc);
+  if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void to_double_kernel(int n, int D, const float* __restrict__ X, int64_t ldx, double* __restrict__ Y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)n * D; i += (int64_t)gridDim.x * blockDim.x)
+    Y[i] = (double)X[(i / D) * ldx + (i % D)];
+}
+
+// Top eigenpairs of the symmetric ne x ne matrix A (global memory): sorted eigenvalues
+// -> lam, eigenvector rows -> Vs (ne x ne).
+__global__ void __launch_bounds__(1024)
+init_eig_kernel(int ne, double* A, double* Vt, double* Vs, double* lam, int* ws_int, double* ws_dbl) {
+  __shared__ double red[32];
+  const int m = ne / 2 + 1;
+  JacobiScratch scr{ws_int, ws_int + m, ws_dbl, ws_dbl + m, ws_dbl + 2 * m, ws_int + 2 * m};
+  double amax = 0.0;
+  for (int i = threadIdx.x; i < ne; i += blockDim.x) amax = fmax(amax, fabs(A[(int64_t)i * ne + i]));
+  amax = block_max(amax, red);
+  jacobi_eig(A, ne, Vt, ne, ne, scr, 60, 1e-20 * amax);
+  eig_sort_desc(A, ne, Vt, ne, ne, lam, Vs, ne, ws_int + 2 * m + 1);
+}
+
+// rho_0, d_0, E_0 and W_0 = E_0^{1/2} R_0.  R0 (R x D,
+// double) holds either eigenvector rows of S_0 (gram = 0) or rows X^T v (gram = 1),
+// which are normalised here by 1/sqrt(N lambda); numerically-null directions are
+// completed to an orthonormal set (their eigenvectors are arbitrary, reading R7).
+__global__ void __launch_bounds__(512)
+init_finalize_kernel(int R, int D, int N, int n_avail, int gram, double trS, double alpha, double eps,
+                     const double* __restrict__ lam, double* __restrict__ R0, float* __restrict__ W,
+                     int64_t ldw, double* __restrict__ dstate) {
+  __shared__ double red[32];
+  __shared__ double lr[kMaxRank];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const double lam0 = n_avail > 0 ? fmax(lam[0], 0.0) : 0.0;
+  for (int r = tid; r < R; r += nt) lr[r] = (r < n_avail) ? fmax(lam[r], 0.0) : 0.0;
+  __syncthreads();
+  for (int r = 0; r < R; ++r) {
+    const bool valid = (r < n_avail) && (lr[r] > 1e-12 * lam0) && (lr[r] > 0.0);
+    double* row = R0 + (int64_t)r * D;
+    if (gram && valid) {
+      const double sc = 1.0 / sqrt((double)N * lr[r]);
+      for (int j = tid; j < D; j += nt) row[j] *= sc;
+      __syncthreads();
+      continue;
+    }
+    if (!gram && r < n_avail) continue;   // S_0 eigenvectors are already orthonormal
+    // completion: e_j orthogonalised against previous rows (twice), first that survives
+    for (int attempt = 0; attempt < D; ++attempt) {
+      const int jj = (int)(((int64_t)r * 7919 + attempt * 104729) % D);
+      for (int j = tid; j < D; j += nt) row[j] = (j == jj) ? 1.0 : 0.0;
+      __syncthreads();
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int s = 0; s < R; ++s) {
+          if (s == r) continue;
+          if (s > r) break;
+          const double* o = R0 + (int64_t)s * D;
+          double dot = 0.0;
+          for (int j = tid; j < D; j += nt) dot += o[j] * row[j];
+          dot = block_sum(dot, red);
+          for (int j = tid; j < D; j += nt) row[j] -= dot * o[j];
+          __syncthreads();
+        }
+      }
+      double nn = 0.0;
+      for (int j = tid; j < D; j += nt) nn += row[j] * row[j];
+      nn = block_sum(nn, red);
+      if (nn > 0.25) {
+        const double sc = 1.0 / sqrt(nn);
+        for (int j = tid; j < D; j += nt) row[j] *= sc;
+        __syncthreads();
+        break;
+      }
+      __syncthreads();
+    }
+  }
+  // rho_0 = max((tr S_0 - sum lambda)/(D - R), eps); d_0 = max(eps, lambda - rho_0)
+  double sl = 0.0;
+  for (int r = tid; r < R; r += nt) sl += lr[r];
+  sl = block_sum(sl, red);
+  const double rho0 = fmax((trS - sl) / (double)(D - R), eps);
+  double sd = 0.0;
+  for (int r = tid; r < R; r += nt) sd += fmax(eps, lr[r] - rho0);
+  sd = block_sum(sd, red);
+  const double beta0 = rho0 * (1.0 + alpha) + (alpha / D) * sd;
+  for (int64_t idx = tid; idx < (int64_t)R * D; idx += nt) {
+    const int r = (int)(idx / D), j = (int)(idx % D);
+    const double d0 = fmax(eps, lr[r] - rho0);
+    const double e0 = 1.0 / (beta0 / d0 + 1.0);
+    W[(int64_t)r * ldw + j] = (float)(sqrt(e0) * R0[idx]);
+  }
+  if (tid == 0) dstate[0] = rho0;
+  for (int r = tid; r < R; r += nt) {
+    const double d0 = fmax(eps, lr[r] - rho0);
+    dstate[1 + r] = d0;
+    dstate[1 + R + r] = 1.0 / (beta0 / d0 + 1.0);
+  }
+}
+
+__global__ void passthrough_kernel(int n, float* p, float* p_out, float* g, float* g_out) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) { p[i] = 0.f; if (p_out) p_out[i] = 0.f; }
+  if (threadIdx.x == 0) { *g = 1.f; if (g_out) *g_out = 1.f; }
+}
+
+// ------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------
+
+static size_t refresh_smem_bytes(int R) {
+  const int m = R / 2 + 1;
+  return sizeof(double) * (2 * R * R + 5 * R + 3 * m + 32) + sizeof(int) * (2 * m + R + 2);
+}
+static size_t reorth_smem_bytes(int R) { return sizeof(double) * (2 * R * R + R + 32); }
+
+template <typename T>
+static ng_status dalloc(T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) { set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e)); return NG_ENOMEM; }
+  return NG_OK;
+}
+
+static ng_status set_kernel_attrs() {
+  static bool done = false;
+  if (done) return NG_OK;
+  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)refresh_smem_bytes(kMaxRank)));
+  NG_CUDA_TRY(cudaFuncSetAttribute(reorth_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)reorth_smem_bytes(kMaxRank)));
+  NG_CUDA_TRY(cudaFuncSetAttribute(apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(sizeof(float) * (kApplyRows * kMaxRank + kMaxRank * kApplyCols))));
+  done = true;
+  return NG_OK;
+}
+
+ng_status ngsgd_create_impl(int dim, int max_rows, const ngsgd_config* cfg, cudaStream_t st, ngsgd_ctx** out) {
+  NG_REQUIRE(out != nullptr && cfg != nullptr, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(dim >= 1 && max_rows >= 1, NG_ESHAPE, "dim and max_rows must be >= 1");
+  NG_REQUIRE(cfg->rank >= 0 && cfg->alpha >= 0.f && cfg->s_samples > 0.f && cfg->update_period >= 1 &&
+                 cfg->always_update_first >= 0 && cfg->epsilon > 0.f,
+             NG_EINVAL, "invalid ngsgd_config");
+  NG_TRY(set_kernel_attrs());
+  ngsgd_ctx* h = new ngsgd_ctx();
+  h->dim = dim;
+  h->cfg = *cfg;
+  h->rank = std::max(0, std::min(cfg->rank, dim - 1));     // reading R29
+  if (h->rank > kMaxRank) {
+    delete h;
+    set_error("ngsgd_create: rank > 112 is not supported");
+    return NG_EINVAL;
+  }
+  h->ldw = (int)round_up(dim, 4);
+  h->max_rows = max_rows;
+  h->st = st;
+  const int R = std::max(1, h->rank);
+  h->h_splits = std::max(1, std::min(32, ceil_div(dim, 256)));
+  h->h_splits = gemm_simt_splits(dim, h->h_splits);
+  h->kl_splits = std::max(1, std::min(32, ceil_div(dim, 256)));
+  h->kl_splits = gemm_simt_splits(dim, h->kl_splits);
+  const int l_splits = std::max(h->kl_splits, gemm_simt_splits(max_rows, std::max(1, max_rows / 128)));
+  h->ctiles = ceil_div(dim, kApplyCols);
+  ng_status s = NG_OK;
+#define ALLOC(ptr, cnt) if (s == NG_OK) s = dalloc(&(ptr), (size_t)(cnt))
+  ALLOC(h->W[0], (size_t)R * h->ldw);
+  ALLOC(h->W[1], (size_t)R * h->ldw);
+  ALLOC(h->dstate, 1 + 2 * R);
+  ALLOC(h->Hpart, (size_t)h->h_splits * max_rows * R);
+  ALLOC(h->H, (size_t)max_rows * R);
+  ALLOC(h->J, (size_t)R * h->ldw);
+  ALLOC(h->Kpart, (size_t)h->kl_splits * R * R);
+  ALLOC(h->Lpart, (size_t)l_splits * R * R);
+  ALLOC(h->KL, 2 * R * R);
+  ALLOC(h->WWpart, (size_t)h->kl_splits * R * R);
+  ALLOC(h->WW, R * R);
+  ALLOC(h->Amat, R * R);
+  ALLOC(h->Mmat, R * R);
+  ALLOC(h->svec, R);
+  ALLOC(h->xxpart, (size_t)h->ctiles * max_rows);
+  ALLOC(h->ppart, (size_t)h->ctiles * max_rows);
+  ALLOC(h->p, max_rows);
+  ALLOC(h->sums, 2);
+  ALLOC(h->gamma, 1);
+  ALLOC(h->flags, 4);
+#undef ALLOC
+  if (s == NG_OK && cudaMallocHost((void**)&h->h_scalar, 4 * sizeof(double)) != cudaSuccess) s = NG_ENOMEM;
+  if (s == NG_OK) {
+    cudaMemsetAsync(h->W[0], 0, sizeof(float) * R * h->ldw, st);
+    cudaMemsetAsync(h->W[1], 0, sizeof(float) * R * h->ldw, st);
+    cudaMemsetAsync(h->J, 0, sizeof(float) * R * h->ldw, st);
+    cudaMemsetAsync(h->flags, 0, sizeof(int) * 4, st);
+    cudaMemsetAsync(h->dstate, 0, sizeof(double) * (1 + 2 * R), st);
+    if (cudaGetLastError() != cudaSuccess) s = NG_ECUDA;
+  }
+  if (s != NG_OK) { ngsgd_destroy_impl(h); return s; }
+  *out = h;
+  return NG_OK;
+}
+
+void ngsgd_destroy_impl(ngsgd_ctx* h) {
+  if (!h) return;
+  float* fp[] = {h->W[0], h->W[1], h->Hpart, h->H, h->J, h->Kpart, h->Lpart, h->KL, h->WWpart, h->WW,
+                 h->Amat, h->Mmat, h->svec, h->xxpart, h->ppart, h->p, h->gamma};
+  for (float* p : fp) if (p) cudaFree(p);
+  if (h->dstate) cudaFree(h->dstate);
+  if (h->sums) cudaFree(h->sums);
+  if (h->flags) cudaFree(h->flags);
+  if (h->h_scalar) cudaFreeHost(h->h_scalar);
+  delete h;
+}
+
+// One-time initialisation from the first non-zero minibatch (B.3.2).
+static ng_status ngsgd_init(ngsgd_ctx* h, int n, const float* x, int64_t ld, double trXX) {
+  const int D = h->dim, R = h->rank;
+  cudaStream_t st = h->st;
+  const bool gram = D > n;                    // N < D: eigenpairs of X X^T / N (Gram trick)
+  const int ne = gram ? n : D;
+  double *X64 = nullptr, *A = nullptr, *Vt = nullptr, *Vs = nullptr, *lam = nullptr, *R0 = nullptr, *wsd = nullptr;
+  int* wsi = nullptr;
+  ng_status s = NG_OK;
+  s = dalloc(&X64, (size_t)n * D);
+  if (s == NG_OK) s = dalloc(&A, (size_t)ne * ne);
+  if (s == NG_OK) s = dalloc(&Vt, (size_t)ne * ne);
+  if (s == NG_OK) s = dalloc(&Vs, (size_t)ne * ne);
+  if (s == NG_OK) s = dalloc(&lam, ne);
+  if (s == NG_OK) s = dalloc(&R0, (size_t)std::max(R, 1) * D);
+  if (s == NG_OK) s = dalloc(&wsd, 3 * (ne / 2 + 1));
+  if (s == NG_OK) s = dalloc(&wsi, 3 * (ne / 2 + 1) + ne + 2);
+  if (s == NG_OK) {
+    to_double_kernel<<<std::min(1024, ceil_div((int64_t)n * D, 256)), 256, 0, st>>>(n, D, x, ld, X64);
+    s = check_launch("to_double_kernel");
+  }
+  if (s == NG_OK) {
+    if (gram)   // A = X X^T / N  (N x N)
+      s = gemm_simt<double, true, true>(st, n, n, D, X64, D, X64, D, EpiStore<double>{A, n, 1.0 / n});
+    else        // A = S_0 = X^T X / N  (D x D)
+      s = gemm_simt<double, false, false>(st, D, D, n, X64, D, X64, D, EpiStore<double>{A, D, 1.0 / n});
+  }
+  if (s == NG_OK) {
+    init_eig_kernel<<<1, 1024, 0, st>>>(ne, A, Vt, Vs, lam, wsi, wsd);
+    s = check_launch("init_eig_kernel");
+  }
+  const int n_avail = std::min(ne, R);
+  if (s == NG_OK && R > 0) {
+    if (gram)   // R0raw = Vs[:R] X  (rows X^T v_r)
+      s = gemm_simt<double, true, false>(st, n_avail, D, n, Vs, n, X64, D, EpiStore<double>{R0, D, 1.0});
+    else
+      NG_CUDA_TRY(cudaMemcpyAsync(R0, Vs, sizeof(double) * (size_t)n_avail * D, cudaMemcpyDeviceToDevice, st));
+  }
+  if (s == NG_OK) {
+    init_finalize_kernel<<<1, 512, 0, st>>>(R, D, n, n_avail, gram ? 1 : 0, trXX / n, h->cfg.alpha,
+                                            h->cfg.epsilon, lam, R0, h->W[h->cur], h->ldw, h->dstate);
+    s = check_launch("init_finalize_kernel");
+  }
+  if (s == NG_OK) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { set_error(std::string("ngsgd init: ") + cudaGetErrorString(e)); s = NG_ECUDA; }
+  }
+  cudaFree(X64); cudaFree(A); cudaFree(Vt); cudaFree(Vs); cudaFree(lam); cudaFree(R0); cudaFree(wsd); cudaFree(wsi);
+  if (s == NG_OK) { h->initialized = true; h->t = 0; }
+  return s;
+}
+
+ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, float* gamma_out,
+                                  float* p_out, int update, int* updated_out) {
+  NG_REQUIRE(h != nullptr && x != nullptr, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(n >= 1 && n <= h->max_rows, NG_ESHAPE, "n must be in [1, max_rows]");
+  NG_REQUIRE(ld >= h->dim, NG_ESHAPE, "ld < dim");
+  const int D = h->dim, R = h->rank;
+  cudaStream_t st = h->st;
+  if (updated_out) *updated_out = 0;
+  h->last_updated = 0;
+  if (!h->initialized) {
+    // Reading R7: defer initialisation to the first minibatch with tr(X^T X) > 0.
+    sumsq_kernel<<<1, 1024, 0, st>>>(n, D, x, ld, h->sums);
+    NG_TRY(check_launch("sumsq_kernel"));
+    NG_CUDA_TRY(cudaMemcpyAsync(h->h_scalar, h->sums, sizeof(double), cudaMemcpyDeviceToHost, st));
+    NG_CUDA_TRY(cudaStreamSynchronize(st));
+    const double trXX = h->h_scalar[0];
+    NG_REQUIRE(std::isfinite(trXX), NG_ENONFINITE, "non-finite input");
+    if (trXX == 0.0) {
+      passthrough_kernel<<<1, 256, 0, st>>>(n, h->p, p_out, h->gamma, gamma_out);
+      return check_launch("passthrough_kernel");
+    }
+    NG_TRY(ngsgd_init(h, n, x, ld, trXX));
+  }
+  const bool upd = (update < 0)
+                       ? (h->t < h->cfg.always_update_first || (h->t % h->cfg.update_period) == 0)
+                       : (update != 0);
+  if (R == 0) {
+    rownorm_part_kernel<<<n, 256, 0, st>>>(n, D, x, ld, h->xxpart, h->ppart);
+    NG_TRY(check_launch("rownorm_part_kernel"));
+    finalize_kernel<<<1, 512, 0, st>>>(n, 1, h->xxpart, h->ppart, h->max_rows, h->p, p_out, h->sums,
+                                       h->gamma, gamma_out, h->flags);
+    NG_TRY(check_launch("finalize_kernel"));
+    h->t += 1;
+    h->last_updated = upd;
+    if (updated_out) *updated_out = upd;
+    return NG_OK;
+  }
+  const double eta = 1.0 - exp(-(double)n / (double)h->cfg.s_samples);   // eqn:eta:ns
+  float* W = h->W[h->cur];
+  // H = X W^T (eqn:ht), split over D, fixed-order reduction
+  NG_TRY((gemm_simt<float, true, true>(st, n, R, D, x, ld, W, h->ldw,
+                                       EpiStoreSplit<float>{h->Hpart, R, (int64_t)n * R}, h->h_splits)));
+  const int hs = gemm_simt_splits(D, h->h_splits);
+  reduce_splits_kernel<<<ceil_div((int64_t)n * R, 256), 256, 0, st>>>(h->H, h->Hpart, (int64_t)n * R, hs, (int64_t)n * R, nullptr);
+  NG_TRY(check_launch("reduce_splits(H)"));
+  if (upd) {
+    // J = H^T X -- before X is overwritten
+    NG_TRY((gemm_simt<float, false, false>(st, R, D, n, h->H, R, x, ld, EpiStore<float>{h->J, h->ldw, 1.f})));
+    // K = J J^T
+    const int ks = gemm_simt_splits(D, h->kl_splits);
+    NG_TRY((gemm_simt<float, true, true>(st, R, R, D, h->J, h->ldw, h->J, h->ldw,
+                                         EpiStoreSplit<float>{h->Kpart, R, (int64_t)R * R}, ks)));
+    reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->KL, h->Kpart, R * R, ks, R * R, nullptr);
+    NG_TRY(check_launch("reduce_splits(K)"));
+    if (n > D) {   // L = W J^T
+      NG_TRY((gemm_simt<float, true, true>(st, R, R, D, W, h->ldw, h->J, h->ldw,
+                                           EpiStoreSplit<float>{h->Lpart, R, (int64_t)R * R}, ks)));
+      reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->KL + R * R, h->Lpart, R * R, ks, R * R, nullptr);
+    } else {       // L = H^T H
+      const int ls = gemm_simt_splits(n, std::max(1, n / 128));
+      NG_TRY((gemm_simt<float, false, false>(st, R, R, n, h->H, R, h->H, R,
+                                             EpiStoreSplit<float>{h->Lpart, R, (int64_t)R * R}, ls)));
+      reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->KL + R * R, h->Lpart, R * R, ls, R * R, nullptr);
+    }
+    NG_TRY(check_launch("reduce_splits(L)"));
+  }
+  // X_hat = X - H W in place, with partial row norms
+  {
+    dim3 grid(ceil_div(n, kApplyRows), ceil_div(D, kApplyCols));
+    const size_t smem = sizeof(float) * (kApplyRows * R + R * kApplyCols);
+    apply_kernel<<<grid, 256, smem, st>>>(n, D, R, x, ld, h->H, W, h->ldw, h->xxpart, h->ppart, h->max_rows);
+    NG_TRY(check_launch("apply_kernel"));
+  }
+  finalize_kernel<<<1, 512, 0, st>>>(n, h->ctiles, h->xxpart, h->ppart, h->max_rows, h->p, p_out, h->sums,
+                                     h->gamma, gamma_out, h->flags);
+  NG_TRY(check_launch("finalize_kernel"));
+  if (upd) {
+    refresh_kernel<<<1, 512, refresh_smem_bytes(R), st>>>(R, D, n, eta, (double)h->cfg.alpha,
+                                                          (double)h->cfg.epsilon, h->KL, h->dstate, h->sums,
+                                                          h->Amat, h->svec, h->flags);
+    NG_TRY(check_launch("refresh_kernel"));
+    bscale_kernel<<<std::min(1024, ceil_div((int64_t)R * D, 256)), 256, 0, st>>>(R, D, h->J, W, h->ldw, h->svec);
+    NG_TRY(check_launch("bscale_kernel"));
+    const int nxt = 1 - h->cur;
+    float* Wn = h->W[nxt];
+    // W_{t+1} = A_t B_t (eqn:wt1)
+    NG_TRY((gemm_simt<float, true, false>(st, R, D, R, h->Amat, R, h->J, h->ldw, EpiStore<float>{Wn, h->ldw, 1.f})));
+    // B.3.1, gated on the device flag (no host synchronisation)
+    const int ks = gemm_simt_splits(D, h->kl_splits);
+    NG_TRY((gemm_simt<float, true, true>(st, R, R, D, Wn, h->ldw, Wn, h->ldw,
+                                         EpiStoreSplit<float>{h->WWpart, R, (int64_t)R * R}, ks, h->flags + 1)));
+    reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->WW, h->WWpart, R * R, ks, R * R, h->flags + 1);
+    NG_TRY(check_launch("reduce_splits(WW)"));
+    reorth_check_kernel<<<1, 256, reorth_smem_bytes(R), st>>>(R, h->WW, h->dstate, h->Mmat, h->flags);
+    NG_TRY(check_launch("reorth_check_kernel"));
+    NG_TRY((gemm_simt<float, true, false>(st, R, D, R, h->Mmat, R, Wn, h->ldw, EpiStore<float>{h->J, h->ldw, 1.f},
+                                          1, h->flags + 2)));
+    copy_gated_kernel<<<std::min(1024, ceil_div((int64_t)R * D, 256)), 256, 0, st>>>(R, D, Wn, h->J, h->ldw, h->flags + 2);
+    NG_TRY(check_launch("copy_gated_kernel"));
+    h->cur = nxt;
+  }
+  h->t += 1;
+  h->last_updated = upd ? 1 : 0;
+  if (updated_out) *updated_out = upd ? 1 : 0;
+  return NG_OK;
+}
+
+}  // namespace ng
+
+// ------------------------------------------------------------------------------------
+// C ABI
+// ------------------------------------------------------------------------------------
+using namespace ng;
+
+extern "C" {
+
+const char* ng_last_error(void) { return ng::last_error(); }
+const char* ng_version(void) { return "libngsgd 0.1 (sm_100a)"; }
+
+void ngsgd_config_default(ngsgd_config* cfg, int32_t rank) {
+  if (!cfg) return;
+  cfg->rank = rank;
+  cfg->alpha = 4.0f;
+  cfg->s_samples = 2000.0f;
+  cfg->update_period = 4;
+  cfg->always_update_first = 10;
+  cfg->epsilon = 1e-10f;
+}
+
+ng_status ngsgd_create(int32_t dim, int32_t max_rows, const ngsgd_config* cfg, void* cuda_stream, ngsgd_t* out) {
+  return ngsgd_create_impl(dim, max_rows, cfg, (cudaStream_t)cuda_stream, out);
+}
+
+ng_status ngsgd_destroy(ngsgd_t h) {
+  if (!h) return NG_EINVAL;
+  cudaStreamSynchronize(h->st);
+  ngsgd_destroy_impl(h);
+  return NG_OK;
+}
+
+ng_status ngsgd_precondition(ngsgd_t h, int32_t n, float* x, int64_t ld, float* gamma_out, float* p_out,
+                             int32_t update) {
+  return ngsgd_precondition_impl(h, n, x, ld, gamma_out, p_out, update, nullptr);
+}
+
+ng_status ngsgd_get_state(ngsgd_t h, ngsgd_state_host* out) {
+  NG_REQUIRE(h != nullptr && out != nullptr, NG_EINVAL, "NULL argument");
+  NG_CUDA_TRY(cudaStreamSynchronize(h->st));
+  const int R = h->rank, D = h->dim;
+  out->dim = D;
+  out->rank = R;
+  out->t = h->t;
+  out->initialized = h->initialized ? 1 : 0;
+  int flags[4];
+  NG_CUDA_TRY(cudaMemcpy(flags, h->flags, sizeof(flags), cudaMemcpyDeviceToHost));
+  std::vector<double> ds(1 + 2 * std::max(R, 1));
+  NG_CUDA_TRY(cudaMemcpy(ds.data(), h->dstate, sizeof(double) * ds.size(), cudaMemcpyDeviceToHost));
+  out->rho = ds[0];
+  if (out->d) for (int i = 0; i < R; ++i) out->d[i] = ds[1 + i];
+  if (out->w && R > 0)
+    NG_CUDA_TRY(cudaMemcpy2D(out->w, sizeof(float) * D, h->W[h->cur], sizeof(float) * h->ldw, sizeof(float) * D, R,
+                             cudaMemcpyDeviceToHost));
+  out->last_updated = h->last_updated;
+  out->last_floored = h->last_updated ? flags[0] : 0;
+  out->last_reorth_checked = h->last_updated ? flags[1] : 0;
+  out->last_reorthogonalized = h->last_updated ? flags[2] : 0;
+  return status_from_flags((uint32_t)flags[3], "ngsgd_get_state");
+}
+
+ng_status ngsgd_set_state(ngsgd_t h, const ngsgd_state_host* in) {
+  NG_REQUIRE(h != nullptr && in != nullptr, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(in->dim == h->dim && in->rank == h->rank, NG_ESHAPE, "state dim/rank mismatch");
+  NG_REQUIRE(in->t >= 0, NG_EINVAL, "t < 0");
+  const int R = h->rank, D = h->dim;
+  NG_CUDA_TRY(cudaStreamSynchronize(h->st));
+  if (R > 0) {
+    NG_REQUIRE(in->d != nullptr && in->w != nullptr, NG_EINVAL, "d and w required");
+    std::vector<double> ds(1 + 2 * R);
+    ds[0] = in->rho;
+    double sd = 0.0;
+    for (int i = 0; i < R; ++i) { ds[1 + i] = in->d[i]; sd += in->d[i]; }
+    const double beta = in->rho * (1.0 + h->cfg.alpha) + (h->cfg.alpha / D) * sd;
+    for (int i = 0; i < R; ++i) ds[1 + R + i] = 1.0 / (beta / in->d[i] + 1.0);
+    NG_CUDA_TRY(cudaMemcpy(h->dstate, ds.data(), sizeof(double) * ds.size(), cudaMemcpyHostToDevice));
+    NG_CUDA_TRY(cudaMemset(h->W[0], 0, sizeof(float) * R * h->ldw));
+    NG_CUDA_TRY(cudaMemcpy2D(h->W[0], sizeof(float) * h->ldw, in->w, sizeof(float) * D, sizeof(float) * D, R,
+                             cudaMemcpyHostToDevice));
+  } else {
+    double rho = in->rho;
+    NG_CUDA_TRY(cudaMemcpy(h->dstate, &rho, sizeof(double), cudaMemcpyHostToDevice));
+  }
+  NG_CUDA_TRY(cudaMemset(h->flags, 0, sizeof(int) * 4));
+  h->cur = 0;
+  h->t = in->t;
+  h->initialized = in->initialized != 0;
+  h->last_updated = 0;
+  return NG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,540 @@
+// nnet.cu -- p-norm/softmax DNN training step with online NG-SGD (arXiv 1410.7455) and
+// the every-K parameter average (section 3.1), on sm_100a.
+//
+//   forward:   Y_1 = [frames, 1];  Z_l = Y_l W_l^T;  Y_{l+1} = [pnorm(Z_l), 1]
+//              (P:281-283);  output log-softmax, objective, X_L = onehot - p
+//
+//   backward:  g = X_l W_l[:, :D_in];  X_{l-1} = g[k/G] z_k / a_{k/G}
+//   update:    X_hat, gamma_x = NG_out(X_l); Y_hat, gamma_y = NG_in(Y_l);
+//              alpha_t = min(1, N max_change / (lr gamma_x gamma_y sum_i sqrt(p_i^x p_i^y)))
+//              (C.3);  W_l += alpha_t lr gamma_x gamma_y X_hat^T Y_hat
+//              (eqn:add:w)
+//   average:   W <- tree_sum_r(W^r) / n over NCCL
+#include <nccl.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gemm_simt.cuh"
+#include "gemm_tc.cuh"
+#include "ngsgd_impl.cuh"
+
+using namespace ng;
+
+struct nnet_ctx {
+  nnet_config cfg{};
+  cudaStream_t st = nullptr;
+  int L = 0;                                 // number of weight matrices I
+  std::vector<int> rows, cols, ldp;          // W_l is rows x cols (cols = D_in + 1)
+  std::vector<size_t> off;                   // offset of W_l in the arena (floats)
+  float* arena = nullptr;                    // all W_l, FP32 master copy
+  size_t arena_count = 0;
+  std::vector<float*> Y, Z, X;               // per layer activations / derivatives
+  std::vector<ngsgd_ctx*> ng_in, ng_out;
+  float* gam = nullptr;       // 2L: gamma_in, gamma_out per layer
+  float* pbuf = nullptr;      // 2L x max_minibatch: p_in, p_out per layer
+  float* scale = nullptr;     // L: alpha_t lr gamma_x gamma_y
+  float* stats = nullptr;     // L x 4: alpha_t, gamma_in, gamma_out, bound
+  double* objrows = nullptr;  // max_minibatch
+  double* obj = nullptr;      // 1
+  int* eflags = nullptr;      // sticky error bits
+  int n_last = 0;
+  bool have_fb = false;
+  // tensor-core (BF16) path
+  TcGemm tc;
+  // NCCL
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  float* recvbuf = nullptr;
+  size_t shard = 0;
+};
+
+// ------------------------------------------------------------------------------------
+// kernels
+// ------------------------------------------------------------------------------------
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// C.6: W ~ N(0, 1/fan-in) (fan-in includes the bias column, reading R20),
+// counter-based (splitmix64 + Box-Muller) so the init is reproducible from the seed.
+__global__ void init_weights_kernel(float* W, int rows, int cols, int ld, uint64_t seed, int layer, float stddev) {
+  const int64_t total = (int64_t)rows * ld;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / ld), c = (int)(i % ld);
+    float v = 0.f;
+    if (c < cols && stddev > 0.f) {
+      const uint64_t key = seed * 0x100000001B3ull + ((uint64_t)layer << 48) + (uint64_t)r * cols + c;
+      const uint64_t a = splitmix64(2 * key), b = splitmix64(2 * key + 1);
+      const double u1 = ((a >> 11) + 1.0) * (1.0 / 9007199254740992.0);
+      const double u2 = (b >> 11) * (1.0 / 9007199254740992.0);
+      v = (float)(stddev * sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2));
+    }
+    W[i] = v;
+  }
+}
+
+// Y_1 = [frames, 1], zero padding columns.
+__global__ void input_kernel(int n, int din, const float* __restrict__ f, int64_t ldf, float* __restrict__ Y,
+                             int ldy, int* eflags) {
+  const int64_t total = (int64_t)n * ldy;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / ldy), c = (int)(i % ldy);
+    float v = 0.f;
+    if (c < din) {
+      v = f[(int64_t)r * ldf + c];
+      if (!isfinite(v)) atomicOr(reinterpret_cast<unsigned*>(eflags), kErrNonFinite);
+    } else if (c == din) v = 1.f;
+    Y[i] = v;
+  }
+}
+
+// p-norm, p = 2: a_j = sqrt(sum_{k in group j} z_k^2); Y_next = [a, 1].
+__global__ void pnorm_kernel(int n, int dout, int G, const float* __restrict__ Z, float* __restrict__ Yn, int ldy) {
+  const int dp = dout / G;
+  const int64_t total = (int64_t)n * ldy;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / ldy), c = (int)(i % ldy);
+    float v = 0.f;
+    if (c < dp) {
+      const float* z = Z + (int64_t)r * dout + (int64_t)c * G;
+      float s = 0.f;
+      for (int k = 0; k < G; ++k) s = fmaf(z[k], z[k], s);
+      v = sqrtf(s);
+    } else if (c == dp) v = 1.f;
+    Yn[i] = v;
+  }
+}
+
+// log p(y|x) = z_y - logsumexp(z); X_L = onehot(y) - softmax(z); one CTA per row.
+__global__ void __launch_bounds__(256)
+softmax_kernel(int n, int C, const float* __restrict__ Z, const int32_t* __restrict__ labels,
+               float* __restrict__ X, double* __restrict__ objrows, int* eflags) {
+  __shared__ float sc[32];
+  const int r = blockIdx.x;
+  const float* z = Z + (int64_t)r * C;
+  float m = -INFINITY;
+  for (int j = threadIdx.x; j < C; j += blockDim.x) m = fmaxf(m, z[j]);
+  m = block_max(m, sc);
+  float s = 0.f;
+  for (int j = threadIdx.x; j < C; j += blockDim.x) s += expf(z[j] - m);
+  s = block_sum(s, sc);
+  const float lse = m + logf(s);
+  int y = labels[r];
+  if (y < 0 || y >= C) {
+    if (threadIdx.x == 0) atomicOr(reinterpret_cast<unsigned*>(eflags), kErrLabel);
+    y = -1;
+  }
+  float* x = X + (int64_t)r * C;
+  for (int j = threadIdx.x; j < C; j += blockDim.x) x[j] = (j == y ? 1.f : 0.f) - expf(z[j] - lse);
+  if (threadIdx.x == 0) {
+    objrows[r] = (y >= 0) ? (double)(z[y] - lse) : 0.0;
+    if (!isfinite(lse)) atomicOr(reinterpret_cast<unsigned*>(eflags), kErrNonFinite);
+  }
+}
+
+__global__ void objsum_kernel(int n, const double* __restrict__ rows, double* __restrict__ out) {
+  __shared__ double sc[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += rows[i];
+  s = block_sum(s, sc);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// p-norm backward fused into the backward-data GEMM epilogue: for output (i, j) of
+// g = X_l W_l[:, :D_in]:  X_{l-1}[i, jG+q] = g z_{jG+q} / a_j  (0 if a_j = 0).
+struct EpiPnormBack {
+  float* Xp; const float* Zp; const float* Yl; int ldx; int ldy; int G;
+  __device__ void operator()(int i, int j, float g, int) const {
+    const float a = Yl[(int64_t)i * ldy + j];
+    const float* z = Zp + (int64_t)i * ldx + (int64_t)j * G;
+    float* xo = Xp + (int64_t)i * ldx + (int64_t)j * G;
+    if (a > 0.f) {
+      const float ga = g / a;
+      for (int q = 0; q < G; ++q) xo[q] = ga * z[q];
+    } else {
+      for (int q = 0; q < G; ++q) xo[q] = 0.f;
+    }
+  }
+};
+
+// plain SGD (precond = 0): p_i = ||row_i||^2, gamma = 1
+__global__ void rowsq_kernel(int n, int D, const float* __restrict__ X, int64_t ld, float* __restrict__ p,
+                             float* __restrict__ gamma) {
+  __shared__ float sc[32];
+  const int r = blockIdx.x;
+  float s = 0.f;
+  for (int j = threadIdx.x; j < D; j += blockDim.x) { const float x = X[(int64_t)r * ld + j]; s = fmaf(x, x, s); }
+  s = block_sum(s, sc);
+  if (threadIdx.x == 0) { p[r] = s; if (r == 0) *gamma = 1.f; }
+}
+
+// C.3: bound = lr gamma_x gamma_y sum_i sqrt(p^x_i p^y_i) on the
+// preconditioned rows; alpha_t = min(1, N max_change_per_sample / bound), 1 if bound = 0.
+// One CTA per layer.
+__global__ void __launch_bounds__(256)
+maxchange_kernel(int n, int maxmb, float lr, float mc, const float* __restrict__ gam, const float* __restrict__ pbuf,
+                 float* __restrict__ scale, float* __restrict__ stats) {
+  __shared__ double sc[32];
+  const int l = blockIdx.x;
+  const float gy = gam[2 * l], gx = gam[2 * l + 1];
+  const float* py = pbuf + (int64_t)(2 * l) * maxmb;
+  const float* px = pbuf + (int64_t)(2 * l + 1) * maxmb;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += sqrt((double)px[i] * (double)py[i]);
+  s = block_sum(s, sc);
+  if (threadIdx.x == 0) {
+    const double bound = (double)lr * gx * gy * s;
+    const double limit = (double)n * mc;
+    const double alpha = (bound > 0.0) ? fmin(1.0, limit / bound) : 1.0;
+    scale[l] = (float)(alpha * lr * gx * gy);
+    stats[4 * l + 0] = (float)alpha;
+    stats[4 * l + 1] = gy;
+    stats[4 * l + 2] = gx;
+    stats[4 * l + 3] = (float)bound;
+  }
+}
+
+// Deterministic average: out = tree_sum(recv[0..n-1]) * inv  (R18).
+__global__ void tree_avg_kernel(int nr, size_t shard, const float* __restrict__ recv, float* __restrict__ out, float inv) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < shard; i += (size_t)gridDim.x * blockDim.x) {
+    float v[64];
+    for (int r = 0; r < nr; ++r) v[r] = recv[(size_t)r * shard + i];
+    for (int w = 1; w < nr; w *= 2)
+      for (int k = 0; k + w < nr; k += 2 * w) v[k] = v[k] + v[k + w];
+    out[i] = v[0] * inv;
+  }
+}
+
+__global__ void scale_kernel(float* x, size_t n, float s) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) x[i] *= s;
+}
+
+// ------------------------------------------------------------------------------------
+// host
+// ------------------------------------------------------------------------------------
+
+static void nnet_free(nnet_ctx* h) {
+  if (!h) return;
+  for (auto* p : h->ng_in) ngsgd_destroy_impl(p);
+  for (auto* p : h->ng_out) ngsgd_destroy_impl(p);
+  for (auto* p : h->Y) if (p) cudaFree(p);
+  for (auto* p : h->Z) if (p) cudaFree(p);
+  for (auto* p : h->X) if (p) cudaFree(p);
+  if (h->arena) cudaFree(h->arena);
+  if (h->gam) cudaFree(h->gam);
+  if (h->pbuf) cudaFree(h->pbuf);
+  if (h->scale) cudaFree(h->scale);
+  if (h->stats) cudaFree(h->stats);
+  if (h->objrows) cudaFree(h->objrows);
+  if (h->obj) cudaFree(h->obj);
+  if (h->eflags) cudaFree(h->eflags);
+  if (h->recvbuf) cudaFree(h->recvbuf);
+  if (h->comm) ncclCommDestroy(h->comm);
+  h->tc.release();
+  delete h;
+}
+
+template <typename T>
+static ng_status nalloc(T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) { set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e)); return NG_ENOMEM; }
+  return NG_OK;
+}
+
+static ng_status read_eflags(nnet_ctx* h, const char* where) {
+  int f = 0;
+  NG_CUDA_TRY(cudaMemcpy(&f, h->eflags, sizeof(int), cudaMemcpyDeviceToHost));
+  return status_from_flags((uint32_t)f, where);
+}
+
+extern "C" {
+
+ng_status nnet_create(const nnet_config* cfg, void* cuda_stream, nnet_t* out) {
+  NG_REQUIRE(cfg != nullptr && out != nullptr, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(cfg->input_dim >= 1 && cfg->num_hidden >= 0 && cfg->num_classes >= 2 && cfg->max_minibatch >= 1,
+             NG_ESHAPE, "bad network dimensions");
+  NG_REQUIRE(cfg->num_hidden == 0 || (cfg->pnorm_group >= 1 && cfg->hidden_dim >= cfg->pnorm_group &&
+                                      cfg->hidden_dim % cfg->pnorm_group == 0),
+             NG_ESHAPE, "hidden_dim must be a multiple of pnorm_group");
+  NG_REQUIRE(cfg->precision == NG_FP32 || cfg->precision == NG_BF16, NG_EINVAL, "bad precision");
+  NG_REQUIRE(cfg->num_hidden + 1 <= 16, NG_EINVAL, "at most 16 weight matrices");
+  nnet_ctx* h = new nnet_ctx();
+  h->cfg = *cfg;
+  h->st = (cudaStream_t)cuda_stream;
+  h->L = cfg->num_hidden + 1;
+  int din = cfg->input_dim;
+  size_t off = 0;
+  for (int l = 0; l < h->L; ++l) {
+    const int r = (l == h->L - 1) ? cfg->num_classes : cfg->hidden_dim;
+    h->rows.push_back(r);
+    h->cols.push_back(din + 1);
+    h->ldp.push_back((int)round_up(din + 1, 8));
+    h->off.push_back(off);
+    off += (size_t)r * h->ldp.back();
+    off = (size_t)round_up((int64_t)off, 64);
+    din = (l == h->L - 1) ? 0 : cfg->hidden_dim / cfg->pnorm_group;
+  }
+  h->arena_count = (size_t)round_up((int64_t)off, 8 * 64);
+  const int N = cfg->max_minibatch;
+  ng_status s = nalloc(&h->arena, h->arena_count);
+  for (int l = 0; l < h->L && s == NG_OK; ++l) {
+    float *y = nullptr, *z = nullptr, *x = nullptr;
+    s = nalloc(&y, (size_t)N * h->ldp[l]);
+    if (s == NG_OK) s = nalloc(&z, (size_t)N * h->rows[l]);
+    if (s == NG_OK) s = nalloc(&x, (size_t)N * h->rows[l]);
+    h->Y.push_back(y); h->Z.push_back(z); h->X.push_back(x);
+    if (s == NG_OK && cfg->precond) {
+      ngsgd_ctx *a = nullptr, *b = nullptr;
+      s = ngsgd_create_impl(h->cols[l], N, &cfg->ng_in, h->st, &a);
+      if (s == NG_OK) s = ngsgd_create_impl(h->rows[l], N, &cfg->ng_out, h->st, &b);
+      h->ng_in.push_back(a); h->ng_out.push_back(b);
+    }
+  }
+  if (s == NG_OK) s = nalloc(&h->gam, 2 * h->L);
+  if (s == NG_OK) s = nalloc(&h->pbuf, (size_t)2 * h->L * N);
+  if (s == NG_OK) s = nalloc(&h->scale, h->L);
+  if (s == NG_OK) s = nalloc(&h->stats, 4 * h->L);
+  if (s == NG_OK) s = nalloc(&h->objrows, N);
+  if (s == NG_OK) s = nalloc(&h->obj, 1);
+  if (s == NG_OK) s = nalloc(&h->eflags, 1);
+  if (s == NG_OK && cfg->precision == NG_BF16) s = h->tc.init(h->rows, h->cols, h->ldp, N, h->st);
+  if (s == NG_OK) {
+    cudaMemsetAsync(h->arena, 0, h->arena_count * sizeof(float), h->st);
+    cudaMemsetAsync(h->eflags, 0, sizeof(int), h->st);
+    for (int l = 0; l < h->L; ++l) {
+      const bool last = (l == h->L - 1);
+      const float sd = last ? 0.f : (float)(1.0 / std::sqrt((double)h->cols[l]));
+      const int64_t tot = (int64_t)h->rows[l] * h->ldp[l];
+      init_weights_kernel<<<std::min(2048, ceil_div(tot, 256)), 256, 0, h->st>>>(
+          h->arena + h->off[l], h->rows[l], h->cols[l], h->ldp[l], cfg->seed, l, sd);
+    }
+    s = check_launch("init_weights_kernel");
+  }
+  if (s == NG_OK && cudaStreamSynchronize(h->st) != cudaSuccess) { set_error("nnet_create: sync failed"); s = NG_ECUDA; }
+  if (s != NG_OK) { nnet_free(h); return s; }
+  *out = h;
+  return NG_OK;
+}
+
+ng_status nnet_destroy(nnet_t h) {
+  if (!h) return NG_EINVAL;
+  cudaStreamSynchronize(h->st);
+  nnet_free(h);
+  return NG_OK;
+}
+
+ng_status nnet_num_layers(nnet_t h, int32_t* out) {
+  NG_REQUIRE(h && out, NG_EINVAL, "NULL argument");
+  *out = h->L;
+  return NG_OK;
+}
+
+ng_status nnet_layer_shape(nnet_t h, int32_t layer, int32_t* rows, int32_t* cols) {
+  NG_REQUIRE(h && rows && cols, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(layer >= 0 && layer < h->L, NG_EINVAL, "layer out of range");
+  *rows = h->rows[layer];
+  *cols = h->cols[layer];
+  return NG_OK;
+}
+
+ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const int32_t* labels, int32_t n,
+                                double* objective_out) {
+  NG_REQUIRE(h && frames && labels, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(n >= 1 && n <= h->cfg.max_minibatch, NG_ESHAPE, "n must be in [1, max_minibatch]");
+  NG_REQUIRE(ld >= h->cfg.input_dim, NG_ESHAPE, "ld < input_dim");
+  cudaStream_t st = h->st;
+  const int L = h->L, G = h->cfg.pnorm_group;
+  const bool tc = h->cfg.precision == NG_BF16;
+  {
+    const int64_t tot = (int64_t)n * h->ldp[0];
+    input_kernel<<<std::min(4096, ceil_div(tot, 256)), 256, 0, st>>>(n, h->cfg.input_dim, frames, ld, h->Y[0],
+                                                                      h->ldp[0], h->eflags);
+    NG_TRY(check_launch("input_kernel"));
+  }
+  // forward
+  for (int l = 0; l < L; ++l) {
+    const float* W = h->arena + h->off[l];
+    if (tc) {
+      NG_TRY(h->tc.forward(l, n, h->Y[l], W, h->Z[l]));
+    } else {
+      NG_TRY((gemm_simt<float, true, true>(st, n, h->rows[l], h->cols[l], h->Y[l], h->ldp[l], W, h->ldp[l],
+                                           EpiStore<float>{h->Z[l], h->rows[l], 1.f})));
+    }
+    if (l < L - 1) {
+      const int64_t tot = (int64_t)n * h->ldp[l + 1];
+      pnorm_kernel<<<std::min(4096, ceil_div(tot, 256)), 256, 0, st>>>(n, h->rows[l], G, h->Z[l], h->Y[l + 1],
+                                                                       h->ldp[l + 1]);
+      NG_TRY(check_launch("pnorm_kernel"));
+    }
+  }
+  softmax_kernel<<<n, 256, 0, st>>>(n, h->rows[L - 1], h->Z[L - 1], labels, h->X[L - 1], h->objrows, h->eflags);
+  NG_TRY(check_launch("softmax_kernel"));
+  // backward with the pre-update weights (reading R21)
+  for (int l = L - 1; l >= 1; --l) {
+    const float* W = h->arena + h->off[l];
+    EpiPnormBack epi{h->X[l - 1], h->Z[l - 1], h->Y[l], h->rows[l - 1], h->ldp[l], G};
+    if (tc) {
+      NG_TRY(h->tc.backward(l, n, h->X[l], W, epi));
+    } else {
+      NG_TRY((gemm_simt<float, true, false>(st, n, h->cols[l] - 1, h->rows[l], h->X[l], h->rows[l], W, h->ldp[l],
+                                            epi)));
+    }
+  }
+  h->n_last = n;
+  h->have_fb = true;
+  if (objective_out) {
+    objsum_kernel<<<1, 512, 0, st>>>(n, h->objrows, h->obj);
+    NG_TRY(check_launch("objsum_kernel"));
+    NG_CUDA_TRY(cudaMemcpyAsync(objective_out, h->obj, sizeof(double), cudaMemcpyDeviceToHost, st));
+    NG_CUDA_TRY(cudaStreamSynchronize(st));
+    NG_TRY(read_eflags(h, "nnet_forward_backward"));
+  }
+  return NG_OK;
+}
+
+ng_status nnet_update(nnet_t h, float lr, float max_change_per_sample, nnet_update_stats* stats_out) {
+  NG_REQUIRE(h != nullptr, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(h->have_fb, NG_ESTATE, "nnet_update before nnet_forward_backward");
+  cudaStream_t st = h->st;
+  const int L = h->L, n = h->n_last, N = h->cfg.max_minibatch;
+  int upd_in[16] = {0}, upd_out[16] = {0};
+  for (int l = 0; l < L; ++l) {
+    float* py = h->pbuf + (size_t)(2 * l) * N;
+    float* px = h->pbuf + (size_t)(2 * l + 1) * N;
+    if (h->cfg.precond) {
+      NG_TRY(ngsgd_precondition_impl(h->ng_out[l], n, h->X[l], h->rows[l], h->gam + 2 * l + 1, px, -1, &upd_out[l]));
+      NG_TRY(ngsgd_precondition_impl(h->ng_in[l], n, h->Y[l], h->ldp[l], h->gam + 2 * l, py, -1, &upd_in[l]));
+    } else {
+      rowsq_kernel<<<n, 256, 0, st>>>(n, h->rows[l], h->X[l], h->rows[l], px, h->gam + 2 * l + 1);
+      rowsq_kernel<<<n, 256, 0, st>>>(n, h->cols[l], h->Y[l], h->ldp[l], py, h->gam + 2 * l);
+      NG_TRY(check_launch("rowsq_kernel"));
+    }
+  }
+  maxchange_kernel<<<L, 256, 0, st>>>(n, N, lr, max_change_per_sample, h->gam, h->pbuf, h->scale, h->stats);
+  NG_TRY(check_launch("maxchange_kernel"));
+  const bool tc = h->cfg.precision == NG_BF16;
+  for (int l = 0; l < L; ++l) {
+    float* W = h->arena + h->off[l];
+    if (tc) {
+      NG_TRY(h->tc.update(l, n, h->X[l], h->Y[l], W, h->scale + l));
+    } else {
+      NG_TRY((gemm_simt<float, false, false>(st, h->rows[l], h->cols[l], n, h->X[l], h->rows[l], h->Y[l], h->ldp[l],
+                                             EpiAxpyDevScale{W, h->ldp[l], h->scale + l})));
+    }
+  }
+  h->have_fb = false;
+  if (stats_out) {
+    std::vector<float> sv(4 * L);
+    NG_CUDA_TRY(cudaMemcpyAsync(sv.data(), h->stats, sizeof(float) * 4 * L, cudaMemcpyDeviceToHost, st));
+    NG_CUDA_TRY(cudaStreamSynchronize(st));
+    std::memset(stats_out, 0, sizeof(*stats_out));
+    for (int l = 0; l < L; ++l) {
+      stats_out->alpha_t[l] = sv[4 * l + 0];
+      stats_out->gamma_in[l] = sv[4 * l + 1];
+      stats_out->gamma_out[l] = sv[4 * l + 2];
+      stats_out->updated_in[l] = upd_in[l];
+      stats_out->updated_out[l] = upd_out[l];
+    }
+    NG_TRY(read_eflags(h, "nnet_update"));
+  }
+  return NG_OK;
+}
+
+ng_status nnet_get_params(nnet_t h, int32_t layer, float* host, int64_t count) {
+  NG_REQUIRE(h && host, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(layer >= 0 && layer < h->L, NG_EINVAL, "layer out of range");
+  NG_REQUIRE(count == (int64_t)h->rows[layer] * h->cols[layer], NG_ESHAPE, "count != rows*cols");
+  NG_CUDA_TRY(cudaStreamSynchronize(h->st));
+  NG_CUDA_TRY(cudaMemcpy2D(host, sizeof(float) * h->cols[layer], h->arena + h->off[layer], sizeof(float) * h->ldp[layer],
+                           sizeof(float) * h->cols[layer], h->rows[layer], cudaMemcpyDeviceToHost));
+  return read_eflags(h, "nnet_get_params");
+}
+
+ng_status nnet_set_params(nnet_t h, int32_t layer, const float* host, int64_t count) {
+  NG_REQUIRE(h && host, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(layer >= 0 && layer < h->L, NG_EINVAL, "layer out of range");
+  NG_REQUIRE(count == (int64_t)h->rows[layer] * h->cols[layer], NG_ESHAPE, "count != rows*cols");
+  NG_CUDA_TRY(cudaStreamSynchronize(h->st));
+  NG_CUDA_TRY(cudaMemcpy2D(h->arena + h->off[layer], sizeof(float) * h->ldp[layer], host, sizeof(float) * h->cols[layer],
+                           sizeof(float) * h->cols[layer], h->rows[layer], cudaMemcpyHostToDevice));
+  return NG_OK;
+}
+
+ng_status nnet_get_ngsgd(nnet_t h, int32_t layer, int32_t side, ngsgd_t* out) {
+  NG_REQUIRE(h && out, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(h->cfg.precond != 0, NG_ESTATE, "network has no preconditioners");
+  NG_REQUIRE(layer >= 0 && layer < h->L && (side == 0 || side == 1), NG_EINVAL, "bad layer/side");
+  *out = side == 0 ? h->ng_in[layer] : h->ng_out[layer];
+  return NG_OK;
+}
+
+int32_t nnet_comm_id_bytes(void) { return (int32_t)sizeof(ncclUniqueId); }
+
+ng_status nnet_comm_get_unique_id(void* id_out) {
+  NG_REQUIRE(id_out != nullptr, NG_EINVAL, "NULL argument");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) { set_error(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r)); return NG_ENCCL; }
+  std::memcpy(id_out, &id, sizeof(id));
+  return NG_OK;
+}
+
+ng_status nnet_comm_init(nnet_t h, const void* nccl_unique_id, int32_t rank, int32_t nranks) {
+  NG_REQUIRE(h && nccl_unique_id, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(nranks >= 1 && nranks <= 64 && rank >= 0 && rank < nranks, NG_EINVAL, "bad rank/nranks");
+  NG_REQUIRE(h->comm == nullptr, NG_ESTATE, "communicator already initialised");
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_unique_id, sizeof(id));
+  ncclResult_t r = ncclCommInitRank(&h->comm, nranks, id, rank);
+  if (r != ncclSuccess) { set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r)); h->comm = nullptr; return NG_ENCCL; }
+  h->rank = rank;
+  h->nranks = nranks;
+  h->shard = h->arena_count / nranks;   // arena_count is a multiple of 512 >= 8 * 64
+  if (h->arena_count % nranks != 0) h->shard = (h->arena_count + nranks - 1) / nranks;
+  NG_TRY(nalloc(&h->recvbuf, h->shard * nranks));
+  return NG_OK;
+}
+
+ng_status nnet_average(nnet_t h, int32_t mode) {
+  NG_REQUIRE(h != nullptr, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(h->comm != nullptr, NG_ENCCL, "nnet_comm_init not called");
+  cudaStream_t st = h->st;
+  const int nr = h->nranks;
+  NG_REQUIRE(h->shard * nr == h->arena_count, NG_ESTATE, "arena not divisible by nranks");
+  ncclResult_t r = ncclSuccess;
+  if (mode == 0) {
+    r = ncclGroupStart();
+    for (int p = 0; p < nr && r == ncclSuccess; ++p) {
+      r = ncclSend(h->arena + (size_t)p * h->shard, h->shard, ncclFloat, p, h->comm, st);
+      if (r == ncclSuccess) r = ncclRecv(h->recvbuf + (size_t)p * h->shard, h->shard, ncclFloat, p, h->comm, st);
+    }
+    ncclResult_t r2 = ncclGroupEnd();
+    if (r == ncclSuccess) r = r2;
+    if (r == ncclSuccess) {
+      tree_avg_kernel<<<std::min<size_t>(4096, (h->shard + 255) / 256), 256, 0, st>>>(
+          nr, h->shard, h->recvbuf, h->arena + (size_t)h->rank * h->shard, 1.0f / (float)nr);
+      NG_TRY(check_launch("tree_avg_kernel"));
+      r = ncclAllGather(h->arena + (size_t)h->rank * h->shard, h->arena, h->shard, ncclFloat, h->comm, st);
+    }
+  } else {
+    r = ncclAllReduce(h->arena, h->arena, h->arena_count, ncclFloat, ncclSum, h->comm, st);
+    if (r == ncclSuccess) {
+      scale_kernel<<<std::min<size_t>(4096, (h->arena_count + 255) / 256), 256, 0, st>>>(h->arena, h->arena_count,
+                                                                                          1.0f / (float)nr);
+      NG_TRY(check_launch("scale_kernel"));
+    }
+  }
+  if (r != ncclSuccess) { set_error(std::string("nnet_average: ") + ncclGetErrorString(r)); return NG_ENCCL; }
+  NG_CUDA_TRY(cudaStreamSynchronize(st));
+  return read_eflags(h, "nnet_average");
+}
+
+}  // extern "C"

@@ -1,0 +1,164 @@
+"""GPU parity of the DNN training step (nnet_forward_backward + nnet_update, FP32 path)
+against the float64 oracle (oracle/nnet.py) on identical injected states and seeded
+synthetic frames.  Tolerance: normwise 1e-4 (north_star), objective relative 1e-5."""
+import numpy as np
+import pytest
+
+from oracle import nnet as onn
+from oracle import online_ng as ong
+from oracle import training as otr
+from synth import spliced_frames, standard_normals
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def api():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1410_7455_b200 import api
+    return api
+
+
+def normwise(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def make_pair(api, cfg, precond, seed, rank_in, rank_out, max_mb, random_softmax=False):
+    net = api.Nnet(cfg.input_dim, cfg.num_hidden, cfg.hidden_dim, cfg.pnorm_group, cfg.num_classes,
+                   max_minibatch=max_mb, precond=precond, rank_in=rank_in, rank_out=rank_out, seed=seed)
+    params = onn.init_params(cfg, standard_normals(seed, cfg.layer_shapes()))
+    if random_softmax:
+        params[-1] = 0.05 * standard_normals(seed + 1, [cfg.layer_shapes()[-1]])[0]
+    params = [p.astype(np.float32).astype(np.float64) for p in params]
+    for l, p in enumerate(params):
+        net.set_params(l, p)
+    states = onn.make_states(cfg, ong.OnlineNgConfig(rank=rank_in), ong.OnlineNgConfig(rank=rank_out)) if precond else None
+    return net, params, states
+
+
+def to_dev(frames, labels):
+    return (torch.from_numpy(np.ascontiguousarray(frames, dtype=np.float32)).cuda(),
+            torch.from_numpy(np.ascontiguousarray(labels, dtype=np.int32)).cuda())
+
+
+def test_device_init_statistics(api):
+    """C.6 init on the device: std 1/sqrt(fan-in) (bias counted), softmax layer zero."""
+    net = api.Nnet(99, 1, 1000, 10, 7, max_minibatch=8, precond=False, seed=3)
+    w0 = net.get_params(0)
+    assert np.std(w0) == pytest.approx(0.1, rel=0.02) and abs(np.mean(w0)) < 0.005
+    assert np.all(net.get_params(1) == 0)
+    net2 = api.Nnet(99, 1, 1000, 10, 7, max_minibatch=8, precond=False, seed=3)
+    assert np.array_equal(net2.get_params(0), w0)
+
+
+def test_objective_and_plain_sgd_step(api):
+    cfg = onn.NnetConfig(input_dim=40, num_hidden=2, hidden_dim=200, pnorm_group=10, num_classes=16)
+    net, params, _ = make_pair(api, cfg, False, 11, 4, 4, 128, random_softmax=True)
+    frames, labels = spliced_frames(21, 100, context=0, num_classes=16)
+    f, y = to_dev(frames, labels)
+    obj = net.forward_backward(f, y, objective=True)
+    fb = onn.forward_backward(params, cfg, frames.astype(np.float64), labels)
+    assert obj == pytest.approx(fb.objective, rel=1e-5)
+    net.update(0.05, 0.075)
+    onn.update(params, fb, 0.05, precond="none")
+    for l in range(len(params)):
+        assert normwise(net.get_params(l), params[l]) <= TOL
+
+
+@pytest.mark.parametrize("n", [128, 16, 1])
+def test_ng_step_parity_tiny_config(api, n):
+    """Config 1 (D=40, 200 -> 20, 16 classes, R = 4): several steps from the same state;
+    includes deferred init of hidden-layer states (zero softmax, reading R7)."""
+    cfg = onn.NnetConfig(input_dim=40, num_hidden=1, hidden_dim=200, pnorm_group=10, num_classes=16)
+    net, params, states = make_pair(api, cfg, True, 5, 4, 4, 128)
+    frames, labels = spliced_frames(7, 6 * n, context=0, num_classes=16)
+    for k in range(6):
+        fr, lb = frames[k * n:(k + 1) * n], labels[k * n:(k + 1) * n]
+        f, y = to_dev(fr, lb)
+        obj = net.forward_backward(f, y, objective=True)
+        fb = onn.forward_backward(params, cfg, fr.astype(np.float64), lb)
+        assert obj == pytest.approx(fb.objective, rel=1e-5, abs=1e-6)
+        lr = otr.lr_at(k * n, 10000, 0.01 / 6, 0.001 / 6)
+        st = net.update(lr, 0.075, stats=True)
+        ost = onn.update(params, fb, lr, states)
+        for l in range(len(params)):
+            assert st.alpha_t[l] == pytest.approx(ost[l].alpha_t, rel=TOL)
+            assert normwise(net.get_params(l), params[l]) <= TOL, (k, l)
+
+
+def test_config1_full_trajectory(api):
+    """Config 1 end to end: 10 000 frames = 78 x 128 + 16, one epoch, lr 0.01/6 ->
+    0.001/6, online NG R = 4; parameters after the run within 1e-4 normwise."""
+    cfg = onn.NnetConfig(input_dim=40, num_hidden=1, hidden_dim=200, pnorm_group=10, num_classes=16)
+    net, params, states = make_pair(api, cfg, True, 1410, 4, 4, 128)
+    frames, labels = spliced_frames(1410, 10000, context=0, num_classes=16)
+    seen = 0
+    objs = []
+    while seen < 10000:
+        n = min(128, 10000 - seen)
+        fr, lb = frames[seen:seen + n], labels[seen:seen + n]
+        f, y = to_dev(fr, lb)
+        net.forward_backward(f, y)
+        lr = otr.lr_at(seen, 10000, 0.01 / 6, 0.001 / 6)
+        net.update(lr, 0.075)
+        obj, _ = onn.train_step(params, cfg, fr.astype(np.float64), lb, lr, states)
+        objs.append(obj / n)
+        seen += n
+    for l in range(len(params)):
+        assert normwise(net.get_params(l), params[l]) <= TOL
+    assert objs[-1] > objs[0]
+
+
+def test_config3_single_step_injected_states(api):
+    """Full config 3 shapes (360 -> 4 x [3000 -> 300] -> 5000, N = 512, R_in = 20,
+    R_out = 80) in the launch configuration bench.py times: one step from injected
+    NG states (update step) and a second (non-update) step."""
+    cfg = onn.NnetConfig(input_dim=360, num_hidden=4, hidden_dim=3000, pnorm_group=10, num_classes=5000)
+    net, params, states = make_pair(api, cfg, True, 77, 20, 80, 512, random_softmax=True)
+    rng = np.random.default_rng(0)
+    for l, (s_in, s_out) in enumerate(states):
+        for side, s in (("in", s_in), ("out", s_out)):
+            q, _ = np.linalg.qr(rng.normal(size=(s.dim, s.rank)))
+            s.d = np.sort(rng.uniform(0.01, 1.0, s.rank))[::-1].copy()
+            s.rho = 1e-3
+            e = ong.e_of(ong.beta_of(s.rho, s.d, 4.0, s.dim), s.d)
+            s.W = (np.sqrt(e)[:, None] * q.T).astype(np.float32).astype(np.float64)
+            s.t, s.initialized = 12, True
+            net.ngsgd(l, side).set_state(s.rho, s.d, s.W.astype(np.float32), s.t)
+    frames, labels = spliced_frames(3, 1024, num_classes=5000)
+    for k in range(2):
+        fr, lb = frames[k * 512:(k + 1) * 512], labels[k * 512:(k + 1) * 512]
+        f, y = to_dev(fr, lb)
+        obj = net.forward_backward(f, y, objective=True)
+        fb = onn.forward_backward(params, cfg, fr.astype(np.float64), lb)
+        assert obj == pytest.approx(fb.objective, rel=1e-5)
+        st = net.update(0.01, 0.075, stats=True)
+        ost = onn.update(params, fb, 0.01, states)
+        for l in range(len(params)):
+            assert st.gamma_in[l] == pytest.approx(ost[l].gamma_in, rel=TOL)
+            assert st.gamma_out[l] == pytest.approx(ost[l].gamma_out, rel=TOL)
+            assert normwise(net.get_params(l), params[l]) <= TOL, (k, l)
+
+
+def test_label_out_of_range_reported(api):
+    net = api.Nnet(8, 1, 20, 10, 4, max_minibatch=4, precond=False)
+    f = torch.zeros((4, 8), device="cuda")
+    y = torch.tensor([0, 1, 9, 2], dtype=torch.int32, device="cuda")
+    with pytest.raises(api.NgError) as ei:
+        net.forward_backward(f, y, objective=True)
+    assert ei.value.code == 4
+
+
+def test_average_single_rank_is_identity(api):
+    """nranks = 1: the average is a bit-exact no-op (n identical models)."""
+    net = api.Nnet(40, 1, 200, 10, 16, max_minibatch=8, precond=False, seed=9)
+    before = [net.get_params(l) for l in range(2)]
+    net.comm_init(api.comm_unique_id(), 0, 1)
+    for mode in (0, 1):
+        net.average(mode)
+        for l in range(2):
+            assert np.array_equal(net.get_params(l), before[l])
