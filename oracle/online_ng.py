@@ -230,10 +230,13 @@ def precondition(state: OnlineNgState, X: np.ndarray, update: bool | None = None
     X_hat = X - H @ W
     p = np.sum(X_hat * X_hat, axis=1)                          # eqn:pi
     sp = float(np.sum(p))
-    tr_xxt = sp - float(np.sum(np.diag(L) * e)) + 2.0 * float(np.trace(L))   # eqn:trxxt
+    # tr(X X^T): the quantity eqn:gammat and eqn:rhodash2 are defined with, computed by its
+    # definition (reading R30).  The paper's shortcut eqn:trxxt is the same
+    # number whenever R_t R_t^T = I; it is evaluated and checked here, not used.
+    tr_xxt = float(np.sum(np.sum(X * X, axis=1)))
     if check_trace:
-        direct = float(np.sum(X * X))
-        assert abs(tr_xxt - direct) <= 1e-8 * max(1.0, abs(direct)), (tr_xxt, direct)
+        shortcut = sp - float(np.sum(np.diag(L) * e)) + 2.0 * float(np.trace(L))   # eqn:trxxt
+        assert abs(shortcut - tr_xxt) <= 1e-8 * max(1.0, abs(tr_xxt)), (shortcut, tr_xxt)
     gamma = math.sqrt(tr_xxt / sp) if sp > 0.0 else 1.0        # eqn:gammat
 
     sqrt_c = np.sqrt(c)

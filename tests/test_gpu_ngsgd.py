@@ -165,7 +165,7 @@ def test_reorthogonalisation_path(api):
     pre = api.OnlinePreconditioner(D, N, rank=R)
     inject(pre, s)
     X = (rng.normal(size=(N, D)) * (10.0 ** -np.linspace(0, 4, D))[None, :]).astype(np.float32).astype(np.float64)
-    o = ong.precondition(s, X, update=True)
+    o = ong.precondition(s, X, update=True, check_trace=False)   # R_t not orthonormal here
     xh, g, p = run_gpu(pre, X, update=1)
     st = compare_state(pre, s, tol=1e-3)
     assert o.reorth_checked and st["reorth_checked"]
