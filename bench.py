@@ -1,0 +1,458 @@
+#!/usr/bin/env python
+"""bench.py -- train frames/s of the online NG-SGD DNN step (arXiv 1410.7455) on B200.
+
+Workload (BASELINE.json configs[2], the config the "train frames/sec" metric is quoted
+on; it fits one GPU): 360-dim spliced input -> 4 x [affine 3000 -> p-norm 300] ->
+affine 5000 -> softmax, minibatch N = 512, online NG-SGD on both sides of all 5 weight
+matrices (R_in = 20, R_out = 80, alpha = 4, S = 2000, J = 4), max-change 0.075/sample,
+per-job lr = n_jobs/6 x (0.01 -> 0.001).  With N > 1 GPUs (torchrun) every rank runs an
+independent job on its own data shard and the parameters are averaged every K = 400 000
+samples (781.25 minibatches) -- "scaling": "weak".
+
+A step = nnet_forward_backward + nnet_update on one 512-frame minibatch (all hot-path
+rows of SURVEY.md 8(a); the average is included at its cadence).  Inputs: a per-rank pool
+of 2^18 synthetic frames (377 MB > 126 MB L2) resident in HBM, cycled.
+
+Also reported: the second half of the metric ("precondition ms/minibatch", configs[1]:
+both sides of one 2000-dim layer, N = 512, R_in = 20 / R_out = 80, 1000 minibatches),
+the live per-kernel-group roofline, the CPU oracle baseline, end-to-end throughput with
+host buffers, clocks and the kernel launch count.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
+
+CFG3 = dict(input_dim=360, num_hidden=4, hidden_dim=3000, pnorm_group=10, num_classes=5000, minibatch=512,
+            rank_in=20, rank_out=80)
+METRIC = "train frames/sec (online NG-SGD)"
+WORKLOAD = ("config3: paper-shaped p-norm DNN 360 -> 4x[3000 -> p-norm 300] -> 5000 softmax, N=512, "
+            "online NG-SGD R_in=20/R_out=80 on all 10 Fisher factors, max-change 0.075")
+POOL_FRAMES = 1 << 18
+TOTAL_SAMPLES = 10 * 400_000          # nominal schedule length for the lr (host scalar)
+FP32_SIMT_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # FP32 FMA lanes x 2 x max clock
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ clocks sampler
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t0 = self.t1 = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.gpu), "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, which):
+        setattr(self, which, time.time())
+
+    def stop(self):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for ts, line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            rows.append((ts, parts))
+        inside = [p for ts, p in rows if self.t0 and self.t1 and self.t0 - 0.05 <= ts <= self.t1 + 0.15] or \
+                 [p for _, p in rows]
+        if not inside:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(p[1]) for p in inside if num(p[1]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for p in inside for i in range(4) if p[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": num(inside[0][2]),
+                "reasons": reasons, "samples": len(inside),
+                "power_w_max": max((num(p[3]) or 0.0) for p in inside)}
+
+
+# ------------------------------------------------------------------ reference arm (the oracle)
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max((i.get("num_threads", 1) for i in info if i.get("user_api") == "blas"), default=1), \
+            ",".join(sorted({i.get("internal_api", "?") for i in info if i.get("user_api") == "blas"}))
+    except Exception:
+        return cpu_cores(), "unknown"
+
+
+def oracle_setup(n: int, seed: int = 1410):
+    """Oracle network of config 3 with injected steady-state NG states (the one-time
+    eigendecomposition init is not part of a steady-state step)."""
+    import numpy as np
+
+    from oracle import nnet as onn
+    from oracle import online_ng as ong
+    from synth import spliced_frames, standard_normals
+    cfg = onn.NnetConfig(CFG3["input_dim"], CFG3["num_hidden"], CFG3["hidden_dim"], CFG3["pnorm_group"],
+                         CFG3["num_classes"])
+    params = onn.init_params(cfg, standard_normals(seed, cfg.layer_shapes()))
+    states = onn.make_states(cfg, ong.OnlineNgConfig(rank=CFG3["rank_in"]), ong.OnlineNgConfig(rank=CFG3["rank_out"]))
+    rng = np.random.default_rng(seed)
+    for s_in, s_out in states:
+        for s in (s_in, s_out):
+            q, _ = np.linalg.qr(rng.normal(size=(s.dim, s.rank)))
+            s.d = np.sort(rng.uniform(0.01, 1.0, s.rank))[::-1].copy()
+            s.rho = 1e-3
+            e = ong.e_of(ong.beta_of(s.rho, s.d, 4.0, s.dim), s.d)
+            s.W = np.sqrt(e)[:, None] * q.T
+            s.t, s.initialized = 10, True
+    frames, labels = spliced_frames(seed, 64 * n, num_classes=CFG3["num_classes"])
+    return cfg, params, states, frames.astype(np.float64), labels
+
+
+def oracle_steps(steps: int, warmup: int, n: int):
+    """Time `steps` oracle train steps (after `warmup`) with minibatch n; returns frames/s."""
+    from oracle import nnet as onn
+    cfg, params, states, frames, labels = oracle_setup(n)
+    nb = frames.shape[0] // n
+    for k in range(warmup):
+        i = k % nb
+        onn.train_step(params, cfg, frames[i * n:(i + 1) * n], labels[i * n:(i + 1) * n], 1e-3, states)
+    t0 = time.perf_counter()
+    for k in range(steps):
+        i = (warmup + k) % nb
+        onn.train_step(params, cfg, frames[i * n:(i + 1) * n], labels[i * n:(i + 1) * n], 1e-3, states)
+    dt = time.perf_counter() - t0
+    return steps * n / dt, dt
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return 0
+    n = 128            # the paper's CPU minibatch: bounds each reference step
+    val, dt = oracle_steps(args.steps, args.warmup, n)
+    thr, api_ = blas_threads()
+    sample = (f"each step = one float64 oracle train step (forward, backward, online NG-SGD on 10 factors, "
+              f"update) of config 3 on a {n}-frame minibatch (paper CPU minibatch, P:1438-1443); "
+              f"steady-state NG states injected")
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD + f" (oracle sample: N={n} per step)", "minibatch": n},
+            "cpu_baseline": {"value": val, "unit": "frames/s", "cores": thr, "kind": "oracle", "sample": sample,
+                             "blas": api_, "host_cores": cpu_cores()},
+            "e2e": {"value": val, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+
+def load_peaks():
+    try:
+        return json.load(open(MEASURED_PEAKS))
+    except Exception:
+        return {}
+
+
+def roofline_for(group: str, prof: dict, precision: str, peaks: dict):
+    g = prof[group]
+    if g["launches"] == 0 or g["ms"] <= 0:
+        return None
+    per_launch_s = g["ms"] / 1e3 / g["launches"]
+    traffic = None
+    try:
+        tr = json.load(open(TRAFFIC_FILE))
+        traffic = tr.get(precision, {}).get(group)
+    except Exception:
+        pass
+    is_gemm = group in ("fwd_gemm", "bwd_gemm", "upd_gemm")
+    if is_gemm or group in ("ng_proj", "ng_refresh"):
+        flops = g["flops"] / g["launches"]
+        achieved = flops / per_launch_s / 1e12
+        if precision == "bf16":
+            peak = peaks.get("bf16_tflops_sustained", 1378.9)
+            bound, src = "tensor", "MEASURED_PEAKS.json bf16_tflops_sustained"
+        else:
+            peak = FP32_SIMT_PEAK_TFLOPS
+            bound, src = "alu", "derived: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md)"
+        return {"kernel": group, "bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": src,
+                "algorithmic_per_launch": flops, "launch_ms": per_launch_s * 1e3}
+    by = g["bytes"] / g["launches"]
+    achieved = by / per_launch_s / 1e9
+    peak = peaks.get("hbm_gbs", 6538.6)
+    return {"kernel": group, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+            "algorithmic_per_launch": by, "launch_ms": per_launch_s * 1e3}
+
+
+def precondition_bench(api, torch, minibatches: int = 1000):
+    """configs[1]: both sides of one 2000-dim layer, N = 512, R_in = 20 / R_out = 80,
+    1000 minibatches (pool of 64 cycled; 257 update steps)."""
+    import numpy as np
+
+    from synth import power_law_rows
+    N = 512
+    xo = [torch.from_numpy(b.astype(np.float32)).cuda() for b in power_law_rows(2000, N, 2000, n_batches=64)]
+    xi = [torch.from_numpy(b.astype(np.float32)).cuda()
+          for b in power_law_rows(2001, N, 2000, n_batches=64, nonneg=True, append_one=True)]
+    out_side = api.OnlinePreconditioner(2000, N, rank=80)
+    in_side = api.OnlinePreconditioner(2001, N, rank=20)
+    work_o = torch.empty_like(xo[0])
+    work_i = torch.empty_like(xi[0])
+    g = torch.zeros(2, device="cuda")
+    p = torch.zeros(2, N, device="cuda")
+
+    def one(k):
+        work_o.copy_(xo[k % 64])
+        work_i.copy_(xi[k % 64])
+        out_side.precondition(work_o, g[0:1], p[0])
+        in_side.precondition(work_i, g[1:2], p[1])
+
+    for k in range(12):            # includes the (host-synchronising) init; not timed
+        one(k)
+    torch.cuda.synchronize()
+    # copy cost measured separately and subtracted (the copy restores the input)
+    ec0, ec1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ec0.record()
+    for k in range(minibatches):
+        work_o.copy_(xo[k % 64]); work_i.copy_(xi[k % 64])
+    ec1.record()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(minibatches):
+        one(12 + k)
+    e1.record()
+    torch.cuda.synchronize()
+    tot = e0.elapsed_time(e1)
+    cp = ec0.elapsed_time(ec1)
+    return {"value": (tot - cp) / minibatches, "unit": "ms/minibatch", "higher_is_better": False,
+            "config": "configs[1]: one 2000-dim layer, both sides (D=2000 R=80; D=2001 R=20), N=512, "
+                      f"{minibatches} minibatches (pool of 64 cycled), policy t<10 or 4|t",
+            "copy_ms_subtracted_per_minibatch": cp / minibatches}
+
+
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import numpy as np
+    import torch
+
+    from paper_1410_7455_b200 import api
+    from paper_1410_7455_b200 import driver
+    from synth import spliced_frames
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    precision = args.precision
+    N = CFG3["minibatch"]
+    t_gen = time.time()
+    frames_np, labels_np = spliced_frames(driver.rank_seed(rank), POOL_FRAMES, num_classes=CFG3["num_classes"])
+    frames = torch.from_numpy(frames_np).to(dev)
+    labels = torch.from_numpy(labels_np).to(dev)
+    pool_mb = POOL_FRAMES // N
+    log(f"[rank {rank}] synthetic pool {frames_np.nbytes / 1e6:.0f} MB in {time.time() - t_gen:.1f}s")
+    net = api.Nnet(CFG3["input_dim"], CFG3["num_hidden"], CFG3["hidden_dim"], CFG3["pnorm_group"],
+                   CFG3["num_classes"], max_minibatch=N, precond=True, rank_in=CFG3["rank_in"],
+                   rank_out=CFG3["rank_out"], precision=precision, seed=1410)
+    if world > 1:
+        uid = api.comm_unique_id() if rank == 0 else None
+        uid = driver.broadcast_bytes(uid)
+        net.comm_init(uid, rank, world)
+    avg_every = max(1, int(round(driver.K_SAMPLES / N)))
+    state = {"step": 0}
+
+    def step():
+        k = state["step"]
+        i = k % pool_mb
+        net.forward_backward(frames[i * N:(i + 1) * N], labels[i * N:(i + 1) * N])
+        lr = driver.job_learning_rate(k * N, TOTAL_SAMPLES, world)
+        net.update(lr, 0.075)
+        if world > 1 and (k + 1) % avg_every == 0:
+            net.average(0)
+        state["step"] = k + 1
+
+    # warm-up (includes the one-time, host-synchronising NG initialisations); all kernel
+    # groups profiled here to find the dominant one
+    api.profile_enable(api._lib.PROF_GROUPS)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    wprof = api.profile_read()
+    steady = {g: v for g, v in wprof.items() if g not in ("ng_init",)}
+    dominant = max(steady, key=lambda g: steady[g]["ms"])
+    api.profile_enable([dominant])
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = api.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.mark("t0")
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    clocks.mark("t1")
+    if dist:
+        dist.barrier()
+    launches = api.kernel_launches() - launches0
+    prof = api.profile_read()
+    api.profile_enable([])
+    clocks.stop()
+    ms = e0.elapsed_time(e1)
+    ms_max = driver.max_over_ranks(ms)
+    value = world * args.steps * N / (ms_max / 1e3)
+    peaks = load_peaks()
+    roof = roofline_for(dominant, prof, precision, peaks)
+    shares = {g: v["ms"] for g, v in wprof.items() if v["launches"]}
+
+    # end-to-end through the public API with host buffers: pinned host frames/labels
+    # copied in every step, the step's objective read back every step
+    e2e = None
+    if not args.no_e2e:
+        hf = torch.from_numpy(frames_np[:64 * N]).pin_memory()
+        hl = torch.from_numpy(labels_np[:64 * N]).pin_memory()
+        df = torch.empty((N, CFG3["input_dim"]), dtype=torch.float32, device=dev)
+        dl = torch.empty((N,), dtype=torch.int32, device=dev)
+        k_e2e = max(10, min(args.steps, 200))
+
+        def e2e_step(k):
+            i = k % 64
+            df.copy_(hf[i * N:(i + 1) * N], non_blocking=True)
+            dl.copy_(hl[i * N:(i + 1) * N], non_blocking=True)
+            net.forward_backward(df, dl, objective=True)           # D2H of the objective (8 bytes)
+            net.update(driver.job_learning_rate(state["step"] * N, TOTAL_SAMPLES, world), 0.075)
+            state["step"] += 1
+
+        for k in range(3):
+            e2e_step(k)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(k_e2e):
+            e2e_step(k)
+        torch.cuda.synchronize()
+        dt = driver.max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": world * k_e2e * N / dt, "unit": "frames/s",
+               "h2d_bytes_per_step": N * CFG3["input_dim"] * 4 + N * 4, "d2h_bytes_per_step": 8,
+               "steps": k_e2e, "timer": "host wall clock around the loop (each step synchronises on its objective)"}
+
+    pre = None
+    if rank == 0 and not args.no_precond_bench:
+        try:
+            pre = precondition_bench(api, torch)
+        except Exception as ex:  # report, do not hide
+            pre = {"error": repr(ex)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n = 128
+        val, dt = oracle_steps(args.cpu_steps, 1, n)
+        thr, api_ = blas_threads()
+        cpu = {"value": val, "unit": "frames/s", "cores": thr, "kind": "oracle",
+               "sample": f"{args.cpu_steps} float64 oracle steps of config 3 on {n}-frame minibatches "
+                         f"(steady-state NG states injected), {dt:.1f} s", "blas": api_, "host_cores": cpu_cores()}
+
+    if dist:
+        dist.barrier()
+    if rank != 0:
+        return 0
+    line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if precision == "fp32" else "bf16", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "minibatch": N, "global_batch": N * world,
+                       "parallelism": f"dp{world} (independent jobs, parameter average every {avg_every} "
+                                      f"minibatches = K 400000 samples)",
+                       "gemm_precision": precision,
+                       "l2": f"input pool {POOL_FRAMES} frames x 360 fp32 = 377 MB > 126 MB L2, cycled"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
+            "gpu_launches": launches, "launches_per_step": launches / args.steps,
+            "kernel_group_ms_warmup": shares, "precondition_ms_per_minibatch": pre}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--precision", choices=["fp32", "bf16"], default=os.environ.get("NG_BENCH_PRECISION", "fp32"))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-precond-bench", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=100)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -194,6 +194,40 @@ ng_status nnet_comm_init(nnet_t h, const void* nccl_unique_id, int32_t rank, int
  * then scale (speed reference; order not fixed).  Synchronises the stream. */
 ng_status nnet_average(nnet_t h, int32_t mode);
 
+
+/* ------------------------------------------------ instrumentation (bench.py) ---- */
+
+/* Kernel groups for live per-group timing.  Each group's algorithmic FLOPs and bytes
+ * are counted per launch from the shapes. */
+typedef enum {
+  NG_PROF_FWD_GEMM = 0,   /* Z_l = Y_l W_l^T (+ p-norm)                               */
+  NG_PROF_BWD_GEMM = 1,   /* g = X_l W_l (+ p-norm backward)                           */
+  NG_PROF_UPD_GEMM = 2,   /* W_l += s X_hat^T Y_hat                                    */
+  NG_PROF_NG_PROJ = 3,    /* H = X W^T                                                 */
+  NG_PROF_NG_APPLY = 4,   /* X_hat = X - H W, p_i, traces, gamma                       */
+  NG_PROF_NG_REFRESH = 5, /* J, K, L, one-CTA refresh, W_{t+1} = A_t B_t, B.3.1         */
+  NG_PROF_NG_INIT = 6,    /* B.3.2 initialisation (once per state)                     */
+  NG_PROF_ELEMWISE = 7,   /* input, p-norm, softmax/objective, max-change              */
+  NG_PROF_AVERAGE = 8,    /* parameter averaging                                       */
+  NG_PROF_NUM = 9
+} ng_prof_group;
+
+typedef struct {
+  int64_t launches[16];   /* launches recorded per group since enable                 */
+  double ms[16];          /* summed CUDA-event durations (ms) per group                */
+  double flops[16];       /* summed algorithmic FLOPs per group                        */
+  double bytes[16];       /* summed algorithmic HBM bytes per group                    */
+} ng_profile_stats;
+
+/* Enable CUDA-event timing around every launch of the groups in `group_mask` (bit g =
+ * group g); 0 disables.  Resets the accumulators.  Events are recorded on the stream
+ * each kernel is launched on. */
+ng_status ng_profile_enable(uint32_t group_mask);
+/* Synchronise the recorded events and return the accumulated statistics. */
+ng_status ng_profile_read(ng_profile_stats* out);
+/* Number of kernels this library has launched since it was loaded. */
+int64_t ng_kernel_launches(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,7 +10,7 @@ The binding is loaded lazily so that ``python -m paper_1410_7455_b200.build`` wo
 before the library exists; any use of the API without the built library raises.
 """
 _API = ("NgError", "Nnet", "NnetStats", "OnlinePreconditioner", "comm_unique_id", "default_ng_config",
-        "library_path", "version")
+        "library_path", "version", "profile_enable", "profile_read", "kernel_launches")
 
 
 def __getattr__(name):

@@ -47,6 +47,14 @@ class NnetUpdateStats(ctypes.Structure):
                 ("updated_in", c_int32 * 16), ("updated_out", c_int32 * 16)]
 
 
+class ProfileStats(ctypes.Structure):
+    _fields_ = [("launches", ctypes.c_int64 * 16), ("ms", c_double * 16), ("flops", c_double * 16),
+                ("bytes", c_double * 16)]
+
+
+PROF_GROUPS = ["fwd_gemm", "bwd_gemm", "upd_gemm", "ng_proj", "ng_apply", "ng_refresh", "ng_init", "elemwise",
+               "average"]
+
 # name -> (restype, argtypes); every symbol include/ngsgd.h declares
 SIGNATURES = {
     "ng_last_error": (ctypes.c_char_p, []),
@@ -70,6 +78,9 @@ SIGNATURES = {
     "nnet_comm_get_unique_id": (c_int32, [c_void_p]),
     "nnet_comm_init": (c_int32, [c_void_p, c_void_p, c_int32, c_int32]),
     "nnet_average": (c_int32, [c_void_p, c_int32]),
+    "ng_profile_enable": (c_int32, [ctypes.c_uint32]),
+    "ng_profile_read": (c_int32, [ctypes.POINTER(ProfileStats)]),
+    "ng_kernel_launches": (ctypes.c_int64, []),
 }
 
 

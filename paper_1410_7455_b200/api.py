@@ -198,6 +198,25 @@ class Nnet:
         check(lib.nnet_average(self._h, int(mode)))
 
 
+def profile_enable(groups) -> None:
+    """Time every launch of the named kernel groups with CUDA events (ng_profile_enable)."""
+    mask = 0
+    for g in groups:
+        mask |= 1 << _lib.PROF_GROUPS.index(g)
+    check(lib.ng_profile_enable(mask))
+
+
+def profile_read() -> dict:
+    st = _lib.ProfileStats()
+    check(lib.ng_profile_read(ctypes.byref(st)))
+    return {g: dict(launches=int(st.launches[i]), ms=float(st.ms[i]), flops=float(st.flops[i]),
+                    bytes=float(st.bytes[i])) for i, g in enumerate(_lib.PROF_GROUPS)}
+
+
+def kernel_launches() -> int:
+    return int(lib.ng_kernel_launches())
+
+
 def comm_unique_id() -> bytes:
     n = lib.nnet_comm_id_bytes()
     buf = ctypes.create_string_buffer(n)

@@ -49,8 +49,18 @@ enum : uint32_t {
 
 ng_status status_from_flags(uint32_t flags, const char* where);
 
+// Launch counter (ng_kernel_launches) and per-group CUDA-event timing (ng_profile_*).
+void count_launch();
+struct ProfScope {
+  int group = -1, slot = -1;
+  cudaStream_t st = nullptr;
+  ProfScope(int group, cudaStream_t st, double flops, double bytes);
+  ~ProfScope();
+};
+
 // Check the last launch; returns NG_ECUDA with a message on failure.
 inline ng_status check_launch(const char* what) {
+  count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("launch of ") + what + " failed: " + cudaGetErrorString(e));

@@ -13,6 +13,7 @@
 #include <cmath>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <string>
 
@@ -25,6 +26,42 @@ namespace ng {
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 const char* last_error() { return g_last_error.c_str(); }
+
+// ---- instrumentation -------------------------------------------------------------
+static std::atomic<int64_t> g_launches{0};
+static uint32_t g_prof_mask = 0;
+static std::vector<cudaEvent_t> g_ev0, g_ev1;
+static std::vector<int> g_ev_group;
+static int g_ev_used = 0;
+static ng_profile_stats g_prof{};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static void prof_flush() {
+  for (int i = 0; i < g_ev_used; ++i) {
+    float ms = 0.f;
+    cudaEventSynchronize(g_ev1[i]);
+    if (cudaEventElapsedTime(&ms, g_ev0[i], g_ev1[i]) == cudaSuccess) g_prof.ms[g_ev_group[i]] += ms;
+  }
+  g_ev_used = 0;
+}
+
+ProfScope::ProfScope(int grp, cudaStream_t s, double flops, double bytes) {
+  if (!((g_prof_mask >> grp) & 1u)) return;
+  if (g_ev_used == (int)g_ev0.size()) prof_flush();
+  group = grp;
+  st = s;
+  slot = g_ev_used++;
+  g_ev_group[slot] = grp;
+  g_prof.launches[grp] += 1;
+  g_prof.flops[grp] += flops;
+  g_prof.bytes[grp] += bytes;
+  cudaEventRecord(g_ev0[slot], s);
+}
+
+ProfScope::~ProfScope() {
+  if (slot >= 0) cudaEventRecord(g_ev1[slot], st);
+}
 
 ng_status status_from_flags(uint32_t f, const char* where) {
   if (f & kErrNotPD) { set_error(std::string(where) + ": Cholesky of O_t failed (corrupted NG state, B.3.1)"); return NG_ENOTPD; }
@@ -640,7 +677,10 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
       passthrough_kernel<<<1, 256, 0, st>>>(n, h->p, p_out, h->gamma, gamma_out);
       return check_launch("passthrough_kernel");
     }
-    NG_TRY(ngsgd_init(h, n, x, ld, trXX));
+    {
+      ProfScope ps(NG_PROF_NG_INIT, st, 0.0, 0.0);
+      NG_TRY(ngsgd_init(h, n, x, ld, trXX));
+    }
   }
   const bool upd = (update < 0)
                        ? (h->t < h->cfg.always_update_first || (h->t % h->cfg.update_period) == 0)
@@ -658,13 +698,19 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
   }
   const double eta = 1.0 - exp(-(double)n / (double)h->cfg.s_samples);   // eqn:eta:ns
   float* W = h->W[h->cur];
+  const double nRD = (double)n * R * D;
   // H = X W^T (eqn:ht), split over D, fixed-order reduction
+  {
+  ProfScope ps(NG_PROF_NG_PROJ, st, 2.0 * nRD, 4.0 * ((double)n * D + (double)R * D));
   NG_TRY((gemm_simt<float, true, true>(st, n, R, D, x, ld, W, h->ldw,
                                        EpiStoreSplit<float>{h->Hpart, R, (int64_t)n * R}, h->h_splits)));
   const int hs = gemm_simt_splits(D, h->h_splits);
   reduce_splits_kernel<<<ceil_div((int64_t)n * R, 256), 256, 0, st>>>(h->H, h->Hpart, (int64_t)n * R, hs, (int64_t)n * R, nullptr);
   NG_TRY(check_launch("reduce_splits(H)"));
+  }
   if (upd) {
+    ProfScope ps(NG_PROF_NG_REFRESH, st, 2.0 * nRD + 4.0 * (double)R * R * D,
+                 4.0 * ((double)n * D + 3.0 * R * D));
     // J = H^T X -- before X is overwritten
     NG_TRY((gemm_simt<float, false, false>(st, R, D, n, h->H, R, x, ld, EpiStore<float>{h->J, h->ldw, 1.f})));
     // K = J J^T
@@ -687,15 +733,17 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
   }
   // X_hat = X - H W in place, with partial row norms
   {
+    ProfScope ps(NG_PROF_NG_APPLY, st, 2.0 * nRD, 4.0 * (2.0 * n * D + (double)R * D));
     dim3 grid(ceil_div(n, kApplyRows), ceil_div(D, kApplyCols));
     const size_t smem = sizeof(float) * (kApplyRows * R + R * kApplyCols);
     apply_kernel<<<grid, 256, smem, st>>>(n, D, R, x, ld, h->H, W, h->ldw, h->xxpart, h->ppart, h->max_rows);
     NG_TRY(check_launch("apply_kernel"));
+    finalize_kernel<<<1, 512, 0, st>>>(n, h->ctiles, h->xxpart, h->ppart, h->max_rows, h->p, p_out, h->sums,
+                                       h->gamma, gamma_out, h->flags);
+    NG_TRY(check_launch("finalize_kernel"));
   }
-  finalize_kernel<<<1, 512, 0, st>>>(n, h->ctiles, h->xxpart, h->ppart, h->max_rows, h->p, p_out, h->sums,
-                                     h->gamma, gamma_out, h->flags);
-  NG_TRY(check_launch("finalize_kernel"));
   if (upd) {
+    ProfScope ps(NG_PROF_NG_REFRESH, st, 2.0 * (double)R * R * D + 2.0 * R * D, 4.0 * (4.0 * R * D));
     refresh_kernel<<<1, 512, refresh_smem_bytes(R), st>>>(R, D, n, eta, (double)h->cfg.alpha,
                                                           (double)h->cfg.epsilon, h->KL, h->dstate, h->sums,
                                                           h->Amat, h->svec, h->flags);
@@ -747,6 +795,30 @@ void ngsgd_config_default(ngsgd_config* cfg, int32_t rank) {
   cfg->always_update_first = 10;
   cfg->epsilon = 1e-10f;
 }
+
+ng_status ng_profile_enable(uint32_t mask) {
+  if (mask != 0 && g_ev0.empty()) {
+    const int pool = 8192;
+    g_ev0.resize(pool); g_ev1.resize(pool); g_ev_group.resize(pool);
+    for (int i = 0; i < pool; ++i) {
+      NG_CUDA_TRY(cudaEventCreate(&g_ev0[i]));
+      NG_CUDA_TRY(cudaEventCreate(&g_ev1[i]));
+    }
+  }
+  if (g_ev_used) prof_flush();
+  std::memset(&g_prof, 0, sizeof(g_prof));
+  g_prof_mask = mask;
+  return NG_OK;
+}
+
+ng_status ng_profile_read(ng_profile_stats* out) {
+  NG_REQUIRE(out != nullptr, NG_EINVAL, "NULL argument");
+  prof_flush();
+  *out = g_prof;
+  return NG_OK;
+}
+
+int64_t ng_kernel_launches(void) { return g_launches.load(); }
 
 ng_status ngsgd_create(int32_t dim, int32_t max_rows, const ngsgd_config* cfg, void* cuda_stream, ngsgd_t* out) {
   return ngsgd_create_impl(dim, max_rows, cfg, (cudaStream_t)cuda_stream, out);

@@ -362,6 +362,8 @@ ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const
   // forward
   for (int l = 0; l < L; ++l) {
     const float* W = h->arena + h->off[l];
+    const double R_ = h->rows[l], C_ = h->cols[l];
+    ProfScope ps(NG_PROF_FWD_GEMM, st, 2.0 * n * R_ * C_, 4.0 * (n * C_ + R_ * C_ + n * R_));
     if (tc) {
       NG_TRY(h->tc.forward(l, n, h->Y[l], W, h->Z[l]));
     } else {
@@ -381,6 +383,8 @@ ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const
   for (int l = L - 1; l >= 1; --l) {
     const float* W = h->arena + h->off[l];
     EpiPnormBack epi{h->X[l - 1], h->Z[l - 1], h->Y[l], h->rows[l - 1], h->ldp[l], G};
+    const double R_ = h->rows[l], C_ = h->cols[l], Rp = h->rows[l - 1];
+    ProfScope ps(NG_PROF_BWD_GEMM, st, 2.0 * n * R_ * (C_ - 1), 4.0 * (n * R_ + R_ * C_ + 2.0 * n * Rp + n * C_));
     if (tc) {
       NG_TRY(h->tc.backward(l, n, h->X[l], W, epi));
     } else {
@@ -423,6 +427,8 @@ ng_status nnet_update(nnet_t h, float lr, float max_change_per_sample, nnet_upda
   const bool tc = h->cfg.precision == NG_BF16;
   for (int l = 0; l < L; ++l) {
     float* W = h->arena + h->off[l];
+    const double R_ = h->rows[l], C_ = h->cols[l];
+    ProfScope ps(NG_PROF_UPD_GEMM, st, 2.0 * n * R_ * C_, 4.0 * (n * R_ + n * C_ + 2.0 * R_ * C_));
     if (tc) {
       NG_TRY(h->tc.update(l, n, h->X[l], h->Y[l], W, h->scale + l));
     } else {
@@ -510,6 +516,7 @@ ng_status nnet_average(nnet_t h, int32_t mode) {
   const int nr = h->nranks;
   NG_REQUIRE(h->shard * nr == h->arena_count, NG_ESTATE, "arena not divisible by nranks");
   ncclResult_t r = ncclSuccess;
+  ProfScope ps(NG_PROF_AVERAGE, st, 0.0, 4.0 * 2.0 * h->arena_count);
   if (mode == 0) {
     r = ncclGroupStart();
     for (int p = 0; p < nr && r == ncclSuccess; ++p) {

@@ -1,0 +1,77 @@
+"""Host-side driver logic for data-parallel training (section 3.1 of arXiv 1410.7455):
+one SGD job per GPU, per-job learning rate, and the every-K parameter average.
+
+Pure host scalars / bookkeeping; every tensor operation runs in libngsgd.so.  Kept free
+of torch.cuda so the multi-rank logic can be exercised with the gloo backend on CPU.
+"""
+from __future__ import annotations
+
+import math
+
+K_SAMPLES = 400_000        # samples per job per outer iteration
+REF_JOBS = 6               # default lr 0.01 -> 0.001 corresponds to 6 jobs
+
+
+def job_learning_rate(samples_seen: float, total_samples: float, n_jobs: int, lr_initial: float = 0.01,
+                      lr_final: float = 0.001, ref_jobs: int = REF_JOBS) -> float:
+    """Per-job rate: exponential schedule from lr_initial to lr_final (reading
+    R17: per minibatch by samples seen), scaled so the effective rate (per-job rate / n_jobs,
+    P:103-109) is that of the ref_jobs-job default."""
+    frac = min(max(samples_seen / float(total_samples), 0.0), 1.0)
+    lr = lr_initial * (lr_final / lr_initial) ** frac
+    return lr * n_jobs / ref_jobs
+
+
+def minibatches_per_outer_iteration(minibatch: int, k_samples: int = K_SAMPLES) -> list:
+    """Sizes of the minibatches one job runs in an outer iteration of exactly K samples
+    (reading R24): 781 x 512 + 1 x 128 for K = 400 000."""
+    full, rem = divmod(k_samples, minibatch)
+    return [minibatch] * full + ([rem] if rem else [])
+
+
+def rank_seed(rank: int, base: int = 1410) -> int:
+    """Disjoint data per job: seed = 1410 + 7455 * rank."""
+    return base + 7455 * int(rank)
+
+
+def shard_bounds(count: int, nranks: int, rank: int):
+    """The slice of the flat parameter arena rank `rank` reduces in the deterministic
+    average (all arenas are padded to a multiple of nranks)."""
+    if count % nranks:
+        raise ValueError("arena must be padded to a multiple of nranks")
+    s = count // nranks
+    return rank * s, (rank + 1) * s
+
+
+def tree_order(n: int) -> list:
+    """The fixed pairwise-tree summation order over rank index used by nnet_average
+    (R18), as a nested tuple, e.g. n = 4 -> ((0, 1), (2, 3))."""
+    level = list(range(n))
+    while len(level) > 1:
+        level = [(level[k], level[k + 1]) if k + 1 < len(level) else level[k] for k in range(0, len(level), 2)]
+    return level[0]
+
+
+def max_over_ranks(value: float, group=None) -> float:
+    """Max of a host scalar over all ranks (timing is max-over-ranks)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(value)
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+def broadcast_bytes(payload: bytes | None, src: int = 0, group=None) -> bytes:
+    """Broadcast a small byte string (the NCCL unique id) from `src` to all ranks."""
+    import torch.distributed as dist
+    obj = [payload]
+    dist.broadcast_object_list(obj, src=src, group=group)
+    return obj[0]
+
+
+def outer_iteration_of(step: int, minibatch: int, k_samples: int = K_SAMPLES) -> int:
+    return int(math.floor(step * minibatch / k_samples))
