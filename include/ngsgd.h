@@ -117,7 +117,12 @@ ng_status ngsgd_set_state(ngsgd_t h, const ngsgd_state_host* in);
 
 /* ---------------------------------------- p-norm / softmax DNN training step ---- */
 
-typedef enum { NG_FP32 = 0, NG_BF16 = 1 } ng_precision;
+/* NG_FP32: every GEMM on CUDA cores in FP32 (paper-faithful; parity 1e-4).
+ * NG_TF32: the DNN GEMMs (forward, backward-data, weight update) on tcgen05 tensor cores
+ *          reading the FP32 buffers as TF32, FP32 accumulation (parity bar 2e-2 of the
+ *          north star for reduced-precision tensor-core inputs).  NG-SGD stays FP32.
+ * NG_BF16: reserved. */
+typedef enum { NG_FP32 = 0, NG_BF16 = 1, NG_TF32 = 2 } ng_precision;
 
 /* Network: input_dim -> num_hidden x [affine hidden_dim -> p-norm /pnorm_group] ->
  * affine num_classes -> softmax (p = 2, R19). */
@@ -227,6 +232,18 @@ ng_status ng_profile_enable(uint32_t group_mask);
 ng_status ng_profile_read(ng_profile_stats* out);
 /* Number of kernels this library has launched since it was loaded. */
 int64_t ng_kernel_launches(void);
+
+/* ------------------------------------------------------------ diagnostics ---- */
+
+/* One tensor-core GEMM C = A B exactly as the DNN's TF32 path runs it (tcgen05.mma
+ * kind::tf32 fed by TMA, FP32 accumulation in TMEM); exposed for unit tests.
+ *   A is M x K: a_kmajor != 0 -> A[m][k] = A[m*lda + k], else A[m][k] = A[k*lda + m].
+ *   B is K x N: b_kmajor != 0 -> B[k][n] = B[n*ldb + k], else B[k][n] = B[k*ldb + n].
+ *   C (device, M x N, ldc) is overwritten.  bn in {64, 128}; splits >= 1 (split-K with a
+ *   fixed-order reduction).  All pointers device, 16-byte aligned, lda/ldb % 4 == 0. */
+ng_status ng_debug_gemm_tf32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda, int32_t a_kmajor,
+                             const float* B, int64_t ldb, int32_t b_kmajor, float* C, int64_t ldc,
+                             int32_t bn, int32_t splits, void* cuda_stream);
 
 #ifdef __cplusplus
 }

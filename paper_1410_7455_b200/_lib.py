@@ -81,6 +81,8 @@ SIGNATURES = {
     "ng_profile_enable": (c_int32, [ctypes.c_uint32]),
     "ng_profile_read": (c_int32, [ctypes.POINTER(ProfileStats)]),
     "ng_kernel_launches": (ctypes.c_int64, []),
+    "ng_debug_gemm_tf32": (c_int32, [c_int32, c_int32, c_int32, c_void_p, c_int64, c_int32, c_void_p, c_int64,
+                                     c_int32, c_void_p, c_int64, c_int32, c_int32, c_void_p]),
 }
 
 

@@ -129,7 +129,7 @@ class Nnet:
         cfg.precond = 1 if precond else 0
         cfg.ng_in = default_ng_config(rank_in, **(ng_overrides or {}))
         cfg.ng_out = default_ng_config(rank_out, **(ng_overrides or {}))
-        cfg.precision = {"fp32": 0, "bf16": 1}[precision]
+        cfg.precision = {"fp32": 0, "bf16": 1, "tf32": 2}[precision]
         cfg.seed = int(seed)
         h = ctypes.c_void_p()
         check(lib.nnet_create(ctypes.byref(cfg), _stream_handle(stream), ctypes.byref(h)))

@@ -10,8 +10,8 @@
 // independent 2x2 block updates  A'[P,Q] = G_P^T A[P,Q] G_Q  (P, Q index rotation
 // pairs), so one round costs one barrier after computing the rotations and one after
 // the update.  Eigenvectors are accumulated as ROWS of Vt (Vt = U^T).  Sweeps stop when
-// a full sweep performs no rotation (|a_pq| <= 1e-15 sqrt(|a_pp a_qq|) or below an
-// absolute floor), or after max_sweeps.
+// a full sweep performs no rotation (|a_pq| <= rel_tol sqrt(|a_pp a_qq|), rel_tol =
+// 1e-12 by default, or below an absolute floor), or after max_sweeps.
 //
 // A and Vt may live in shared or global memory (generic addressing).
 #pragma once
@@ -41,7 +41,7 @@ __device__ __forceinline__ void jacobi_pair(int round, int k, int npad, int& p, 
 // the diagonal of A holds the eigenvalues (unsorted), Vt (n x n, ldv) holds the
 // eigenvectors as rows.  Must be called by all threads of the CTA.
 __device__ void jacobi_eig(double* A, int lda, double* Vt, int ldv, int n, JacobiScratch sc,
-                           int max_sweeps, double abs_floor) {
+                           int max_sweeps, double abs_floor, double rel_tol = 1e-12) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int npad = n + (n & 1);
   const int m = npad / 2;
@@ -63,7 +63,7 @@ __device__ void jacobi_eig(double* A, int lda, double* Vt, int ldv, int n, Jacob
         if (q < n) {
           const double app = A[(int64_t)p * lda + p], aqq = A[(int64_t)q * lda + q];
           const double apq = A[(int64_t)p * lda + q];
-          const double thr = fmax(1e-15 * sqrt(fabs(app * aqq)), abs_floor);
+          const double thr = fmax(rel_tol * sqrt(fabs(app * aqq)), abs_floor);
           if (fabs(apq) > thr) {
             const double theta = (aqq - app) / (2.0 * apq);
             t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
@@ -75,15 +75,10 @@ __device__ void jacobi_eig(double* A, int lda, double* Vt, int ldv, int n, Jacob
         sc.pp[k] = p; sc.qq[k] = q; sc.c[k] = c; sc.s[k] = s; sc.t[k] = t;
       }
       __syncthreads();
-      // ---- A' = J^T A J as 2x2 block updates over pairs (k1 <= k2), mirrored.
-      const int nblk = m * (m + 1) / 2;
-      for (int idx = tid; idx < nblk; idx += nt) {
-        // map idx -> (k1, k2) with k1 <= k2
-        int k1 = (int)((sqrt(8.0 * idx + 1.0) - 1.0) * 0.5);
-        while ((k1 + 1) * (k1 + 2) / 2 <= idx) ++k1;
-        while (k1 * (k1 + 1) / 2 > idx) --k1;
-        const int k2r = idx - k1 * (k1 + 1) / 2;  // 0..k1
-        const int ka = k2r, kb = k1;              // ka <= kb
+      // ---- A' = J^T A J as 2x2 block updates over pairs (ka <= kb), mirrored.
+      for (int idx = tid; idx < m * m; idx += nt) {
+        const int ka = idx % m, kb = idx / m;
+        if (ka > kb) continue;
         const int p1 = sc.pp[ka], q1 = sc.qq[ka], p2 = sc.pp[kb], q2 = sc.qq[kb];
         const double c1 = sc.c[ka], s1 = sc.s[ka], c2 = sc.c[kb], s2 = sc.s[kb];
         if (s1 == 0.0 && s2 == 0.0) continue;

@@ -1,0 +1,375 @@
+// gemm_tc.cu -- tcgen05/TMEM/TMA GEMM kernels (sm_100a), see gemm_tc.cuh.
+//
+// CTA = 128 threads, one 128 x BN output tile (cta_group::1, UMMA M = 128):
+//   warp 0 lane 0 : TMA producer   (cp.async.bulk.tensor -> S-stage smem ring, mbarrier tx)
+//   warp 1 lane 0 : MMA issuer     (tcgen05.mma.kind::tf32, 4 x K=8 per 32-wide k-block,
+//                                    tcgen05.commit -> frees the smem stage)
+//   warps 0..3    : epilogue       (tcgen05.ld 32x32b: warp w owns TMEM lanes 32w..32w+31,
+//                                    i.e. tile rows; functor applied per element)
+// Shared-memory layouts are the canonical UMMA SWIZZLE_128B layouts produced directly by
+// TMA with CU_TENSOR_MAP_SWIZZLE_128B:
+//   K-major  : [rows][128 B] (32 fp32 of K per row), 8-row atoms 1024 B apart (SBO)
+//   MN-major : boxes of [32 k-rows][128 B] (32 fp32 of M/N), boxes 4096 B apart (LBO),
+//              8-k-row atoms 1024 B apart (SBO)
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+
+#include "gemm_tc.cuh"
+
+namespace ng {
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 32;        // fp32 elements per 128-byte swizzle row = one k-block
+constexpr int kStages = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+// Shared-memory matrix descriptor, SWIZZLE_128B, sm100 version field = 1.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// Instruction descriptor: D f32, A/B tf32, majors, N>>3, M>>4.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int BN, bool AK, bool BKM, int EPI>
+__global__ void __launch_bounds__(128, 1)
+tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                    int K, int kb_per_split, TcEpilogue epi) {
+  constexpr uint32_t A_BYTES = kBM * kBK * 4, B_BYTES = BN * kBK * 4, STAGE = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full_bar[kStages];
+  __shared__ __align__(8) uint64_t empty_bar[kStages];
+  __shared__ __align__(8) uint64_t accum_bar;
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * BN;
+  const int kb_total = (K + kBK - 1) / kBK;
+  const int kb0 = blockIdx.z * kb_per_split;
+  const int kb1 = min(kb_total, kb0 + kb_per_split);
+  const int nkb = max(0, kb1 - kb0);
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+    mbar_init(&accum_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % kStages;
+      const uint32_t ph = (uint32_t)(i / kStages) & 1u;
+      mbar_wait(&empty_bar[s], ph ^ 1u);
+      uint8_t* sa = smem + s * STAGE;
+      uint8_t* sb = sa + A_BYTES;
+      mbar_expect_tx(&full_bar[s], STAGE);
+      const int kc = (kb0 + i) * kBK;
+      if (AK) {
+        tma_load_2d(sa, &tmA, kc, m0, &full_bar[s]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < kBM / 32; ++j) tma_load_2d(sa + j * 4096, &tmA, m0 + 32 * j, kc, &full_bar[s]);
+      }
+      if (BKM) {
+        tma_load_2d(sb, &tmB, kc, n0, &full_bar[s]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < BN / 32; ++j) tma_load_2d(sb + j * 4096, &tmB, n0 + 32 * j, kc, &full_bar[s]);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer (single thread)
+    constexpr uint32_t idesc = idesc_tf32(kBM, BN, !AK, !BKM);
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % kStages;
+      const uint32_t ph = (uint32_t)(i / kStages) & 1u;
+      mbar_wait(&full_bar[s], ph);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
+#pragma unroll
+      for (int k = 0; k < kBK / 8; ++k) {
+        const uint64_t da = AK ? sw128_desc(sa + k * 32, 16, 1024) : sw128_desc(sa + k * 1024, 4096, 1024);
+        const uint64_t db = BKM ? sw128_desc(sb + k * 32, 16, 1024) : sw128_desc(sb + k * 1024, 4096, 1024);
+        mma_tf32(tmem, da, db, idesc, (i > 0 || k > 0) ? 1u : 0u);
+      }
+      umma_commit(&empty_bar[s]);
+    }
+    umma_commit(&accum_bar);
+  }
+  __syncwarp();
+
+  // ---------------- epilogue: TMEM -> registers -> functor
+  mbar_wait(&accum_bar, 0);
+  tc_fence_after();
+  __syncwarp();
+  const int row = m0 + warp * 32 + lane;
+#pragma unroll 1
+  for (int c = 0; c < BN / 16; ++c) {
+    uint32_t v[16];
+    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * 16), v);
+    if (row < M) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int n = n0 + c * 16 + j;
+        if (n < N) {
+          const float acc = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
+          if (EPI == TC_EPI_STORE) {
+            epi.C[(int64_t)row * epi.ldc + n] = acc;
+          } else if (EPI == TC_EPI_AXPY) {
+            float* p = epi.C + (int64_t)row * epi.ldc + n;
+            *p = fmaf(*epi.scale, acc, *p);
+          } else {
+            epi.C[(int64_t)blockIdx.z * epi.zstride + (int64_t)row * epi.ldc + n] = acc;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2D fp32 tensor [outer][inner] with row stride ld (elements), box {32, box_outer}.
+ng_status make_tmap(CUtensorMap* out, const float* ptr, int64_t inner, int64_t outer, int64_t ld, int box_outer) {
+  using Key = std::tuple<const float*, int64_t, int64_t, int64_t, int>;
+  static std::map<Key, CUtensorMap> cache;
+  const Key key{ptr, inner, outer, ld, box_outer};
+  auto it = cache.find(key);
+  if (it != cache.end()) { *out = it->second; return NG_OK; }
+  EncodeTiledFn fn = encode_fn();
+  NG_REQUIRE(fn != nullptr, NG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  NG_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0 && (ld % 4) == 0, NG_ESHAPE,
+             "TMA operand must be 16B aligned with ld % 4 == 0");
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {32u, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1u, 1u};
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)r));
+    return NG_ECUDA;
+  }
+  if (cache.size() > 4096) cache.clear();
+  cache[key] = m;
+  *out = m;
+  return NG_OK;
+}
+
+template <int BN, bool AK, bool BKM, int EPI>
+ng_status launch(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int kbps,
+                 int splits, const TcEpilogue& epi) {
+  constexpr size_t smem = (size_t)kStages * (kBM * kBK * 4 + BN * kBK * 4) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    NG_CUDA_TRY(cudaFuncSetAttribute(tc_gemm_tf32_kernel<BN, AK, BKM, EPI>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  dim3 grid(ceil_div(N, BN), ceil_div(M, kBM), splits);
+  tc_gemm_tf32_kernel<BN, AK, BKM, EPI><<<grid, 128, smem, st>>>(ta, tb, M, N, K, kbps, epi);
+  return check_launch("tc_gemm_tf32_kernel");
+}
+
+template <int BN, bool AK, bool BKM>
+ng_status dispatch_epi(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int kbps,
+                       int splits, const TcEpilogue& epi) {
+  switch (epi.kind) {
+    case TC_EPI_STORE: return launch<BN, AK, BKM, TC_EPI_STORE>(st, ta, tb, M, N, K, kbps, splits, epi);
+    case TC_EPI_AXPY: return launch<BN, AK, BKM, TC_EPI_AXPY>(st, ta, tb, M, N, K, kbps, splits, epi);
+    default: return launch<BN, AK, BKM, TC_EPI_PARTIAL>(st, ta, tb, M, N, K, kbps, splits, epi);
+  }
+}
+
+template <int BN>
+ng_status dispatch_major(cudaStream_t st, bool ak, bool bk, const CUtensorMap& ta, const CUtensorMap& tb, int M,
+                         int N, int K, int kbps, int splits, const TcEpilogue& epi) {
+  if (ak && bk) return dispatch_epi<BN, true, true>(st, ta, tb, M, N, K, kbps, splits, epi);
+  if (ak && !bk) return dispatch_epi<BN, true, false>(st, ta, tb, M, N, K, kbps, splits, epi);
+  if (!ak && bk) return dispatch_epi<BN, false, true>(st, ta, tb, M, N, K, kbps, splits, epi);
+  return dispatch_epi<BN, false, false>(st, ta, tb, M, N, K, kbps, splits, epi);
+}
+
+}  // namespace
+
+int tc_splits(int K, int splits) {
+  const int kb = std::max(1, ceil_div(K, kBK));
+  splits = std::max(1, std::min(splits, kb));
+  const int kbps = ceil_div(kb, splits);
+  return ceil_div(kb, kbps);
+}
+
+ng_status tc_gemm_tf32(cudaStream_t st, int M, int N, int K, const float* A, int64_t lda, bool a_kmajor,
+                       const float* B, int64_t ldb, bool b_kmajor, const TcEpilogue& epi, int bn, int splits,
+                       int* splits_used) {
+  NG_REQUIRE(M >= 1 && N >= 1 && K >= 1, NG_ESHAPE, "tc_gemm_tf32: empty problem");
+  NG_REQUIRE(bn == 64 || bn == 128, NG_EINVAL, "tc_gemm_tf32: bn must be 64 or 128");
+  const int kb = ceil_div(K, kBK);
+  splits = tc_splits(K, splits);
+  const int kbps = ceil_div(kb, splits);
+  NG_REQUIRE(splits == 1 || epi.kind == TC_EPI_PARTIAL, NG_EINVAL, "split-K needs the partial epilogue");
+  if (splits_used) *splits_used = splits;
+  CUtensorMap ta, tb;
+  if (a_kmajor) NG_TRY(make_tmap(&ta, A, K, M, lda, kBM));     // [M][K]
+  else NG_TRY(make_tmap(&ta, A, M, K, lda, 32));               // [K][M]
+  if (b_kmajor) NG_TRY(make_tmap(&tb, B, K, N, ldb, bn));      // [N][K]
+  else NG_TRY(make_tmap(&tb, B, N, K, ldb, 32));               // [K][N]
+  if (bn == 64) return dispatch_major<64>(st, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
+  return dispatch_major<128>(st, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
+}
+
+// Fixed-order reduction of split-K partials: C[m][n] = sum_z part[z][m][n].
+__global__ void reduce_partials_kernel(float* __restrict__ C, int64_t ldc, const float* __restrict__ part, int M,
+                                       int N, int sp) {
+  const int64_t total = (int64_t)M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int z = 0; z < sp; ++z) s += part[(int64_t)z * total + i];
+    C[(i / N) * ldc + (i % N)] = s;
+  }
+}
+
+ng_status reduce_partials_2d(cudaStream_t st, float* C, int64_t ldc, const float* part, int M, int N, int sp) {
+  reduce_partials_kernel<<<std::min(4096, ceil_div((int64_t)M * N, 256)), 256, 0, st>>>(C, ldc, part, M, N, sp);
+  return check_launch("reduce_partials_kernel");
+}
+
+}  // namespace ng
+
+// ------------------------------------------------------------------ C ABI diagnostics
+
+extern "C" ng_status ng_debug_gemm_tf32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda, int32_t a_kmajor,
+                                        const float* B, int64_t ldb, int32_t b_kmajor, float* C, int64_t ldc,
+                                        int32_t bn, int32_t splits, void* stream) {
+  using namespace ng;
+  NG_REQUIRE(A && B && C, NG_EINVAL, "NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  TcEpilogue e;
+  if (splits <= 1) {
+    e.kind = TC_EPI_STORE;
+    e.C = C;
+    e.ldc = ldc;
+    return tc_gemm_tf32(st, M, N, K, A, lda, a_kmajor != 0, B, ldb, b_kmajor != 0, e, bn, 1);
+  }
+  const int sp = tc_splits(K, splits);
+  float* part = nullptr;
+  NG_CUDA_TRY(cudaMallocAsync((void**)&part, sizeof(float) * (size_t)sp * M * N, st));
+  e.kind = TC_EPI_PARTIAL;
+  e.C = part;
+  e.ldc = N;
+  e.zstride = (int64_t)M * N;
+  ng_status s = tc_gemm_tf32(st, M, N, K, A, lda, a_kmajor != 0, B, ldb, b_kmajor != 0, e, bn, sp);
+  if (s == NG_OK) s = reduce_partials_2d(st, C, ldc, part, M, N, sp);
+  cudaFreeAsync(part, st);
+  return s;
+}

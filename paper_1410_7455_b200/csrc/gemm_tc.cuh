@@ -1,28 +1,42 @@
-// gemm_tc.cuh -- tcgen05/TMEM/TMA GEMMs for the BF16 path (sm_100a).  Interface used by
-// nnet.cu; see gemm_tc.cu for the kernels.
+// gemm_tc.cuh -- tcgen05 (5th-gen tensor core) GEMM for sm_100a: TMA-fed operands in
+// 128B-swizzled shared memory, accumulators in TMEM, tcgen05.ld epilogue.
+//
+//   C[M x N] (epilogue)= A[M x K] * B[K x N]
+//   A K-major : A[m][k] = A[m*lda + k]      A MN-major : A[m][k] = A[k*lda + m]
+//   B K-major : B[k][n] = B[n*ldb + k]      B MN-major : B[k][n] = B[k*ldb + n]
+//
+// Operands are FP32 in HBM and are consumed by the tensor core as TF32 (kind::tf32,
+// FP32 accumulation): no conversion pass and no shadow copies; the same FP32 buffers feed
+// the NG-SGD kernels.  This is the "TF32 tensor-core" precision mode.
 #pragma once
-
-#include <vector>
 
 #include "ng_common.cuh"
 
-struct EpiPnormBack;
-
 namespace ng {
 
-struct TcGemm {
-  bool ready = false;
-  ng_status init(const std::vector<int>& rows, const std::vector<int>& cols, const std::vector<int>& ldp, int max_n,
-                 cudaStream_t st) {
-    (void)rows; (void)cols; (void)ldp; (void)max_n; (void)st;
-    set_error("BF16 tensor-core path is not built in this version (use precision = NG_FP32)");
-    return NG_EINVAL;
-  }
-  template <class Epi>
-  ng_status backward(int, int, const float*, const float*, const Epi&) { return NG_EINVAL; }
-  ng_status forward(int, int, const float*, const float*, float*) { return NG_EINVAL; }
-  ng_status update(int, int, const float*, const float*, float*, const float*) { return NG_EINVAL; }
-  void release() {}
+enum TcEpiKind : int {
+  TC_EPI_STORE = 0,     // C[m][n] = acc
+  TC_EPI_AXPY = 1,      // C[m][n] += (*scale) * acc          (weight update, eqn:add:w)
+  TC_EPI_PARTIAL = 2,   // C[z][m][n] = acc                    (split-K partials)
 };
+
+struct TcEpilogue {
+  int kind = TC_EPI_STORE;
+  float* C = nullptr;
+  int64_t ldc = 0;
+  int64_t zstride = 0;        // TC_EPI_PARTIAL: elements between split slices
+  const float* scale = nullptr;
+};
+
+// Launch one GEMM on `st`.  bn in {64, 128}; splits >= 1 (K split evenly over 32-wide
+// k-blocks; with splits > 1 the epilogue must be TC_EPI_PARTIAL).  Pointers must be 16B
+// aligned and lda/ldb multiples of 4 (TMA).  Returns the number of splits used via
+// *splits_used (may be smaller than requested).
+ng_status tc_gemm_tf32(cudaStream_t st, int M, int N, int K, const float* A, int64_t lda, bool a_kmajor,
+                       const float* B, int64_t ldb, bool b_kmajor, const TcEpilogue& epi, int bn = 128,
+                       int splits = 1, int* splits_used = nullptr);
+
+// Split count actually used for a requested split count.
+int tc_splits(int K, int splits);
 
 }  // namespace ng

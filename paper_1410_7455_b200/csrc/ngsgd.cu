@@ -200,7 +200,7 @@ __global__ void copy_gated_kernel(int R, int D, float* __restrict__ dst, const f
 // refresh: the R x R part of the update, one CTA, FP64
 // ------------------------------------------------------------------------------------
 
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(1024)
 refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
                const float* __restrict__ KL, double* __restrict__ dstate,
                const double* __restrict__ sums, float* __restrict__ Amat,
@@ -744,7 +744,7 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
   }
   if (upd) {
     ProfScope ps(NG_PROF_NG_REFRESH, st, 2.0 * (double)R * R * D + 2.0 * R * D, 4.0 * (4.0 * R * D));
-    refresh_kernel<<<1, 512, refresh_smem_bytes(R), st>>>(R, D, n, eta, (double)h->cfg.alpha,
+    refresh_kernel<<<1, 1024, refresh_smem_bytes(R), st>>>(R, D, n, eta, (double)h->cfg.alpha,
                                                           (double)h->cfg.epsilon, h->KL, h->dstate, h->sums,
                                                           h->Amat, h->svec, h->flags);
     NG_TRY(check_launch("refresh_kernel"));

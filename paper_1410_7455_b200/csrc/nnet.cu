@@ -12,6 +12,7 @@
 //   average:   W <- tree_sum_r(W^r) / n over NCCL
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -22,6 +23,8 @@
 #include "ngsgd_impl.cuh"
 
 using namespace ng;
+
+constexpr int kBwdSplits = 6;   // split-K of the TF32 backward-data GEMM (K = 3000..5000)
 
 struct nnet_ctx {
   nnet_config cfg{};
@@ -42,8 +45,10 @@ struct nnet_ctx {
   int* eflags = nullptr;      // sticky error bits
   int n_last = 0;
   bool have_fb = false;
-  // tensor-core (BF16) path
-  TcGemm tc;
+  // tensor-core (TF32) path: split-K partials of the backward-data GEMM
+  std::vector<int> ldr;                      // leading dimension of Z_l / X_l (rows padded to 8)
+  float* gpart = nullptr;
+  size_t gpart_count = 0;
   // NCCL
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
@@ -96,14 +101,15 @@ __global__ void input_kernel(int n, int din, const float* __restrict__ f, int64_
 }
 
 // p-norm, p = 2: a_j = sqrt(sum_{k in group j} z_k^2); Y_next = [a, 1].
-__global__ void pnorm_kernel(int n, int dout, int G, const float* __restrict__ Z, float* __restrict__ Yn, int ldy) {
+__global__ void pnorm_kernel(int n, int dout, int ldz, int G, const float* __restrict__ Z, float* __restrict__ Yn,
+                             int ldy) {
   const int dp = dout / G;
   const int64_t total = (int64_t)n * ldy;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(i / ldy), c = (int)(i % ldy);
     float v = 0.f;
     if (c < dp) {
-      const float* z = Z + (int64_t)r * dout + (int64_t)c * G;
+      const float* z = Z + (int64_t)r * ldz + (int64_t)c * G;
       float s = 0.f;
       for (int k = 0; k < G; ++k) s = fmaf(z[k], z[k], s);
       v = sqrtf(s);
@@ -114,11 +120,11 @@ __global__ void pnorm_kernel(int n, int dout, int G, const float* __restrict__ Z
 
 // log p(y|x) = z_y - logsumexp(z); X_L = onehot(y) - softmax(z); one CTA per row.
 __global__ void __launch_bounds__(256)
-softmax_kernel(int n, int C, const float* __restrict__ Z, const int32_t* __restrict__ labels,
+softmax_kernel(int n, int C, int ld, const float* __restrict__ Z, const int32_t* __restrict__ labels,
                float* __restrict__ X, double* __restrict__ objrows, int* eflags) {
   __shared__ float sc[32];
   const int r = blockIdx.x;
-  const float* z = Z + (int64_t)r * C;
+  const float* z = Z + (int64_t)r * ld;
   float m = -INFINITY;
   for (int j = threadIdx.x; j < C; j += blockDim.x) m = fmaxf(m, z[j]);
   m = block_max(m, sc);
@@ -131,7 +137,7 @@ softmax_kernel(int n, int C, const float* __restrict__ Z, const int32_t* __restr
     if (threadIdx.x == 0) atomicOr(reinterpret_cast<unsigned*>(eflags), kErrLabel);
     y = -1;
   }
-  float* x = X + (int64_t)r * C;
+  float* x = X + (int64_t)r * ld;
   for (int j = threadIdx.x; j < C; j += blockDim.x) x[j] = (j == y ? 1.f : 0.f) - expf(z[j] - lse);
   if (threadIdx.x == 0) {
     objrows[r] = (y >= 0) ? (double)(z[y] - lse) : 0.0;
@@ -163,6 +169,22 @@ struct EpiPnormBack {
     }
   }
 };
+
+// TF32 path: g = sum_z partial_z (fixed order), then the p-norm backward of EpiPnormBack.
+__global__ void pnorm_back_kernel(const float* __restrict__ part, int splits, int n, int din, const float* __restrict__ Zp,
+                                  const float* __restrict__ Yl, float* __restrict__ Xp, int ldx, int ldy, int G) {
+  const int64_t total = (int64_t)n * din;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    float g = 0.f;
+    for (int z = 0; z < splits; ++z) g += part[(int64_t)z * total + i];
+    const int r = (int)(i / din), j = (int)(i % din);
+    const float a = Yl[(int64_t)r * ldy + j];
+    const float* zz = Zp + (int64_t)r * ldx + (int64_t)j * G;
+    float* xo = Xp + (int64_t)r * ldx + (int64_t)j * G;
+    const float ga = a > 0.f ? g / a : 0.f;
+    for (int q = 0; q < G; ++q) xo[q] = ga * zz[q];
+  }
+}
 
 // plain SGD (precond = 0): p_i = ||row_i||^2, gamma = 1
 __global__ void rowsq_kernel(int n, int D, const float* __restrict__ X, int64_t ld, float* __restrict__ p,
@@ -237,7 +259,7 @@ static void nnet_free(nnet_ctx* h) {
   if (h->eflags) cudaFree(h->eflags);
   if (h->recvbuf) cudaFree(h->recvbuf);
   if (h->comm) ncclCommDestroy(h->comm);
-  h->tc.release();
+  if (h->gpart) cudaFree(h->gpart);
   delete h;
 }
 
@@ -264,7 +286,8 @@ ng_status nnet_create(const nnet_config* cfg, void* cuda_stream, nnet_t* out) {
   NG_REQUIRE(cfg->num_hidden == 0 || (cfg->pnorm_group >= 1 && cfg->hidden_dim >= cfg->pnorm_group &&
                                       cfg->hidden_dim % cfg->pnorm_group == 0),
              NG_ESHAPE, "hidden_dim must be a multiple of pnorm_group");
-  NG_REQUIRE(cfg->precision == NG_FP32 || cfg->precision == NG_BF16, NG_EINVAL, "bad precision");
+  NG_REQUIRE(cfg->precision == NG_FP32 || cfg->precision == NG_TF32, NG_EINVAL,
+             "precision must be NG_FP32 or NG_TF32 (NG_BF16 is reserved)");
   NG_REQUIRE(cfg->num_hidden + 1 <= 16, NG_EINVAL, "at most 16 weight matrices");
   nnet_ctx* h = new nnet_ctx();
   h->cfg = *cfg;
@@ -277,6 +300,7 @@ ng_status nnet_create(const nnet_config* cfg, void* cuda_stream, nnet_t* out) {
     h->rows.push_back(r);
     h->cols.push_back(din + 1);
     h->ldp.push_back((int)round_up(din + 1, 8));
+    h->ldr.push_back((int)round_up(r, 8));
     h->off.push_back(off);
     off += (size_t)r * h->ldp.back();
     off = (size_t)round_up((int64_t)off, 64);
@@ -288,8 +312,8 @@ ng_status nnet_create(const nnet_config* cfg, void* cuda_stream, nnet_t* out) {
   for (int l = 0; l < h->L && s == NG_OK; ++l) {
     float *y = nullptr, *z = nullptr, *x = nullptr;
     s = nalloc(&y, (size_t)N * h->ldp[l]);
-    if (s == NG_OK) s = nalloc(&z, (size_t)N * h->rows[l]);
-    if (s == NG_OK) s = nalloc(&x, (size_t)N * h->rows[l]);
+    if (s == NG_OK) s = nalloc(&z, (size_t)N * h->ldr[l]);
+    if (s == NG_OK) s = nalloc(&x, (size_t)N * h->ldr[l]);
     h->Y.push_back(y); h->Z.push_back(z); h->X.push_back(x);
     if (s == NG_OK && cfg->precond) {
       ngsgd_ctx *a = nullptr, *b = nullptr;
@@ -305,7 +329,12 @@ ng_status nnet_create(const nnet_config* cfg, void* cuda_stream, nnet_t* out) {
   if (s == NG_OK) s = nalloc(&h->objrows, N);
   if (s == NG_OK) s = nalloc(&h->obj, 1);
   if (s == NG_OK) s = nalloc(&h->eflags, 1);
-  if (s == NG_OK && cfg->precision == NG_BF16) s = h->tc.init(h->rows, h->cols, h->ldp, N, h->st);
+  if (s == NG_OK && cfg->precision == NG_TF32) {
+    size_t mx = 0;
+    for (int l = 1; l < h->L; ++l) mx = std::max(mx, (size_t)kBwdSplits * N * (h->cols[l] - 1));
+    h->gpart_count = mx;
+    s = nalloc(&h->gpart, mx);
+  }
   if (s == NG_OK) {
     cudaMemsetAsync(h->arena, 0, h->arena_count * sizeof(float), h->st);
     cudaMemsetAsync(h->eflags, 0, sizeof(int), h->st);
@@ -352,7 +381,7 @@ ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const
   NG_REQUIRE(ld >= h->cfg.input_dim, NG_ESHAPE, "ld < input_dim");
   cudaStream_t st = h->st;
   const int L = h->L, G = h->cfg.pnorm_group;
-  const bool tc = h->cfg.precision == NG_BF16;
+  const bool tc = h->cfg.precision == NG_TF32;
   {
     const int64_t tot = (int64_t)n * h->ldp[0];
     input_kernel<<<std::min(4096, ceil_div(tot, 256)), 256, 0, st>>>(n, h->cfg.input_dim, frames, ld, h->Y[0],
@@ -365,30 +394,42 @@ ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const
     const double R_ = h->rows[l], C_ = h->cols[l];
     ProfScope ps(NG_PROF_FWD_GEMM, st, 2.0 * n * R_ * C_, 4.0 * (n * C_ + R_ * C_ + n * R_));
     if (tc) {
-      NG_TRY(h->tc.forward(l, n, h->Y[l], W, h->Z[l]));
+      TcEpilogue e;
+      e.kind = TC_EPI_STORE; e.C = h->Z[l]; e.ldc = h->ldr[l];
+      NG_TRY(tc_gemm_tf32(st, n, h->rows[l], h->cols[l], h->Y[l], h->ldp[l], true, W, h->ldp[l], true, e, 128, 1));
     } else {
       NG_TRY((gemm_simt<float, true, true>(st, n, h->rows[l], h->cols[l], h->Y[l], h->ldp[l], W, h->ldp[l],
-                                           EpiStore<float>{h->Z[l], h->rows[l], 1.f})));
+                                           EpiStore<float>{h->Z[l], h->ldr[l], 1.f})));
     }
     if (l < L - 1) {
       const int64_t tot = (int64_t)n * h->ldp[l + 1];
-      pnorm_kernel<<<std::min(4096, ceil_div(tot, 256)), 256, 0, st>>>(n, h->rows[l], G, h->Z[l], h->Y[l + 1],
-                                                                       h->ldp[l + 1]);
+      pnorm_kernel<<<std::min(4096, ceil_div(tot, 256)), 256, 0, st>>>(n, h->rows[l], h->ldr[l], G, h->Z[l],
+                                                                       h->Y[l + 1], h->ldp[l + 1]);
       NG_TRY(check_launch("pnorm_kernel"));
     }
   }
-  softmax_kernel<<<n, 256, 0, st>>>(n, h->rows[L - 1], h->Z[L - 1], labels, h->X[L - 1], h->objrows, h->eflags);
+  softmax_kernel<<<n, 256, 0, st>>>(n, h->rows[L - 1], h->ldr[L - 1], h->Z[L - 1], labels, h->X[L - 1], h->objrows,
+                                    h->eflags);
   NG_TRY(check_launch("softmax_kernel"));
   // backward with the pre-update weights (reading R21)
   for (int l = L - 1; l >= 1; --l) {
     const float* W = h->arena + h->off[l];
-    EpiPnormBack epi{h->X[l - 1], h->Z[l - 1], h->Y[l], h->rows[l - 1], h->ldp[l], G};
+    EpiPnormBack epi{h->X[l - 1], h->Z[l - 1], h->Y[l], h->ldr[l - 1], h->ldp[l], G};
     const double R_ = h->rows[l], C_ = h->cols[l], Rp = h->rows[l - 1];
     ProfScope ps(NG_PROF_BWD_GEMM, st, 2.0 * n * R_ * (C_ - 1), 4.0 * (n * R_ + R_ * C_ + 2.0 * n * Rp + n * C_));
     if (tc) {
-      NG_TRY(h->tc.backward(l, n, h->X[l], W, epi));
+      const int din = h->cols[l] - 1;
+      TcEpilogue e;
+      e.kind = TC_EPI_PARTIAL; e.C = h->gpart; e.ldc = din; e.zstride = (int64_t)n * din;
+      int sp = 1;
+      NG_TRY(tc_gemm_tf32(st, n, din, h->rows[l], h->X[l], h->ldr[l], true, W, h->ldp[l], false, e, 64, kBwdSplits,
+                          &sp));
+      const int64_t tot = (int64_t)n * din;
+      pnorm_back_kernel<<<std::min(4096, ceil_div(tot, 256)), 256, 0, st>>>(h->gpart, sp, n, din, h->Z[l - 1], h->Y[l],
+                                                                            h->X[l - 1], h->ldr[l - 1], h->ldp[l], G);
+      NG_TRY(check_launch("pnorm_back_kernel"));
     } else {
-      NG_TRY((gemm_simt<float, true, false>(st, n, h->cols[l] - 1, h->rows[l], h->X[l], h->rows[l], W, h->ldp[l],
+      NG_TRY((gemm_simt<float, true, false>(st, n, h->cols[l] - 1, h->rows[l], h->X[l], h->ldr[l], W, h->ldp[l],
                                             epi)));
     }
   }
@@ -414,25 +455,28 @@ ng_status nnet_update(nnet_t h, float lr, float max_change_per_sample, nnet_upda
     float* py = h->pbuf + (size_t)(2 * l) * N;
     float* px = h->pbuf + (size_t)(2 * l + 1) * N;
     if (h->cfg.precond) {
-      NG_TRY(ngsgd_precondition_impl(h->ng_out[l], n, h->X[l], h->rows[l], h->gam + 2 * l + 1, px, -1, &upd_out[l]));
+      NG_TRY(ngsgd_precondition_impl(h->ng_out[l], n, h->X[l], h->ldr[l], h->gam + 2 * l + 1, px, -1, &upd_out[l]));
       NG_TRY(ngsgd_precondition_impl(h->ng_in[l], n, h->Y[l], h->ldp[l], h->gam + 2 * l, py, -1, &upd_in[l]));
     } else {
-      rowsq_kernel<<<n, 256, 0, st>>>(n, h->rows[l], h->X[l], h->rows[l], px, h->gam + 2 * l + 1);
+      rowsq_kernel<<<n, 256, 0, st>>>(n, h->rows[l], h->X[l], h->ldr[l], px, h->gam + 2 * l + 1);
       rowsq_kernel<<<n, 256, 0, st>>>(n, h->cols[l], h->Y[l], h->ldp[l], py, h->gam + 2 * l);
       NG_TRY(check_launch("rowsq_kernel"));
     }
   }
   maxchange_kernel<<<L, 256, 0, st>>>(n, N, lr, max_change_per_sample, h->gam, h->pbuf, h->scale, h->stats);
   NG_TRY(check_launch("maxchange_kernel"));
-  const bool tc = h->cfg.precision == NG_BF16;
+  const bool tc = h->cfg.precision == NG_TF32;
   for (int l = 0; l < L; ++l) {
     float* W = h->arena + h->off[l];
     const double R_ = h->rows[l], C_ = h->cols[l];
     ProfScope ps(NG_PROF_UPD_GEMM, st, 2.0 * n * R_ * C_, 4.0 * (n * R_ + n * C_ + 2.0 * R_ * C_));
     if (tc) {
-      NG_TRY(h->tc.update(l, n, h->X[l], h->Y[l], W, h->scale + l));
+      TcEpilogue e;
+      e.kind = TC_EPI_AXPY; e.C = W; e.ldc = h->ldp[l]; e.scale = h->scale + l;
+      NG_TRY(tc_gemm_tf32(st, h->rows[l], h->cols[l], n, h->X[l], h->ldr[l], false, h->Y[l], h->ldp[l], false, e, 64,
+                          1));
     } else {
-      NG_TRY((gemm_simt<float, false, false>(st, h->rows[l], h->cols[l], n, h->X[l], h->rows[l], h->Y[l], h->ldp[l],
+      NG_TRY((gemm_simt<float, false, false>(st, h->rows[l], h->cols[l], n, h->X[l], h->ldr[l], h->Y[l], h->ldp[l],
                                              EpiAxpyDevScale{W, h->ldp[l], h->scale + l})));
     }
   }

@@ -7,7 +7,7 @@ import pytest
 from oracle import nnet as onn
 from oracle import online_ng as ong
 from oracle import training as otr
-from synth import spliced_frames, standard_normals
+from synth import gaussian_rows, labels_uniform, spliced_frames, standard_normals
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -27,9 +27,10 @@ def normwise(a, b):
     return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
 
 
-def make_pair(api, cfg, precond, seed, rank_in, rank_out, max_mb, random_softmax=False):
+def make_pair(api, cfg, precond, seed, rank_in, rank_out, max_mb, random_softmax=False, precision="fp32"):
     net = api.Nnet(cfg.input_dim, cfg.num_hidden, cfg.hidden_dim, cfg.pnorm_group, cfg.num_classes,
-                   max_minibatch=max_mb, precond=precond, rank_in=rank_in, rank_out=rank_out, seed=seed)
+                   max_minibatch=max_mb, precond=precond, rank_in=rank_in, rank_out=rank_out, seed=seed,
+                   precision=precision)
     params = onn.init_params(cfg, standard_normals(seed, cfg.layer_shapes()))
     if random_softmax:
         params[-1] = 0.05 * standard_normals(seed + 1, [cfg.layer_shapes()[-1]])[0]
@@ -69,13 +70,16 @@ def test_objective_and_plain_sgd_step(api):
         assert normwise(net.get_params(l), params[l]) <= TOL
 
 
-@pytest.mark.parametrize("n", [128, 16, 1])
+@pytest.mark.parametrize("n", [128, 16])
 def test_ng_step_parity_tiny_config(api, n):
     """Config 1 (D=40, 200 -> 20, 16 classes, R = 4): several steps from the same state;
-    includes deferred init of hidden-layer states (zero softmax, reading R7)."""
+    includes deferred init of hidden-layer states (zero softmax, reading R7).  Labels are
+    i.i.d. uniform so every init minibatch has rank >= R (a rank-deficient S_0 has an
+    arbitrary null-space basis: parity unpinned, reading R7)."""
     cfg = onn.NnetConfig(input_dim=40, num_hidden=1, hidden_dim=200, pnorm_group=10, num_classes=16)
     net, params, states = make_pair(api, cfg, True, 5, 4, 4, 128)
-    frames, labels = spliced_frames(7, 6 * n, context=0, num_classes=16)
+    frames = gaussian_rows(7, 6 * n, 40).astype(np.float32)
+    labels = labels_uniform(8, 6 * n, 16)
     for k in range(6):
         fr, lb = frames[k * n:(k + 1) * n], labels[k * n:(k + 1) * n]
         f, y = to_dev(fr, lb)
@@ -87,6 +91,23 @@ def test_ng_step_parity_tiny_config(api, n):
         ost = onn.update(params, fb, lr, states)
         for l in range(len(params)):
             assert st.alpha_t[l] == pytest.approx(ost[l].alpha_t, rel=TOL)
+            assert normwise(net.get_params(l), params[l]) <= TOL, (k, l)
+
+
+@pytest.mark.parametrize("n_short", [1, 16, 77])
+def test_short_last_minibatch(api, n_short):
+    """The last minibatch may be short (eta recomputed from its N, R10)."""
+    cfg = onn.NnetConfig(input_dim=40, num_hidden=1, hidden_dim=200, pnorm_group=10, num_classes=16)
+    net, params, states = make_pair(api, cfg, True, 6, 4, 4, 128)
+    frames = gaussian_rows(17, 3 * 128, 40).astype(np.float32)
+    labels = labels_uniform(18, 3 * 128, 16)
+    for k, n in enumerate([128, 128, n_short]):
+        fr, lb = frames[k * 128:k * 128 + n], labels[k * 128:k * 128 + n]
+        f, y = to_dev(fr, lb)
+        net.forward_backward(f, y)
+        net.update(0.01, 0.075)
+        onn.train_step(params, cfg, fr.astype(np.float64), lb, 0.01, states)
+        for l in range(len(params)):
             assert normwise(net.get_params(l), params[l]) <= TOL, (k, l)
 
 
@@ -162,3 +183,47 @@ def test_average_single_rank_is_identity(api):
         net.average(mode)
         for l in range(2):
             assert np.array_equal(net.get_params(l), before[l])
+
+
+def inject_states(net, states, seed):
+    rng = np.random.default_rng(seed)
+    for l, (s_in, s_out) in enumerate(states):
+        for side, s in (("in", s_in), ("out", s_out)):
+            q, _ = np.linalg.qr(rng.normal(size=(s.dim, s.rank)))
+            s.d = np.sort(rng.uniform(0.01, 1.0, s.rank))[::-1].copy()
+            s.rho = 1e-3
+            e = ong.e_of(ong.beta_of(s.rho, s.d, 4.0, s.dim), s.d)
+            s.W = (np.sqrt(e)[:, None] * q.T).astype(np.float32).astype(np.float64)
+            s.t, s.initialized = 12, True
+            net.ngsgd(l, side).set_state(s.rho, s.d, s.W.astype(np.float32), s.t)
+
+
+@pytest.mark.parametrize("shape", ["tiny", "config3"])
+def test_tf32_tensor_core_step(api, shape):
+    """NG_TF32: the DNN GEMMs on tcgen05 (TF32 inputs, FP32 accumulate).  Bar (north
+    star, reduced-precision tensor-core inputs): the preconditioned update
+    Delta W = alpha lr gamma_x gamma_y X_hat^T Y_hat within 2e-2 normwise of the float64
+    oracle's, per weight matrix; objective within 1e-3 relative."""
+    if shape == "tiny":
+        cfg = onn.NnetConfig(input_dim=40, num_hidden=2, hidden_dim=200, pnorm_group=10, num_classes=16)
+        N, rin, rout = 128, 4, 8
+    else:
+        cfg = onn.NnetConfig(input_dim=360, num_hidden=4, hidden_dim=3000, pnorm_group=10, num_classes=5000)
+        N, rin, rout = 512, 20, 80
+    net, params, states = make_pair(api, cfg, True, 91, rin, rout, N, random_softmax=True, precision="tf32")
+    inject_states(net, states, 3)
+    frames, labels = spliced_frames(13, 2 * N, num_classes=cfg.num_classes, context=4 if cfg.input_dim == 360 else 0)
+    for k in range(2):
+        fr, lb = frames[k * N:(k + 1) * N], labels[k * N:(k + 1) * N]
+        f, y = to_dev(fr, lb)
+        before = [net.get_params(l).astype(np.float64) for l in range(len(params))]
+        obj = net.forward_backward(f, y, objective=True)
+        fb = onn.forward_backward(before, cfg, fr.astype(np.float64), lb)
+        assert obj == pytest.approx(fb.objective, rel=1e-3)
+        net.update(0.01, 0.075)
+        ref = [b.copy() for b in before]
+        onn.update(ref, fb, 0.01, states)
+        for l in range(len(params)):
+            d_gpu = net.get_params(l).astype(np.float64) - before[l]
+            d_ref = ref[l] - before[l]
+            assert normwise(d_gpu, d_ref) <= 2e-2, (k, l, normwise(d_gpu, d_ref))
