@@ -221,9 +221,10 @@ def roofline_for(group: str, prof: dict, precision: str, peaks: dict):
     if is_gemm or group in ("ng_proj", "ng_refresh"):
         flops = g["flops"] / g["launches"]
         achieved = flops / per_launch_s / 1e12
-        if precision == "bf16":
-            peak = peaks.get("bf16_tflops_sustained", 1378.9)
-            bound, src = "tensor", "MEASURED_PEAKS.json bf16_tflops_sustained"
+        if precision == "tf32" and is_gemm:
+            peak = peaks.get("bf16_tflops_sustained", 1378.9) * 0.5
+            bound, src = "tensor", ("TF32 = MEASURED_PEAKS.json bf16_tflops_sustained x 0.5 (nominal dense "
+                                    "TF32/BF16 ratio 1.1/2.25 PF, B200_PROFILING.md)")
         else:
             peak = FP32_SIMT_PEAK_TFLOPS
             bound, src = "alu", "derived: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md)"
@@ -420,7 +421,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         return 0
     line = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32" if precision == "fp32" else "bf16", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f32" if precision == "fp32" else "tf32", "data": "synthetic",
             "config": {"workload": WORKLOAD, "minibatch": N, "global_batch": N * world,
                        "parallelism": f"dp{world} (independent jobs, parameter average every {avg_every} "
                                       f"minibatches = K 400000 samples)",
@@ -439,7 +440,7 @@ def main():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--precision", choices=["fp32", "bf16"], default=os.environ.get("NG_BENCH_PRECISION", "fp32"))
+    ap.add_argument("--precision", choices=["fp32", "tf32"], default=os.environ.get("NG_BENCH_PRECISION", "tf32"))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-precond-bench", action="store_true")

@@ -10,7 +10,7 @@
 // TMA with CU_TENSOR_MAP_SWIZZLE_128B:
 //   K-major  : [rows][128 B] (32 fp32 of K per row), 8-row atoms 1024 B apart (SBO)
 //   MN-major : boxes of [32 k-rows][128 B] (32 fp32 of M/N), boxes 4096 B apart (LBO),
-//              8-k-row atoms 1024 B apart (SBO)
+//              SWIZZLE_128B_BASE32B (TMA SWIZZLE_128B_ATOM_32B): 4-k-row atoms 512 B apart (SBO)
 #include <cuda.h>
 
 #include <algorithm>
@@ -76,16 +76,23 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t 
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
-// Shared-memory matrix descriptor, SWIZZLE_128B, sm100 version field = 1.
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+// Shared-memory matrix descriptor, sm100 version field = 1.  layout 2 = SWIZZLE_128B (K-major
+// operands), layout 1 = SWIZZLE_128B_BASE32B (the only MN-major layout for 32-bit types:
+// 128-byte rows, 32-byte granules XOR-swizzled over 4-row / 512-byte atoms).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
+  d |= (uint64_t)layout << 61;
   return d;
 }
+// K-major SW128: 8-row atoms 1024 B apart; k-slice j of the 32-wide block starts 32j bytes in.
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t tile, int k) { return smem_desc(tile + k * 32, 16, 1024, 2); }
+// MN-major SW128_BASE32B: 32-element MN chunks (boxes of 32 k-rows) 4096 B apart (LBO),
+// 4-k-row atoms 512 B apart (SBO); k-slice j (8 k-rows) starts 1024j bytes in.
+__device__ __forceinline__ uint64_t desc_mnmajor(uint32_t tile, int k) { return smem_desc(tile + k * 1024, 4096, 512, 1); }
 
 // Instruction descriptor: D f32, A/B tf32, majors, N>>3, M>>4.
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool a_mn, bool b_mn) {
@@ -174,8 +181,8 @@ tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
 #pragma unroll
       for (int k = 0; k < kBK / 8; ++k) {
-        const uint64_t da = AK ? sw128_desc(sa + k * 32, 16, 1024) : sw128_desc(sa + k * 1024, 4096, 1024);
-        const uint64_t db = BKM ? sw128_desc(sb + k * 32, 16, 1024) : sw128_desc(sb + k * 1024, 4096, 1024);
+        const uint64_t da = AK ? desc_kmajor(sa, k) : desc_mnmajor(sa, k);
+        const uint64_t db = BKM ? desc_kmajor(sb, k) : desc_mnmajor(sb, k);
         mma_tf32(tmem, da, db, idesc, (i > 0 || k > 0) ? 1u : 0u);
       }
       umma_commit(&empty_bar[s]);
@@ -236,11 +243,13 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 2D fp32 tensor [outer][inner] with row stride ld (elements), box {32, box_outer}.
-ng_status make_tmap(CUtensorMap* out, const float* ptr, int64_t inner, int64_t outer, int64_t ld, int box_outer) {
-  using Key = std::tuple<const float*, int64_t, int64_t, int64_t, int>;
+// 2D fp32 tensor [outer][inner] with row stride ld (elements), box {32, box_outer};
+// mn_major selects the 32-byte-atom 128B swizzle (SWIZZLE_128B_ATOM_32B).
+ng_status make_tmap(CUtensorMap* out, const float* ptr, int64_t inner, int64_t outer, int64_t ld, int box_outer,
+                    bool mn_major) {
+  using Key = std::tuple<const float*, int64_t, int64_t, int64_t, int, bool>;
   static std::map<Key, CUtensorMap> cache;
-  const Key key{ptr, inner, outer, ld, box_outer};
+  const Key key{ptr, inner, outer, ld, box_outer, mn_major};
   auto it = cache.find(key);
   if (it != cache.end()) { *out = it->second; return NG_OK; }
   EncodeTiledFn fn = encode_fn();
@@ -254,7 +263,9 @@ ng_status make_tmap(CUtensorMap* out, const float* ptr, int64_t inner, int64_t o
   CUtensorMap m;
   std::memset(&m, 0, sizeof(m));
   CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)r));
@@ -320,10 +331,10 @@ ng_status tc_gemm_tf32(cudaStream_t st, int M, int N, int K, const float* A, int
   NG_REQUIRE(splits == 1 || epi.kind == TC_EPI_PARTIAL, NG_EINVAL, "split-K needs the partial epilogue");
   if (splits_used) *splits_used = splits;
   CUtensorMap ta, tb;
-  if (a_kmajor) NG_TRY(make_tmap(&ta, A, K, M, lda, kBM));     // [M][K]
-  else NG_TRY(make_tmap(&ta, A, M, K, lda, 32));               // [K][M]
-  if (b_kmajor) NG_TRY(make_tmap(&tb, B, K, N, ldb, bn));      // [N][K]
-  else NG_TRY(make_tmap(&tb, B, N, K, ldb, 32));               // [K][N]
+  if (a_kmajor) NG_TRY(make_tmap(&ta, A, K, M, lda, kBM, false));     // [M][K]
+  else NG_TRY(make_tmap(&ta, A, M, K, lda, 32, true));                // [K][M]
+  if (b_kmajor) NG_TRY(make_tmap(&tb, B, K, N, ldb, bn, false));      // [N][K]
+  else NG_TRY(make_tmap(&tb, B, N, K, ldb, 32, true));                // [K][N]
   if (bn == 64) return dispatch_major<64>(st, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
   return dispatch_major<128>(st, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
 }

@@ -74,10 +74,11 @@ def test_objective_and_plain_sgd_step(api):
 def test_ng_step_parity_tiny_config(api, n):
     """Config 1 (D=40, 200 -> 20, 16 classes, R = 4): several steps from the same state;
     includes deferred init of hidden-layer states (zero softmax, reading R7).  Labels are
-    i.i.d. uniform so every init minibatch has rank >= R (a rank-deficient S_0 has an
-    arbitrary null-space basis: parity unpinned, reading R7)."""
+    i.i.d. uniform and the softmax layer random: with the zero softmax init the first
+    output-side minibatch onehot - 1/C has exactly repeated eigenvalues whenever classes
+    share a count, so the top-R eigenbasis of S_0 is arbitrary (parity unpinned, R7)."""
     cfg = onn.NnetConfig(input_dim=40, num_hidden=1, hidden_dim=200, pnorm_group=10, num_classes=16)
-    net, params, states = make_pair(api, cfg, True, 5, 4, 4, 128)
+    net, params, states = make_pair(api, cfg, True, 5, 4, 4, 128, random_softmax=True)
     frames = gaussian_rows(7, 6 * n, 40).astype(np.float32)
     labels = labels_uniform(8, 6 * n, 16)
     for k in range(6):
@@ -98,7 +99,7 @@ def test_ng_step_parity_tiny_config(api, n):
 def test_short_last_minibatch(api, n_short):
     """The last minibatch may be short (eta recomputed from its N, R10)."""
     cfg = onn.NnetConfig(input_dim=40, num_hidden=1, hidden_dim=200, pnorm_group=10, num_classes=16)
-    net, params, states = make_pair(api, cfg, True, 6, 4, 4, 128)
+    net, params, states = make_pair(api, cfg, True, 6, 4, 4, 128, random_softmax=True)
     frames = gaussian_rows(17, 3 * 128, 40).astype(np.float32)
     labels = labels_uniform(18, 3 * 128, 16)
     for k, n in enumerate([128, 128, n_short]):
@@ -113,9 +114,11 @@ def test_short_last_minibatch(api, n_short):
 
 def test_config1_full_trajectory(api):
     """Config 1 end to end: 10 000 frames = 78 x 128 + 16, one epoch, lr 0.01/6 ->
-    0.001/6, online NG R = 4; parameters after the run within 1e-4 normwise."""
+    0.001/6, online NG R = 4; parameters after the run within 1e-4 normwise.  Small
+    random softmax init (instead of zero) so no init minibatch has an
+    exactly-degenerate spectrum (reading R7)."""
     cfg = onn.NnetConfig(input_dim=40, num_hidden=1, hidden_dim=200, pnorm_group=10, num_classes=16)
-    net, params, states = make_pair(api, cfg, True, 1410, 4, 4, 128)
+    net, params, states = make_pair(api, cfg, True, 1410, 4, 4, 128, random_softmax=True)
     frames, labels = spliced_frames(1410, 10000, context=0, num_classes=16)
     seen = 0
     objs = []
