@@ -276,6 +276,8 @@ def precondition_bench(api, torch, minibatches: int = 1000):
     e0.record()
     for k in range(minibatches):
         one(12 + k)
+    out_side.join()
+    in_side.join()
     e1.record()
     torch.cuda.synchronize()
     tot = e0.elapsed_time(e1)
@@ -351,6 +353,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e0.record()
     for _ in range(args.steps):
         step()
+    net.join()                       # side-stream NG refreshes belong to the timed region
     e1.record()
     torch.cuda.synchronize()
     clocks.mark("t1")

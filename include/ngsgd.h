@@ -98,6 +98,11 @@ ng_status ngsgd_destroy(ngsgd_t h);
 ng_status ngsgd_precondition(ngsgd_t h, int32_t n, float* x, int64_t ld,
                              float* gamma_out, float* p_out, int32_t update);
 
+/* Enqueue on the handle's stream a wait for the state's internal side-stream work (the
+ * R x R refresh and W_{t+1} = A_t B_t of the last update step run on a side stream and
+ * are otherwise joined lazily by the next call on this state).  Asynchronous. */
+ng_status ngsgd_join(ngsgd_t h);
+
 /* Host snapshot of a state (B.5: the stored variables are rho_t, D_t, W_t). */
 typedef struct {
   int32_t dim, rank, t, initialized;
@@ -169,6 +174,10 @@ typedef struct {
 ng_status nnet_update(nnet_t h, float lr, float max_change_per_sample,
                       nnet_update_stats* stats_or_null);
 
+/* Make the network's stream wait for all internal side-stream work (NG refreshes).
+ * Asynchronous; use before timing the stream or handing buffers to other streams. */
+ng_status nnet_join(nnet_t h);
+
 /* Number of weight matrices I and the shape (rows = D_out, cols = D_in + 1) of each. */
 ng_status nnet_num_layers(nnet_t h, int32_t* out);
 ng_status nnet_layer_shape(nnet_t h, int32_t layer, int32_t* rows, int32_t* cols);
@@ -214,7 +223,8 @@ typedef enum {
   NG_PROF_NG_INIT = 6,    /* B.3.2 initialisation (once per state)                     */
   NG_PROF_ELEMWISE = 7,   /* input, p-norm, softmax/objective, max-change              */
   NG_PROF_AVERAGE = 8,    /* parameter averaging                                       */
-  NG_PROF_NUM = 9
+  NG_PROF_NG_EIG = 9,     /* the one-CTA R x R refresh (Z_t, Jacobi eigensolver, A_t)   */
+  NG_PROF_NUM = 10
 } ng_prof_group;
 
 typedef struct {

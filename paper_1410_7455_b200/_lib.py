@@ -53,7 +53,7 @@ class ProfileStats(ctypes.Structure):
 
 
 PROF_GROUPS = ["fwd_gemm", "bwd_gemm", "upd_gemm", "ng_proj", "ng_apply", "ng_refresh", "ng_init", "elemwise",
-               "average"]
+               "average", "ng_eig"]
 
 # name -> (restype, argtypes); every symbol include/ngsgd.h declares
 SIGNATURES = {
@@ -64,6 +64,8 @@ SIGNATURES = {
     "ngsgd_destroy": (c_int32, [c_void_p]),
     "ngsgd_precondition": (c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_void_p, c_void_p, c_int32]),
     "ngsgd_get_state": (c_int32, [c_void_p, ctypes.POINTER(NgsgdStateHost)]),
+    "ngsgd_join": (c_int32, [c_void_p]),
+    "nnet_join": (c_int32, [c_void_p]),
     "ngsgd_set_state": (c_int32, [c_void_p, ctypes.POINTER(NgsgdStateHost)]),
     "nnet_create": (c_int32, [ctypes.POINTER(NnetConfig), c_void_p, ctypes.POINTER(c_void_p)]),
     "nnet_destroy": (c_int32, [c_void_p]),

@@ -78,6 +78,10 @@ class OnlinePreconditioner:
         ld = _check_matrix(x)
         check(lib.ngsgd_precondition(self._h, x.shape[0], _ptr(x), ld, _ptr(gamma), _ptr(p), int(update)))
 
+    def join(self) -> None:
+        """Make the stream wait for this state's side-stream refresh (ngsgd_join)."""
+        check(lib.ngsgd_join(self._h))
+
     def get_state(self) -> dict:
         st = _lib.NgsgdStateHost()
         check_q = lib.ngsgd_get_state(self._h, ctypes.byref(st))
@@ -172,6 +176,10 @@ class Nnet:
         L = self.num_layers
         return NnetStats(np.array(st.alpha_t[:L]), np.array(st.gamma_in[:L]), np.array(st.gamma_out[:L]),
                          np.array(st.updated_in[:L]), np.array(st.updated_out[:L]))
+
+    def join(self) -> None:
+        """Make the stream wait for all side-stream NG refreshes (nnet_join)."""
+        check(lib.nnet_join(self._h))
 
     def get_params(self, layer: int) -> np.ndarray:
         r, c = self.shapes[layer]

@@ -9,7 +9,9 @@
 // floor(n/2) disjoint plane rotations simultaneously.  A' = J^T A J is done as
 // independent 2x2 block updates  A'[P,Q] = G_P^T A[P,Q] G_Q  (P, Q index rotation
 // pairs), so one round costs one barrier after computing the rotations and one after
-// the update.  Eigenvectors are accumulated as ROWS of Vt (Vt = U^T).  Sweeps stop when
+// the update.  The rotation angle is computed in FP32 and turned into an exactly
+// orthogonal FP64 rotation (c = rsqrt(1 + t^2), s = t c), so convergence is governed by
+// the FP64 skip threshold while the per-round latency chain stays short.  Eigenvectors are accumulated as ROWS of Vt (Vt = U^T).  Sweeps stop when
 // a full sweep performs no rotation (|a_pq| <= rel_tol sqrt(|a_pp a_qq|), rel_tol =
 // 1e-12 by default, or below an absolute floor), or after max_sweeps.
 //
@@ -65,9 +67,19 @@ __device__ void jacobi_eig(double* A, int lda, double* Vt, int ldv, int n, Jacob
           const double apq = A[(int64_t)p * lda + q];
           const double thr = fmax(rel_tol * sqrt(fabs(app * aqq)), abs_floor);
           if (fabs(apq) > thr) {
-            const double theta = (aqq - app) / (2.0 * apq);
-            t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-            c = 1.0 / sqrt(t * t + 1.0);
+            // tan of the annihilating angle in FP32 (short latency chain), then an exactly
+            // orthogonal FP64 rotation from it: the residual a'_pq ~ 1e-7 a_pq is removed
+            // by the next sweep.
+            const double thd = (aqq - app) / (2.0 * apq);
+            float tf;
+            if (fabs(thd) > 1e18) {
+              tf = (float)(0.5 / thd);
+            } else {
+              const float th = (float)thd;
+              tf = copysignf(1.f, th) / (fabsf(th) + sqrtf(fmaf(th, th, 1.f)));
+            }
+            t = (double)tf;
+            c = rsqrt(fma(t, t, 1.0));
             s = t * c;
             atomicAdd(sc.nrot, 1);
           }
@@ -84,13 +96,17 @@ __device__ void jacobi_eig(double* A, int lda, double* Vt, int ldv, int n, Jacob
         if (s1 == 0.0 && s2 == 0.0) continue;
         const bool v1 = q1 < n, v2 = q2 < n;
         if (ka == kb) {
-          // diagonal block: closed form a' = a - t apq, d' = d + t apq, off-diagonal 0
-          const double tt = sc.t[ka];
-          const double apq = A[(int64_t)p1 * lda + q1];
-          A[(int64_t)p1 * lda + p1] -= tt * apq;
-          A[(int64_t)q1 * lda + q1] += tt * apq;
-          A[(int64_t)p1 * lda + q1] = 0.0;
-          A[(int64_t)q1 * lda + p1] = 0.0;
+          // diagonal block: G^T [[a, b], [b, d]] G
+          const double a = A[(int64_t)p1 * lda + p1], d = A[(int64_t)q1 * lda + q1];
+          const double b = A[(int64_t)p1 * lda + q1];
+          const double cc = c1 * c1, ss = s1 * s1, cs = c1 * s1;
+          const double an = cc * a - 2.0 * cs * b + ss * d;
+          const double dn = ss * a + 2.0 * cs * b + cc * d;
+          const double bn = (cc - ss) * b + cs * (a - d);
+          A[(int64_t)p1 * lda + p1] = an;
+          A[(int64_t)q1 * lda + q1] = dn;
+          A[(int64_t)p1 * lda + q1] = bn;
+          A[(int64_t)q1 * lda + p1] = bn;
           continue;
         }
         const double m00 = A[(int64_t)p1 * lda + p2];

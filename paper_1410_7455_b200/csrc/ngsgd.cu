@@ -259,7 +259,7 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   zmax = block_max(zmax, red);
   // Z = U C U^T (eqn:zt:eig:repeat)
   JacobiScratch scr{jp, jq, jc, js, jt, nrot};
-  jacobi_eig(Z, R, Vt, R, R, scr, 40, 1e-18 * zmax);
+  jacobi_eig(Z, R, Vt, R, R, scr, 20, 1e-15 * zmax);
   // descending order
   for (int i = tid; i < R; i += nt) {
     const double li = Z[i * R + i];
@@ -413,7 +413,7 @@ init_eig_kernel(int ne, double* A, double* Vt, double* Vs, double* lam, int* ws_
   double amax = 0.0;
   for (int i = threadIdx.x; i < ne; i += blockDim.x) amax = fmax(amax, fabs(A[(int64_t)i * ne + i]));
   amax = block_max(amax, red);
-  jacobi_eig(A, ne, Vt, ne, ne, scr, 60, 1e-20 * amax);
+  jacobi_eig(A, ne, Vt, ne, ne, scr, 30, 1e-15 * amax);
   eig_sort_desc(A, ne, Vt, ne, ne, lam, Vs, ne, ws_int + 2 * m + 1);
 }
 
@@ -579,6 +579,12 @@ ng_status ngsgd_create_impl(int dim, int max_rows, const ngsgd_config* cfg, cuda
   ALLOC(h->flags, 4);
 #undef ALLOC
   if (s == NG_OK && cudaMallocHost((void**)&h->h_scalar, 4 * sizeof(double)) != cudaSuccess) s = NG_ENOMEM;
+  if (s == NG_OK && (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
+                     cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+                     cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess)) {
+    set_error("ngsgd_create: stream/event creation failed");
+    s = NG_ECUDA;
+  }
   if (s == NG_OK) {
     cudaMemsetAsync(h->W[0], 0, sizeof(float) * R * h->ldw, st);
     cudaMemsetAsync(h->W[1], 0, sizeof(float) * R * h->ldw, st);
@@ -601,6 +607,9 @@ void ngsgd_destroy_impl(ngsgd_ctx* h) {
   if (h->sums) cudaFree(h->sums);
   if (h->flags) cudaFree(h->flags);
   if (h->h_scalar) cudaFreeHost(h->h_scalar);
+  if (h->side) { cudaStreamSynchronize(h->side); cudaStreamDestroy(h->side); }
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   delete h;
 }
 
@@ -656,6 +665,15 @@ static ng_status ngsgd_init(ngsgd_ctx* h, int n, const float* x, int64_t ld, dou
   return s;
 }
 
+// Make the handle's stream wait for the side-stream refresh of the previous update.
+ng_status ngsgd_join_impl(ngsgd_ctx* h) {
+  if (h->pending) {
+    NG_CUDA_TRY(cudaStreamWaitEvent(h->st, h->ev_join, 0));
+    h->pending = false;
+  }
+  return NG_OK;
+}
+
 ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, float* gamma_out,
                                   float* p_out, int update, int* updated_out) {
   NG_REQUIRE(h != nullptr && x != nullptr, NG_EINVAL, "NULL argument");
@@ -663,6 +681,7 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
   NG_REQUIRE(ld >= h->dim, NG_ESHAPE, "ld < dim");
   const int D = h->dim, R = h->rank;
   cudaStream_t st = h->st;
+  NG_TRY(ngsgd_join_impl(h));
   if (updated_out) *updated_out = 0;
   h->last_updated = 0;
   if (!h->initialized) {
@@ -743,29 +762,40 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
     NG_TRY(check_launch("finalize_kernel"));
   }
   if (upd) {
-    ProfScope ps(NG_PROF_NG_REFRESH, st, 2.0 * (double)R * R * D + 2.0 * R * D, 4.0 * (4.0 * R * D));
-    refresh_kernel<<<1, 1024, refresh_smem_bytes(R), st>>>(R, D, n, eta, (double)h->cfg.alpha,
-                                                          (double)h->cfg.epsilon, h->KL, h->dstate, h->sums,
-                                                          h->Amat, h->svec, h->flags);
-    NG_TRY(check_launch("refresh_kernel"));
-    bscale_kernel<<<std::min(1024, ceil_div((int64_t)R * D, 256)), 256, 0, st>>>(R, D, h->J, W, h->ldw, h->svec);
+    // The R x R refresh and W_{t+1} = A_t B_t only gate this state's NEXT call, so they
+    // run on the state's side stream, overlapping later work on the main stream (the
+    // other states' preconditioning, the weight update, the next forward/backward).
+    NG_CUDA_TRY(cudaEventRecord(h->ev_fork, st));
+    NG_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+    cudaStream_t ss = h->side;
+    {
+      ProfScope pe(NG_PROF_NG_EIG, ss, 0.0, 0.0);
+      refresh_kernel<<<1, 1024, refresh_smem_bytes(R), ss>>>(R, D, n, eta, (double)h->cfg.alpha,
+                                                            (double)h->cfg.epsilon, h->KL, h->dstate, h->sums,
+                                                            h->Amat, h->svec, h->flags);
+      NG_TRY(check_launch("refresh_kernel"));
+    }
+    ProfScope ps(NG_PROF_NG_REFRESH, ss, 2.0 * (double)R * R * D + 2.0 * R * D, 4.0 * (4.0 * R * D));
+    bscale_kernel<<<std::min(1024, ceil_div((int64_t)R * D, 256)), 256, 0, ss>>>(R, D, h->J, W, h->ldw, h->svec);
     NG_TRY(check_launch("bscale_kernel"));
     const int nxt = 1 - h->cur;
     float* Wn = h->W[nxt];
     // W_{t+1} = A_t B_t (eqn:wt1)
-    NG_TRY((gemm_simt<float, true, false>(st, R, D, R, h->Amat, R, h->J, h->ldw, EpiStore<float>{Wn, h->ldw, 1.f})));
+    NG_TRY((gemm_simt<float, true, false>(ss, R, D, R, h->Amat, R, h->J, h->ldw, EpiStore<float>{Wn, h->ldw, 1.f})));
     // B.3.1, gated on the device flag (no host synchronisation)
     const int ks = gemm_simt_splits(D, h->kl_splits);
-    NG_TRY((gemm_simt<float, true, true>(st, R, R, D, Wn, h->ldw, Wn, h->ldw,
+    NG_TRY((gemm_simt<float, true, true>(ss, R, R, D, Wn, h->ldw, Wn, h->ldw,
                                          EpiStoreSplit<float>{h->WWpart, R, (int64_t)R * R}, ks, h->flags + 1)));
-    reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->WW, h->WWpart, R * R, ks, R * R, h->flags + 1);
+    reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, ss>>>(h->WW, h->WWpart, R * R, ks, R * R, h->flags + 1);
     NG_TRY(check_launch("reduce_splits(WW)"));
-    reorth_check_kernel<<<1, 256, reorth_smem_bytes(R), st>>>(R, h->WW, h->dstate, h->Mmat, h->flags);
+    reorth_check_kernel<<<1, 256, reorth_smem_bytes(R), ss>>>(R, h->WW, h->dstate, h->Mmat, h->flags);
     NG_TRY(check_launch("reorth_check_kernel"));
-    NG_TRY((gemm_simt<float, true, false>(st, R, D, R, h->Mmat, R, Wn, h->ldw, EpiStore<float>{h->J, h->ldw, 1.f},
+    NG_TRY((gemm_simt<float, true, false>(ss, R, D, R, h->Mmat, R, Wn, h->ldw, EpiStore<float>{h->J, h->ldw, 1.f},
                                           1, h->flags + 2)));
-    copy_gated_kernel<<<std::min(1024, ceil_div((int64_t)R * D, 256)), 256, 0, st>>>(R, D, Wn, h->J, h->ldw, h->flags + 2);
+    copy_gated_kernel<<<std::min(1024, ceil_div((int64_t)R * D, 256)), 256, 0, ss>>>(R, D, Wn, h->J, h->ldw, h->flags + 2);
     NG_TRY(check_launch("copy_gated_kernel"));
+    NG_CUDA_TRY(cudaEventRecord(h->ev_join, ss));
+    h->pending = true;
     h->cur = nxt;
   }
   h->t += 1;
@@ -824,8 +854,14 @@ ng_status ngsgd_create(int32_t dim, int32_t max_rows, const ngsgd_config* cfg, v
   return ngsgd_create_impl(dim, max_rows, cfg, (cudaStream_t)cuda_stream, out);
 }
 
+ng_status ngsgd_join(ngsgd_t h) {
+  NG_REQUIRE(h != nullptr, NG_EINVAL, "NULL argument");
+  return ngsgd_join_impl(h);
+}
+
 ng_status ngsgd_destroy(ngsgd_t h) {
   if (!h) return NG_EINVAL;
+  ngsgd_join_impl(h);
   cudaStreamSynchronize(h->st);
   ngsgd_destroy_impl(h);
   return NG_OK;
@@ -838,6 +874,7 @@ ng_status ngsgd_precondition(ngsgd_t h, int32_t n, float* x, int64_t ld, float* 
 
 ng_status ngsgd_get_state(ngsgd_t h, ngsgd_state_host* out) {
   NG_REQUIRE(h != nullptr && out != nullptr, NG_EINVAL, "NULL argument");
+  NG_TRY(ngsgd_join_impl(h));
   NG_CUDA_TRY(cudaStreamSynchronize(h->st));
   const int R = h->rank, D = h->dim;
   out->dim = D;
@@ -865,6 +902,7 @@ ng_status ngsgd_set_state(ngsgd_t h, const ngsgd_state_host* in) {
   NG_REQUIRE(in->dim == h->dim && in->rank == h->rank, NG_ESHAPE, "state dim/rank mismatch");
   NG_REQUIRE(in->t >= 0, NG_EINVAL, "t < 0");
   const int R = h->rank, D = h->dim;
+  NG_TRY(ngsgd_join_impl(h));
   NG_CUDA_TRY(cudaStreamSynchronize(h->st));
   if (R > 0) {
     NG_REQUIRE(in->d != nullptr && in->w != nullptr, NG_EINVAL, "d and w required");

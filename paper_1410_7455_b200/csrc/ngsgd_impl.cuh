@@ -38,6 +38,10 @@ struct ngsgd_ctx {
   int* flags = nullptr;     // [0] floored [1] reorth check [2] repaired [3] error bits
   // pinned host mirror for the (one-time) initialisation sync
   double* h_scalar = nullptr;
+  // side stream for the refresh (Z_t eigensolve, W_{t+1}); joined before the next use
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool pending = false;
 };
 
 namespace ng {
@@ -48,4 +52,5 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
 ng_status ngsgd_create_impl(int dim, int max_rows, const ngsgd_config* cfg, cudaStream_t st,
                             ngsgd_ctx** out);
 void ngsgd_destroy_impl(ngsgd_ctx* h);
+ng_status ngsgd_join_impl(ngsgd_ctx* h);
 }  // namespace ng

@@ -355,8 +355,16 @@ ng_status nnet_create(const nnet_config* cfg, void* cuda_stream, nnet_t* out) {
 
 ng_status nnet_destroy(nnet_t h) {
   if (!h) return NG_EINVAL;
+  nnet_join(h);
   cudaStreamSynchronize(h->st);
   nnet_free(h);
+  return NG_OK;
+}
+
+ng_status nnet_join(nnet_t h) {
+  NG_REQUIRE(h != nullptr, NG_EINVAL, "NULL argument");
+  for (auto* p : h->ng_in) NG_TRY(ngsgd_join_impl(p));
+  for (auto* p : h->ng_out) NG_TRY(ngsgd_join_impl(p));
   return NG_OK;
 }
 
@@ -502,6 +510,7 @@ ng_status nnet_get_params(nnet_t h, int32_t layer, float* host, int64_t count) {
   NG_REQUIRE(h && host, NG_EINVAL, "NULL argument");
   NG_REQUIRE(layer >= 0 && layer < h->L, NG_EINVAL, "layer out of range");
   NG_REQUIRE(count == (int64_t)h->rows[layer] * h->cols[layer], NG_ESHAPE, "count != rows*cols");
+  NG_TRY(nnet_join(h));
   NG_CUDA_TRY(cudaStreamSynchronize(h->st));
   NG_CUDA_TRY(cudaMemcpy2D(host, sizeof(float) * h->cols[layer], h->arena + h->off[layer], sizeof(float) * h->ldp[layer],
                            sizeof(float) * h->cols[layer], h->rows[layer], cudaMemcpyDeviceToHost));
