@@ -75,3 +75,16 @@ def broadcast_bytes(payload: bytes | None, src: int = 0, group=None) -> bytes:
 
 def outer_iteration_of(step: int, minibatch: int, k_samples: int = K_SAMPLES) -> int:
     return int(math.floor(step * minibatch / k_samples))
+
+
+def tree_reduce_stride(values):
+    """The summation schedule of tree_avg_kernel (nnet.cu), written out on the host: for
+    w = 1, 2, 4, ...: v[k] += v[k + w] for k = 0, 2w, 4w, ...  Used by tests to pin the
+    device schedule to the oracle's pairwise tree (oracle.training.tree_sum)."""
+    v = [x.copy() for x in values]
+    w = 1
+    while w < len(v):
+        for k in range(0, len(v) - w, 2 * w):
+            v[k] = (v[k] + v[k + w]).astype(v[k].dtype)
+        w *= 2
+    return v[0]

@@ -1,0 +1,86 @@
+"""Multi-process (world_size 2, gloo, CPU) tests of the data-parallel host logic of
+section 3.1: NCCL unique-id broadcast, max-over-ranks timing, per-rank data seeds,
+per-job learning rate, arena sharding and the fixed summation tree of nnet_average,
+emulated with gloo collectives and checked bit-exactly against the oracle average."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import training as otr
+from paper_1410_7455_b200 import driver
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = {}
+        uid = bytes(range(128)) if rank == 0 else None
+        out["uid"] = driver.broadcast_bytes(uid)
+        out["max"] = driver.max_over_ranks(float(rank + 3))
+        # every job starts from the same model, trains on its own shard (seed per rank)
+        rng = np.random.default_rng(driver.rank_seed(rank))
+        count = 8 * 64 * world
+        arena = rng.normal(size=count).astype(np.float32)
+        # deterministic average: rank r reduces shard r of every rank in tree order
+        gathered = [torch.zeros(count) for _ in range(world)]
+        dist.all_gather(gathered, torch.from_numpy(arena))
+        lo, hi = driver.shard_bounds(count, world, rank)
+        shards = [g.numpy()[lo:hi].astype(np.float32) for g in gathered]
+        mine = (driver.tree_reduce_stride(shards) * np.float32(1.0 / world)).astype(np.float32)
+        pieces = [torch.zeros(hi - lo) for _ in range(world)]
+        dist.all_gather(pieces, torch.from_numpy(mine))
+        out["avg"] = np.concatenate([p.numpy() for p in pieces]).astype(np.float32)
+        out["all"] = [g.numpy().astype(np.float32) for g in gathered]
+        out["lr"] = driver.job_learning_rate(0, 1, world)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_average_and_helpers():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0]["uid"] == res[1]["uid"] == bytes(range(128))
+    assert res[0]["max"] == res[1]["max"] == 4.0
+    assert np.array_equal(res[0]["avg"], res[1]["avg"])            # identical on every rank
+    ref = otr.average_models([[a] for a in res[0]["all"]], dtype=np.float32)[0]
+    assert np.array_equal(res[0]["avg"], ref)                       # bit-exact vs oracle tree
+    assert res[0]["lr"] == pytest.approx(0.01 * 2 / 6)              # lr x n_jobs / 6
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 8])
+def test_tree_schedule_matches_oracle_tree(n):
+    rng = np.random.default_rng(n)
+    vals = [rng.normal(size=33).astype(np.float32) for _ in range(n)]
+    assert np.array_equal(driver.tree_reduce_stride(vals), otr.tree_sum(vals, np.float32))
+
+
+def test_outer_iteration_sizes():
+    mbs = driver.minibatches_per_outer_iteration(512)
+    assert len(mbs) == 782 and sum(mbs) == 400_000 and mbs[-1] == 128     # reading R24
+    assert driver.rank_seed(0) != driver.rank_seed(1)
+    lo, hi = driver.shard_bounds(1024, 4, 3)
+    assert (lo, hi) == (768, 1024)
