@@ -239,7 +239,7 @@ def roofline_for(group: str, prof: dict, precision: str, peaks: dict):
             "algorithmic_per_launch": by, "launch_ms": per_launch_s * 1e3}
 
 
-def precondition_bench(api, torch, minibatches: int = 1000):
+def precondition_bench(api, torch, precision: str, minibatches: int = 1000):
     """configs[1]: both sides of one 2000-dim layer, N = 512, R_in = 20 / R_out = 80,
     1000 minibatches (pool of 64 cycled; 257 update steps)."""
     import numpy as np
@@ -249,10 +249,11 @@ def precondition_bench(api, torch, minibatches: int = 1000):
     xo = [torch.from_numpy(b.astype(np.float32)).cuda() for b in power_law_rows(2000, N, 2000, n_batches=64)]
     xi = [torch.from_numpy(b.astype(np.float32)).cuda()
           for b in power_law_rows(2001, N, 2000, n_batches=64, nonneg=True, append_one=True)]
-    out_side = api.OnlinePreconditioner(2000, N, rank=80)
-    in_side = api.OnlinePreconditioner(2001, N, rank=20)
+    out_side = api.OnlinePreconditioner(2000, N, rank=80, precision=precision)
+    in_side = api.OnlinePreconditioner(2001, N, rank=20, precision=precision)
     work_o = torch.empty_like(xo[0])
-    work_i = torch.empty_like(xi[0])
+    work_i_buf = torch.zeros((N, 2004), dtype=torch.float32, device="cuda")   # ld % 4 == 0 (TMA)
+    work_i = work_i_buf[:, :2001]
     g = torch.zeros(2, device="cuda")
     p = torch.zeros(2, N, device="cuda")
 
@@ -284,7 +285,7 @@ def precondition_bench(api, torch, minibatches: int = 1000):
     cp = ec0.elapsed_time(ec1)
     return {"value": (tot - cp) / minibatches, "unit": "ms/minibatch", "higher_is_better": False,
             "config": "configs[1]: one 2000-dim layer, both sides (D=2000 R=80; D=2001 R=20), N=512, "
-                      f"{minibatches} minibatches (pool of 64 cycled), policy t<10 or 4|t",
+                      f"{minibatches} minibatches (pool of 64 cycled), policy t<10 or 4|t, NG projections {precision}",
             "copy_ms_subtracted_per_minibatch": cp / minibatches}
 
 
@@ -405,7 +406,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     pre = None
     if rank == 0 and not args.no_precond_bench:
         try:
-            pre = precondition_bench(api, torch)
+            pre = precondition_bench(api, torch, precision)
         except Exception as ex:  # report, do not hide
             pre = {"error": repr(ex)}
 

@@ -65,6 +65,10 @@ typedef struct {
   int32_t update_period;       /* J = 4                             */
   int32_t always_update_first; /* 10: always update on the first 10 minibatches  */
   float epsilon;               /* floor of rho and d, 1e-10      */
+  int32_t precision;           /* ng_precision (below) of the NG projections: NG_FP32 = CUDA
+                                  cores in FP32 (default); NG_TF32 = H, J, K, L, X_hat, W_{t+1}
+                                  on tcgen05 tensor cores (needs ld % 4 == 0 and R % 4 == 0,
+                                  otherwise that call uses FP32).  The R x R math is FP64.   */
 } ngsgd_config;
 
 void ngsgd_config_default(ngsgd_config* cfg, int32_t rank);

@@ -27,7 +27,7 @@ class NgError(RuntimeError):
 
 class NgsgdConfig(ctypes.Structure):
     _fields_ = [("rank", c_int32), ("alpha", c_float), ("s_samples", c_float), ("update_period", c_int32),
-                ("always_update_first", c_int32), ("epsilon", c_float)]
+                ("always_update_first", c_int32), ("epsilon", c_float), ("precision", c_int32)]
 
 
 class NgsgdStateHost(ctypes.Structure):

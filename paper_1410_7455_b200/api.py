@@ -51,12 +51,12 @@ class OnlinePreconditioner:
     """One online NG-SGD state (Appendix B; ngsgd_create / ngsgd_precondition)."""
 
     def __init__(self, dim: int, max_rows: int, rank: int = 20, stream: Optional[torch.cuda.Stream] = None,
-                 _borrowed: Optional[int] = None, **cfg_overrides):
+                 _borrowed: Optional[int] = None, precision: str = "fp32", **cfg_overrides):
         self._owned = _borrowed is None
         if _borrowed is not None:
             self._h = ctypes.c_void_p(_borrowed)
             return
-        cfg = default_ng_config(rank, **cfg_overrides)
+        cfg = default_ng_config(rank, precision={"fp32": 0, "tf32": 2}[precision], **cfg_overrides)
         h = ctypes.c_void_p()
         check(lib.ngsgd_create(int(dim), int(max_rows), ctypes.byref(cfg), _stream_handle(stream), ctypes.byref(h)))
         self._h = h
@@ -131,9 +131,10 @@ class Nnet:
         cfg.input_dim, cfg.num_hidden, cfg.hidden_dim = input_dim, num_hidden, hidden_dim
         cfg.pnorm_group, cfg.num_classes, cfg.max_minibatch = pnorm_group, num_classes, max_minibatch
         cfg.precond = 1 if precond else 0
-        cfg.ng_in = default_ng_config(rank_in, **(ng_overrides or {}))
-        cfg.ng_out = default_ng_config(rank_out, **(ng_overrides or {}))
-        cfg.precision = {"fp32": 0, "bf16": 1, "tf32": 2}[precision]
+        prec = {"fp32": 0, "bf16": 1, "tf32": 2}[precision]
+        cfg.ng_in = default_ng_config(rank_in, **dict({"precision": prec}, **(ng_overrides or {})))
+        cfg.ng_out = default_ng_config(rank_out, **dict({"precision": prec}, **(ng_overrides or {})))
+        cfg.precision = prec
         cfg.seed = int(seed)
         h = ctypes.c_void_p()
         check(lib.nnet_create(ctypes.byref(cfg), _stream_handle(stream), ctypes.byref(h)))

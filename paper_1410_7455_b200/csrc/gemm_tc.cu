@@ -196,27 +196,65 @@ tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   tc_fence_after();
   __syncwarp();
   const int row = m0 + warp * 32 + lane;
+  const float scale = (EPI == TC_EPI_AXPY) ? __ldg(epi.scale) : 0.f;
+  float* __restrict__ crow = epi.C + (EPI == TC_EPI_PARTIAL ? (int64_t)blockIdx.z * epi.zstride : 0) +
+                             (int64_t)row * epi.ldc;
+  float xx = 0.f, pp = 0.f;   // TC_EPI_NGAPPLY row partial sums over this tile's columns
 #pragma unroll 1
   for (int c = 0; c < BN / 16; ++c) {
     uint32_t v[16];
     tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * 16), v);
-    if (row < M) {
+    const int nb = n0 + c * 16;
+    if (row < M && nb < N) {
+      float acc[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int n = n0 + c * 16 + j;
-        if (n < N) {
-          const float acc = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
-          if (EPI == TC_EPI_STORE) {
-            epi.C[(int64_t)row * epi.ldc + n] = acc;
-          } else if (EPI == TC_EPI_AXPY) {
-            float* p = epi.C + (int64_t)row * epi.ldc + n;
-            *p = fmaf(*epi.scale, acc, *p);
-          } else {
-            epi.C[(int64_t)blockIdx.z * epi.zstride + (int64_t)row * epi.ldc + n] = acc;
+      for (int j = 0; j < 16; ++j) acc[j] = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
+      const bool full = (nb + 16 <= N) && ((reinterpret_cast<uintptr_t>(crow + nb) & 15) == 0);
+      if (EPI == TC_EPI_STORE || EPI == TC_EPI_PARTIAL) {
+        if (full) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<float4*>(crow + nb + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        } else {
+          for (int j = 0; j < 16 && nb + j < N; ++j) crow[nb + j] = acc[j];
+        }
+      } else {
+        // read-modify-write epilogues: issue all loads of the chunk first
+        float old[16];
+        if (full) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4) {
+            const float4 o = *reinterpret_cast<const float4*>(crow + nb + j);
+            old[j] = o.x; old[j + 1] = o.y; old[j + 2] = o.z; old[j + 3] = o.w;
           }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) old[j] = (nb + j < N) ? crow[nb + j] : 0.f;
+        }
+        float nw[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (EPI == TC_EPI_AXPY) {
+            nw[j] = fmaf(scale, acc[j], old[j]);
+          } else {   // TC_EPI_NGAPPLY: x_hat = x - (H W)  (eqn:hatxt:compute:2), row norms
+            nw[j] = old[j] - acc[j];
+            xx = fmaf(old[j], old[j], xx);
+            pp = fmaf(nw[j], nw[j], pp);
+          }
+        }
+        if (full) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<float4*>(crow + nb + j) = make_float4(nw[j], nw[j + 1], nw[j + 2], nw[j + 3]);
+        } else {
+          for (int j = 0; j < 16 && nb + j < N; ++j) crow[nb + j] = nw[j];
         }
       }
     }
+  }
+  if (EPI == TC_EPI_NGAPPLY && row < M) {
+    epi.xx[(int64_t)blockIdx.x * epi.part_ld + row] = xx;
+    epi.pp[(int64_t)blockIdx.x * epi.part_ld + row] = pp;
   }
   tc_fence_before();
   __syncthreads();
@@ -298,6 +336,7 @@ ng_status dispatch_epi(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap
   switch (epi.kind) {
     case TC_EPI_STORE: return launch<BN, AK, BKM, TC_EPI_STORE>(st, ta, tb, M, N, K, kbps, splits, epi);
     case TC_EPI_AXPY: return launch<BN, AK, BKM, TC_EPI_AXPY>(st, ta, tb, M, N, K, kbps, splits, epi);
+    case TC_EPI_NGAPPLY: return launch<BN, AK, BKM, TC_EPI_NGAPPLY>(st, ta, tb, M, N, K, kbps, splits, epi);
     default: return launch<BN, AK, BKM, TC_EPI_PARTIAL>(st, ta, tb, M, N, K, kbps, splits, epi);
   }
 }
@@ -324,7 +363,7 @@ ng_status tc_gemm_tf32(cudaStream_t st, int M, int N, int K, const float* A, int
                        const float* B, int64_t ldb, bool b_kmajor, const TcEpilogue& epi, int bn, int splits,
                        int* splits_used) {
   NG_REQUIRE(M >= 1 && N >= 1 && K >= 1, NG_ESHAPE, "tc_gemm_tf32: empty problem");
-  NG_REQUIRE(bn == 64 || bn == 128, NG_EINVAL, "tc_gemm_tf32: bn must be 64 or 128");
+  NG_REQUIRE(bn == 32 || bn == 64 || bn == 128, NG_EINVAL, "tc_gemm_tf32: bn must be 32, 64 or 128");
   const int kb = ceil_div(K, kBK);
   splits = tc_splits(K, splits);
   const int kbps = ceil_div(kb, splits);
@@ -335,6 +374,7 @@ ng_status tc_gemm_tf32(cudaStream_t st, int M, int N, int K, const float* A, int
   else NG_TRY(make_tmap(&ta, A, M, K, lda, 32, true));                // [K][M]
   if (b_kmajor) NG_TRY(make_tmap(&tb, B, K, N, ldb, bn, false));      // [N][K]
   else NG_TRY(make_tmap(&tb, B, N, K, ldb, 32, true));                // [K][N]
+  if (bn == 32) return dispatch_major<32>(st, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
   if (bn == 64) return dispatch_major<64>(st, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
   return dispatch_major<128>(st, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
 }

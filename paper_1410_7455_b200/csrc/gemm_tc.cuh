@@ -18,6 +18,8 @@ enum TcEpiKind : int {
   TC_EPI_STORE = 0,     // C[m][n] = acc
   TC_EPI_AXPY = 1,      // C[m][n] += (*scale) * acc          (weight update, eqn:add:w)
   TC_EPI_PARTIAL = 2,   // C[z][m][n] = acc                    (split-K partials)
+  TC_EPI_NGAPPLY = 3,   // C[m][n] -= acc, with per-row partial sums of old^2 / new^2 of this
+                        // column tile in xx / pp [blockIdx.x * part_ld + m]  (NG apply)
 };
 
 struct TcEpilogue {
@@ -26,9 +28,12 @@ struct TcEpilogue {
   int64_t ldc = 0;
   int64_t zstride = 0;        // TC_EPI_PARTIAL: elements between split slices
   const float* scale = nullptr;
+  float* xx = nullptr;        // TC_EPI_NGAPPLY partial ||x_i||^2
+  float* pp = nullptr;        // TC_EPI_NGAPPLY partial ||x_hat_i||^2
+  int64_t part_ld = 0;
 };
 
-// Launch one GEMM on `st`.  bn in {64, 128}; splits >= 1 (K split evenly over 32-wide
+// Launch one GEMM on `st`.  bn in {32, 64, 128}; splits >= 1 (K split evenly over 32-wide
 // k-blocks; with splits > 1 the epilogue must be TC_EPI_PARTIAL).  Pointers must be 16B
 // aligned and lda/ldb multiples of 4 (TMA).  Returns the number of splits used via
 // *splits_used (may be smaller than requested).

@@ -19,6 +19,7 @@
 
 #include "eig_jacobi.cuh"
 #include "gemm_simt.cuh"
+#include "gemm_tc.cuh"
 #include "ngsgd_impl.cuh"
 
 namespace ng {
@@ -71,6 +72,8 @@ ng_status status_from_flags(uint32_t f, const char* where) {
 }
 
 constexpr int kApplyRows = 16, kApplyCols = 128;
+constexpr int kTcMaxSplits = 32;   // split-K capacity (H, K, L) of the tensor-core path
+constexpr int kTcJSplits = 4;      // split-K of J = H^T X (K = N)
 constexpr int kMaxRank = 112;
 
 // ------------------------------------------------------------------------------------
@@ -173,6 +176,18 @@ __global__ void reduce_splits_kernel(float* __restrict__ out, const float* __res
     float s = 0.f;
     for (int z = 0; z < splits; ++z) s += part[(int64_t)z * zstride + i];
     out[i] = s;
+  }
+}
+
+// out[r][j] = sum_z part[z][r][j] (row-strided 2D, fixed order).
+__global__ void reduce_rows_kernel(float* __restrict__ out, int64_t ld, const float* __restrict__ part, int64_t zstride,
+                                   int splits, int R, int D) {
+  const int64_t total = (int64_t)R * D;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t off = (i / D) * ld + (i % D);
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += part[(int64_t)z * zstride + off];
+    out[off] = s;
   }
 }
 
@@ -533,7 +548,8 @@ ng_status ngsgd_create_impl(int dim, int max_rows, const ngsgd_config* cfg, cuda
   NG_REQUIRE(out != nullptr && cfg != nullptr, NG_EINVAL, "NULL argument");
   NG_REQUIRE(dim >= 1 && max_rows >= 1, NG_ESHAPE, "dim and max_rows must be >= 1");
   NG_REQUIRE(cfg->rank >= 0 && cfg->alpha >= 0.f && cfg->s_samples > 0.f && cfg->update_period >= 1 &&
-                 cfg->always_update_first >= 0 && cfg->epsilon > 0.f,
+                 cfg->always_update_first >= 0 && cfg->epsilon > 0.f &&
+                 (cfg->precision == NG_FP32 || cfg->precision == NG_TF32),
              NG_EINVAL, "invalid ngsgd_config");
   NG_TRY(set_kernel_attrs());
   ngsgd_ctx* h = new ngsgd_ctx();
@@ -553,14 +569,19 @@ ng_status ngsgd_create_impl(int dim, int max_rows, const ngsgd_config* cfg, cuda
   h->h_splits = gemm_simt_splits(dim, h->h_splits);
   h->kl_splits = std::max(1, std::min(32, ceil_div(dim, 256)));
   h->kl_splits = gemm_simt_splits(dim, h->kl_splits);
-  const int l_splits = std::max(h->kl_splits, gemm_simt_splits(max_rows, std::max(1, max_rows / 128)));
+  int l_splits = std::max(h->kl_splits, gemm_simt_splits(max_rows, std::max(1, max_rows / 128)));
+  if (cfg->precision == NG_TF32) {   // split-K capacities of the tensor-core path
+    h->h_splits = std::max(h->h_splits, kTcMaxSplits);
+    h->kl_splits = std::max(h->kl_splits, kTcMaxSplits);
+    l_splits = std::max(l_splits, kTcMaxSplits);
+  }
   h->ctiles = ceil_div(dim, kApplyCols);
   ng_status s = NG_OK;
 #define ALLOC(ptr, cnt) if (s == NG_OK) s = dalloc(&(ptr), (size_t)(cnt))
   ALLOC(h->W[0], (size_t)R * h->ldw);
   ALLOC(h->W[1], (size_t)R * h->ldw);
   ALLOC(h->dstate, 1 + 2 * R);
-  ALLOC(h->Hpart, (size_t)h->h_splits * max_rows * R);
+  ALLOC(h->Hpart, std::max((size_t)h->h_splits * max_rows * R, (size_t)kTcJSplits * R * h->ldw));
   ALLOC(h->H, (size_t)max_rows * R);
   ALLOC(h->J, (size_t)R * h->ldw);
   ALLOC(h->Kpart, (size_t)h->kl_splits * R * R);
@@ -718,45 +739,92 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
   const double eta = 1.0 - exp(-(double)n / (double)h->cfg.s_samples);   // eqn:eta:ns
   float* W = h->W[h->cur];
   const double nRD = (double)n * R * D;
+  // Tensor-core (TF32) projections when requested and the operands satisfy TMA alignment.
+  const bool tc = h->cfg.precision == NG_TF32 && (ld % 4) == 0 && (R % 4) == 0 &&
+                  (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  const int bnR = R <= 32 ? 32 : (R <= 64 ? 64 : 128);
+  const int m_tiles = ceil_div(n, 128);
   // H = X W^T (eqn:ht), split over D, fixed-order reduction
   {
-  ProfScope ps(NG_PROF_NG_PROJ, st, 2.0 * nRD, 4.0 * ((double)n * D + (double)R * D));
-  NG_TRY((gemm_simt<float, true, true>(st, n, R, D, x, ld, W, h->ldw,
-                                       EpiStoreSplit<float>{h->Hpart, R, (int64_t)n * R}, h->h_splits)));
-  const int hs = gemm_simt_splits(D, h->h_splits);
-  reduce_splits_kernel<<<ceil_div((int64_t)n * R, 256), 256, 0, st>>>(h->H, h->Hpart, (int64_t)n * R, hs, (int64_t)n * R, nullptr);
-  NG_TRY(check_launch("reduce_splits(H)"));
+    ProfScope ps(NG_PROF_NG_PROJ, st, 2.0 * nRD, 4.0 * ((double)n * D + (double)R * D));
+    int hs = 1;
+    if (tc) {
+      TcEpilogue e;
+      e.kind = TC_EPI_PARTIAL; e.C = h->Hpart; e.ldc = R; e.zstride = (int64_t)n * R;
+      const int want = std::min(kTcMaxSplits, std::max(1, 148 / (m_tiles * ceil_div(R, bnR))));
+      NG_TRY(tc_gemm_tf32(st, n, R, D, x, ld, true, W, h->ldw, true, e, bnR, want, &hs));
+    } else {
+      NG_TRY((gemm_simt<float, true, true>(st, n, R, D, x, ld, W, h->ldw,
+                                           EpiStoreSplit<float>{h->Hpart, R, (int64_t)n * R}, h->h_splits)));
+      hs = gemm_simt_splits(D, h->h_splits);
+    }
+    reduce_splits_kernel<<<ceil_div((int64_t)n * R, 256), 256, 0, st>>>(h->H, h->Hpart, (int64_t)n * R, hs,
+                                                                       (int64_t)n * R, nullptr);
+    NG_TRY(check_launch("reduce_splits(H)"));
   }
   if (upd) {
     ProfScope ps(NG_PROF_NG_REFRESH, st, 2.0 * nRD + 4.0 * (double)R * R * D,
                  4.0 * ((double)n * D + 3.0 * R * D));
-    // J = H^T X -- before X is overwritten
-    NG_TRY((gemm_simt<float, false, false>(st, R, D, n, h->H, R, x, ld, EpiStore<float>{h->J, h->ldw, 1.f})));
-    // K = J J^T
-    const int ks = gemm_simt_splits(D, h->kl_splits);
-    NG_TRY((gemm_simt<float, true, true>(st, R, R, D, h->J, h->ldw, h->J, h->ldw,
-                                         EpiStoreSplit<float>{h->Kpart, R, (int64_t)R * R}, ks)));
-    reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->KL, h->Kpart, R * R, ks, R * R, nullptr);
-    NG_TRY(check_launch("reduce_splits(K)"));
-    if (n > D) {   // L = W J^T
-      NG_TRY((gemm_simt<float, true, true>(st, R, R, D, W, h->ldw, h->J, h->ldw,
-                                           EpiStoreSplit<float>{h->Lpart, R, (int64_t)R * R}, ks)));
-      reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->KL + R * R, h->Lpart, R * R, ks, R * R, nullptr);
-    } else {       // L = H^T H
-      const int ls = gemm_simt_splits(n, std::max(1, n / 128));
-      NG_TRY((gemm_simt<float, false, false>(st, R, R, n, h->H, R, h->H, R,
-                                             EpiStoreSplit<float>{h->Lpart, R, (int64_t)R * R}, ls)));
+    if (tc) {
+      // J = H^T X: A = H (MN-major), B = X (MN-major), split over N
+      TcEpilogue e;
+      e.kind = TC_EPI_PARTIAL; e.C = h->Hpart; e.ldc = h->ldw; e.zstride = (int64_t)R * h->ldw;
+      int js = 1;
+      NG_TRY(tc_gemm_tf32(st, R, D, n, h->H, R, false, x, ld, false, e, 128, kTcJSplits, &js));
+      reduce_rows_kernel<<<std::min(1024, ceil_div((int64_t)R * D, 256)), 256, 0, st>>>(
+          h->J, h->ldw, h->Hpart, (int64_t)R * h->ldw, js, R, D);
+      NG_TRY(check_launch("reduce_rows(J)"));
+      // K = J J^T: K-major both, split over D
+      int ks = 1;
+      TcEpilogue ek;
+      ek.kind = TC_EPI_PARTIAL; ek.C = h->Kpart; ek.ldc = R; ek.zstride = (int64_t)R * R;
+      NG_TRY(tc_gemm_tf32(st, R, R, D, h->J, h->ldw, true, h->J, h->ldw, true, ek, bnR, 32, &ks));
+      reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->KL, h->Kpart, R * R, ks, R * R, nullptr);
+      NG_TRY(check_launch("reduce_splits(K)"));
+      int ls = 1;
+      TcEpilogue el;
+      el.kind = TC_EPI_PARTIAL; el.C = h->Lpart; el.ldc = R; el.zstride = (int64_t)R * R;
+      if (n > D)   // L = W J^T
+        NG_TRY(tc_gemm_tf32(st, R, R, D, W, h->ldw, true, h->J, h->ldw, true, el, bnR, 32, &ls));
+      else         // L = H^T H
+        NG_TRY(tc_gemm_tf32(st, R, R, n, h->H, R, false, h->H, R, false, el, bnR, 8, &ls));
       reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->KL + R * R, h->Lpart, R * R, ls, R * R, nullptr);
+      NG_TRY(check_launch("reduce_splits(L)"));
+    } else {
+      // J = H^T X -- before X is overwritten
+      NG_TRY((gemm_simt<float, false, false>(st, R, D, n, h->H, R, x, ld, EpiStore<float>{h->J, h->ldw, 1.f})));
+      // K = J J^T
+      const int ks = gemm_simt_splits(D, h->kl_splits);
+      NG_TRY((gemm_simt<float, true, true>(st, R, R, D, h->J, h->ldw, h->J, h->ldw,
+                                           EpiStoreSplit<float>{h->Kpart, R, (int64_t)R * R}, ks)));
+      reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->KL, h->Kpart, R * R, ks, R * R, nullptr);
+      NG_TRY(check_launch("reduce_splits(K)"));
+      if (n > D) {   // L = W J^T
+        NG_TRY((gemm_simt<float, true, true>(st, R, R, D, W, h->ldw, h->J, h->ldw,
+                                             EpiStoreSplit<float>{h->Lpart, R, (int64_t)R * R}, ks)));
+        reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->KL + R * R, h->Lpart, R * R, ks, R * R, nullptr);
+      } else {       // L = H^T H
+        const int ls = gemm_simt_splits(n, std::max(1, n / 128));
+        NG_TRY((gemm_simt<float, false, false>(st, R, R, n, h->H, R, h->H, R,
+                                               EpiStoreSplit<float>{h->Lpart, R, (int64_t)R * R}, ls)));
+        reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->KL + R * R, h->Lpart, R * R, ls, R * R, nullptr);
+      }
+      NG_TRY(check_launch("reduce_splits(L)"));
     }
-    NG_TRY(check_launch("reduce_splits(L)"));
   }
   // X_hat = X - H W in place, with partial row norms
   {
     ProfScope ps(NG_PROF_NG_APPLY, st, 2.0 * nRD, 4.0 * (2.0 * n * D + (double)R * D));
-    dim3 grid(ceil_div(n, kApplyRows), ceil_div(D, kApplyCols));
-    const size_t smem = sizeof(float) * (kApplyRows * R + R * kApplyCols);
-    apply_kernel<<<grid, 256, smem, st>>>(n, D, R, x, ld, h->H, W, h->ldw, h->xxpart, h->ppart, h->max_rows);
-    NG_TRY(check_launch("apply_kernel"));
+    if (tc) {
+      TcEpilogue e;
+      e.kind = TC_EPI_NGAPPLY; e.C = x; e.ldc = ld; e.xx = h->xxpart; e.pp = h->ppart; e.part_ld = h->max_rows;
+      NG_TRY(tc_gemm_tf32(st, n, D, R, h->H, R, true, W, h->ldw, false, e, 128, 1));
+    } else {
+      dim3 grid(ceil_div(n, kApplyRows), ceil_div(D, kApplyCols));
+      const size_t smem = sizeof(float) * (kApplyRows * R + R * kApplyCols);
+      apply_kernel<<<grid, 256, smem, st>>>(n, D, R, x, ld, h->H, W, h->ldw, h->xxpart, h->ppart, h->max_rows);
+      NG_TRY(check_launch("apply_kernel"));
+    }
     finalize_kernel<<<1, 512, 0, st>>>(n, h->ctiles, h->xxpart, h->ppart, h->max_rows, h->p, p_out, h->sums,
                                        h->gamma, gamma_out, h->flags);
     NG_TRY(check_launch("finalize_kernel"));
@@ -781,7 +849,13 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
     const int nxt = 1 - h->cur;
     float* Wn = h->W[nxt];
     // W_{t+1} = A_t B_t (eqn:wt1)
-    NG_TRY((gemm_simt<float, true, false>(ss, R, D, R, h->Amat, R, h->J, h->ldw, EpiStore<float>{Wn, h->ldw, 1.f})));
+    if (tc) {
+      TcEpilogue e;
+      e.kind = TC_EPI_STORE; e.C = Wn; e.ldc = h->ldw;
+      NG_TRY(tc_gemm_tf32(ss, R, D, R, h->Amat, R, true, h->J, h->ldw, false, e, 128, 1));
+    } else {
+      NG_TRY((gemm_simt<float, true, false>(ss, R, D, R, h->Amat, R, h->J, h->ldw, EpiStore<float>{Wn, h->ldw, 1.f})));
+    }
     // B.3.1, gated on the device flag (no host synchronisation)
     const int ks = gemm_simt_splits(D, h->kl_splits);
     NG_TRY((gemm_simt<float, true, true>(ss, R, R, D, Wn, h->ldw, Wn, h->ldw,
@@ -824,6 +898,7 @@ void ngsgd_config_default(ngsgd_config* cfg, int32_t rank) {
   cfg->update_period = 4;
   cfg->always_update_first = 10;
   cfg->epsilon = 1e-10f;
+  cfg->precision = NG_FP32;
 }
 
 ng_status ng_profile_enable(uint32_t mask) {

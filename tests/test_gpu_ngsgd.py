@@ -171,3 +171,24 @@ def test_reorthogonalisation_path(api):
     assert o.reorth_checked and st["reorth_checked"]
     assert st["reorthogonalized"] == o.reorthogonalized
     assert normwise(g * xh, o.x_bar) <= TOL
+
+
+@pytest.mark.parametrize("N,D,R,steps", [(512, 2000, 80, 14), (512, 2001, 20, 14), (130, 300, 20, 12)])
+def test_tf32_tensor_core_trajectory(api, N, D, R, steps):
+    """NG_TF32: H, J, K, L, X_hat and W_{t+1} on tcgen05 tensor cores (TF32 inputs, FP32
+    accumulation; the R x R math stays FP64).  Bar for reduced-precision tensor-core
+    inputs (north star): preconditioned output within 2e-2 normwise of the float64 oracle
+    at every step of a trajectory from initialisation; state within 2e-2."""
+    ld = (D + 3) // 4 * 4
+    batches = power_law_rows(700 + D, N, D, n_batches=steps, nonneg=(D % 2 == 1))
+    batches = [b.astype(np.float32).astype(np.float64) for b in batches]
+    pre = api.OnlinePreconditioner(D, N, rank=R, precision="tf32")
+    s = ong.OnlineNgState(D, ong.OnlineNgConfig(rank=R))
+    for t, X in enumerate(batches):
+        o = ong.precondition(s, X)
+        xh, g, p = run_gpu(pre, X, ld=ld)
+        assert normwise(g * xh, o.x_bar) <= 2e-2, t
+        st = pre.get_state()
+        W = st["W"].astype(np.float64)
+        assert normwise(W.T @ W, s.W.T @ s.W) <= 2e-2, t
+        assert st["updated"] == o.updated
