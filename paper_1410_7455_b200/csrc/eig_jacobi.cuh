@@ -167,3 +167,136 @@ __device__ void eig_sort_desc(const double* A, int lda, const double* Vt, int ld
 }
 
 }  // namespace ng
+
+namespace ng {
+
+// ---------------------------------------------------------------------------------------
+// Lean shared-memory variant for the per-update R x R refresh (R <= 112): the pair table of
+// every round and the list of 2x2 blocks are precomputed once, eigenvector rows are
+// rotated warp-per-pair with contiguous, conflict-free accesses, and warp-uniform skips
+// drop converged pairs.  Same algorithm (cyclic round-robin Jacobi, FP32 angle -> exactly
+// orthogonal FP64 rotation) and stopping rule as jacobi_eig.
+//   A: n x n, row stride lda (shared);  Vt: n x n, row stride ldv (shared)
+//   ptab: (npad-1) * m uint16 pairs (p | q << 8);  blk: m(m+1)/2 uint16 (ka | kb << 8)
+// ---------------------------------------------------------------------------------------
+struct JacobiSmem {
+  uint16_t* ptab;
+  uint16_t* blk;
+  double* c;
+  double* s;
+  int* nrot;
+};
+
+__device__ void jacobi_eig_smem(double* __restrict__ A, int lda, double* __restrict__ Vt, int ldv, int n,
+                                JacobiSmem sc, int max_sweeps, double abs_floor, double rel_tol) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+  const int npad = n + (n & 1);
+  const int m = npad / 2;
+  const int rounds = npad - 1;
+  const int nblk = m * (m + 1) / 2;
+  for (int idx = tid; idx < rounds * m; idx += nt) {
+    const int r = idx / m, k = idx % m;
+    int p, q;
+    jacobi_pair(r, k, npad, p, q);
+    sc.ptab[idx] = (uint16_t)(p | (q << 8));
+  }
+  for (int idx = tid; idx < m * m; idx += nt) {
+    const int ka = idx % m, kb = idx / m;
+    if (ka <= kb) {
+      const int pos = kb * (kb + 1) / 2 + ka;
+      sc.blk[pos] = (uint16_t)(ka | (kb << 8));
+    }
+  }
+  for (int idx = tid; idx < n * n; idx += nt) {
+    const int i = idx / n, j = idx % n;
+    Vt[i * ldv + j] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  if (n <= 1) return;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) *sc.nrot = 0;
+    __syncthreads();
+    for (int round = 0; round < rounds; ++round) {
+      const uint16_t* pr = sc.ptab + round * m;
+      if (tid < m) {
+        const int k = tid;
+        const int p = pr[k] & 0xFF, q = pr[k] >> 8;
+        double c = 1.0, s = 0.0;
+        if (q < n) {
+          const double app = A[p * lda + p], aqq = A[q * lda + q], apq = A[p * lda + q];
+          const double thr = fmax(rel_tol * sqrt(fabs(app * aqq)), abs_floor);
+          if (fabs(apq) > thr) {
+            const double thd = (aqq - app) / (2.0 * apq);
+            float tf;
+            if (fabs(thd) > 1e18) {
+              tf = (float)(0.5 / thd);
+            } else {
+              const float th = (float)thd;
+              tf = copysignf(1.f, th) / (fabsf(th) + sqrtf(fmaf(th, th, 1.f)));
+            }
+            const double t = (double)tf;
+            c = rsqrt(fma(t, t, 1.0));
+            s = t * c;
+            atomicAdd(sc.nrot, 1);
+          }
+        }
+        sc.c[k] = c;
+        sc.s[k] = s;
+      }
+      __syncthreads();
+      // A' = J^T A J, 2x2 blocks (ka <= kb), mirrored
+      for (int b = tid; b < nblk; b += nt) {
+        const uint16_t kk = sc.blk[b];
+        const int ka = kk & 0xFF, kb = kk >> 8;
+        const double s1 = sc.s[ka], s2 = sc.s[kb];
+        if (s1 == 0.0 && s2 == 0.0) continue;
+        const double c1 = sc.c[ka], c2 = sc.c[kb];
+        const int p1 = pr[ka] & 0xFF, q1 = pr[ka] >> 8, p2 = pr[kb] & 0xFF, q2 = pr[kb] >> 8;
+        if (ka == kb) {
+          const double a = A[p1 * lda + p1], d = A[q1 * lda + q1], bb = A[p1 * lda + q1];
+          const double cc = c1 * c1, ss = s1 * s1, cs = c1 * s1;
+          const double bn = (cc - ss) * bb + cs * (a - d);
+          A[p1 * lda + p1] = cc * a - 2.0 * cs * bb + ss * d;
+          A[q1 * lda + q1] = ss * a + 2.0 * cs * bb + cc * d;
+          A[p1 * lda + q1] = bn;
+          A[q1 * lda + p1] = bn;
+          continue;
+        }
+        const bool v1 = q1 < n, v2 = q2 < n;
+        const double m00 = A[p1 * lda + p2];
+        const double m01 = v2 ? A[p1 * lda + q2] : 0.0;
+        const double m10 = v1 ? A[q1 * lda + p2] : 0.0;
+        const double m11 = (v1 && v2) ? A[q1 * lda + q2] : 0.0;
+        const double t00 = c1 * m00 - s1 * m10, t01 = c1 * m01 - s1 * m11;
+        const double t10 = s1 * m00 + c1 * m10, t11 = s1 * m01 + c1 * m11;
+        const double r00 = c2 * t00 - s2 * t01, r01 = s2 * t00 + c2 * t01;
+        const double r10 = c2 * t10 - s2 * t11, r11 = s2 * t10 + c2 * t11;
+        A[p1 * lda + p2] = r00; A[p2 * lda + p1] = r00;
+        if (v2) { A[p1 * lda + q2] = r01; A[q2 * lda + p1] = r01; }
+        if (v1) { A[q1 * lda + p2] = r10; A[p2 * lda + q1] = r10; }
+        if (v1 && v2) { A[q1 * lda + q2] = r11; A[q2 * lda + q1] = r11; }
+      }
+      // eigenvector rows, one warp per pair, contiguous columns
+      for (int k = warp; k < m; k += nwarps) {
+        const double s = sc.s[k];
+        if (s == 0.0) continue;
+        const double c = sc.c[k];
+        const int p = pr[k] & 0xFF, q = pr[k] >> 8;
+        double* vp = Vt + p * ldv;
+        double* vq = Vt + q * ldv;
+        for (int j = lane; j < n; j += 32) {
+          const double a = vp[j], b = vq[j];
+          vp[j] = c * a - s * b;
+          vq[j] = s * a + c * b;
+        }
+      }
+      __syncthreads();
+    }
+    const int rot = *sc.nrot;
+    __syncthreads();
+    if (rot == 0) break;
+  }
+}
+
+}  // namespace ng

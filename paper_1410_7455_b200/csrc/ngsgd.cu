@@ -222,23 +222,23 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
                float* __restrict__ svec, int* __restrict__ flags) {
   extern __shared__ __align__(16) unsigned char ng_smem[];
   double* sm = reinterpret_cast<double*>(ng_smem);
-  double* Z = sm;                 // R*R
-  double* Vt = Z + R * R;         // R*R
-  double* d = Vt + R * R;         // R   old d
-  double* emh = d + R;            // R   E_t^{-1/2}
-  double* dr = emh + R;           // R   d + rho
-  double* c = dr + R;             // R   sorted eigenvalues
-  double* dn = c + R;             // R   new d
-  double* jc = dn + R;            // R/2+1 rotation c
-  double* js = jc + (R / 2 + 1);  // s
-  double* jt = js + (R / 2 + 1);  // t
-  double* red = jt + (R / 2 + 1); // 32 reduction scratch
-  int* ip = reinterpret_cast<int*>(red + 32);
-  int* jp = ip;                   // R/2+1
-  int* jq = jp + (R / 2 + 1);     // R/2+1
-  int* perm = jq + (R / 2 + 1);   // R
-  int* nrot = perm + R;           // 1
-  int* iflag = nrot + 1;          // 1 (floored)
+  const int LD = R + 1;            // odd row stride: fewer bank conflicts
+  const int mp = R / 2 + 1;        // >= number of rotation pairs
+  double* Z = sm;                  // R*LD
+  double* Vt = Z + R * LD;         // R*LD
+  double* d = Vt + R * LD;         // R   old d
+  double* emh = d + R;             // R   E_t^{-1/2}
+  double* dr = emh + R;            // R   d + rho
+  double* c = dr + R;              // R   sorted eigenvalues
+  double* dn = c + R;              // R   new d
+  double* jc = dn + R;             // mp rotation c
+  double* js = jc + mp;            // mp rotation s
+  double* red = js + mp;           // 32 reduction scratch
+  int* perm = reinterpret_cast<int*>(red + 32);   // R
+  int* nrot = perm + R;            // 1
+  uint16_t* ptab = reinterpret_cast<uint16_t*>(nrot + 2);   // (2mp-1) * mp
+  uint16_t* blk = ptab + (2 * mp) * mp;                     // mp(mp+1)/2
+  int* iflag = nrot + 1;           // 1 (floored)
   const int tid = threadIdx.x, nt = blockDim.x;
 
   const double rho = dstate[0];
@@ -266,27 +266,27 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
     const double ls = 0.5 * ((double)L[i * R + j] + (double)L[j * R + i]);
     double z = a1 * emh[i] * ks * emh[j] + a3 * emh[i] * ls * emh[j] * (dr[i] + dr[j]);
     if (i == j) z += a2 * dr[i] * dr[i];
-    Z[idx] = z;
+    Z[i * LD + j] = z;
   }
   __syncthreads();
   double zmax = 0.0;
-  for (int i = tid; i < R; i += nt) zmax = fmax(zmax, fabs(Z[i * R + i]));
+  for (int i = tid; i < R; i += nt) zmax = fmax(zmax, fabs(Z[i * LD + i]));
   zmax = block_max(zmax, red);
   // Z = U C U^T (eqn:zt:eig:repeat)
-  JacobiScratch scr{jp, jq, jc, js, jt, nrot};
-  jacobi_eig(Z, R, Vt, R, R, scr, 20, 1e-15 * zmax);
+  JacobiSmem scr{ptab, blk, jc, js, nrot};
+  jacobi_eig_smem(Z, LD, Vt, LD, R, scr, 20, 1e-15 * zmax, 1e-9);
   // descending order
   for (int i = tid; i < R; i += nt) {
-    const double li = Z[i * R + i];
+    const double li = Z[i * LD + i];
     int r = 0;
-    for (int j = 0; j < R; ++j) { const double lj = Z[j * R + j]; r += (lj > li) || (lj == li && j < i); }
+    for (int j = 0; j < R; ++j) { const double lj = Z[j * LD + j]; r += (lj > li) || (lj == li && j < i); }
     perm[r] = i;
   }
   __syncthreads();
   // floor C at (1-eta)^2 rho_t^2 (reading R13)
   const double cf = a2 * rho * rho;
   for (int r = tid; r < R; r += nt) {
-    double cr = Z[perm[r] * R + perm[r]];
+    double cr = Z[perm[r] * LD + perm[r]];
     if (cr < cf) { cr = cf; atomicOr(iflag, 1); }
     c[r] = cr;
   }
@@ -308,7 +308,7 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   for (int idx = tid; idx < R * R; idx += nt) {
     const int r = idx / R, j = idx % R;
     const double en = 1.0 / (beta_new / dn[r] + 1.0);
-    Amat[idx] = (float)((eta / N) * sqrt(en) / sqrt(c[r]) * Vt[perm[r] * R + j] * emh[j]);
+    Amat[idx] = (float)((eta / N) * sqrt(en) / sqrt(c[r]) * Vt[perm[r] * LD + j] * emh[j]);
   }
   // row scale of B_t with the OLD d, rho
   for (int k = tid; k < R; k += nt) svec[k] = (float)((N * (1.0 - eta) / eta) * dr[k]);
@@ -518,8 +518,9 @@ __global__ void passthrough_kernel(int n, float* p, float* p_out, float* g, floa
 // ------------------------------------------------------------------------------------
 
 static size_t refresh_smem_bytes(int R) {
-  const int m = R / 2 + 1;
-  return sizeof(double) * (2 * R * R + 5 * R + 3 * m + 32) + sizeof(int) * (2 * m + R + 2);
+  const int mp = R / 2 + 1;
+  return sizeof(double) * (2 * (size_t)R * (R + 1) + 5 * R + 2 * mp + 32) + sizeof(int) * (R + 2) +
+         sizeof(uint16_t) * (2 * mp * mp + mp * (mp + 1) / 2) + 64;
 }
 static size_t reorth_smem_bytes(int R) { return sizeof(double) * (2 * R * R + R + 32); }
 
