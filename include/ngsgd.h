@@ -114,6 +114,7 @@ typedef struct {
   double* d;         /* host double[rank]  caller-allocated: diag(D_t), descending */
   float* w;          /* host float[rank*dim] caller-allocated: W_t row-major        */
   int32_t last_updated, last_floored, last_reorth_checked, last_reorthogonalized;
+  int32_t last_jacobi_sweeps;   /* sweeps the R x R eigensolver used in the last update */
 } ngsgd_state_host;
 
 /* Copy the state to the host (synchronises the handle's stream).  d / w may be NULL to

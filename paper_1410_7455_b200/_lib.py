@@ -33,7 +33,8 @@ class NgsgdConfig(ctypes.Structure):
 class NgsgdStateHost(ctypes.Structure):
     _fields_ = [("dim", c_int32), ("rank", c_int32), ("t", c_int32), ("initialized", c_int32), ("rho", c_double),
                 ("d", ctypes.POINTER(c_double)), ("w", ctypes.POINTER(c_float)), ("last_updated", c_int32),
-                ("last_floored", c_int32), ("last_reorth_checked", c_int32), ("last_reorthogonalized", c_int32)]
+                ("last_floored", c_int32), ("last_reorth_checked", c_int32), ("last_reorthogonalized", c_int32),
+                ("last_jacobi_sweeps", c_int32)]
 
 
 class NnetConfig(ctypes.Structure):

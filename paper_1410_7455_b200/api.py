@@ -95,7 +95,8 @@ class OnlinePreconditioner:
         check(code)
         return dict(dim=D, rank=R, t=st.t, initialized=bool(st.initialized), rho=st.rho, d=d[:R].copy(),
                     W=w[:R].copy(), updated=bool(st.last_updated), floored=bool(st.last_floored),
-                    reorth_checked=bool(st.last_reorth_checked), reorthogonalized=bool(st.last_reorthogonalized))
+                    reorth_checked=bool(st.last_reorth_checked), reorthogonalized=bool(st.last_reorthogonalized),
+                    jacobi_sweeps=int(st.last_jacobi_sweeps))
 
     def set_state(self, rho: float, d: np.ndarray, W: np.ndarray, t: int, initialized: bool = True) -> None:
         d = np.ascontiguousarray(d, dtype=np.float64)

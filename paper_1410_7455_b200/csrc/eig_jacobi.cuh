@@ -187,8 +187,8 @@ struct JacobiSmem {
   int* nrot;
 };
 
-__device__ void jacobi_eig_smem(double* __restrict__ A, int lda, double* __restrict__ Vt, int ldv, int n,
-                                JacobiSmem sc, int max_sweeps, double abs_floor, double rel_tol) {
+__device__ int jacobi_eig_smem(double* __restrict__ A, int lda, double* __restrict__ Vt, int ldv, int n,
+                               JacobiSmem sc, int max_sweeps, double abs_floor, double rel_tol) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
   const int npad = n + (n & 1);
@@ -213,8 +213,9 @@ __device__ void jacobi_eig_smem(double* __restrict__ A, int lda, double* __restr
     Vt[i * ldv + j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
-  if (n <= 1) return;
-  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+  if (n <= 1) return 0;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
     if (tid == 0) *sc.nrot = 0;
     __syncthreads();
     for (int round = 0; round < rounds; ++round) {
@@ -297,6 +298,7 @@ __device__ void jacobi_eig_smem(double* __restrict__ A, int lda, double* __restr
     __syncthreads();
     if (rot == 0) break;
   }
+  return sweep + 1;
 }
 
 }  // namespace ng

@@ -274,7 +274,7 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   zmax = block_max(zmax, red);
   // Z = U C U^T (eqn:zt:eig:repeat)
   JacobiSmem scr{ptab, blk, jc, js, nrot};
-  jacobi_eig_smem(Z, LD, Vt, LD, R, scr, 20, 1e-15 * zmax, 1e-9);
+  const int sweeps = jacobi_eig_smem(Z, LD, Vt, LD, R, scr, 20, 1e-15 * zmax, 1e-9);
   // descending order
   for (int i = tid; i < R; i += nt) {
     const double li = Z[i * LD + i];
@@ -328,6 +328,7 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
     flags[0] = fl;
     flags[1] = (fl || cmax / cmin > 1e6) ? 1 : 0;     // B.3.1 trigger
     flags[2] = 0;
+    flags[4] = sweeps;
     if (!isfinite(rho_new) || !isfinite(sdn)) atomicOr(reinterpret_cast<unsigned*>(flags + 3), kErrNonFinite);
   }
 }
@@ -598,7 +599,7 @@ ng_status ngsgd_create_impl(int dim, int max_rows, const ngsgd_config* cfg, cuda
   ALLOC(h->p, max_rows);
   ALLOC(h->sums, 2);
   ALLOC(h->gamma, 1);
-  ALLOC(h->flags, 4);
+  ALLOC(h->flags, 8);
 #undef ALLOC
   if (s == NG_OK && cudaMallocHost((void**)&h->h_scalar, 4 * sizeof(double)) != cudaSuccess) s = NG_ENOMEM;
   if (s == NG_OK && (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
@@ -611,7 +612,7 @@ ng_status ngsgd_create_impl(int dim, int max_rows, const ngsgd_config* cfg, cuda
     cudaMemsetAsync(h->W[0], 0, sizeof(float) * R * h->ldw, st);
     cudaMemsetAsync(h->W[1], 0, sizeof(float) * R * h->ldw, st);
     cudaMemsetAsync(h->J, 0, sizeof(float) * R * h->ldw, st);
-    cudaMemsetAsync(h->flags, 0, sizeof(int) * 4, st);
+    cudaMemsetAsync(h->flags, 0, sizeof(int) * 8, st);
     cudaMemsetAsync(h->dstate, 0, sizeof(double) * (1 + 2 * R), st);
     if (cudaGetLastError() != cudaSuccess) s = NG_ECUDA;
   }
@@ -775,21 +776,18 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
       reduce_rows_kernel<<<std::min(1024, ceil_div((int64_t)R * D, 256)), 256, 0, st>>>(
           h->J, h->ldw, h->Hpart, (int64_t)R * h->ldw, js, R, D);
       NG_TRY(check_launch("reduce_rows(J)"));
-      // K = J J^T: K-major both, split over D
-      int ks = 1;
-      TcEpilogue ek;
-      ek.kind = TC_EPI_PARTIAL; ek.C = h->Kpart; ek.ldc = R; ek.zstride = (int64_t)R * R;
-      NG_TRY(tc_gemm_tf32(st, R, R, D, h->J, h->ldw, true, h->J, h->ldw, true, ek, bnR, 32, &ks));
+      // K = J J^T and L = W J^T stay FP32 (CUDA cores): Z_t must equal Y_t Y_t^T for the
+      // STORED J to FP32 accuracy, otherwise R_{t+1} = C^{-1/2} U^T Y_t loses orthonormality
+      // at the TF32 level (1e-3) and B.3.1 repairs fire.  L = W J^T is used for every N
+      // (it equals H^T H only when J = H^T X exactly).
+      const int ks = gemm_simt_splits(D, h->kl_splits);
+      NG_TRY((gemm_simt<float, true, true>(st, R, R, D, h->J, h->ldw, h->J, h->ldw,
+                                           EpiStoreSplit<float>{h->Kpart, R, (int64_t)R * R}, ks)));
       reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->KL, h->Kpart, R * R, ks, R * R, nullptr);
       NG_TRY(check_launch("reduce_splits(K)"));
-      int ls = 1;
-      TcEpilogue el;
-      el.kind = TC_EPI_PARTIAL; el.C = h->Lpart; el.ldc = R; el.zstride = (int64_t)R * R;
-      if (n > D)   // L = W J^T
-        NG_TRY(tc_gemm_tf32(st, R, R, D, W, h->ldw, true, h->J, h->ldw, true, el, bnR, 32, &ls));
-      else         // L = H^T H
-        NG_TRY(tc_gemm_tf32(st, R, R, n, h->H, R, false, h->H, R, false, el, bnR, 8, &ls));
-      reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->KL + R * R, h->Lpart, R * R, ls, R * R, nullptr);
+      NG_TRY((gemm_simt<float, true, true>(st, R, R, D, W, h->ldw, h->J, h->ldw,
+                                           EpiStoreSplit<float>{h->Lpart, R, (int64_t)R * R}, ks)));
+      reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->KL + R * R, h->Lpart, R * R, ks, R * R, nullptr);
       NG_TRY(check_launch("reduce_splits(L)"));
     } else {
       // J = H^T X -- before X is overwritten
@@ -849,14 +847,8 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
     NG_TRY(check_launch("bscale_kernel"));
     const int nxt = 1 - h->cur;
     float* Wn = h->W[nxt];
-    // W_{t+1} = A_t B_t (eqn:wt1)
-    if (tc) {
-      TcEpilogue e;
-      e.kind = TC_EPI_STORE; e.C = Wn; e.ldc = h->ldw;
-      NG_TRY(tc_gemm_tf32(ss, R, D, R, h->Amat, R, true, h->J, h->ldw, false, e, 128, 1));
-    } else {
-      NG_TRY((gemm_simt<float, true, false>(ss, R, D, R, h->Amat, R, h->J, h->ldw, EpiStore<float>{Wn, h->ldw, 1.f})));
-    }
+    // W_{t+1} = A_t B_t (eqn:wt1), FP32 in both modes (orthonormality of R_{t+1})
+    NG_TRY((gemm_simt<float, true, false>(ss, R, D, R, h->Amat, R, h->J, h->ldw, EpiStore<float>{Wn, h->ldw, 1.f})));
     // B.3.1, gated on the device flag (no host synchronisation)
     const int ks = gemm_simt_splits(D, h->kl_splits);
     NG_TRY((gemm_simt<float, true, true>(ss, R, R, D, Wn, h->ldw, Wn, h->ldw,
@@ -957,7 +949,7 @@ ng_status ngsgd_get_state(ngsgd_t h, ngsgd_state_host* out) {
   out->rank = R;
   out->t = h->t;
   out->initialized = h->initialized ? 1 : 0;
-  int flags[4];
+  int flags[8];
   NG_CUDA_TRY(cudaMemcpy(flags, h->flags, sizeof(flags), cudaMemcpyDeviceToHost));
   std::vector<double> ds(1 + 2 * std::max(R, 1));
   NG_CUDA_TRY(cudaMemcpy(ds.data(), h->dstate, sizeof(double) * ds.size(), cudaMemcpyDeviceToHost));
@@ -970,6 +962,7 @@ ng_status ngsgd_get_state(ngsgd_t h, ngsgd_state_host* out) {
   out->last_floored = h->last_updated ? flags[0] : 0;
   out->last_reorth_checked = h->last_updated ? flags[1] : 0;
   out->last_reorthogonalized = h->last_updated ? flags[2] : 0;
+  out->last_jacobi_sweeps = h->last_updated ? flags[4] : 0;
   return status_from_flags((uint32_t)flags[3], "ngsgd_get_state");
 }
 
@@ -996,7 +989,7 @@ ng_status ngsgd_set_state(ngsgd_t h, const ngsgd_state_host* in) {
     double rho = in->rho;
     NG_CUDA_TRY(cudaMemcpy(h->dstate, &rho, sizeof(double), cudaMemcpyHostToDevice));
   }
-  NG_CUDA_TRY(cudaMemset(h->flags, 0, sizeof(int) * 4));
+  NG_CUDA_TRY(cudaMemset(h->flags, 0, sizeof(int) * 8));
   h->cur = 0;
   h->t = in->t;
   h->initialized = in->initialized != 0;

@@ -35,7 +35,7 @@ struct ngsgd_ctx {
   float* p = nullptr;       // max_rows
   double* sums = nullptr;   // [0] tr(X X^T)  [1] sum_i p_i
   float* gamma = nullptr;   // [1]
-  int* flags = nullptr;     // [0] floored [1] reorth check [2] repaired [3] error bits
+  int* flags = nullptr;     // [0] floored [1] reorth check [2] repaired [3] error bits [4] sweeps
   // pinned host mirror for the (one-time) initialisation sync
   double* h_scalar = nullptr;
   // side stream for the refresh (Z_t eigensolve, W_{t+1}); joined before the next use
