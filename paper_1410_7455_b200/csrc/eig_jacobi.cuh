@@ -171,30 +171,46 @@ __device__ void eig_sort_desc(const double* A, int lda, const double* Vt, int ld
 namespace ng {
 
 // ---------------------------------------------------------------------------------------
-// Lean shared-memory variant for the per-update R x R refresh (R <= 112): the pair table of
-// every round and the list of 2x2 blocks are precomputed once, eigenvector rows are
-// rotated warp-per-pair with contiguous, conflict-free accesses, and warp-uniform skips
-// drop converged pairs.  Same algorithm (cyclic round-robin Jacobi, FP32 angle -> exactly
-// orthogonal FP64 rotation) and stopping rule as jacobi_eig.
+// Lean shared-memory variant for the per-update R x R refresh (R <= 112), templated on
+// the element type (double in the FP32 path, float in the TF32 path -- the paper ran
+// this eigendecomposition in single precision).  The pair table of every round
+// and the list of 2x2 blocks are precomputed once, eigenvector rows are rotated with
+// contiguous, conflict-free accesses over all threads, warp-uniform skips drop converged
+// pairs.  Rotation test without square roots:  a_pq^2 > tol^2 |a_pp a_qq|  and
+// a_pq^2 > floor^2.  The angle comes from FP32 and is turned into an exactly orthogonal
+// rotation (c = rsqrt(1 + t^2), s = t c) in T.  Stopping: a sweep with no rotation, or a
+// sweep whose largest relative off-diagonal was below sqrt(tol) (the rotations of that
+// sweep leave O(tol) behind: Jacobi converges quadratically).
 //   A: n x n, row stride lda (shared);  Vt: n x n, row stride ldv (shared)
 //   ptab: (npad-1) * m uint16 pairs (p | q << 8);  blk: m(m+1)/2 uint16 (ka | kb << 8)
 // ---------------------------------------------------------------------------------------
+template <typename T>
 struct JacobiSmem {
   uint16_t* ptab;
   uint16_t* blk;
-  double* c;
-  double* s;
+  T* c;
+  T* s;
   int* nrot;
+  float* offmax;
 };
 
-__device__ int jacobi_eig_smem(double* __restrict__ A, int lda, double* __restrict__ Vt, int ldv, int n,
-                               JacobiSmem sc, int max_sweeps, double abs_floor, double rel_tol) {
+template <typename T>
+__device__ __forceinline__ T rsqrt_t(T x);
+template <>
+__device__ __forceinline__ double rsqrt_t<double>(double x) { return rsqrt(x); }
+template <>
+__device__ __forceinline__ float rsqrt_t<float>(float x) { return rsqrtf(x); }
+
+template <typename T>
+__device__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __restrict__ Vt, int ldv, int n, JacobiSmem<T> sc,
+                               int max_sweeps, double abs_floor, double rel_tol) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
   const int npad = n + (n & 1);
   const int m = npad / 2;
   const int rounds = npad - 1;
   const int nblk = m * (m + 1) / 2;
+  const T tol2 = (T)(rel_tol * rel_tol), flo2 = (T)(abs_floor * abs_floor);
+  const float stop_ratio = (float)sqrt(rel_tol);
   for (int idx = tid; idx < rounds * m; idx += nt) {
     const int r = idx / m, k = idx % m;
     int p, q;
@@ -203,41 +219,37 @@ __device__ int jacobi_eig_smem(double* __restrict__ A, int lda, double* __restri
   }
   for (int idx = tid; idx < m * m; idx += nt) {
     const int ka = idx % m, kb = idx / m;
-    if (ka <= kb) {
-      const int pos = kb * (kb + 1) / 2 + ka;
-      sc.blk[pos] = (uint16_t)(ka | (kb << 8));
-    }
+    if (ka <= kb) sc.blk[kb * (kb + 1) / 2 + ka] = (uint16_t)(ka | (kb << 8));
   }
   for (int idx = tid; idx < n * n; idx += nt) {
     const int i = idx / n, j = idx % n;
-    Vt[i * ldv + j] = (i == j) ? 1.0 : 0.0;
+    Vt[i * ldv + j] = (i == j) ? T(1) : T(0);
   }
   __syncthreads();
   if (n <= 1) return 0;
+  const float inv_n = 1.f / (float)n;
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
-    if (tid == 0) *sc.nrot = 0;
+    if (tid == 0) { *sc.nrot = 0; *sc.offmax = 0.f; }
     __syncthreads();
     for (int round = 0; round < rounds; ++round) {
       const uint16_t* pr = sc.ptab + round * m;
       if (tid < m) {
         const int k = tid;
         const int p = pr[k] & 0xFF, q = pr[k] >> 8;
-        double c = 1.0, s = 0.0;
+        T c = T(1), s = T(0);
         if (q < n) {
-          const double app = A[p * lda + p], aqq = A[q * lda + q], apq = A[p * lda + q];
-          const double thr = fmax(rel_tol * sqrt(fabs(app * aqq)), abs_floor);
-          if (fabs(apq) > thr) {
-            const double thd = (aqq - app) / (2.0 * apq);
+          const T app = A[p * lda + p], aqq = A[q * lda + q], apq = A[p * lda + q];
+          const T apq2 = apq * apq, dd = fabs(app * aqq);
+          if (apq2 > tol2 * dd && apq2 > flo2) {
+            const float ratio = (float)(apq2 / dd);
+            atomicMax(reinterpret_cast<int*>(sc.offmax), __float_as_int(ratio));   // ratio >= 0
+            const float th = (float)(aqq - app) / (2.f * (float)apq);
             float tf;
-            if (fabs(thd) > 1e18) {
-              tf = (float)(0.5 / thd);
-            } else {
-              const float th = (float)thd;
-              tf = copysignf(1.f, th) / (fabsf(th) + sqrtf(fmaf(th, th, 1.f)));
-            }
-            const double t = (double)tf;
-            c = rsqrt(fma(t, t, 1.0));
+            if (!(fabsf(th) < 1e18f)) tf = 0.5f / th;
+            else tf = copysignf(1.f, th) / (fabsf(th) + sqrtf(fmaf(th, th, 1.f)));
+            const T t = (T)tf;
+            c = rsqrt_t<T>(t * t + T(1));
             s = t * c;
             atomicAdd(sc.nrot, 1);
           }
@@ -250,53 +262,53 @@ __device__ int jacobi_eig_smem(double* __restrict__ A, int lda, double* __restri
       for (int b = tid; b < nblk; b += nt) {
         const uint16_t kk = sc.blk[b];
         const int ka = kk & 0xFF, kb = kk >> 8;
-        const double s1 = sc.s[ka], s2 = sc.s[kb];
-        if (s1 == 0.0 && s2 == 0.0) continue;
-        const double c1 = sc.c[ka], c2 = sc.c[kb];
+        const T s1 = sc.s[ka], s2 = sc.s[kb];
+        if (s1 == T(0) && s2 == T(0)) continue;
+        const T c1 = sc.c[ka], c2 = sc.c[kb];
         const int p1 = pr[ka] & 0xFF, q1 = pr[ka] >> 8, p2 = pr[kb] & 0xFF, q2 = pr[kb] >> 8;
         if (ka == kb) {
-          const double a = A[p1 * lda + p1], d = A[q1 * lda + q1], bb = A[p1 * lda + q1];
-          const double cc = c1 * c1, ss = s1 * s1, cs = c1 * s1;
-          const double bn = (cc - ss) * bb + cs * (a - d);
-          A[p1 * lda + p1] = cc * a - 2.0 * cs * bb + ss * d;
-          A[q1 * lda + q1] = ss * a + 2.0 * cs * bb + cc * d;
+          const T a = A[p1 * lda + p1], d = A[q1 * lda + q1], bb = A[p1 * lda + q1];
+          const T cc = c1 * c1, ss = s1 * s1, cs = c1 * s1;
+          const T bn = (cc - ss) * bb + cs * (a - d);
+          A[p1 * lda + p1] = cc * a - T(2) * cs * bb + ss * d;
+          A[q1 * lda + q1] = ss * a + T(2) * cs * bb + cc * d;
           A[p1 * lda + q1] = bn;
           A[q1 * lda + p1] = bn;
           continue;
         }
         const bool v1 = q1 < n, v2 = q2 < n;
-        const double m00 = A[p1 * lda + p2];
-        const double m01 = v2 ? A[p1 * lda + q2] : 0.0;
-        const double m10 = v1 ? A[q1 * lda + p2] : 0.0;
-        const double m11 = (v1 && v2) ? A[q1 * lda + q2] : 0.0;
-        const double t00 = c1 * m00 - s1 * m10, t01 = c1 * m01 - s1 * m11;
-        const double t10 = s1 * m00 + c1 * m10, t11 = s1 * m01 + c1 * m11;
-        const double r00 = c2 * t00 - s2 * t01, r01 = s2 * t00 + c2 * t01;
-        const double r10 = c2 * t10 - s2 * t11, r11 = s2 * t10 + c2 * t11;
+        const T m00 = A[p1 * lda + p2];
+        const T m01 = v2 ? A[p1 * lda + q2] : T(0);
+        const T m10 = v1 ? A[q1 * lda + p2] : T(0);
+        const T m11 = (v1 && v2) ? A[q1 * lda + q2] : T(0);
+        const T t00 = c1 * m00 - s1 * m10, t01 = c1 * m01 - s1 * m11;
+        const T t10 = s1 * m00 + c1 * m10, t11 = s1 * m01 + c1 * m11;
+        const T r00 = c2 * t00 - s2 * t01, r01 = s2 * t00 + c2 * t01;
+        const T r10 = c2 * t10 - s2 * t11, r11 = s2 * t10 + c2 * t11;
         A[p1 * lda + p2] = r00; A[p2 * lda + p1] = r00;
         if (v2) { A[p1 * lda + q2] = r01; A[q2 * lda + p1] = r01; }
         if (v1) { A[q1 * lda + p2] = r10; A[p2 * lda + q1] = r10; }
         if (v1 && v2) { A[q1 * lda + q2] = r11; A[q2 * lda + q1] = r11; }
       }
-      // eigenvector rows, one warp per pair, contiguous columns
-      for (int k = warp; k < m; k += nwarps) {
-        const double s = sc.s[k];
-        if (s == 0.0) continue;
-        const double c = sc.c[k];
+      // eigenvector rows: items (pair k, column j) spread over all threads
+      for (int it = tid; it < m * n; it += nt) {
+        int k = (int)(((float)it + 0.5f) * inv_n);
+        int j = it - k * n;
+        if (j < 0) { --k; j += n; } else if (j >= n) { ++k; j -= n; }
+        const T s = sc.s[k];
+        if (s == T(0)) continue;
+        const T c = sc.c[k];
         const int p = pr[k] & 0xFF, q = pr[k] >> 8;
-        double* vp = Vt + p * ldv;
-        double* vq = Vt + q * ldv;
-        for (int j = lane; j < n; j += 32) {
-          const double a = vp[j], b = vq[j];
-          vp[j] = c * a - s * b;
-          vq[j] = s * a + c * b;
-        }
+        const T a = Vt[p * ldv + j], b = Vt[q * ldv + j];
+        Vt[p * ldv + j] = c * a - s * b;
+        Vt[q * ldv + j] = s * a + c * b;
       }
       __syncthreads();
     }
     const int rot = *sc.nrot;
+    const float om = *sc.offmax;
     __syncthreads();
-    if (rot == 0) break;
+    if (rot == 0 || om < stop_ratio * stop_ratio) break;
   }
   return sweep + 1;
 }

@@ -215,6 +215,8 @@ __global__ void copy_gated_kernel(int R, int D, float* __restrict__ dst, const f
 // refresh: the R x R part of the update, one CTA, FP64
 // ------------------------------------------------------------------------------------
 
+// T = element type of the eigensolve: double (NG_FP32 path), float (NG_TF32 path).
+template <typename T>
 __global__ void __launch_bounds__(1024)
 refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
                const float* __restrict__ KL, double* __restrict__ dstate,
@@ -224,21 +226,22 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   double* sm = reinterpret_cast<double*>(ng_smem);
   const int LD = R + 1;            // odd row stride: fewer bank conflicts
   const int mp = R / 2 + 1;        // >= number of rotation pairs
-  double* Z = sm;                  // R*LD
-  double* Vt = Z + R * LD;         // R*LD
-  double* d = Vt + R * LD;         // R   old d
+  double* d = sm;                  // R   old d
   double* emh = d + R;             // R   E_t^{-1/2}
   double* dr = emh + R;            // R   d + rho
   double* c = dr + R;              // R   sorted eigenvalues
   double* dn = c + R;              // R   new d
-  double* jc = dn + R;             // mp rotation c
-  double* js = jc + mp;            // mp rotation s
-  double* red = js + mp;           // 32 reduction scratch
-  int* perm = reinterpret_cast<int*>(red + 32);   // R
+  double* red = dn + R;            // 32 reduction scratch
+  T* Z = reinterpret_cast<T*>(red + 32);   // R*LD
+  T* Vt = Z + R * LD;              // R*LD
+  T* jc = Vt + R * LD;             // mp rotation c
+  T* js = jc + mp;                 // mp rotation s
+  int* perm = reinterpret_cast<int*>(js + mp + (mp & 1));   // R
   int* nrot = perm + R;            // 1
-  uint16_t* ptab = reinterpret_cast<uint16_t*>(nrot + 2);   // (2mp-1) * mp
-  uint16_t* blk = ptab + (2 * mp) * mp;                     // mp(mp+1)/2
   int* iflag = nrot + 1;           // 1 (floored)
+  float* offmax = reinterpret_cast<float*>(nrot + 2);      // 1
+  uint16_t* ptab = reinterpret_cast<uint16_t*>(nrot + 4);  // (2mp-1) * mp
+  uint16_t* blk = ptab + (2 * mp) * mp;                     // mp(mp+1)/2
   const int tid = threadIdx.x, nt = blockDim.x;
 
   const double rho = dstate[0];
@@ -266,27 +269,28 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
     const double ls = 0.5 * ((double)L[i * R + j] + (double)L[j * R + i]);
     double z = a1 * emh[i] * ks * emh[j] + a3 * emh[i] * ls * emh[j] * (dr[i] + dr[j]);
     if (i == j) z += a2 * dr[i] * dr[i];
-    Z[i * LD + j] = z;
+    Z[i * LD + j] = (T)z;
   }
   __syncthreads();
   double zmax = 0.0;
   for (int i = tid; i < R; i += nt) zmax = fmax(zmax, fabs(Z[i * LD + i]));
   zmax = block_max(zmax, red);
   // Z = U C U^T (eqn:zt:eig:repeat)
-  JacobiSmem scr{ptab, blk, jc, js, nrot};
-  const int sweeps = jacobi_eig_smem(Z, LD, Vt, LD, R, scr, 20, 1e-15 * zmax, 1e-9);
+  JacobiSmem<T> scr{ptab, blk, jc, js, nrot, offmax};
+  const bool dbl = sizeof(T) == 8;
+  const int sweeps = jacobi_eig_smem<T>(Z, LD, Vt, LD, R, scr, 20, (dbl ? 1e-15 : 1e-9) * zmax, dbl ? 1e-9 : 1e-6);
   // descending order
   for (int i = tid; i < R; i += nt) {
-    const double li = Z[i * LD + i];
+    const double li = (double)Z[i * LD + i];
     int r = 0;
-    for (int j = 0; j < R; ++j) { const double lj = Z[j * LD + j]; r += (lj > li) || (lj == li && j < i); }
+    for (int j = 0; j < R; ++j) { const double lj = (double)Z[j * LD + j]; r += (lj > li) || (lj == li && j < i); }
     perm[r] = i;
   }
   __syncthreads();
   // floor C at (1-eta)^2 rho_t^2 (reading R13)
   const double cf = a2 * rho * rho;
   for (int r = tid; r < R; r += nt) {
-    double cr = Z[perm[r] * LD + perm[r]];
+    double cr = (double)Z[perm[r] * LD + perm[r]];
     if (cr < cf) { cr = cf; atomicOr(iflag, 1); }
     c[r] = cr;
   }
@@ -308,7 +312,7 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   for (int idx = tid; idx < R * R; idx += nt) {
     const int r = idx / R, j = idx % R;
     const double en = 1.0 / (beta_new / dn[r] + 1.0);
-    Amat[idx] = (float)((eta / N) * sqrt(en) / sqrt(c[r]) * Vt[perm[r] * LD + j] * emh[j]);
+    Amat[idx] = (float)((eta / N) * sqrt(en) / sqrt(c[r]) * (double)Vt[perm[r] * LD + j] * emh[j]);
   }
   // row scale of B_t with the OLD d, rho
   for (int k = tid; k < R; k += nt) svec[k] = (float)((N * (1.0 - eta) / eta) * dr[k]);
@@ -518,10 +522,10 @@ __global__ void passthrough_kernel(int n, float* p, float* p_out, float* g, floa
 // host side
 // ------------------------------------------------------------------------------------
 
-static size_t refresh_smem_bytes(int R) {
+static size_t refresh_smem_bytes(int R, size_t tsize = sizeof(double)) {
   const int mp = R / 2 + 1;
-  return sizeof(double) * (2 * (size_t)R * (R + 1) + 5 * R + 2 * mp + 32) + sizeof(int) * (R + 2) +
-         sizeof(uint16_t) * (2 * mp * mp + mp * (mp + 1) / 2) + 64;
+  return sizeof(double) * (5 * (size_t)R + 32) + tsize * (2 * (size_t)R * (R + 1) + 2 * mp + 2) +
+         sizeof(int) * (R + 4) + sizeof(uint16_t) * (2 * mp * mp + mp * (mp + 1) / 2) + 64;
 }
 static size_t reorth_smem_bytes(int R) { return sizeof(double) * (2 * R * R + R + 32); }
 
@@ -536,8 +540,10 @@ static ng_status dalloc(T** p, size_t count) {
 static ng_status set_kernel_attrs() {
   static bool done = false;
   if (done) return NG_OK;
-  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)refresh_smem_bytes(kMaxRank)));
+  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)refresh_smem_bytes(kMaxRank, sizeof(double))));
+  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)refresh_smem_bytes(kMaxRank, sizeof(float))));
   NG_CUDA_TRY(cudaFuncSetAttribute(reorth_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)reorth_smem_bytes(kMaxRank)));
   NG_CUDA_TRY(cudaFuncSetAttribute(apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -837,9 +843,14 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
     cudaStream_t ss = h->side;
     {
       ProfScope pe(NG_PROF_NG_EIG, ss, 0.0, 0.0);
-      refresh_kernel<<<1, 1024, refresh_smem_bytes(R), ss>>>(R, D, n, eta, (double)h->cfg.alpha,
-                                                            (double)h->cfg.epsilon, h->KL, h->dstate, h->sums,
-                                                            h->Amat, h->svec, h->flags);
+      if (h->cfg.precision == NG_TF32)
+        refresh_kernel<float><<<1, 1024, refresh_smem_bytes(R, sizeof(float)), ss>>>(
+            R, D, n, eta, (double)h->cfg.alpha, (double)h->cfg.epsilon, h->KL, h->dstate, h->sums, h->Amat, h->svec,
+            h->flags);
+      else
+        refresh_kernel<double><<<1, 1024, refresh_smem_bytes(R, sizeof(double)), ss>>>(
+            R, D, n, eta, (double)h->cfg.alpha, (double)h->cfg.epsilon, h->KL, h->dstate, h->sums, h->Amat, h->svec,
+            h->flags);
       NG_TRY(check_launch("refresh_kernel"));
     }
     ProfScope ps(NG_PROF_NG_REFRESH, ss, 2.0 * (double)R * R * D + 2.0 * R * D, 4.0 * (4.0 * R * D));
