@@ -18,6 +18,8 @@
 // A and Vt may live in shared or global memory (generic addressing).
 #pragma once
 
+#include <type_traits>
+
 #include "ng_common.cuh"
 
 namespace ng {
@@ -181,13 +183,12 @@ namespace ng {
 // rotation (c = rsqrt(1 + t^2), s = t c) in T.  Stopping: a sweep with no rotation, or a
 // sweep whose largest relative off-diagonal was below sqrt(tol) (the rotations of that
 // sweep leave O(tol) behind: Jacobi converges quadratically).
-//   A: n x n, row stride lda (shared);  Vt: n x n, row stride ldv (shared)
-//   ptab: (npad-1) * m uint16 pairs (p | q << 8);  blk: m(m+1)/2 uint16 (ka | kb << 8)
+//   A: n x n, row stride lda (shared);  Vt: n x n, row stride ldv (shared, 16-byte
+//   aligned rows: ldv * sizeof(T) % 16 == 0).  Pairs of round r come from the circle
+//   method by arithmetic; each thread's <= 2 blocks (ka <= kb) are decoded once.
 // ---------------------------------------------------------------------------------------
 template <typename T>
 struct JacobiSmem {
-  uint16_t* ptab;
-  uint16_t* blk;
   T* c;
   T* s;
   int* nrot;
@@ -201,42 +202,54 @@ __device__ __forceinline__ double rsqrt_t<double>(double x) { return rsqrt(x); }
 template <>
 __device__ __forceinline__ float rsqrt_t<float>(float x) { return rsqrtf(x); }
 
+__device__ __forceinline__ void circle_pair(int r, int k, int m1, int& p, int& q) {
+  if (k == 0) { p = m1; q = r; }
+  else {
+    p = r + k; if (p >= m1) p -= m1;
+    q = r - k; if (q < 0) q += m1;
+  }
+  if (p > q) { const int t = p; p = q; q = t; }
+}
+
 template <typename T>
 __device__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __restrict__ Vt, int ldv, int n, JacobiSmem<T> sc,
                                int max_sweeps, double abs_floor, double rel_tol) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+  // ldv * sizeof(T) must be a multiple of 16 (vectorised eigenvector rows)
+  constexpr int VEC = 16 / sizeof(T);
+  using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
   const int npad = n + (n & 1);
-  const int m = npad / 2;
+  const int m = npad / 2, m1 = npad - 1;
   const int rounds = npad - 1;
   const int nblk = m * (m + 1) / 2;
   const T tol2 = (T)(rel_tol * rel_tol), flo2 = (T)(abs_floor * abs_floor);
-  const float stop_ratio = (float)sqrt(rel_tol);
-  for (int idx = tid; idx < rounds * m; idx += nt) {
-    const int r = idx / m, k = idx % m;
-    int p, q;
-    jacobi_pair(r, k, npad, p, q);
-    sc.ptab[idx] = (uint16_t)(p | (q << 8));
+  const float stop2 = (float)rel_tol;
+  // this thread's 2x2 blocks (ka <= kb), decoded once
+  int bka[2], bkb[2], nb = 0;
+  for (int bb = tid; bb < nblk && nb < 2; bb += nt) {
+    int kb = (int)((sqrtf(8.f * bb + 1.f) - 1.f) * 0.5f);
+    while (kb * (kb + 1) / 2 > bb) --kb;
+    while ((kb + 1) * (kb + 2) / 2 <= bb) ++kb;
+    bka[nb] = bb - kb * (kb + 1) / 2;
+    bkb[nb] = kb;
+    ++nb;
   }
-  for (int idx = tid; idx < m * m; idx += nt) {
-    const int ka = idx % m, kb = idx / m;
-    if (ka <= kb) sc.blk[kb * (kb + 1) / 2 + ka] = (uint16_t)(ka | (kb << 8));
-  }
-  for (int idx = tid; idx < n * n; idx += nt) {
-    const int i = idx / n, j = idx % n;
-    Vt[i * ldv + j] = (i == j) ? T(1) : T(0);
+  for (int idx = tid; idx < n * ldv; idx += nt) {
+    const int i = idx / ldv, j = idx % ldv;
+    Vt[idx] = (i == j) ? T(1) : T(0);
   }
   __syncthreads();
   if (n <= 1) return 0;
-  const float inv_n = 1.f / (float)n;
+  const int nvec = (n + VEC - 1) / VEC;   // vectors per eigenvector row
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
     if (tid == 0) { *sc.nrot = 0; *sc.offmax = 0.f; }
     __syncthreads();
     for (int round = 0; round < rounds; ++round) {
-      const uint16_t* pr = sc.ptab + round * m;
       if (tid < m) {
         const int k = tid;
-        const int p = pr[k] & 0xFF, q = pr[k] >> 8;
+        int p, q;
+        circle_pair(round, k, m1, p, q);
         T c = T(1), s = T(0);
         if (q < n) {
           const T app = A[p * lda + p], aqq = A[q * lda + q], apq = A[p * lda + q];
@@ -259,13 +272,14 @@ __device__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __restrict__ Vt, i
       }
       __syncthreads();
       // A' = J^T A J, 2x2 blocks (ka <= kb), mirrored
-      for (int b = tid; b < nblk; b += nt) {
-        const uint16_t kk = sc.blk[b];
-        const int ka = kk & 0xFF, kb = kk >> 8;
+      for (int i = 0; i < nb; ++i) {
+        const int ka = bka[i], kb = bkb[i];
         const T s1 = sc.s[ka], s2 = sc.s[kb];
         if (s1 == T(0) && s2 == T(0)) continue;
         const T c1 = sc.c[ka], c2 = sc.c[kb];
-        const int p1 = pr[ka] & 0xFF, q1 = pr[ka] >> 8, p2 = pr[kb] & 0xFF, q2 = pr[kb] >> 8;
+        int p1, q1, p2, q2;
+        circle_pair(round, ka, m1, p1, q1);
+        circle_pair(round, kb, m1, p2, q2);
         if (ka == kb) {
           const T a = A[p1 * lda + p1], d = A[q1 * lda + q1], bb = A[p1 * lda + q1];
           const T cc = c1 * c1, ss = s1 * s1, cs = c1 * s1;
@@ -290,177 +304,36 @@ __device__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __restrict__ Vt, i
         if (v1) { A[q1 * lda + p2] = r10; A[p2 * lda + q1] = r10; }
         if (v1 && v2) { A[q1 * lda + q2] = r11; A[q2 * lda + q1] = r11; }
       }
-      // eigenvector rows: items (pair k, column j) spread over all threads
-      for (int it = tid; it < m * n; it += nt) {
-        int k = (int)(((float)it + 0.5f) * inv_n);
-        int j = it - k * n;
-        if (j < 0) { --k; j += n; } else if (j >= n) { ++k; j -= n; }
+      // eigenvector rows p, q of each rotating pair: one warp per pair, VEC columns per lane
+      for (int k = warp; k < m; k += nwarps) {
         const T s = sc.s[k];
         if (s == T(0)) continue;
         const T c = sc.c[k];
-        const int p = pr[k] & 0xFF, q = pr[k] >> 8;
-        const T a = Vt[p * ldv + j], b = Vt[q * ldv + j];
-        Vt[p * ldv + j] = c * a - s * b;
-        Vt[q * ldv + j] = s * a + c * b;
+        int p, q;
+        circle_pair(round, k, m1, p, q);
+        V* vp = reinterpret_cast<V*>(Vt + p * ldv);
+        V* vq = reinterpret_cast<V*>(Vt + q * ldv);
+        for (int j = lane; j < nvec; j += 32) {
+          const V a = vp[j], b = vq[j];
+          V na, nb2;
+          if constexpr (VEC == 2) {
+            na.x = c * a.x - s * b.x; na.y = c * a.y - s * b.y;
+            nb2.x = s * a.x + c * b.x; nb2.y = s * a.y + c * b.y;
+          } else {
+            na.x = c * a.x - s * b.x; na.y = c * a.y - s * b.y; na.z = c * a.z - s * b.z; na.w = c * a.w - s * b.w;
+            nb2.x = s * a.x + c * b.x; nb2.y = s * a.y + c * b.y; nb2.z = s * a.z + c * b.z; nb2.w = s * a.w + c * b.w;
+          }
+          vp[j] = na;
+          vq[j] = nb2;
+        }
       }
       __syncthreads();
     }
     const int rot = *sc.nrot;
     const float om = *sc.offmax;
     __syncthreads();
-    if (rot == 0 || om < stop_ratio * stop_ratio) break;
+    if (rot == 0 || om < stop2) { ++sweep; break; }
   }
-  return sweep + 1;
-}
-
-}  // namespace ng
-
-namespace ng {
-
-// ---------------------------------------------------------------------------------------
-// Double-buffered variant (one barrier per round).  Every warp computes all rotations of
-// the round itself from the read-only buffer A_cur (warp-private copy of c, s), updates its
-// 2x2 blocks into A_next (every element is rewritten each round) and its eigenvector items,
-// then ONE __syncthreads ends the round.  Pairs come from the circle method by arithmetic
-// (no tables); each thread's block and eigenvector items are decoded once.  Same rotation
-// test, angle computation and stopping rule as jacobi_eig_smem.
-//   A0, A1: n x n, row stride lda; Vt: n x n, row stride ldv; wcs: nwarps * 2 * m values;
-//   ctrl: int[4] scratch.  Returns the number of sweeps; the eigenvalues are on the
-//   diagonal of *Aout on return.
-// ---------------------------------------------------------------------------------------
-constexpr int kJacMaxBlkPerThread = 2;   // m(m+1)/2 <= 2 * 1024  ->  m <= 63
-constexpr int kJacMaxVtPerThread = 7;    // m * n <= 7 * 1024     ->  n <= 112
-
-__device__ __forceinline__ void circle_pair(int r, int k, int m1, int& p, int& q) {
-  if (k == 0) { p = m1; q = r; }
-  else {
-    p = r + k; if (p >= m1) p -= m1;
-    q = r - k; if (q < 0) q += m1;
-  }
-  if (p > q) { const int t = p; p = q; q = t; }
-}
-
-template <typename T>
-__device__ int jacobi_eig_db(T* __restrict__ A0, T* __restrict__ A1, int lda, T* __restrict__ Vt, int ldv, int n,
-                             T* __restrict__ wcs, int* __restrict__ ctrl, int max_sweeps, double abs_floor,
-                             double rel_tol, T** Aout) {
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  const int npad = n + (n & 1), m = npad / 2, m1 = npad - 1, rounds = npad - 1;
-  const int nblk = m * (m + 1) / 2;
-  const T tol2 = (T)(rel_tol * rel_tol), flo2 = (T)(abs_floor * abs_floor);
-  const float stop2 = (float)rel_tol;   // (sqrt(rel_tol))^2
-  T* cs = wcs + warp * 2 * m;           // this warp's c[0..m), s[0..m)
-  int bka[kJacMaxBlkPerThread], bkb[kJacMaxBlkPerThread], nb = 0;
-  for (int b = tid; b < nblk && nb < kJacMaxBlkPerThread; b += nt) {
-    int kb = (int)((sqrtf(8.f * b + 1.f) - 1.f) * 0.5f);
-    while (kb * (kb + 1) / 2 > b) --kb;
-    while ((kb + 1) * (kb + 2) / 2 <= b) ++kb;
-    bka[nb] = b - kb * (kb + 1) / 2;
-    bkb[nb] = kb;
-    ++nb;
-  }
-  int vk[kJacMaxVtPerThread], vj[kJacMaxVtPerThread], nv = 0;
-  for (int it = tid; it < m * n && nv < kJacMaxVtPerThread; it += nt) { vk[nv] = it / n; vj[nv] = it % n; ++nv; }
-  for (int idx = tid; idx < n * n; idx += nt) {
-    const int i = idx / n, j = idx % n;
-    Vt[i * ldv + j] = (i == j) ? T(1) : T(0);
-  }
-  if (tid == 0) { ctrl[0] = 0; ctrl[1] = 0; }
-  __syncthreads();
-  T* Ac = A0;
-  T* An = A1;
-  int sweep = 0;
-  if (n > 1) {
-    for (; sweep < max_sweeps; ++sweep) {
-      int nrot = 0;
-      float offmax = 0.f;
-      for (int r = 0; r < rounds; ++r) {
-        // ---- every warp: all rotations of this round from the read-only A_cur
-        for (int k = lane; k < m; k += 32) {
-          int p, q;
-          circle_pair(r, k, m1, p, q);
-          T c = T(1), s = T(0);
-          if (q < n) {
-            const T app = Ac[p * lda + p], aqq = Ac[q * lda + q], apq = Ac[p * lda + q];
-            const T apq2 = apq * apq, dd = fabs(app * aqq);
-            if (apq2 > tol2 * dd && apq2 > flo2) {
-              offmax = fmaxf(offmax, (float)(apq2 / dd));
-              ++nrot;
-              const float th = (float)(aqq - app) / (2.f * (float)apq);
-              float tf;
-              if (!(fabsf(th) < 1e18f)) tf = 0.5f / th;
-              else tf = copysignf(1.f, th) / (fabsf(th) + sqrtf(fmaf(th, th, 1.f)));
-              const T t = (T)tf;
-              c = rsqrt_t<T>(t * t + T(1));
-              s = t * c;
-            }
-          }
-          cs[k] = c;
-          cs[m + k] = s;
-        }
-        __syncwarp();
-        // ---- 2x2 blocks: A_next[P,Q] = G_P^T A_cur[P,Q] G_Q (mirrored)
-        for (int i = 0; i < nb; ++i) {
-          const int ka = bka[i], kb = bkb[i];
-          int p1, q1, p2, q2;
-          circle_pair(r, ka, m1, p1, q1);
-          circle_pair(r, kb, m1, p2, q2);
-          const T c1 = cs[ka], s1 = cs[m + ka], c2 = cs[kb], s2 = cs[m + kb];
-          const bool v1 = q1 < n, v2 = q2 < n;
-          if (ka == kb) {
-            const T a = Ac[p1 * lda + p1];
-            if (!v1) { An[p1 * lda + p1] = a; continue; }
-            const T d = Ac[q1 * lda + q1], bb = Ac[p1 * lda + q1];
-            const T cc = c1 * c1, ss = s1 * s1, csx = c1 * s1;
-            const T bn = (cc - ss) * bb + csx * (a - d);
-            An[p1 * lda + p1] = cc * a - T(2) * csx * bb + ss * d;
-            An[q1 * lda + q1] = ss * a + T(2) * csx * bb + cc * d;
-            An[p1 * lda + q1] = bn;
-            An[q1 * lda + p1] = bn;
-            continue;
-          }
-          const T m00 = Ac[p1 * lda + p2];
-          const T m01 = v2 ? Ac[p1 * lda + q2] : T(0);
-          const T m10 = v1 ? Ac[q1 * lda + p2] : T(0);
-          const T m11 = (v1 && v2) ? Ac[q1 * lda + q2] : T(0);
-          const T t00 = c1 * m00 - s1 * m10, t01 = c1 * m01 - s1 * m11;
-          const T t10 = s1 * m00 + c1 * m10, t11 = s1 * m01 + c1 * m11;
-          const T r00 = c2 * t00 - s2 * t01, r01 = s2 * t00 + c2 * t01;
-          const T r10 = c2 * t10 - s2 * t11, r11 = s2 * t10 + c2 * t11;
-          An[p1 * lda + p2] = r00; An[p2 * lda + p1] = r00;
-          if (v2) { An[p1 * lda + q2] = r01; An[q2 * lda + p1] = r01; }
-          if (v1) { An[q1 * lda + p2] = r10; An[p2 * lda + q1] = r10; }
-          if (v1 && v2) { An[q1 * lda + q2] = r11; An[q2 * lda + q1] = r11; }
-        }
-        // ---- eigenvector rows
-        for (int i = 0; i < nv; ++i) {
-          const int k = vk[i], j = vj[i];
-          const T s = cs[m + k];
-          if (s == T(0)) continue;
-          const T c = cs[k];
-          int p, q;
-          circle_pair(r, k, m1, p, q);
-          const T a = Vt[p * ldv + j], b = Vt[q * ldv + j];
-          Vt[p * ldv + j] = c * a - s * b;
-          Vt[q * ldv + j] = s * a + c * b;
-        }
-        __syncthreads();
-        T* tmp = Ac; Ac = An; An = tmp;
-      }
-      // every warp counted the same rotations; warp 0 decides
-      if (warp == 0) {
-        nrot = warp_sum(nrot);
-        offmax = warp_max(offmax);
-        if (lane == 0) { ctrl[0] = nrot; ctrl[1] = __float_as_int(offmax); }
-      }
-      __syncthreads();
-      const int rot = ctrl[0];
-      const float om = __int_as_float(ctrl[1]);
-      __syncthreads();
-      if (rot == 0 || om < stop2) { ++sweep; break; }
-    }
-  }
-  *Aout = Ac;
   return sweep;
 }
 

@@ -216,8 +216,7 @@ __global__ void copy_gated_kernel(int R, int D, float* __restrict__ dst, const f
 // ------------------------------------------------------------------------------------
 
 // T = element type of the eigensolve: double (NG_FP32 path), float (NG_TF32 path).
-// DB = double-buffered one-barrier-per-round Jacobi (when it fits in shared memory).
-template <typename T, bool DB>
+template <typename T>
 __global__ void __launch_bounds__(1024)
 refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
                const float* __restrict__ KL, double* __restrict__ dstate,
@@ -225,27 +224,23 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
                float* __restrict__ svec, int* __restrict__ flags) {
   extern __shared__ __align__(16) unsigned char ng_smem[];
   double* sm = reinterpret_cast<double*>(ng_smem);
-  const int LD = R + 1;            // odd row stride: fewer bank conflicts
-  const int mp = R / 2 + 1;        // >= number of rotation pairs
-  double* d = sm;                  // R   old d
-  double* emh = d + R;             // R   E_t^{-1/2}
-  double* dr = emh + R;            // R   d + rho
-  double* c = dr + R;              // R   sorted eigenvalues
-  double* dn = c + R;              // R   new d
-  double* red = dn + R;            // 32 reduction scratch
-  T* Z = reinterpret_cast<T*>(red + 32);   // R*LD
-  T* Vt = Z + R * LD;              // R*LD
-  T* Z2 = Vt + R * LD;             // R*LD (DB only)
-  T* jc = DB ? Z2 + R * LD : Z2;   // DB: 32 warps x 2 x mp;  else: mp rotation c
-  T* js = jc + mp;                 // mp rotation s (non-DB)
-  T* tail = DB ? jc + 64 * mp : js + mp;
-  int* perm = reinterpret_cast<int*>(tail + 2);             // R
-  int* nrot = perm + R;            // 1 (+1 spare)
-  int* iflag = nrot + 1;           // 1 (floored)
-  float* offmax = reinterpret_cast<float*>(nrot + 2);      // 1
-  int* ctrl = nrot + 4;            // 4
-  uint16_t* ptab = reinterpret_cast<uint16_t*>(nrot + 8);  // (2mp-1) * mp      (non-DB)
-  uint16_t* blk = ptab + (2 * mp) * mp;                     // mp(mp+1)/2        (non-DB)
+  const int LD = R + 1;                 // odd row stride of Z: fewer bank conflicts
+  const int LDV = (R + 3) / 4 * 4;      // eigenvector rows: 16-byte vectors
+  const int mp = R / 2 + 1;             // >= number of rotation pairs
+  double* d = sm;                       // R   old d
+  double* emh = d + R;                  // R   E_t^{-1/2}
+  double* dr = emh + R;                 // R   d + rho
+  double* c = dr + R;                   // R   sorted eigenvalues
+  double* dn = c + R;                   // R   new d
+  double* red = dn + R;                 // 32 reduction scratch
+  T* Z = reinterpret_cast<T*>(red + 32);                                    // R*LD
+  T* Vt = reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(Z + R * LD) + 15) & ~uintptr_t(15));   // R*LDV
+  T* jc = Vt + R * LDV;                 // mp rotation c
+  T* js = jc + mp;                      // mp rotation s
+  int* perm = reinterpret_cast<int*>(js + mp + 2);   // R
+  int* nrot = perm + R;                 // 1
+  int* iflag = nrot + 1;                // 1 (floored)
+  float* offmax = reinterpret_cast<float*>(nrot + 2);   // 1
   const int tid = threadIdx.x, nt = blockDim.x;
 
   const double rho = dstate[0];
@@ -281,16 +276,8 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   zmax = block_max(zmax, red);
   // Z = U C U^T (eqn:zt:eig:repeat)
   const bool dbl = sizeof(T) == 8;
-  int sweeps;
-  if (DB) {
-    T* Zout = Z;
-    sweeps = jacobi_eig_db<T>(Z, Z2, LD, Vt, LD, R, jc, ctrl, 20, (dbl ? 1e-15 : 1e-9) * zmax, dbl ? 1e-9 : 1e-6,
-                              &Zout);
-    Z = Zout;
-  } else {
-    JacobiSmem<T> scr{ptab, blk, jc, js, nrot, offmax};
-    sweeps = jacobi_eig_smem<T>(Z, LD, Vt, LD, R, scr, 20, (dbl ? 1e-15 : 1e-9) * zmax, dbl ? 1e-9 : 1e-6);
-  }
+  JacobiSmem<T> scr{jc, js, nrot, offmax};
+  const int sweeps = jacobi_eig_smem<T>(Z, LD, Vt, LDV, R, scr, 20, (dbl ? 1e-15 : 1e-9) * zmax, dbl ? 1e-9 : 1e-6);
   // descending order
   for (int i = tid; i < R; i += nt) {
     const double li = (double)Z[i * LD + i];
@@ -324,7 +311,7 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   for (int idx = tid; idx < R * R; idx += nt) {
     const int r = idx / R, j = idx % R;
     const double en = 1.0 / (beta_new / dn[r] + 1.0);
-    Amat[idx] = (float)((eta / N) * sqrt(en) / sqrt(c[r]) * (double)Vt[perm[r] * LD + j] * emh[j]);
+    Amat[idx] = (float)((eta / N) * sqrt(en) / sqrt(c[r]) * (double)Vt[perm[r] * LDV + j] * emh[j]);
   }
   // row scale of B_t with the OLD d, rho
   for (int k = tid; k < R; k += nt) svec[k] = (float)((N * (1.0 - eta) / eta) * dr[k]);
@@ -534,14 +521,11 @@ __global__ void passthrough_kernel(int n, float* p, float* p_out, float* g, floa
 // host side
 // ------------------------------------------------------------------------------------
 
-static size_t refresh_smem_bytes(int R, size_t tsize, bool db) {
+static size_t refresh_smem_bytes(int R, size_t tsize) {
   const int mp = R / 2 + 1;
-  const size_t tcount = db ? (3 * (size_t)R * (R + 1) + 64 * mp + 2) : (2 * (size_t)R * (R + 1) + 2 * mp + 2);
-  return sizeof(double) * (5 * (size_t)R + 32) + tsize * tcount + sizeof(int) * (R + 8) +
-         (db ? 0 : sizeof(uint16_t) * (2 * mp * mp + mp * (mp + 1) / 2)) + 64;
+  const size_t tcount = (size_t)R * (R + 1) + (size_t)R * ((R + 3) / 4 * 4) + 2 * mp + 2 + 16 / tsize;
+  return sizeof(double) * (5 * (size_t)R + 32) + tsize * tcount + sizeof(int) * (R + 4) + 64;
 }
-constexpr size_t kMaxSmem = 227 * 1024;
-static bool refresh_db_fits(int R, size_t tsize) { return refresh_smem_bytes(R, tsize, true) <= kMaxSmem; }
 static size_t reorth_smem_bytes(int R) { return sizeof(double) * (2 * R * R + R + 32); }
 
 template <typename T>
@@ -555,14 +539,10 @@ static ng_status dalloc(T** p, size_t count) {
 static ng_status set_kernel_attrs() {
   static bool done = false;
   if (done) return NG_OK;
-  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)refresh_smem_bytes(kMaxRank, sizeof(double), false)));
-  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)refresh_smem_bytes(kMaxRank, sizeof(float), false)));
-  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kMaxSmem));
-  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kMaxSmem));
+  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)refresh_smem_bytes(kMaxRank, sizeof(double))));
+  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)refresh_smem_bytes(kMaxRank, sizeof(float))));
   NG_CUDA_TRY(cudaFuncSetAttribute(reorth_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)reorth_smem_bytes(kMaxRank)));
   NG_CUDA_TRY(cudaFuncSetAttribute(apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -863,21 +843,12 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
     {
       ProfScope pe(NG_PROF_NG_EIG, ss, 0.0, 0.0);
       const double a_ = (double)h->cfg.alpha, e_ = (double)h->cfg.epsilon;
-      if (h->cfg.precision == NG_TF32) {
-        if (refresh_db_fits(R, sizeof(float)))
-          refresh_kernel<float, true><<<1, 1024, refresh_smem_bytes(R, sizeof(float), true), ss>>>(
-              R, D, n, eta, a_, e_, h->KL, h->dstate, h->sums, h->Amat, h->svec, h->flags);
-        else
-          refresh_kernel<float, false><<<1, 1024, refresh_smem_bytes(R, sizeof(float), false), ss>>>(
-              R, D, n, eta, a_, e_, h->KL, h->dstate, h->sums, h->Amat, h->svec, h->flags);
-      } else {
-        if (refresh_db_fits(R, sizeof(double)))
-          refresh_kernel<double, true><<<1, 1024, refresh_smem_bytes(R, sizeof(double), true), ss>>>(
-              R, D, n, eta, a_, e_, h->KL, h->dstate, h->sums, h->Amat, h->svec, h->flags);
-        else
-          refresh_kernel<double, false><<<1, 1024, refresh_smem_bytes(R, sizeof(double), false), ss>>>(
-              R, D, n, eta, a_, e_, h->KL, h->dstate, h->sums, h->Amat, h->svec, h->flags);
-      }
+      if (h->cfg.precision == NG_TF32)
+        refresh_kernel<float><<<1, 1024, refresh_smem_bytes(R, sizeof(float)), ss>>>(
+            R, D, n, eta, a_, e_, h->KL, h->dstate, h->sums, h->Amat, h->svec, h->flags);
+      else
+        refresh_kernel<double><<<1, 1024, refresh_smem_bytes(R, sizeof(double)), ss>>>(
+            R, D, n, eta, a_, e_, h->KL, h->dstate, h->sums, h->Amat, h->svec, h->flags);
       NG_TRY(check_launch("refresh_kernel"));
     }
     ProfScope ps(NG_PROF_NG_REFRESH, ss, 2.0 * (double)R * R * D + 2.0 * R * D, 4.0 * (4.0 * R * D));
