@@ -212,7 +212,7 @@ __device__ __forceinline__ void circle_pair(int r, int k, int m1, int& p, int& q
 }
 
 template <typename T>
-__device__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __restrict__ Vt, int ldv, int n, JacobiSmem<T> sc,
+__device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __restrict__ Vt, int ldv, int n, JacobiSmem<T> sc,
                                int max_sweeps, double abs_floor, double rel_tol) {
   // ldv * sizeof(T) must be a multiple of 16 (vectorised eigenvector rows)
   constexpr int VEC = 16 / sizeof(T);

@@ -234,7 +234,8 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   double* dn = c + R;                   // R   new d
   double* red = dn + R;                 // 32 reduction scratch
   T* Z = reinterpret_cast<T*>(red + 32);                                    // R*LD
-  T* Vt = reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(Z + R * LD) + 15) & ~uintptr_t(15));   // R*LDV
+  constexpr int kVec = 16 / sizeof(T);
+  T* Vt = Z + (R * LD + kVec - 1) / kVec * kVec;   // R*LDV, 16-byte aligned (Z is)
   T* jc = Vt + R * LDV;                 // mp rotation c
   T* js = jc + mp;                      // mp rotation s
   int* perm = reinterpret_cast<int*>(js + mp + 2);   // R
