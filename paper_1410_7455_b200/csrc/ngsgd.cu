@@ -233,7 +233,7 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   double* c = dr + R;                   // R   sorted eigenvalues
   double* dn = c + R;                   // R   new d
   double* red = dn + R;                 // 32 reduction scratch
-  T* Z = reinterpret_cast<T*>(red + 32);                                    // R*LD
+  T* Z = reinterpret_cast<T*>(red + 32 + (R & 1));                          // R*LD, 16-byte aligned
   constexpr int kVec = 16 / sizeof(T);
   T* Vt = Z + (R * LD + kVec - 1) / kVec * kVec;   // R*LDV, 16-byte aligned (Z is)
   T* jc = Vt + R * LDV;                 // mp rotation c
@@ -525,7 +525,7 @@ __global__ void passthrough_kernel(int n, float* p, float* p_out, float* g, floa
 static size_t refresh_smem_bytes(int R, size_t tsize) {
   const int mp = R / 2 + 1;
   const size_t tcount = (size_t)R * (R + 1) + (size_t)R * ((R + 3) / 4 * 4) + 2 * mp + 2 + 16 / tsize;
-  return sizeof(double) * (5 * (size_t)R + 32) + tsize * tcount + sizeof(int) * (R + 4) + 64;
+  return sizeof(double) * (5 * (size_t)R + 33) + tsize * tcount + sizeof(int) * (R + 4) + 64;
 }
 static size_t reorth_smem_bytes(int R) { return sizeof(double) * (2 * R * R + R + 32); }
 
