@@ -243,8 +243,8 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
   const int nvec = (n + VEC - 1) / VEC;   // vectors per eigenvector row
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
-    if (tid == 0) { *sc.nrot = 0; *sc.offmax = 0.f; }
-    __syncthreads();
+    int my_rot = 0;          // per-thread counters, reduced once per sweep (no atomics)
+    float my_off = 0.f;
     for (int round = 0; round < rounds; ++round) {
       if (tid < m) {
         const int k = tid;
@@ -255,8 +255,7 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
           const T app = A[p * lda + p], aqq = A[q * lda + q], apq = A[p * lda + q];
           const T apq2 = apq * apq, dd = fabs(app * aqq);
           if (apq2 > tol2 * dd && apq2 > flo2) {
-            const float ratio = (float)(apq2 / dd);
-            atomicMax(reinterpret_cast<int*>(sc.offmax), __float_as_int(ratio));   // ratio >= 0
+            my_off = fmaxf(my_off, (float)(apq2 / dd));
             const float th = (float)(aqq - app) / (2.f * (float)apq);
             float tf;
             if (!(fabsf(th) < 1e18f)) tf = 0.5f / th;
@@ -264,7 +263,7 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
             const T t = (T)tf;
             c = rsqrt_t<T>(t * t + T(1));
             s = t * c;
-            atomicAdd(sc.nrot, 1);
+            ++my_rot;
           }
         }
         sc.c[k] = c;
@@ -329,8 +328,14 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
       }
       __syncthreads();
     }
-    const int rot = *sc.nrot;
-    const float om = *sc.offmax;
+    // sweep totals (threads >= m contribute 0); reduction scratch = the c/s arrays
+    my_rot = warp_sum(my_rot);
+    my_off = warp_max(my_off);
+    if (lane == 0) { sc.nrot[warp] = my_rot; sc.offmax[warp] = my_off; }
+    __syncthreads();
+    int rot = 0;
+    float om = 0.f;
+    for (int w = 0; w < nwarps; ++w) { rot += sc.nrot[w]; om = fmaxf(om, sc.offmax[w]); }
     __syncthreads();
     if (rot == 0 || om < stop2) { ++sweep; break; }
   }
