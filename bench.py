@@ -313,7 +313,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     log(f"[rank {rank}] synthetic pool {frames_np.nbytes / 1e6:.0f} MB in {time.time() - t_gen:.1f}s")
     net = api.Nnet(CFG3["input_dim"], CFG3["num_hidden"], CFG3["hidden_dim"], CFG3["pnorm_group"],
                    CFG3["num_classes"], max_minibatch=N, precond=True, rank_in=CFG3["rank_in"],
-                   rank_out=CFG3["rank_out"], precision=precision, seed=1410)
+                   rank_out=CFG3["rank_out"], precision=precision, seed=1410,
+                   ng_overrides=None if args.update_period == 4 else {"update_period": args.update_period})
     if world > 1:
         uid = api.comm_unique_id() if rank == 0 else None
         uid = driver.broadcast_bytes(uid)
@@ -449,6 +450,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-precond-bench", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=100)
+    ap.add_argument("--update-period", type=int, default=4, help="NG J (P:1295-1297); experiments only")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank = int(os.environ.get("RANK", "0"))

@@ -256,10 +256,15 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
           const T apq2 = apq * apq, dd = fabs(app * aqq);
           if (apq2 > tol2 * dd && apq2 > flo2) {
             my_off = fmaxf(my_off, (float)(apq2 / dd));
-            const float th = (float)(aqq - app) / (2.f * (float)apq);
+            // MUFU-based angle (the FP32 angle only has to be ~1e-7 accurate)
+            const float th = __fdividef((float)(aqq - app), 2.f * (float)apq);
             float tf;
-            if (!(fabsf(th) < 1e18f)) tf = 0.5f / th;
-            else tf = copysignf(1.f, th) / (fabsf(th) + sqrtf(fmaf(th, th, 1.f)));
+            if (!(fabsf(th) < 1e18f)) {
+              tf = __fdividef(0.5f, th);
+            } else {
+              const float r2 = fmaf(th, th, 1.f);
+              tf = copysignf(__fdividef(1.f, fabsf(th) + r2 * rsqrtf(r2)), th);
+            }
             const T t = (T)tf;
             c = rsqrt_t<T>(t * t + T(1));
             s = t * c;
