@@ -110,10 +110,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// One 128 x BN output tile: rows m0.., columns n0.., k-blocks kb0 .. kb0+nkb-1.  ntile /
+// ztile are the column-tile and split indices used by the NGAPPLY / PARTIAL epilogues.
 template <int BN, bool AK, bool BKM, int EPI>
-__global__ void __launch_bounds__(128, 1)
-tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                    int K, int kb_per_split, TcEpilogue epi) {
+__device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int m0, int n0,
+                                        int kb0, int nkb, int ntile, int ztile, const TcEpilogue& epi) {
   constexpr uint32_t A_BYTES = kBM * kBK * 4, B_BYTES = BN * kBK * 4, STAGE = A_BYTES + B_BYTES;
   constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
   extern __shared__ uint8_t smem_raw[];
@@ -124,15 +125,10 @@ tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * BN;
-  const int kb_total = (K + kBK - 1) / kBK;
-  const int kb0 = blockIdx.z * kb_per_split;
-  const int kb1 = min(kb_total, kb0 + kb_per_split);
-  const int nkb = max(0, kb1 - kb0);
 
   if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmB)) : "memory");
     for (int s = 0; s < kStages; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
     mbar_init(&accum_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -158,16 +154,16 @@ tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       mbar_expect_tx(&full_bar[s], STAGE);
       const int kc = (kb0 + i) * kBK;
       if (AK) {
-        tma_load_2d(sa, &tmA, kc, m0, &full_bar[s]);
+        tma_load_2d(sa, tmA, kc, m0, &full_bar[s]);
       } else {
 #pragma unroll
-        for (int j = 0; j < kBM / 32; ++j) tma_load_2d(sa + j * 4096, &tmA, m0 + 32 * j, kc, &full_bar[s]);
+        for (int j = 0; j < kBM / 32; ++j) tma_load_2d(sa + j * 4096, tmA, m0 + 32 * j, kc, &full_bar[s]);
       }
       if (BKM) {
-        tma_load_2d(sb, &tmB, kc, n0, &full_bar[s]);
+        tma_load_2d(sb, tmB, kc, n0, &full_bar[s]);
       } else {
 #pragma unroll
-        for (int j = 0; j < BN / 32; ++j) tma_load_2d(sb + j * 4096, &tmB, n0 + 32 * j, kc, &full_bar[s]);
+        for (int j = 0; j < BN / 32; ++j) tma_load_2d(sb + j * 4096, tmB, n0 + 32 * j, kc, &full_bar[s]);
       }
     }
   } else if (warp == 1 && lane == 0) {
@@ -197,7 +193,7 @@ tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   __syncwarp();
   const int row = m0 + warp * 32 + lane;
   const float scale = (EPI == TC_EPI_AXPY) ? __ldg(epi.scale) : 0.f;
-  float* __restrict__ crow = epi.C + (EPI == TC_EPI_PARTIAL ? (int64_t)blockIdx.z * epi.zstride : 0) +
+  float* __restrict__ crow = epi.C + (EPI == TC_EPI_PARTIAL ? (int64_t)ztile * epi.zstride : 0) +
                              (int64_t)row * epi.ldc;
   float xx = 0.f, pp = 0.f;   // TC_EPI_NGAPPLY row partial sums over this tile's columns
 #pragma unroll 1
@@ -253,14 +249,41 @@ tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     }
   }
   if (EPI == TC_EPI_NGAPPLY && row < M) {
-    epi.xx[(int64_t)blockIdx.x * epi.part_ld + row] = xx;
-    epi.pp[(int64_t)blockIdx.x * epi.part_ld + row] = pp;
+    epi.xx[(int64_t)ntile * epi.part_ld + row] = xx;
+    epi.pp[(int64_t)ntile * epi.part_ld + row] = pp;
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   }
+}
+
+template <int BN, bool AK, bool BKM, int EPI>
+__global__ void __launch_bounds__(128, 1)
+tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                    int K, int kb_per_split, TcEpilogue epi) {
+  const int kb_total = (K + kBK - 1) / kBK;
+  const int kb0 = blockIdx.z * kb_per_split;
+  const int nkb = max(0, min(kb_total, kb0 + kb_per_split) - kb0);
+  tc_tile<BN, AK, BKM, EPI>(&tmA, &tmB, M, N, blockIdx.y * kBM, blockIdx.x * BN, kb0, nkb, blockIdx.x, blockIdx.z,
+                            epi);
+}
+
+// Grouped launch: problem g owns tiles [tile_begin, tile_begin + mt*nt*splits); each tile
+// (z, m, n) of it is one CTA.  Problems share BN, operand majors and epilogue kind.
+template <int BN, bool AK, bool BKM, int EPI>
+__global__ void __launch_bounds__(128, 1) tc_gemm_tf32_grouped_kernel(const __grid_constant__ TcGroup grp) {
+  int g = 0;
+  while (g + 1 < grp.count && (int)blockIdx.x >= grp.p[g + 1].tile_begin) ++g;
+  const TcProblem& P = grp.p[g];
+  const int local = (int)blockIdx.x - P.tile_begin;
+  const int nt = (P.N + BN - 1) / BN, mt = (P.M + kBM - 1) / kBM;
+  const int ntile = local % nt, mtile = (local / nt) % mt, z = local / (nt * mt);
+  const int kb_total = (P.K + kBK - 1) / kBK;
+  const int kb0 = z * P.kbps;
+  const int nkb = max(0, min(kb_total, kb0 + P.kbps) - kb0);
+  tc_tile<BN, AK, BKM, EPI>(&P.tmA, &P.tmB, P.M, P.N, mtile * kBM, ntile * BN, kb0, nkb, ntile, z, P.epi);
 }
 
 // ------------------------------------------------------------------ host side
@@ -377,6 +400,66 @@ ng_status tc_gemm_tf32(cudaStream_t st, int M, int N, int K, const float* A, int
   if (bn == 32) return dispatch_major<32>(st, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
   if (bn == 64) return dispatch_major<64>(st, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
   return dispatch_major<128>(st, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
+}
+
+template <int BN, bool AK, bool BKM, int EPI>
+ng_status launch_grouped(cudaStream_t st, const TcGroup& grp, int tiles) {
+  constexpr size_t smem = (size_t)kStages * (kBM * kBK * 4 + BN * kBK * 4) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    NG_CUDA_TRY(cudaFuncSetAttribute(tc_gemm_tf32_grouped_kernel<BN, AK, BKM, EPI>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  tc_gemm_tf32_grouped_kernel<BN, AK, BKM, EPI><<<tiles, 128, smem, st>>>(grp);
+  return check_launch("tc_gemm_tf32_grouped_kernel");
+}
+
+ng_status tc_gemm_tf32_grouped(cudaStream_t st, const TcGroupDesc* desc, int count, bool a_kmajor, bool b_kmajor,
+                               int epi_kind, int bn) {
+  NG_REQUIRE(count >= 1 && count <= kTcGroupMax, NG_EINVAL, "tc_gemm_tf32_grouped: bad problem count");
+  NG_REQUIRE(bn == 32 || bn == 64 || bn == 128, NG_EINVAL, "tc_gemm_tf32_grouped: bad bn");
+  TcGroup grp;
+  std::memset(&grp, 0, sizeof(grp));
+  grp.count = count;
+  int tiles = 0;
+  for (int g = 0; g < count; ++g) {
+    const TcGroupDesc& d = desc[g];
+    NG_REQUIRE(d.M >= 1 && d.N >= 1 && d.K >= 1, NG_ESHAPE, "tc_gemm_tf32_grouped: empty problem");
+    const int kb = ceil_div(d.K, kBK);
+    const int sp = tc_splits(d.K, d.splits);
+    NG_REQUIRE(sp == 1 || epi_kind == TC_EPI_PARTIAL, NG_EINVAL, "split-K needs the partial epilogue");
+    TcProblem& P = grp.p[g];
+    if (a_kmajor) NG_TRY(make_tmap(&P.tmA, d.A, d.K, d.M, d.lda, kBM, false));
+    else NG_TRY(make_tmap(&P.tmA, d.A, d.M, d.K, d.lda, 32, true));
+    if (b_kmajor) NG_TRY(make_tmap(&P.tmB, d.B, d.K, d.N, d.ldb, bn, false));
+    else NG_TRY(make_tmap(&P.tmB, d.B, d.N, d.K, d.ldb, 32, true));
+    P.M = d.M; P.N = d.N; P.K = d.K;
+    P.kbps = ceil_div(kb, sp);
+    P.tile_begin = tiles;
+    P.epi = d.epi;
+    if (d.splits_used) *d.splits_used = sp;
+    tiles += ceil_div(d.M, kBM) * ceil_div(d.N, bn) * sp;
+  }
+#define NG_GRP(BN_, AK_, BK_, E_) return launch_grouped<BN_, AK_, BK_, E_>(st, grp, tiles)
+#define NG_GRP_E(BN_, AK_, BK_)                                         \
+  switch (epi_kind) {                                                  \
+    case TC_EPI_STORE: NG_GRP(BN_, AK_, BK_, TC_EPI_STORE);            \
+    case TC_EPI_AXPY: NG_GRP(BN_, AK_, BK_, TC_EPI_AXPY);              \
+    case TC_EPI_NGAPPLY: NG_GRP(BN_, AK_, BK_, TC_EPI_NGAPPLY);        \
+    default: NG_GRP(BN_, AK_, BK_, TC_EPI_PARTIAL);                    \
+  }
+#define NG_GRP_M(BN_)                                                  \
+  if (a_kmajor && b_kmajor) { NG_GRP_E(BN_, true, true) }              \
+  if (a_kmajor && !b_kmajor) { NG_GRP_E(BN_, true, false) }            \
+  if (!a_kmajor && b_kmajor) { NG_GRP_E(BN_, false, true) }            \
+  NG_GRP_E(BN_, false, false)
+  if (bn == 32) { NG_GRP_M(32) }
+  if (bn == 64) { NG_GRP_M(64) }
+  NG_GRP_M(128)
+#undef NG_GRP_M
+#undef NG_GRP_E
+#undef NG_GRP
 }
 
 // Fixed-order reduction of split-K partials: C[m][n] = sum_z part[z][m][n].

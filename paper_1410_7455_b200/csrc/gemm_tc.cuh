@@ -10,6 +10,8 @@
 // the NG-SGD kernels.  This is the "TF32 tensor-core" precision mode.
 #pragma once
 
+#include <cuda.h>
+
 #include "ng_common.cuh"
 
 namespace ng {
@@ -40,6 +42,32 @@ struct TcEpilogue {
 ng_status tc_gemm_tf32(cudaStream_t st, int M, int N, int K, const float* A, int64_t lda, bool a_kmajor,
                        const float* B, int64_t ldb, bool b_kmajor, const TcEpilogue& epi, int bn = 128,
                        int splits = 1, int* splits_used = nullptr);
+
+// ---- grouped launch: several independent problems (same majors / epilogue kind / BN)
+// in ONE kernel launch; each CTA finds its problem from the tile index.
+constexpr int kTcGroupMax = 16;
+
+struct TcGroupDesc {       // host-side description of one problem
+  int M, N, K, splits;
+  const float* A; int64_t lda;
+  const float* B; int64_t ldb;
+  TcEpilogue epi;
+  int* splits_used;         // optional out
+};
+
+struct alignas(64) TcProblem {
+  CUtensorMap tmA, tmB;
+  int M, N, K, kbps, tile_begin, pad_[3];
+  TcEpilogue epi;
+};
+
+struct TcGroup {
+  TcProblem p[kTcGroupMax];
+  int count;
+};
+
+ng_status tc_gemm_tf32_grouped(cudaStream_t st, const TcGroupDesc* desc, int count, bool a_kmajor, bool b_kmajor,
+                               int epi_kind, int bn);
 
 // Split count actually used for a requested split count.
 int tc_splits(int K, int splits);

@@ -16,6 +16,7 @@
 #include <atomic>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "eig_jacobi.cuh"
 #include "gemm_simt.cuh"
@@ -703,6 +704,54 @@ ng_status ngsgd_join_impl(ngsgd_ctx* h) {
   return NG_OK;
 }
 
+// The R x R refresh (Z_t, eigendecomposition, rho', D', E', A_t), W_{t+1} = A_t B_t and
+// the gated B.3.1 repair.  They only gate this state's NEXT call, so they run on the
+// state's side stream, overlapping later work on the main stream (the other states'
+// preconditioning, the weight update, the next forward/backward).  J holds J_t, KL holds
+// K_t, L_t and sums[0] tr(X X^T) on entry (all written on the main stream before the fork).
+static ng_status launch_refresh_chain(ngsgd_ctx* h, int n, double eta) {
+  const int D = h->dim, R = h->rank;
+  cudaStream_t st = h->st;
+  float* W = h->W[h->cur];
+  NG_CUDA_TRY(cudaEventRecord(h->ev_fork, st));
+  NG_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+  cudaStream_t ss = h->side;
+  {
+    ProfScope pe(NG_PROF_NG_EIG, ss, 0.0, 0.0);
+    const double a_ = (double)h->cfg.alpha, e_ = (double)h->cfg.epsilon;
+    if (h->cfg.precision == NG_TF32)
+      refresh_kernel<float><<<1, 1024, refresh_smem_bytes(R, sizeof(float)), ss>>>(
+          R, D, n, eta, a_, e_, h->KL, h->dstate, h->sums, h->Amat, h->svec, h->flags);
+    else
+      refresh_kernel<double><<<1, 1024, refresh_smem_bytes(R, sizeof(double)), ss>>>(
+          R, D, n, eta, a_, e_, h->KL, h->dstate, h->sums, h->Amat, h->svec, h->flags);
+    NG_TRY(check_launch("refresh_kernel"));
+  }
+  ProfScope ps(NG_PROF_NG_REFRESH, ss, 2.0 * (double)R * R * D + 2.0 * R * D, 4.0 * (4.0 * R * D));
+  bscale_kernel<<<std::min(1024, ceil_div((int64_t)R * D, 256)), 256, 0, ss>>>(R, D, h->J, W, h->ldw, h->svec);
+  NG_TRY(check_launch("bscale_kernel"));
+  const int nxt = 1 - h->cur;
+  float* Wn = h->W[nxt];
+  // W_{t+1} = A_t B_t (eqn:wt1), FP32 in both modes (orthonormality of R_{t+1})
+  NG_TRY((gemm_simt<float, true, false>(ss, R, D, R, h->Amat, R, h->J, h->ldw, EpiStore<float>{Wn, h->ldw, 1.f})));
+  // B.3.1, gated on the device flag (no host synchronisation)
+  const int ks = gemm_simt_splits(D, h->kl_splits);
+  NG_TRY((gemm_simt<float, true, true>(ss, R, R, D, Wn, h->ldw, Wn, h->ldw,
+                                       EpiStoreSplit<float>{h->WWpart, R, (int64_t)R * R}, ks, h->flags + 1)));
+  reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, ss>>>(h->WW, h->WWpart, R * R, ks, R * R, h->flags + 1);
+  NG_TRY(check_launch("reduce_splits(WW)"));
+  reorth_check_kernel<<<1, 256, reorth_smem_bytes(R), ss>>>(R, h->WW, h->dstate, h->Mmat, h->flags);
+  NG_TRY(check_launch("reorth_check_kernel"));
+  NG_TRY((gemm_simt<float, true, false>(ss, R, D, R, h->Mmat, R, Wn, h->ldw, EpiStore<float>{h->J, h->ldw, 1.f},
+                                        1, h->flags + 2)));
+  copy_gated_kernel<<<std::min(1024, ceil_div((int64_t)R * D, 256)), 256, 0, ss>>>(R, D, Wn, h->J, h->ldw, h->flags + 2);
+  NG_TRY(check_launch("copy_gated_kernel"));
+  NG_CUDA_TRY(cudaEventRecord(h->ev_join, ss));
+  h->pending = true;
+  h->cur = nxt;
+  return NG_OK;
+}
+
 ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, float* gamma_out,
                                   float* p_out, int update, int* updated_out) {
   NG_REQUIRE(h != nullptr && x != nullptr, NG_EINVAL, "NULL argument");
@@ -834,50 +883,247 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
                                        h->gamma, gamma_out, h->flags);
     NG_TRY(check_launch("finalize_kernel"));
   }
-  if (upd) {
-    // The R x R refresh and W_{t+1} = A_t B_t only gate this state's NEXT call, so they
-    // run on the state's side stream, overlapping later work on the main stream (the
-    // other states' preconditioning, the weight update, the next forward/backward).
-    NG_CUDA_TRY(cudaEventRecord(h->ev_fork, st));
-    NG_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
-    cudaStream_t ss = h->side;
-    {
-      ProfScope pe(NG_PROF_NG_EIG, ss, 0.0, 0.0);
-      const double a_ = (double)h->cfg.alpha, e_ = (double)h->cfg.epsilon;
-      if (h->cfg.precision == NG_TF32)
-        refresh_kernel<float><<<1, 1024, refresh_smem_bytes(R, sizeof(float)), ss>>>(
-            R, D, n, eta, a_, e_, h->KL, h->dstate, h->sums, h->Amat, h->svec, h->flags);
-      else
-        refresh_kernel<double><<<1, 1024, refresh_smem_bytes(R, sizeof(double)), ss>>>(
-            R, D, n, eta, a_, e_, h->KL, h->dstate, h->sums, h->Amat, h->svec, h->flags);
-      NG_TRY(check_launch("refresh_kernel"));
-    }
-    ProfScope ps(NG_PROF_NG_REFRESH, ss, 2.0 * (double)R * R * D + 2.0 * R * D, 4.0 * (4.0 * R * D));
-    bscale_kernel<<<std::min(1024, ceil_div((int64_t)R * D, 256)), 256, 0, ss>>>(R, D, h->J, W, h->ldw, h->svec);
-    NG_TRY(check_launch("bscale_kernel"));
-    const int nxt = 1 - h->cur;
-    float* Wn = h->W[nxt];
-    // W_{t+1} = A_t B_t (eqn:wt1), FP32 in both modes (orthonormality of R_{t+1})
-    NG_TRY((gemm_simt<float, true, false>(ss, R, D, R, h->Amat, R, h->J, h->ldw, EpiStore<float>{Wn, h->ldw, 1.f})));
-    // B.3.1, gated on the device flag (no host synchronisation)
-    const int ks = gemm_simt_splits(D, h->kl_splits);
-    NG_TRY((gemm_simt<float, true, true>(ss, R, R, D, Wn, h->ldw, Wn, h->ldw,
-                                         EpiStoreSplit<float>{h->WWpart, R, (int64_t)R * R}, ks, h->flags + 1)));
-    reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, ss>>>(h->WW, h->WWpart, R * R, ks, R * R, h->flags + 1);
-    NG_TRY(check_launch("reduce_splits(WW)"));
-    reorth_check_kernel<<<1, 256, reorth_smem_bytes(R), ss>>>(R, h->WW, h->dstate, h->Mmat, h->flags);
-    NG_TRY(check_launch("reorth_check_kernel"));
-    NG_TRY((gemm_simt<float, true, false>(ss, R, D, R, h->Mmat, R, Wn, h->ldw, EpiStore<float>{h->J, h->ldw, 1.f},
-                                          1, h->flags + 2)));
-    copy_gated_kernel<<<std::min(1024, ceil_div((int64_t)R * D, 256)), 256, 0, ss>>>(R, D, Wn, h->J, h->ldw, h->flags + 2);
-    NG_TRY(check_launch("copy_gated_kernel"));
-    NG_CUDA_TRY(cudaEventRecord(h->ev_join, ss));
-    h->pending = true;
-    h->cur = nxt;
-  }
+  if (upd) NG_TRY(launch_refresh_chain(h, n, eta));
   h->t += 1;
   h->last_updated = upd ? 1 : 0;
   if (updated_out) *updated_out = upd ? 1 : 0;
+  return NG_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// grouped (multi-state) preconditioning: one launch per phase
+// ------------------------------------------------------------------------------------
+
+constexpr int kSegMax = 16;
+struct SegReduce {            // out[i*ldo + j] = sum_z src[z*zstride + i*lds + j], i < rows, j < cols
+  float* out[kSegMax];
+  const float* src[kSegMax];
+  int64_t ldo[kSegMax], lds[kSegMax], zstride[kSegMax];
+  int rows[kSegMax], cols[kSegMax], splits[kSegMax], block_begin[kSegMax + 1];
+  int count;
+};
+
+__global__ void __launch_bounds__(256) seg_reduce_kernel(const __grid_constant__ SegReduce sr) {
+  int g = 0;
+  while (g + 1 < sr.count && (int)blockIdx.x >= sr.block_begin[g + 1]) ++g;
+  const int64_t total = (int64_t)sr.rows[g] * sr.cols[g];
+  const int cols = sr.cols[g], sp = sr.splits[g];
+  for (int64_t i = (int64_t)(blockIdx.x - sr.block_begin[g]) * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)(sr.block_begin[g + 1] - sr.block_begin[g]) * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    const float* src = sr.src[g] + r * sr.lds[g] + c;
+    float acc = 0.f;
+    for (int z = 0; z < sp; ++z) acc += src[(int64_t)z * sr.zstride[g]];
+    sr.out[g][r * sr.ldo[g] + c] = acc;
+  }
+}
+
+struct FinalizeGroup {
+  int n[kSegMax], tiles[kSegMax];
+  const float* xxpart[kSegMax];
+  const float* ppart[kSegMax];
+  int64_t part_ld[kSegMax];
+  float* p_int[kSegMax];
+  float* p_out[kSegMax];
+  double* sums[kSegMax];
+  float* gamma_int[kSegMax];
+  float* gamma_out[kSegMax];
+  int* flags[kSegMax];
+  int count;
+};
+
+// One CTA per state: identical arithmetic to finalize_kernel.
+__global__ void __launch_bounds__(512) finalize_group_kernel(const __grid_constant__ FinalizeGroup fg) {
+  const int g = blockIdx.x;
+  __shared__ double sc[32];
+  const int n = fg.n[g], tiles = fg.tiles[g];
+  const int64_t pl = fg.part_ld[g];
+  double sxx = 0.0, spp = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    float xx = 0.f, pp = 0.f;
+    for (int t = 0; t < tiles; ++t) { xx += fg.xxpart[g][(int64_t)t * pl + i]; pp += fg.ppart[g][(int64_t)t * pl + i]; }
+    fg.p_int[g][i] = pp;
+    if (fg.p_out[g]) fg.p_out[g][i] = pp;
+    sxx += (double)xx;
+    spp += (double)pp;
+  }
+  sxx = block_sum(sxx, sc);
+  spp = block_sum(spp, sc);
+  if (threadIdx.x == 0) {
+    fg.sums[g][0] = sxx;
+    fg.sums[g][1] = spp;
+    const float gm = (spp > 0.0) ? (float)sqrt(sxx / spp) : 1.0f;
+    *fg.gamma_int[g] = gm;
+    if (fg.gamma_out[g]) *fg.gamma_out[g] = gm;
+    if (!isfinite(sxx) || !isfinite(spp)) atomicOr(reinterpret_cast<unsigned*>(fg.flags[g] + 3), kErrNonFinite);
+  }
+}
+
+static ng_status launch_seg_reduce(cudaStream_t st, SegReduce& sr) {
+  int blocks = 0;
+  for (int g = 0; g < sr.count; ++g) {
+    sr.block_begin[g] = blocks;
+    blocks += std::max(1, std::min(64, ceil_div((int64_t)sr.rows[g] * sr.cols[g], 256)));
+  }
+  sr.block_begin[sr.count] = blocks;
+  seg_reduce_kernel<<<blocks, 256, 0, st>>>(sr);
+  return check_launch("seg_reduce_kernel");
+}
+
+ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
+  NG_REQUIRE(calls != nullptr && count >= 0, NG_EINVAL, "NULL argument");
+  std::vector<int> grp;          // indices of tensor-core group members
+  std::vector<char> upd(count, 0);
+  cudaStream_t st = nullptr;
+  for (int i = 0; i < count; ++i) {
+    NgCall& c = calls[i];
+    ngsgd_ctx* h = c.h;
+    NG_REQUIRE(h != nullptr && c.x != nullptr, NG_EINVAL, "NULL argument");
+    const bool eligible = h->initialized && h->rank > 0 && h->rank <= 128 && h->cfg.precision == NG_TF32 &&
+                          (c.ld % 4) == 0 && (h->rank % 4) == 0 && (reinterpret_cast<uintptr_t>(c.x) & 15) == 0 &&
+                          c.n >= 1 && c.n <= h->max_rows && c.ld >= h->dim && (int)grp.size() < kTcGroupMax &&
+                          (grp.empty() || h->st == st);
+    if (!eligible) {           // initialisation, FP32, odd shapes: the single-state path
+      NG_TRY(ngsgd_precondition_impl(h, c.n, c.x, c.ld, c.gamma_out, c.p_out, c.update, c.updated_out));
+      continue;
+    }
+    st = h->st;
+    NG_TRY(ngsgd_join_impl(h));
+    h->last_updated = 0;
+    upd[i] = (c.update < 0) ? (h->t < h->cfg.always_update_first || (h->t % h->cfg.update_period) == 0)
+                            : (c.update != 0);
+    grp.push_back(i);
+  }
+  if (grp.empty()) return NG_OK;
+  const int G = (int)grp.size();
+  // ---- phase A: H = X W^T for every state (split-K partials), one launch
+  {
+    double flops = 0, bytes = 0;
+    int64_t total_kt = 0;
+    for (int i : grp) total_kt += (int64_t)ceil_div(calls[i].n, 128) * ceil_div(calls[i].h->dim, 32);
+    const int64_t target_kb = std::max<int64_t>(4, ceil_div(total_kt, 2 * 148));
+    std::vector<TcGroupDesc> d(G);
+    std::vector<int> sp(G);
+    for (int g = 0; g < G; ++g) {
+      NgCall& c = calls[grp[g]];
+      ngsgd_ctx* h = c.h;
+      const int R = h->rank, D = h->dim;
+      flops += 2.0 * c.n * R * D;
+      bytes += 4.0 * ((double)c.n * D + (double)R * D);
+      TcGroupDesc& q = d[g];
+      q.M = c.n; q.N = R; q.K = D;
+      q.splits = (int)std::min<int64_t>(kTcMaxSplits, std::max<int64_t>(1, ceil_div(ceil_div(D, 32), target_kb)));
+      q.A = c.x; q.lda = c.ld; q.B = h->W[h->cur]; q.ldb = h->ldw;
+      q.epi.kind = TC_EPI_PARTIAL; q.epi.C = h->Hpart; q.epi.ldc = R; q.epi.zstride = (int64_t)c.n * R;
+      q.splits_used = &sp[g];
+    }
+    ProfScope ps(NG_PROF_NG_PROJ, st, flops, bytes);
+    NG_TRY(tc_gemm_tf32_grouped(st, d.data(), G, true, true, TC_EPI_PARTIAL, 128));
+    SegReduce sr;
+    std::memset(&sr, 0, sizeof(sr));
+    sr.count = G;
+    for (int g = 0; g < G; ++g) {
+      NgCall& c = calls[grp[g]];
+      const int R = c.h->rank;
+      sr.out[g] = c.h->H; sr.src[g] = c.h->Hpart; sr.ldo[g] = R; sr.lds[g] = R;
+      sr.zstride[g] = (int64_t)c.n * R; sr.rows[g] = c.n; sr.cols[g] = R; sr.splits[g] = sp[g];
+    }
+    NG_TRY(launch_seg_reduce(st, sr));
+  }
+  // ---- phase B (update states): J = H^T X (one launch), K = J J^T, L = W J^T (FP32)
+  std::vector<int> ug;
+  for (int g = 0; g < G; ++g) if (upd[grp[g]]) ug.push_back(g);
+  if (!ug.empty()) {
+    double flops = 0, bytes = 0;
+    std::vector<TcGroupDesc> d(ug.size());
+    std::vector<int> sp(ug.size());
+    for (size_t u = 0; u < ug.size(); ++u) {
+      NgCall& c = calls[grp[ug[u]]];
+      ngsgd_ctx* h = c.h;
+      const int R = h->rank, D = h->dim;
+      flops += 2.0 * c.n * R * D + 4.0 * (double)R * R * D;
+      bytes += 4.0 * ((double)c.n * D + 3.0 * R * D);
+      TcGroupDesc& q = d[u];
+      q.M = R; q.N = D; q.K = c.n; q.splits = kTcJSplits;
+      q.A = h->H; q.lda = R; q.B = c.x; q.ldb = c.ld;
+      q.epi.kind = TC_EPI_PARTIAL; q.epi.C = h->Hpart; q.epi.ldc = h->ldw; q.epi.zstride = (int64_t)R * h->ldw;
+      q.splits_used = &sp[u];
+    }
+    ProfScope ps(NG_PROF_NG_REFRESH, st, flops, bytes);
+    NG_TRY(tc_gemm_tf32_grouped(st, d.data(), (int)ug.size(), false, false, TC_EPI_PARTIAL, 128));
+    SegReduce sr;
+    std::memset(&sr, 0, sizeof(sr));
+    sr.count = (int)ug.size();
+    for (size_t u = 0; u < ug.size(); ++u) {
+      ngsgd_ctx* h = calls[grp[ug[u]]].h;
+      sr.out[u] = h->J; sr.src[u] = h->Hpart; sr.ldo[u] = h->ldw; sr.lds[u] = h->ldw;
+      sr.zstride[u] = (int64_t)h->rank * h->ldw; sr.rows[u] = h->rank; sr.cols[u] = h->dim; sr.splits[u] = sp[u];
+    }
+    NG_TRY(launch_seg_reduce(st, sr));
+    for (int g : ug) {
+      ngsgd_ctx* h = calls[grp[g]].h;
+      const int R = h->rank, D = h->dim;
+      const int ks = gemm_simt_splits(D, h->kl_splits);
+      NG_TRY((gemm_simt<float, true, true>(st, R, R, D, h->J, h->ldw, h->J, h->ldw,
+                                           EpiStoreSplit<float>{h->Kpart, R, (int64_t)R * R}, ks)));
+      NG_TRY((gemm_simt<float, true, true>(st, R, R, D, h->W[h->cur], h->ldw, h->J, h->ldw,
+                                           EpiStoreSplit<float>{h->Lpart, R, (int64_t)R * R}, ks)));
+    }
+    SegReduce kl;
+    std::memset(&kl, 0, sizeof(kl));
+    kl.count = 0;
+    for (int g : ug) {
+      ngsgd_ctx* h = calls[grp[g]].h;
+      const int R = h->rank, ks = gemm_simt_splits(h->dim, h->kl_splits);
+      for (int w = 0; w < 2; ++w) {
+        if (kl.count == kSegMax) { NG_TRY(launch_seg_reduce(st, kl)); kl.count = 0; }
+        const int k = kl.count++;
+        kl.out[k] = h->KL + w * R * R; kl.src[k] = w ? h->Lpart : h->Kpart; kl.ldo[k] = R; kl.lds[k] = R;
+        kl.zstride[k] = (int64_t)R * R; kl.rows[k] = R; kl.cols[k] = R; kl.splits[k] = ks;
+      }
+    }
+    if (kl.count) NG_TRY(launch_seg_reduce(st, kl));
+  }
+  // ---- phase C: X_hat = X - H W with fused row norms (one launch), finalize (one launch)
+  {
+    double flops = 0, bytes = 0;
+    std::vector<TcGroupDesc> d(G);
+    FinalizeGroup fg;
+    std::memset(&fg, 0, sizeof(fg));
+    fg.count = G;
+    for (int g = 0; g < G; ++g) {
+      NgCall& c = calls[grp[g]];
+      ngsgd_ctx* h = c.h;
+      const int R = h->rank, D = h->dim;
+      flops += 2.0 * c.n * R * D;
+      bytes += 4.0 * (2.0 * c.n * D + (double)R * D);
+      TcGroupDesc& q = d[g];
+      q.M = c.n; q.N = D; q.K = R; q.splits = 1;
+      q.A = h->H; q.lda = R; q.B = h->W[h->cur]; q.ldb = h->ldw;
+      q.epi.kind = TC_EPI_NGAPPLY; q.epi.C = c.x; q.epi.ldc = c.ld; q.epi.xx = h->xxpart; q.epi.pp = h->ppart;
+      q.epi.part_ld = h->max_rows;
+      q.splits_used = nullptr;
+      fg.n[g] = c.n; fg.tiles[g] = h->ctiles; fg.xxpart[g] = h->xxpart; fg.ppart[g] = h->ppart;
+      fg.part_ld[g] = h->max_rows; fg.p_int[g] = h->p; fg.p_out[g] = c.p_out; fg.sums[g] = h->sums;
+      fg.gamma_int[g] = h->gamma; fg.gamma_out[g] = c.gamma_out; fg.flags[g] = h->flags;
+    }
+    ProfScope ps(NG_PROF_NG_APPLY, st, flops, bytes);
+    NG_TRY(tc_gemm_tf32_grouped(st, d.data(), G, true, false, TC_EPI_NGAPPLY, 128));
+    finalize_group_kernel<<<G, 512, 0, st>>>(fg);
+    NG_TRY(check_launch("finalize_group_kernel"));
+  }
+  // ---- phase D: refresh chains on the side streams; bookkeeping
+  for (int g = 0; g < G; ++g) {
+    NgCall& c = calls[grp[g]];
+    ngsgd_ctx* h = c.h;
+    if (upd[grp[g]]) {
+      const double eta = 1.0 - exp(-(double)c.n / (double)h->cfg.s_samples);   // eqn:eta:ns
+      NG_TRY(launch_refresh_chain(h, c.n, eta));
+    }
+    h->t += 1;
+    h->last_updated = upd[grp[g]] ? 1 : 0;
+    if (c.updated_out) *c.updated_out = upd[grp[g]] ? 1 : 0;
+  }
   return NG_OK;
 }
 

@@ -53,4 +53,21 @@ ng_status ngsgd_create_impl(int dim, int max_rows, const ngsgd_config* cfg, cuda
                             ngsgd_ctx** out);
 void ngsgd_destroy_impl(ngsgd_ctx* h);
 ng_status ngsgd_join_impl(ngsgd_ctx* h);
+
+// One preconditioning call of a group (see ngsgd_precondition_group_impl).
+struct NgCall {
+  ngsgd_ctx* h;
+  int n;
+  float* x;
+  int64_t ld;
+  float* gamma_out;
+  float* p_out;
+  int update;          // -1 policy, 0/1 forced
+  int* updated_out;    // optional
+};
+// Precondition several independent states on one stream with ONE launch per phase for
+// all tensor-core-eligible states (H projections, their reduction, J, X_hat, finalize);
+// other calls fall back to ngsgd_precondition_impl.  Results identical to calling
+// ngsgd_precondition_impl on each call in turn.
+ng_status ngsgd_precondition_group_impl(NgCall* calls, int count);
 }  // namespace ng

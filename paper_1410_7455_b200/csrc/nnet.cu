@@ -459,12 +459,22 @@ ng_status nnet_update(nnet_t h, float lr, float max_change_per_sample, nnet_upda
   cudaStream_t st = h->st;
   const int L = h->L, n = h->n_last, N = h->cfg.max_minibatch;
   int upd_in[16] = {0}, upd_out[16] = {0};
+  if (h->cfg.precond) {
+    // all 2I preconditioning calls of the step as one group: one launch per
+    // NG phase for every tensor-core-eligible state
+    std::vector<NgCall> calls;
+    for (int l = 0; l < L; ++l) {
+      float* py = h->pbuf + (size_t)(2 * l) * N;
+      float* px = h->pbuf + (size_t)(2 * l + 1) * N;
+      calls.push_back(NgCall{h->ng_out[l], n, h->X[l], h->ldr[l], h->gam + 2 * l + 1, px, -1, &upd_out[l]});
+      calls.push_back(NgCall{h->ng_in[l], n, h->Y[l], h->ldp[l], h->gam + 2 * l, py, -1, &upd_in[l]});
+    }
+    NG_TRY(ngsgd_precondition_group_impl(calls.data(), (int)calls.size()));
+  }
   for (int l = 0; l < L; ++l) {
     float* py = h->pbuf + (size_t)(2 * l) * N;
     float* px = h->pbuf + (size_t)(2 * l + 1) * N;
     if (h->cfg.precond) {
-      NG_TRY(ngsgd_precondition_impl(h->ng_out[l], n, h->X[l], h->ldr[l], h->gam + 2 * l + 1, px, -1, &upd_out[l]));
-      NG_TRY(ngsgd_precondition_impl(h->ng_in[l], n, h->Y[l], h->ldp[l], h->gam + 2 * l, py, -1, &upd_in[l]));
     } else {
       rowsq_kernel<<<n, 256, 0, st>>>(n, h->rows[l], h->X[l], h->ldr[l], px, h->gam + 2 * l + 1);
       rowsq_kernel<<<n, 256, 0, st>>>(n, h->cols[l], h->Y[l], h->ldp[l], py, h->gam + 2 * l);
