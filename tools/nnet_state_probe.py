@@ -19,5 +19,11 @@ for k in range(int(sys.argv[1]) if len(sys.argv) > 1 else 30):
         for side in ("in", "out"):
             s = net.ngsgd(l, side).get_state()
             if s["updated"]:
-                row.append(f"{l}{side[0]}:{s['jacobi_sweeps']}{'C' if s['reorth_checked'] else ''}{'R' if s['reorthogonalized'] else ''}")
+                W, d, rho = s["W"].astype(np.float64), s["d"], s["rho"]
+                D = W.shape[1]
+                beta = rho * 5.0 + 4.0 / D * d.sum()
+                e = 1.0 / (beta / d + 1.0)
+                Rm = W / np.sqrt(e)[:, None]
+                dev = np.max(np.abs(Rm @ Rm.T - np.eye(len(d))))
+                row.append(f"{l}{side[0]}:{s['jacobi_sweeps']}{'C' if s['reorth_checked'] else ''}{'R' if s['reorthogonalized'] else ''}({dev:.0e},{d.max()/max(d.min(),1e-30):.0e})")
     print(k, " ".join(row), "alpha", np.round(st.alpha_t, 3))
