@@ -212,11 +212,12 @@ __device__ __forceinline__ void circle_pair(int r, int k, int m1, int& p, int& q
 }
 
 template <typename T>
-__device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __restrict__ Vt, int ldv, int n, JacobiSmem<T> sc,
-                               int max_sweeps, double abs_floor, double rel_tol) {
+__device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __restrict__ Vt, int ldv, int n,
+                                               JacobiSmem<T> sc, int max_sweeps, double abs_floor, double rel_tol) {
   // ldv * sizeof(T) must be a multiple of 16 (vectorised eigenvector rows)
   constexpr int VEC = 16 / sizeof(T);
   using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+  using CS = typename std::conditional<sizeof(T) == 8, double2, float2>::type;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
   const int npad = n + (n & 1);
   const int m = npad / 2, m1 = npad - 1;
@@ -224,6 +225,8 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
   const int nblk = m * (m + 1) / 2;
   const T tol2 = (T)(rel_tol * rel_tol), flo2 = (T)(abs_floor * abs_floor);
   const float stop2 = (float)rel_tol;
+  CS* cs2 = reinterpret_cast<CS*>(sc.c);          // (c, s) of pair k, m entries
+  int* pqt = sc.nrot + 64;                         // p | q << 16 of pair k (this round)
   // this thread's 2x2 blocks (ka <= kb), decoded once
   int bka[2], bkb[2], nb = 0;
   for (int bb = tid; bb < nblk && nb < 2; bb += nt) {
@@ -235,7 +238,7 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
     ++nb;
   }
   for (int idx = tid; idx < n * ldv; idx += nt) {
-    const int i = idx / ldv, j = idx % ldv;
+    const int i = idx / ldv, j = idx - i * ldv;
     Vt[idx] = (i == j) ? T(1) : T(0);
   }
   __syncthreads();
@@ -271,52 +274,55 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
             ++my_rot;
           }
         }
-        sc.c[k] = c;
-        sc.s[k] = s;
+        CS v;
+        v.x = c;
+        v.y = s;
+        cs2[k] = v;
+        pqt[k] = p | (q << 16);
       }
       __syncthreads();
       // A' = J^T A J, 2x2 blocks (ka <= kb), mirrored
       for (int i = 0; i < nb; ++i) {
         const int ka = bka[i], kb = bkb[i];
-        const T s1 = sc.s[ka], s2 = sc.s[kb];
+        const CS r1 = cs2[ka], r2 = cs2[kb];
+        const T c1 = r1.x, s1 = r1.y, c2 = r2.x, s2 = r2.y;
         if (s1 == T(0) && s2 == T(0)) continue;
-        const T c1 = sc.c[ka], c2 = sc.c[kb];
-        int p1, q1, p2, q2;
-        circle_pair(round, ka, m1, p1, q1);
-        circle_pair(round, kb, m1, p2, q2);
+        const int pq1 = pqt[ka], pq2 = pqt[kb];
+        const int p1 = pq1 & 0xFFFF, q1 = pq1 >> 16, p2 = pq2 & 0xFFFF, q2 = pq2 >> 16;
+        const int rp1 = p1 * lda, rq1 = q1 * lda;
         if (ka == kb) {
-          const T a = A[p1 * lda + p1], d = A[q1 * lda + q1], bb = A[p1 * lda + q1];
-          const T cc = c1 * c1, ss = s1 * s1, cs = c1 * s1;
-          const T bn = (cc - ss) * bb + cs * (a - d);
-          A[p1 * lda + p1] = cc * a - T(2) * cs * bb + ss * d;
-          A[q1 * lda + q1] = ss * a + T(2) * cs * bb + cc * d;
-          A[p1 * lda + q1] = bn;
-          A[q1 * lda + p1] = bn;
+          const T a = A[rp1 + p1], d = A[rq1 + q1], bb = A[rp1 + q1];
+          const T cc = c1 * c1, ss = s1 * s1, csx = c1 * s1;
+          const T bn = (cc - ss) * bb + csx * (a - d);
+          A[rp1 + p1] = cc * a - T(2) * csx * bb + ss * d;
+          A[rq1 + q1] = ss * a + T(2) * csx * bb + cc * d;
+          A[rp1 + q1] = bn;
+          A[rq1 + p1] = bn;
           continue;
         }
+        const int rp2 = p2 * lda, rq2 = q2 * lda;
         const bool v1 = q1 < n, v2 = q2 < n;
-        const T m00 = A[p1 * lda + p2];
-        const T m01 = v2 ? A[p1 * lda + q2] : T(0);
-        const T m10 = v1 ? A[q1 * lda + p2] : T(0);
-        const T m11 = (v1 && v2) ? A[q1 * lda + q2] : T(0);
+        const T m00 = A[rp1 + p2];
+        const T m01 = v2 ? A[rp1 + q2] : T(0);
+        const T m10 = v1 ? A[rq1 + p2] : T(0);
+        const T m11 = (v1 && v2) ? A[rq1 + q2] : T(0);
         const T t00 = c1 * m00 - s1 * m10, t01 = c1 * m01 - s1 * m11;
         const T t10 = s1 * m00 + c1 * m10, t11 = s1 * m01 + c1 * m11;
         const T r00 = c2 * t00 - s2 * t01, r01 = s2 * t00 + c2 * t01;
         const T r10 = c2 * t10 - s2 * t11, r11 = s2 * t10 + c2 * t11;
-        A[p1 * lda + p2] = r00; A[p2 * lda + p1] = r00;
-        if (v2) { A[p1 * lda + q2] = r01; A[q2 * lda + p1] = r01; }
-        if (v1) { A[q1 * lda + p2] = r10; A[p2 * lda + q1] = r10; }
-        if (v1 && v2) { A[q1 * lda + q2] = r11; A[q2 * lda + q1] = r11; }
+        A[rp1 + p2] = r00; A[rp2 + p1] = r00;
+        if (v2) { A[rp1 + q2] = r01; A[rq2 + p1] = r01; }
+        if (v1) { A[rq1 + p2] = r10; A[rp2 + q1] = r10; }
+        if (v1 && v2) { A[rq1 + q2] = r11; A[rq2 + q1] = r11; }
       }
       // eigenvector rows p, q of each rotating pair: one warp per pair, VEC columns per lane
       for (int k = warp; k < m; k += nwarps) {
-        const T s = sc.s[k];
+        const CS r = cs2[k];
+        const T c = r.x, s = r.y;
         if (s == T(0)) continue;
-        const T c = sc.c[k];
-        int p, q;
-        circle_pair(round, k, m1, p, q);
-        V* vp = reinterpret_cast<V*>(Vt + p * ldv);
-        V* vq = reinterpret_cast<V*>(Vt + q * ldv);
+        const int pq = pqt[k];
+        V* vp = reinterpret_cast<V*>(Vt + (pq & 0xFFFF) * ldv);
+        V* vq = reinterpret_cast<V*>(Vt + (pq >> 16) * ldv);
         for (int j = lane; j < nvec; j += 32) {
           const V a = vp[j], b = vq[j];
           V na, nb2;
@@ -333,7 +339,7 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
       }
       __syncthreads();
     }
-    // sweep totals (threads >= m contribute 0); reduction scratch = the c/s arrays
+    // sweep totals (threads >= m contribute 0)
     my_rot = warp_sum(my_rot);
     my_off = warp_max(my_off);
     if (lane == 0) { sc.nrot[warp] = my_rot; sc.offmax[warp] = my_off; }

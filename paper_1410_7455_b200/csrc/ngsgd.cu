@@ -238,11 +238,11 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   T* Z = reinterpret_cast<T*>(red + 32 + (R & 1));                          // R*LD, 16-byte aligned
   constexpr int kVec = 16 / sizeof(T);
   T* Vt = Z + (R * LD + kVec - 1) / kVec * kVec;   // R*LDV, 16-byte aligned (Z is)
-  T* jc = Vt + R * LDV;                 // mp rotation c
-  T* js = jc + mp;                      // mp rotation s
+  T* jc = Vt + R * LDV;                 // 2*mp: (c, s) pairs (16-byte aligned: R*LDV even)
+  T* js = jc + mp;                      // (unused by the packed layout)
   int* perm = reinterpret_cast<int*>(js + mp + 2);   // R
-  int* nrot = perm + R;                 // 32 (per-warp sweep counts)
-  int* iflag = nrot + 32;               // 1 (floored)
+  int* nrot = perm + R;                 // 32 per-warp sweep counts, 32 spare, then mp pair table
+  int* iflag = nrot + 64 + mp;          // 1 (floored)
   float* offmax = reinterpret_cast<float*>(iflag + 1);  // 32 (per-warp max ratio)
   const int tid = threadIdx.x, nt = blockDim.x;
 
@@ -527,7 +527,7 @@ __global__ void passthrough_kernel(int n, float* p, float* p_out, float* g, floa
 static size_t refresh_smem_bytes(int R, size_t tsize) {
   const int mp = R / 2 + 1;
   const size_t tcount = (size_t)R * (R + 1) + (size_t)R * ((R + 3) / 4 * 4) + 2 * mp + 2 + 16 / tsize;
-  return sizeof(double) * (5 * (size_t)R + 33) + tsize * tcount + sizeof(int) * (R + 68) + 64;
+  return sizeof(double) * (5 * (size_t)R + 33) + tsize * tcount + sizeof(int) * (R + 100 + mp) + 64;
 }
 static size_t reorth_smem_bytes(int R) { return sizeof(double) * (2 * R * R + R + 32); }
 
