@@ -213,7 +213,8 @@ __device__ __forceinline__ void circle_pair(int r, int k, int m1, int& p, int& q
 
 template <typename T>
 __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __restrict__ Vt, int ldv, int n,
-                                               JacobiSmem<T> sc, int max_sweeps, double abs_floor, double rel_tol) {
+                                               JacobiSmem<T> sc, int max_sweeps, double abs_floor, double rel_tol,
+                                               int dbg = 0) {
   // ldv * sizeof(T) must be a multiple of 16 (vectorised eigenvector rows)
   constexpr int VEC = 16 / sizeof(T);
   using V = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
@@ -244,6 +245,9 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
   __syncthreads();
   if (n <= 1) return 0;
   const int nvec = (n + VEC - 1) / VEC;   // vectors per eigenvector row
+  // this thread's eigenvector items (pair k, vector column j), decoded once
+  int vk[4], vj[4], nvi = 0;
+  for (int it = tid; it < m * nvec && nvi < 4; it += nt) { vk[nvi] = it / nvec; vj[nvi] = it - vk[nvi] * nvec; ++nvi; }
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
     int my_rot = 0;          // per-thread counters, reduced once per sweep (no atomics)
@@ -258,7 +262,7 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
           const T app = A[p * lda + p], aqq = A[q * lda + q], apq = A[p * lda + q];
           const T apq2 = apq * apq, dd = fabs(app * aqq);
           if (apq2 > tol2 * dd && apq2 > flo2) {
-            my_off = fmaxf(my_off, (float)(apq2 / dd));
+            my_off = fmaxf(my_off, __fdividef((float)apq2, (float)dd));
             // MUFU-based angle (the FP32 angle only has to be ~1e-7 accurate)
             const float th = __fdividef((float)(aqq - app), 2.f * (float)apq);
             float tf;
@@ -269,7 +273,9 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
               tf = copysignf(__fdividef(1.f, fabsf(th) + r2 * rsqrtf(r2)), th);
             }
             const T t = (T)tf;
-            c = rsqrt_t<T>(t * t + T(1));
+            const T x = t * t + T(1);
+            const T c0 = (T)rsqrtf((float)x);
+            c = c0 * (T(1.5) - T(0.5) * x * c0 * c0);      // one Newton step: ~1e-14 relative
             s = t * c;
             ++my_rot;
           }
@@ -282,7 +288,7 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
       }
       __syncthreads();
       // A' = J^T A J, 2x2 blocks (ka <= kb), mirrored
-      for (int i = 0; i < nb; ++i) {
+      for (int i = 0; i < ((dbg & 1) ? 0 : nb); ++i) {
         const int ka = bka[i], kb = bkb[i];
         const CS r1 = cs2[ka], r2 = cs2[kb];
         const T c1 = r1.x, s1 = r1.y, c2 = r2.x, s2 = r2.y;
@@ -315,27 +321,27 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
         if (v1) { A[rq1 + p2] = r10; A[rp2 + q1] = r10; }
         if (v1 && v2) { A[rq1 + q2] = r11; A[rq2 + q1] = r11; }
       }
-      // eigenvector rows p, q of each rotating pair: one warp per pair, VEC columns per lane
-      for (int k = warp; k < m; k += nwarps) {
+      // eigenvector rows p, q of each rotating pair: (pair, vector column) items spread
+      // evenly over all threads
+      for (int i = 0; i < ((dbg & 2) ? 0 : nvi); ++i) {
+        const int k = vk[i], j = vj[i];
         const CS r = cs2[k];
         const T c = r.x, s = r.y;
         if (s == T(0)) continue;
         const int pq = pqt[k];
-        V* vp = reinterpret_cast<V*>(Vt + (pq & 0xFFFF) * ldv);
-        V* vq = reinterpret_cast<V*>(Vt + (pq >> 16) * ldv);
-        for (int j = lane; j < nvec; j += 32) {
-          const V a = vp[j], b = vq[j];
-          V na, nb2;
-          if constexpr (VEC == 2) {
-            na.x = c * a.x - s * b.x; na.y = c * a.y - s * b.y;
-            nb2.x = s * a.x + c * b.x; nb2.y = s * a.y + c * b.y;
-          } else {
-            na.x = c * a.x - s * b.x; na.y = c * a.y - s * b.y; na.z = c * a.z - s * b.z; na.w = c * a.w - s * b.w;
-            nb2.x = s * a.x + c * b.x; nb2.y = s * a.y + c * b.y; nb2.z = s * a.z + c * b.z; nb2.w = s * a.w + c * b.w;
-          }
-          vp[j] = na;
-          vq[j] = nb2;
+        V* vp = reinterpret_cast<V*>(Vt + (pq & 0xFFFF) * ldv) + j;
+        V* vq = reinterpret_cast<V*>(Vt + (pq >> 16) * ldv) + j;
+        const V a = *vp, b = *vq;
+        V na, nb2;
+        if constexpr (VEC == 2) {
+          na.x = c * a.x - s * b.x; na.y = c * a.y - s * b.y;
+          nb2.x = s * a.x + c * b.x; nb2.y = s * a.y + c * b.y;
+        } else {
+          na.x = c * a.x - s * b.x; na.y = c * a.y - s * b.y; na.z = c * a.z - s * b.z; na.w = c * a.w - s * b.w;
+          nb2.x = s * a.x + c * b.x; nb2.y = s * a.y + c * b.y; nb2.z = s * a.z + c * b.z; nb2.w = s * a.w + c * b.w;
         }
+        *vp = na;
+        *vq = nb2;
       }
       __syncthreads();
     }
@@ -348,7 +354,7 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
     float om = 0.f;
     for (int w = 0; w < nwarps; ++w) { rot += sc.nrot[w]; om = fmaxf(om, sc.offmax[w]); }
     __syncthreads();
-    if (rot == 0 || om < stop2) { ++sweep; break; }
+    if (rot == 0 || om < stop2 || ((dbg & 4) && sweep + 1 >= 5)) { ++sweep; break; }
   }
   return sweep;
 }

@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(1024)
 refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
                const float* __restrict__ KL, double* __restrict__ dstate,
                const double* __restrict__ sums, float* __restrict__ Amat,
-               float* __restrict__ svec, int* __restrict__ flags) {
+               float* __restrict__ svec, int* __restrict__ flags, int dbg_mask) {
   extern __shared__ __align__(16) unsigned char ng_smem[];
   double* sm = reinterpret_cast<double*>(ng_smem);
   const int LD = R + 1;                 // odd row stride of Z: fewer bank conflicts
@@ -280,7 +280,10 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   // Z = U C U^T (eqn:zt:eig:repeat)
   const bool dbl = sizeof(T) == 8;
   JacobiSmem<T> scr{jc, js, nrot, offmax};
-  const int sweeps = jacobi_eig_smem<T>(Z, LD, Vt, LDV, R, scr, 20, (dbl ? 1e-15 : 1e-9) * zmax, dbl ? 1e-9 : 1e-6);
+  // rel_tol 1e-7: rotations stop once every |z_pq| <= 1e-7 sqrt(z_pp z_qq) (eigenvector error
+  // ~1e-7 / relative gap, far below the FP32 storage of A_t and W_{t+1})
+  const int sweeps = jacobi_eig_smem<T>(Z, LD, Vt, LDV, R, scr, 20, (dbl ? 1e-15 : 1e-9) * zmax, dbl ? 1e-7 : 1e-6,
+                                        dbg_mask);
   // descending order
   for (int i = tid; i < R; i += nt) {
     const double li = (double)Z[i * LD + i];
@@ -730,8 +733,9 @@ static ng_status launch_refresh_chain(ngsgd_ctx* h, int n, double eta) {
     // FP64 eigensolve in both precision modes: with cond(C) > 1e6 (common) an
     // FP32 solve leaves R_{t+1} non-orthonormal beyond 1e-3 and B.3.1 repairs would fire on
     // most updates (measured on the config-3 network).
+    static const int dbg = getenv("NG_PROFILE_JACOBI_MASK") ? atoi(getenv("NG_PROFILE_JACOBI_MASK")) : 0;
     refresh_kernel<double><<<1, 1024, refresh_smem_bytes(R, sizeof(double)), ss>>>(
-        R, D, n, eta, a_, e_, h->KL, h->dstate, h->sums, h->Amat, h->svec, h->flags);
+        R, D, n, eta, a_, e_, h->KL, h->dstate, h->sums, h->Amat, h->svec, h->flags, dbg);
     NG_TRY(check_launch("refresh_kernel"));
   }
   ProfScope ps(NG_PROF_NG_REFRESH, ss, 2.0 * (double)R * R * D + 2.0 * R * D, 4.0 * (4.0 * R * D));
