@@ -45,6 +45,7 @@ WORKLOAD = ("config3: paper-shaped p-norm DNN 360 -> 4x[3000 -> p-norm 300] -> 5
 POOL_FRAMES = 1 << 18
 TOTAL_SAMPLES = 10 * 400_000          # nominal schedule length for the lr (host scalar)
 FP32_SIMT_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # FP32 FMA lanes x 2 x max clock
+FP64_SM_PEAK_GFLOPS = 64 * 2 * 1.965e9 / 1e9              # one SM: 64 FP64 FMA/clk x 2 x max clock
 
 
 def log(*a):
@@ -218,6 +219,15 @@ def roofline_for(group: str, prof: dict, precision: str, peaks: dict):
     except Exception:
         pass
     is_gemm = group in ("fwd_gemm", "bwd_gemm", "upd_gemm")
+    if group == "ng_eig":
+        # one CTA by design (FP64 Jacobi of the R x R matrix Z_t): peak = ONE SM's FP64 FMA rate
+        flops = g["flops"] / g["launches"]
+        achieved = flops / per_launch_s / 1e9
+        peak = FP64_SM_PEAK_GFLOPS
+        return {"kernel": group, "bound": "alu", "achieved": achieved, "peak": peak, "unit": "GFLOP/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "peak_source": "derived: one SM, 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md); algorithmic 9 R^3 flop",
+                "algorithmic_per_launch": flops, "launch_ms": per_launch_s * 1e3}
     if is_gemm or group in ("ng_proj", "ng_refresh"):
         flops = g["flops"] / g["launches"]
         achieved = flops / per_launch_s / 1e12
@@ -371,6 +381,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     peaks = load_peaks()
     roof = roofline_for(dominant, prof, precision, peaks)
     shares = {g: v["ms"] for g, v in wprof.items() if v["launches"]}
+    roof_groups = {g: roofline_for(g, wprof, precision, load_peaks()) for g, v in wprof.items()
+                   if v["launches"] and g not in ("ng_init", "elemwise", "average")}
 
     # end-to-end through the public API with host buffers: pinned host frames/labels
     # copied in every step, the step's objective read back every step
@@ -434,7 +446,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                        "l2": f"input pool {POOL_FRAMES} frames x 360 fp32 = 377 MB > 126 MB L2, cycled"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
             "gpu_launches": launches, "launches_per_step": launches / args.steps,
-            "kernel_group_ms_warmup": shares, "precondition_ms_per_minibatch": pre}
+            "kernel_group_ms_warmup": shares, "roofline_groups_warmup": roof_groups,
+            "precondition_ms_per_minibatch": pre}
     print(json.dumps(line), flush=True)
     return 0
 

@@ -728,7 +728,8 @@ static ng_status launch_refresh_chain(ngsgd_ctx* h, int n, double eta) {
   NG_CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
   cudaStream_t ss = h->side;
   {
-    ProfScope pe(NG_PROF_NG_EIG, ss, 0.0, 0.0);
+    // algorithmic work of a dense symmetric eigendecomposition with eigenvectors: ~9 R^3 flop
+    ProfScope pe(NG_PROF_NG_EIG, ss, 9.0 * (double)R * R * R, 8.0 * 2.0 * R * R);
     const double a_ = (double)h->cfg.alpha, e_ = (double)h->cfg.epsilon;
     // FP64 eigensolve in both precision modes: with cond(C) > 1e6 (common) an
     // FP32 solve leaves R_{t+1} non-orthonormal beyond 1e-3 and B.3.1 repairs would fire on

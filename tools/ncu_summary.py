@@ -41,7 +41,7 @@ def full_table(rep, title, note):
         wr = val(d, "dram__bytes_write.sum", "MB")
         lines.append(
             f"| `{name}` | {d['Grid Size'][1]} x {d['Block Size'][1]} | {t:.1f} | {rd:.2f} | {wr:.2f} | "
-            f"{(rd + wr) / t * 1e-3 * 1e3:.0f} | {val(d, 'sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active'):.1f} | "
+            f"{(rd + wr) / t * 1e3:.0f} | {val(d, 'sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active'):.1f} | "
             f"{val(d, 'sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active'):.2f} | "
             f"{val(d, 'sm__throughput.avg.pct_of_peak_sustained_elapsed'):.1f} | "
             f"{val(d, 'sm__instruction_throughput.avg.pct_of_peak_sustained_active'):.1f} | "
