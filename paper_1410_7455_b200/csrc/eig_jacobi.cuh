@@ -229,7 +229,7 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
   CS* cs2 = reinterpret_cast<CS*>(sc.c);          // (c, s) of pair k, m entries
   int* pqt = sc.nrot + 64;                         // p | q << 16 of pair k (this round)
   // this thread's 2x2 blocks (ka <= kb), decoded once
-  int bka[2], bkb[2], nb = 0;
+  int bka[2], bkb[2], nb = 0;   // nblk <= 2 * blockDim (R <= 112 with 1024 threads)
   for (int bb = tid; bb < nblk && nb < 2; bb += nt) {
     int kb = (int)((sqrtf(8.f * bb + 1.f) - 1.f) * 0.5f);
     while (kb * (kb + 1) / 2 > bb) --kb;
@@ -246,7 +246,7 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
   if (n <= 1) return 0;
   const int nvec = (n + VEC - 1) / VEC;   // vectors per eigenvector row
   // this thread's eigenvector items (pair k, vector column j), decoded once
-  int vk[4], vj[4], nvi = 0;
+  int vk[4], vj[4], nvi = 0;    // m * nvec <= 4 * blockDim
   for (int it = tid; it < m * nvec && nvi < 4; it += nt) { vk[nvi] = it / nvec; vj[nvi] = it - vk[nvi] * nvec; ++nvi; }
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
