@@ -188,67 +188,80 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
   }
   __syncwarp();
 
-  // ---------------- epilogue: TMEM -> registers -> smem transpose -> coalesced global
-  // Each warp owns TMEM lanes (tile rows) 32w..32w+31.  A 32-column chunk is loaded with two
-  // tcgen05.ld (row-per-lane), staged in shared memory (the drained pipeline ring), and read
-  // back so that lane l handles column l of one row at a time: every global access of the
-  // epilogue is a contiguous 128-byte row segment.
+  // ---------------- epilogue: TMEM -> registers -> global (row per thread)
+  // Warp w owns TMEM lanes (tile rows) 32w..32w+31.  Chunks of 32 columns (two tcgen05.ld):
+  // each thread moves one full 128-byte line of its row per chunk with 8 independent
+  // 16-byte accesses (all loads of a read-modify-write chunk are issued first).
   mbar_wait(&accum_bar, 0);
   tc_fence_after();
   __syncwarp();
-  float* stage = reinterpret_cast<float*>(smem) + warp * (32 * 33);   // [32 rows][33]
+  const int row = m0 + warp * 32 + lane;
   const float scale = (EPI == TC_EPI_AXPY) ? __ldg(epi.scale) : 0.f;
-  float* __restrict__ cbase = epi.C + (EPI == TC_EPI_PARTIAL ? (int64_t)ztile * epi.zstride : 0);
-  float xx_mine = 0.f, pp_mine = 0.f;   // NGAPPLY: row (32w + lane) partial sums
+  float* __restrict__ crow = epi.C + (EPI == TC_EPI_PARTIAL ? (int64_t)ztile * epi.zstride : 0) +
+                             (int64_t)row * epi.ldc;
+  float xx = 0.f, pp = 0.f;   // TC_EPI_NGAPPLY row partial sums over this tile's columns
+  constexpr int CW = BN >= 32 ? 32 : 16;
 #pragma unroll 1
-  for (int cc = 0; cc < (BN + 31) / 32; ++cc) {
-    uint32_t v[16];
-    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(cc * 32), v);
+  for (int c = 0; c < BN / CW; ++c) {
+    float acc[CW];
+    {
+      uint32_t v[16];
+      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * CW), v);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) stage[lane * 33 + j] = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
-    if (BN >= 32) {
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(cc * 32 + 16), v);
+      for (int j = 0; j < 16; ++j) acc[j] = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
+      if (CW == 32) {
+        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * CW + 16), v);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) stage[lane * 33 + 16 + j] = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
-    }
-    __syncwarp();
-    const int col = n0 + cc * 32 + lane;
-    const bool colok = col < N && (BN >= 32 || lane < 16);
-#pragma unroll 4
-    for (int r = 0; r < 32; ++r) {
-      const int grow = m0 + warp * 32 + r;
-      const float acc = stage[r * 33 + lane];
-      float xo = 0.f, xn = 0.f;
-      if (grow < M && colok) {
-        float* p = cbase + (int64_t)grow * epi.ldc + col;
-        if (EPI == TC_EPI_STORE || EPI == TC_EPI_PARTIAL) {
-          *p = acc;
-        } else if (EPI == TC_EPI_AXPY) {
-          *p = fmaf(scale, acc, *p);
-        } else {   // TC_EPI_NGAPPLY: x_hat = x - (H W)  (eqn:hatxt:compute:2)
-          xo = *p;
-          xn = xo - acc;
-          *p = xn;
-        }
-      }
-      if (EPI == TC_EPI_NGAPPLY) {
-        float a2 = xo * xo, b2 = xn * xn;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          a2 += __shfl_xor_sync(0xffffffffu, a2, o);
-          b2 += __shfl_xor_sync(0xffffffffu, b2, o);
-        }
-        if (lane == r) { xx_mine += a2; pp_mine += b2; }
+        for (int j = 0; j < 16; ++j) acc[16 + j] = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
       }
     }
-    __syncwarp();
+    const int nb = n0 + c * CW;
+    if (row < M && nb < N) {
+      const bool full = (nb + CW <= N) && ((reinterpret_cast<uintptr_t>(crow + nb) & 15) == 0);
+      if (EPI == TC_EPI_STORE || EPI == TC_EPI_PARTIAL) {
+        if (full) {
+#pragma unroll
+          for (int j = 0; j < CW; j += 4)
+            *reinterpret_cast<float4*>(crow + nb + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        } else {
+          for (int j = 0; j < CW && nb + j < N; ++j) crow[nb + j] = acc[j];
+        }
+      } else {
+        float old[CW];
+        if (full) {
+#pragma unroll
+          for (int j = 0; j < CW; j += 4) {
+            const float4 o = *reinterpret_cast<const float4*>(crow + nb + j);
+            old[j] = o.x; old[j + 1] = o.y; old[j + 2] = o.z; old[j + 3] = o.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < CW; ++j) old[j] = (nb + j < N) ? crow[nb + j] : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+          if (EPI == TC_EPI_AXPY) {
+            acc[j] = fmaf(scale, acc[j], old[j]);
+          } else {   // TC_EPI_NGAPPLY: x_hat = x - (H W)  (eqn:hatxt:compute:2), row norms
+            const float xn = old[j] - acc[j];
+            xx = fmaf(old[j], old[j], xx);
+            pp = fmaf(xn, xn, pp);
+            acc[j] = xn;
+          }
+        }
+        if (full) {
+#pragma unroll
+          for (int j = 0; j < CW; j += 4)
+            *reinterpret_cast<float4*>(crow + nb + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        } else {
+          for (int j = 0; j < CW && nb + j < N; ++j) crow[nb + j] = acc[j];
+        }
+      }
+    }
   }
-  if (EPI == TC_EPI_NGAPPLY) {
-    const int row = m0 + warp * 32 + lane;
-    if (row < M) {
-      epi.xx[(int64_t)ntile * epi.part_ld + row] = xx_mine;
-      epi.pp[(int64_t)ntile * epi.part_ld + row] = pp_mine;
-    }
+  if (EPI == TC_EPI_NGAPPLY && row < M) {
+    epi.xx[(int64_t)ntile * epi.part_ld + row] = xx;
+    epi.pp[(int64_t)ntile * epi.part_ld + row] = pp;
   }
   tc_fence_before();
   __syncthreads();
