@@ -149,7 +149,8 @@ typedef struct nnet_ctx* nnet_t;
 
 /* Create a network with C.6 initialisation: N(0, 1/fan-in) with the bias
  * column counted in the fan-in (R20), softmax layer zero.  Parameters live in
- * one contiguous FP32 device arena (for nnet_average). */
+ * one contiguous FP32 device arena (for nnet_average).  NG_ESHAPE if hidden_dim or
+ * num_classes exceeds 50000 (one activation row is staged in shared memory). */
 ng_status nnet_create(const nnet_config* cfg, void* cuda_stream, nnet_t* out);
 ng_status nnet_destroy(nnet_t h);
 

@@ -14,6 +14,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -27,7 +28,17 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 32;        // fp32 elements per 128-byte swizzle row = one k-block
-constexpr int kStages = 4;
+constexpr int kStages = 8;     // barrier slots; the ring depth used is tc_stages() (<= kStages)
+
+// Ring depth: 4 unless NG_TUNE_TC_STAGES (tuning knob, 1..8) says otherwise.
+int tc_stages() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("NG_TUNE_TC_STAGES");
+    v = e ? std::max(1, std::min(kStages, atoi(e))) : 4;
+  }
+  return v;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -114,7 +125,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 // ztile are the column-tile and split indices used by the NGAPPLY / PARTIAL epilogues.
 template <int BN, bool AK, bool BKM, int EPI>
 __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int m0, int n0,
-                                        int kb0, int nkb, int ntile, int ztile, const TcEpilogue& epi) {
+                                        int kb0, int nkb, int ntile, int ztile, const TcEpilogue& epi,
+                                        int nstages) {
   constexpr uint32_t A_BYTES = kBM * kBK * 4, B_BYTES = BN * kBK * 4, STAGE = A_BYTES + B_BYTES;
   constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
   extern __shared__ uint8_t smem_raw[];
@@ -130,7 +142,7 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmB)) : "memory");
-    for (int s = 0; s < kStages; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+    for (int s = 0; s < nstages; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
     mbar_init(&accum_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -146,9 +158,9 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
+    int s = 0;
+    uint32_t ph = 0;
     for (int i = 0; i < nkb; ++i) {
-      const int s = i % kStages;
-      const uint32_t ph = (uint32_t)(i / kStages) & 1u;
       mbar_wait(&empty_bar[s], ph ^ 1u);
       uint8_t* sa = smem + s * STAGE;
       uint8_t* sb = sa + A_BYTES;
@@ -166,13 +178,14 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
 #pragma unroll
         for (int j = 0; j < BN / 32; ++j) tma_load_2d(sb + j * 4096, tmB, n0 + 32 * j, kc, &full_bar[s]);
       }
+      if (++s == nstages) { s = 0; ph ^= 1u; }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (single thread)
     constexpr uint32_t idesc = idesc_tf32(kBM, BN, !AK, !BKM);
+    int s = 0;
+    uint32_t ph = 0;
     for (int i = 0; i < nkb; ++i) {
-      const int s = i % kStages;
-      const uint32_t ph = (uint32_t)(i / kStages) & 1u;
       mbar_wait(&full_bar[s], ph);
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
@@ -183,6 +196,7 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
         mma_tf32(tmem, da, db, idesc, (i > 0 || k > 0) ? 1u : 0u);
       }
       umma_commit(&empty_bar[s]);
+      if (++s == nstages) { s = 0; ph ^= 1u; }
     }
     umma_commit(&accum_bar);
   }
@@ -271,20 +285,20 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
 }
 
 template <int BN, bool AK, bool BKM, int EPI>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(128)
 tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                    int K, int kb_per_split, TcEpilogue epi) {
+                    int K, int kb_per_split, TcEpilogue epi, int nstages) {
   const int kb_total = (K + kBK - 1) / kBK;
   const int kb0 = blockIdx.z * kb_per_split;
   const int nkb = max(0, min(kb_total, kb0 + kb_per_split) - kb0);
   tc_tile<BN, AK, BKM, EPI>(&tmA, &tmB, M, N, blockIdx.y * kBM, blockIdx.x * BN, kb0, nkb, blockIdx.x, blockIdx.z,
-                            epi);
+                            epi, nstages);
 }
 
 // Grouped launch: problem g owns tiles [tile_begin, tile_begin + mt*nt*splits); each tile
 // (z, m, n) of it is one CTA.  Problems share BN, operand majors and epilogue kind.
 template <int BN, bool AK, bool BKM, int EPI>
-__global__ void __launch_bounds__(128, 1) tc_gemm_tf32_grouped_kernel(const __grid_constant__ TcGroup grp) {
+__global__ void __launch_bounds__(128) tc_gemm_tf32_grouped_kernel(const __grid_constant__ TcGroup grp) {
   int g = 0;
   while (g + 1 < grp.count && (int)blockIdx.x >= grp.p[g + 1].tile_begin) ++g;
   const TcProblem& P = grp.p[g];
@@ -294,7 +308,8 @@ __global__ void __launch_bounds__(128, 1) tc_gemm_tf32_grouped_kernel(const __gr
   const int kb_total = (P.K + kBK - 1) / kBK;
   const int kb0 = z * P.kbps;
   const int nkb = max(0, min(kb_total, kb0 + P.kbps) - kb0);
-  tc_tile<BN, AK, BKM, EPI>(&P.tmA, &P.tmB, P.M, P.N, mtile * kBM, ntile * BN, kb0, nkb, ntile, z, P.epi);
+  tc_tile<BN, AK, BKM, EPI>(&P.tmA, &P.tmB, P.M, P.N, mtile * kBM, ntile * BN, kb0, nkb, ntile, z, P.epi,
+                            grp.nstages);
 }
 
 // ------------------------------------------------------------------ host side
@@ -349,18 +364,28 @@ ng_status make_tmap(CUtensorMap* out, const float* ptr, int64_t inner, int64_t o
   return NG_OK;
 }
 
+inline size_t ring_smem(int bn, int stages) { return (size_t)stages * (kBM * kBK * 4 + bn * kBK * 4) + 1024; }
+// Ring depth for BN, capped by the 227 KB dynamic shared memory limit.
+inline int ring_stages(int bn) {
+  int ns = tc_stages();
+  while (ns > 1 && ring_smem(bn, ns) > 227u * 1024u) --ns;
+  return ns;
+}
+
 template <int BN, bool AK, bool BKM, int EPI>
 ng_status launch(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int kbps,
                  int splits, const TcEpilogue& epi) {
-  constexpr size_t smem = (size_t)kStages * (kBM * kBK * 4 + BN * kBK * 4) + 1024;
   static bool attr = false;
   if (!attr) {
     NG_CUDA_TRY(cudaFuncSetAttribute(tc_gemm_tf32_kernel<BN, AK, BKM, EPI>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_smem(BN, ring_stages(BN))));
     attr = true;
   }
+  // Only as many ring stages as k-blocks per tile: short-K tiles leave room for more
+  // co-resident CTAs per SM.
+  const int ns = std::max(1, std::min(ring_stages(BN), kbps));
   dim3 grid(ceil_div(N, BN), ceil_div(M, kBM), splits);
-  tc_gemm_tf32_kernel<BN, AK, BKM, EPI><<<grid, 128, smem, st>>>(ta, tb, M, N, K, kbps, epi);
+  tc_gemm_tf32_kernel<BN, AK, BKM, EPI><<<grid, 128, ring_smem(BN, ns), st>>>(ta, tb, M, N, K, kbps, epi, ns);
   return check_launch("tc_gemm_tf32_kernel");
 }
 
@@ -415,14 +440,13 @@ ng_status tc_gemm_tf32(cudaStream_t st, int M, int N, int K, const float* A, int
 
 template <int BN, bool AK, bool BKM, int EPI>
 ng_status launch_grouped(cudaStream_t st, const TcGroup& grp, int tiles) {
-  constexpr size_t smem = (size_t)kStages * (kBM * kBK * 4 + BN * kBK * 4) + 1024;
   static bool attr = false;
   if (!attr) {
     NG_CUDA_TRY(cudaFuncSetAttribute(tc_gemm_tf32_grouped_kernel<BN, AK, BKM, EPI>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_smem(BN, ring_stages(BN))));
     attr = true;
   }
-  tc_gemm_tf32_grouped_kernel<BN, AK, BKM, EPI><<<tiles, 128, smem, st>>>(grp);
+  tc_gemm_tf32_grouped_kernel<BN, AK, BKM, EPI><<<tiles, 128, ring_smem(BN, grp.nstages), st>>>(grp);
   return check_launch("tc_gemm_tf32_grouped_kernel");
 }
 
@@ -433,7 +457,7 @@ ng_status tc_gemm_tf32_grouped(cudaStream_t st, const TcGroupDesc* desc, int cou
   TcGroup grp;
   std::memset(&grp, 0, sizeof(grp));
   grp.count = count;
-  int tiles = 0;
+  int tiles = 0, kbps_max = 1;
   for (int g = 0; g < count; ++g) {
     const TcGroupDesc& d = desc[g];
     NG_REQUIRE(d.M >= 1 && d.N >= 1 && d.K >= 1, NG_ESHAPE, "tc_gemm_tf32_grouped: empty problem");
@@ -447,11 +471,13 @@ ng_status tc_gemm_tf32_grouped(cudaStream_t st, const TcGroupDesc* desc, int cou
     else NG_TRY(make_tmap(&P.tmB, d.B, d.N, d.K, d.ldb, 32, true));
     P.M = d.M; P.N = d.N; P.K = d.K;
     P.kbps = ceil_div(kb, sp);
+    kbps_max = std::max(kbps_max, P.kbps);
     P.tile_begin = tiles;
     P.epi = d.epi;
     if (d.splits_used) *d.splits_used = sp;
     tiles += ceil_div(d.M, kBM) * ceil_div(d.N, bn) * sp;
   }
+  grp.nstages = std::min(ring_stages(bn), kbps_max);
 #define NG_GRP(BN_, AK_, BK_, E_) return launch_grouped<BN_, AK_, BK_, E_>(st, grp, tiles)
 #define NG_GRP_E(BN_, AK_, BK_)                                         \
   switch (epi_kind) {                                                  \

@@ -64,6 +64,7 @@ struct alignas(64) TcProblem {
 struct TcGroup {
   TcProblem p[kTcGroupMax];
   int count;
+  int nstages;              // smem ring depth = min(kStages, max k-blocks per tile)
 };
 
 ng_status tc_gemm_tf32_grouped(cudaStream_t st, const TcGroupDesc* desc, int count, bool a_kmajor, bool b_kmajor,

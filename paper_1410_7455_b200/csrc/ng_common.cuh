@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <string>
 
@@ -67,6 +68,12 @@ inline ng_status check_launch(const char* what) {
     return NG_ECUDA;
   }
   return NG_OK;
+}
+
+// Integer tuning knob from the environment (read by the caller once and cached).
+inline int tune_int(const char* name, int def) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : def;
 }
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }

@@ -74,6 +74,11 @@ ng_status status_from_flags(uint32_t f, const char* where) {
 }
 
 constexpr int kApplyRows = 16, kApplyCols = 128;
+// Column tile of the tensor-core NG apply (NG_TUNE_APPLY_BN: 32, 64 or 128).
+inline int apply_bn() {
+  static const int v = tune_int("NG_TUNE_APPLY_BN", 128);
+  return (v == 32 || v == 64) ? v : 128;
+}
 constexpr int kTcMaxSplits = 32;   // split-K capacity (H, K, L) of the tensor-core path
 constexpr int kTcJSplits = 4;      // split-K of J = H^T X (K = N)
 constexpr int kMaxRank = 112;
@@ -217,8 +222,110 @@ __global__ void copy_gated_kernel(int R, int D, float* __restrict__ dst, const f
 // refresh: the R x R part of the update, one CTA, FP64
 // ------------------------------------------------------------------------------------
 
-// T = element type of the eigensolve: double (NG_FP32 path), float (NG_TF32 path).
-template <typename T>
+// Eigensolver variants of refresh_kernel:
+//   REFRESH_INPLACE  one CTA, in-place two-barrier Jacobi (any R <= kMaxRank)
+//   REFRESH_PP       one CTA, permuted ping-pong Jacobi with the eigenvectors (R <= 80)
+//   REFRESH_CLUSTER  thread-block cluster: rank 0 runs the permuted Jacobi on Z, ranks
+//                    1..nv keep column slices of the eigenvectors and apply each round's
+//                    rotations as they arrive (DSMEM ring, eig_jacobi.cuh); the shared-
+//                    memory traffic of the eigenvector update leaves the Z CTA (R <= 80)
+enum RefreshMode : int { REFRESH_INPLACE = 0, REFRESH_PP = 1, REFRESH_CLUSTER = 2 };
+constexpr int kPPRing = 16;
+
+// Shared-memory plan (offsets in doubles from the 16-byte aligned dynamic base).
+struct RefreshSmem {
+  int R, npad, m, ldp, LD, LDV, mp, mode, nv, w;
+  size_t o_bar, o_cmd, o_d, o_lam, o_share, o_z0, o_z1, o_v0, o_v1, o_cs, o_ring, o_int, total_bytes;
+};
+__host__ __device__ inline RefreshSmem refresh_plan(int R, int mode) {
+  RefreshSmem p;
+  p.R = R;
+  p.npad = R + (R & 1);
+  p.m = p.npad / 2;
+  p.ldp = pp_ldp(p.npad);
+  p.LD = R + 1;
+  p.LDV = (R + 3) / 4 * 4;
+  p.mp = R / 2 + 1;
+  p.mode = mode;
+  p.nv = 0;
+  p.w = 0;
+  if (mode == REFRESH_CLUSTER) {
+    const int items = p.m * p.npad / 2;                 // (pair, double2 column) items
+    p.nv = (items + 1023) / 1024;
+    const int w = (p.npad + p.nv - 1) / p.nv;
+    p.w = w + (w & 1);
+  }
+  size_t o = 0;
+  p.o_bar = o;  o += kPPRing;                          // ring mbarriers (empty: rank 0, full: V ranks)
+  p.o_cmd = o;  o += kPPRing / 2;                      // ring command words (u32)
+  p.o_d = o;    o += 5 * (size_t)R + 32;               // d, emh, dr, c, dn, red[32]
+  p.o_lam = o;  o += (size_t)p.npad + 2;               // eigenvalues (slot / index order)
+  p.o_share = o; o += (size_t)R;                       // A_t row factors (cluster)
+  o = (o + 1) & ~(size_t)1;                            // 16-byte alignment
+  if (mode == REFRESH_INPLACE) {
+    p.o_z0 = o; o += ((size_t)R * p.LD + 1) & ~(size_t)1;
+    p.o_z1 = p.o_z0;
+    p.o_v0 = o; o += (size_t)R * p.LDV;
+    p.o_v1 = p.o_v0;
+    p.o_cs = o; o += 2 * (size_t)p.mp + 2;
+    p.o_ring = o;
+  } else {
+    const size_t zsz = (size_t)p.m * p.ldp;
+    const size_t vsz = (size_t)p.npad * (mode == REFRESH_PP ? p.npad : p.w);
+    const size_t z_part = 2 * zsz + 4 * (size_t)p.m;                   // rank 0 (and PP)
+    const size_t v_part = (mode == REFRESH_PP) ? 2 * vsz : 2 * vsz + 2 * (size_t)kPPRing * p.m;
+    p.o_z0 = o; p.o_z1 = o + zsz; p.o_cs = o + 2 * zsz;
+    if (mode == REFRESH_PP) {
+      p.o_v0 = o + z_part; p.o_v1 = p.o_v0 + vsz; p.o_ring = p.o_v1 + vsz;
+      o += z_part + v_part;
+    } else {   // the V ranks reuse the Z region
+      p.o_v0 = o; p.o_v1 = o + vsz; p.o_ring = o + 2 * vsz;
+      o += (z_part > v_part ? z_part : v_part);
+    }
+  }
+  p.o_int = o;
+  // ints: perm[npad], nrot[64 + 2 mp], iflag, phantom, fb, offmax[32] (float)
+  p.total_bytes = sizeof(double) * o + sizeof(int) * ((size_t)p.npad + 64 + 2 * p.mp + 3 + 32) + 64;
+  return p;
+}
+
+// V ranks of the cluster refresh: rotate the eigenvector slice, then write their columns
+// of A_t from the row factors / permutation rank 0 publishes.
+__device__ void refresh_vrank(const RefreshSmem& P, uint32_t rank, double* sm, float* __restrict__ Amat) {
+  const int R = P.R, tid = threadIdx.x, nt = blockDim.x;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + P.o_bar);
+  uint32_t* cmd = reinterpret_cast<uint32_t*>(sm + P.o_cmd);
+  PPCluster cl{P.nv, kPPRing, sh_addr(sm + P.o_ring), sh_addr(cmd), sh_addr(bars), sh_addr(bars)};
+  if (tid == 0) {
+    for (int s2 = 0; s2 < kPPRing; ++s2) mb_init(cl.full_bar + 8u * s2, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s2 = 0; s2 < kPPRing; ++s2) mb_arm(cl.full_bar + 8u * s2, 16u * P.m + 4u);
+  }
+  cl_sync();   // (0) every barrier of the cluster initialised
+  const int j0 = ((int)rank - 1) * P.w;
+  double* V0 = sm + P.o_v0;
+  double* V1 = sm + P.o_v1;
+  const int rounds = jacobi_pp_vworker(V0, V1, R, j0, P.w, reinterpret_cast<const double2*>(sm + P.o_ring), cmd, cl);
+  const double* Vf = (rounds & 1) ? V1 : V0;
+  cl_sync();   // (1) rank 0 published perm, row factors, E_t^{-1/2}
+  double* fr = sm + P.o_share;
+  double* emh = sm + P.o_d + R;
+  int* perm = reinterpret_cast<int*>(sm + P.o_int);
+  for (int i = tid; i < R; i += nt) {
+    fr[i] = ld_cluster_d(cl_map(sh_addr(fr + i), 0));
+    emh[i] = ld_cluster_d(cl_map(sh_addr(emh + i), 0));
+    perm[i] = ld_cluster_i(cl_map(sh_addr(perm + i), 0));
+  }
+  __syncthreads();
+  const int jn = min(R, j0 + P.w) - j0;
+  for (int idx = tid; idx < R * (jn > 0 ? jn : 0); idx += nt) {
+    const int r = idx / jn, jj = idx - r * jn, j = j0 + jj;
+    Amat[r * R + j] = (float)(fr[r] * Vf[perm[r] * P.w + jj] * emh[j]);
+  }
+  cl_sync();   // (2) rank 0's shared memory is no longer read
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(1024)
 refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
                const float* __restrict__ KL, double* __restrict__ dstate,
@@ -226,25 +333,34 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
                float* __restrict__ svec, int* __restrict__ flags, int dbg_mask) {
   extern __shared__ __align__(16) unsigned char ng_smem[];
   double* sm = reinterpret_cast<double*>(ng_smem);
-  const int LD = R + 1;                 // odd row stride of Z: fewer bank conflicts
-  const int LDV = (R + 3) / 4 * 4;      // eigenvector rows: 16-byte vectors
-  const int mp = R / 2 + 1;             // >= number of rotation pairs
-  double* d = sm;                       // R   old d
+  const RefreshSmem P = refresh_plan(R, MODE);
+  PPCluster cl{};
+  if constexpr (MODE == REFRESH_CLUSTER) {
+    const uint32_t rank = cl_rank();
+    if (rank != 0) { refresh_vrank(P, rank, sm, Amat); return; }
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + P.o_bar);
+    cl = PPCluster{P.nv, kPPRing, sh_addr(sm + P.o_ring), sh_addr(sm + P.o_cmd), sh_addr(bars), sh_addr(bars)};
+    if (threadIdx.x == 0) {
+      for (int s2 = 0; s2 < kPPRing; ++s2) mb_init(cl.empty_bar + 8u * s2, (uint32_t)P.nv);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cl_sync();   // (0)
+  }
+  double* d = sm + P.o_d;               // R   old d
   double* emh = d + R;                  // R   E_t^{-1/2}
   double* dr = emh + R;                 // R   d + rho
   double* c = dr + R;                   // R   sorted eigenvalues
   double* dn = c + R;                   // R   new d
   double* red = dn + R;                 // 32 reduction scratch
-  T* Z = reinterpret_cast<T*>(red + 32 + (R & 1));                          // R*LD, 16-byte aligned
-  constexpr int kVec = 16 / sizeof(T);
-  T* Vt = Z + (R * LD + kVec - 1) / kVec * kVec;   // R*LDV, 16-byte aligned (Z is)
-  T* jc = Vt + R * LDV;                 // 2*mp: (c, s) pairs (16-byte aligned: R*LDV even)
-  T* js = jc + mp;                      // (unused by the packed layout)
-  int* perm = reinterpret_cast<int*>(js + mp + 2);   // R
-  int* nrot = perm + R;                 // 32 per-warp sweep counts, 32 spare, then mp pair table
-  int* iflag = nrot + 64 + mp;          // 1 (floored)
-  float* offmax = reinterpret_cast<float*>(iflag + 1);  // 32 (per-warp max ratio)
+  double* lam = sm + P.o_lam;           // eigenvalues
+  int* perm = reinterpret_cast<int*>(sm + P.o_int);   // npad
+  int* nrot = perm + P.npad;            // 32 per-warp sweep counts, 32 spare, then 2*mp pair table
+  int* iflag = nrot + 64 + 2 * P.mp;    // floored
+  int* phantom = iflag + 1;
+  int* fbuf = phantom + 1;
+  float* offmax = reinterpret_cast<float*>(fbuf + 1);  // 32 (per-warp max ratio)
   const int tid = threadIdx.x, nt = blockDim.x;
+  constexpr bool PPK = MODE != REFRESH_INPLACE;
 
   const double rho = dstate[0];
   for (int i = tid; i < R; i += nt) d[i] = dstate[1 + i];
@@ -265,37 +381,75 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   const float* K = KL;
   const float* L = KL + R * R;
   const double a1 = eta * eta / ((double)N * N), a2 = (1.0 - eta) * (1.0 - eta), a3 = eta * (1.0 - eta) / N;
-  for (int idx = tid; idx < R * R; idx += nt) {
-    const int i = idx / R, j = idx % R;
+  auto zval = [&](int i, int j) -> double {
     const double ks = 0.5 * ((double)K[i * R + j] + (double)K[j * R + i]);
     const double ls = 0.5 * ((double)L[i * R + j] + (double)L[j * R + i]);
     double z = a1 * emh[i] * ks * emh[j] + a3 * emh[i] * ls * emh[j] * (dr[i] + dr[j]);
     if (i == j) z += a2 * dr[i] * dr[i];
-    Z[i * LD + j] = (T)z;
+    return z;
+  };
+  double* Z = sm + P.o_z0;
+  if (PPK) {
+    // slot-pair block layout, upper block triangle (eig_jacobi.cuh), zero padding row
+    const int np = P.npad;
+    for (int idx = tid; idx < np * np; idx += nt) {
+      const int i = idx / np, j = idx % np;
+      if ((i >> 1) > (j >> 1)) continue;
+      Z[(i >> 1) * P.ldp + 2 * j + (i & 1)] = (i < R && j < R) ? zval(i, j) : 0.0;
+    }
+  } else {
+    for (int idx = tid; idx < R * R; idx += nt) {
+      const int i = idx / R, j = idx % R;
+      Z[i * P.LD + j] = zval(i, j);
+    }
+  }
+  double zmax = 0.0;
+  for (int i = tid; i < R; i += nt) zmax = fmax(zmax, fabs(zval(i, i)));
+  zmax = block_max(zmax, red);   // (its barriers also complete Z)
+  // Z = U C U^T (eqn:zt:eig:repeat).  rel_tol 1e-7: rotations stop once every
+  // |z_pq| <= 1e-7 sqrt(z_pp z_qq) (eigenvector error ~1e-7 / relative gap, far below the
+  // FP32 storage of A_t and W_{t+1})
+  int sweeps;
+  const double* V = nullptr;   // eigenvector rows (index / slot order), row stride ldv
+  int ldv = 0, nlam;
+  if (PPK) {
+    JacobiPPBuf jb{{sm + P.o_z0, sm + P.o_z1}, {sm + P.o_v0, sm + P.o_v1},
+                   reinterpret_cast<double2*>(sm + P.o_cs), nrot, offmax};
+    int fb_local = 0;
+    if (MODE == REFRESH_CLUSTER)
+      sweeps = jacobi_pp<false>(jb, R, 20, 1e-15 * zmax, 1e-7, &fb_local, phantom, dbg_mask, cl);
+    else
+      sweeps = jacobi_pp<true>(jb, R, 20, 1e-15 * zmax, 1e-7, &fb_local, phantom, dbg_mask, cl);
+    __syncthreads();
+    const double* Zf = fb_local ? jb.Z[1] : jb.Z[0];
+    const int ph = *phantom;
+    for (int s2 = tid; s2 < P.npad; s2 += nt)
+      lam[s2] = (s2 == ph) ? -INFINITY : Zf[(s2 >> 1) * P.ldp + 2 * s2 + (s2 & 1)];
+    V = fb_local ? jb.V[1] : jb.V[0];
+    ldv = P.npad;
+    nlam = P.npad;
+  } else {
+    JacobiSmem<double> scr{sm + P.o_cs, sm + P.o_cs + P.mp, nrot, offmax};
+    double* Vt = sm + P.o_v0;
+    sweeps = jacobi_eig_smem<double>(Z, P.LD, Vt, P.LDV, R, scr, 20, 1e-15 * zmax, 1e-7, dbg_mask);
+    for (int i = tid; i < R; i += nt) lam[i] = Z[i * P.LD + i];
+    V = Vt;
+    ldv = P.LDV;
+    nlam = R;
   }
   __syncthreads();
-  double zmax = 0.0;
-  for (int i = tid; i < R; i += nt) zmax = fmax(zmax, fabs(Z[i * LD + i]));
-  zmax = block_max(zmax, red);
-  // Z = U C U^T (eqn:zt:eig:repeat)
-  const bool dbl = sizeof(T) == 8;
-  JacobiSmem<T> scr{jc, js, nrot, offmax};
-  // rel_tol 1e-7: rotations stop once every |z_pq| <= 1e-7 sqrt(z_pp z_qq) (eigenvector error
-  // ~1e-7 / relative gap, far below the FP32 storage of A_t and W_{t+1})
-  const int sweeps = jacobi_eig_smem<T>(Z, LD, Vt, LDV, R, scr, 20, (dbl ? 1e-15 : 1e-9) * zmax, dbl ? 1e-7 : 1e-6,
-                                        dbg_mask);
   // descending order
-  for (int i = tid; i < R; i += nt) {
-    const double li = (double)Z[i * LD + i];
+  for (int i = tid; i < nlam; i += nt) {
+    const double li = lam[i];
     int r = 0;
-    for (int j = 0; j < R; ++j) { const double lj = (double)Z[j * LD + j]; r += (lj > li) || (lj == li && j < i); }
+    for (int j = 0; j < nlam; ++j) { const double lj = lam[j]; r += (lj > li) || (lj == li && j < i); }
     perm[r] = i;
   }
   __syncthreads();
   // floor C at (1-eta)^2 rho_t^2 (reading R13)
   const double cf = a2 * rho * rho;
   for (int r = tid; r < R; r += nt) {
-    double cr = (double)Z[perm[r] * LD + perm[r]];
+    double cr = lam[perm[r]];
     if (cr < cf) { cr = cf; atomicOr(iflag, 1); }
     c[r] = cr;
   }
@@ -314,10 +468,20 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   sdn = block_sum(sdn, red);
   const double beta_new = rho_new * (1.0 + alpha) + (alpha / D) * sdn;
   // A_t = (eta/N) E_{t+1}^{1/2} C^{-1/2} U^T E_t^{-1/2}
-  for (int idx = tid; idx < R * R; idx += nt) {
-    const int r = idx / R, j = idx % R;
-    const double en = 1.0 / (beta_new / dn[r] + 1.0);
-    Amat[idx] = (float)((eta / N) * sqrt(en) / sqrt(c[r]) * (double)Vt[perm[r] * LDV + j] * emh[j]);
+  if (MODE == REFRESH_CLUSTER) {
+    // row factors for the V ranks, which hold U (eig_jacobi.cuh); they write A_t
+    double* fr = sm + P.o_share;
+    for (int r = tid; r < R; r += nt) {
+      const double en = 1.0 / (beta_new / dn[r] + 1.0);
+      fr[r] = (eta / N) * sqrt(en) / sqrt(c[r]);
+    }
+    cl_sync();   // (1) published
+  } else {
+    for (int idx = tid; idx < R * R; idx += nt) {
+      const int r = idx / R, j = idx % R;
+      const double en = 1.0 / (beta_new / dn[r] + 1.0);
+      Amat[idx] = (float)((eta / N) * sqrt(en) / sqrt(c[r]) * V[perm[r] * ldv + j] * emh[j]);
+    }
   }
   // row scale of B_t with the OLD d, rho
   for (int k = tid; k < R; k += nt) svec[k] = (float)((N * (1.0 - eta) / eta) * dr[k]);
@@ -340,6 +504,7 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
     flags[4] = sweeps;
     if (!isfinite(rho_new) || !isfinite(sdn)) atomicOr(reinterpret_cast<unsigned*>(flags + 3), kErrNonFinite);
   }
+  if (MODE == REFRESH_CLUSTER) cl_sync();   // (2) the V ranks are done with this CTA's shared memory
 }
 
 // B.3.1 (reading R5): O = E^{-1/2} (W W^T) E^{-1/2} for the NEW state; if
@@ -527,11 +692,6 @@ __global__ void passthrough_kernel(int n, float* p, float* p_out, float* g, floa
 // host side
 // ------------------------------------------------------------------------------------
 
-static size_t refresh_smem_bytes(int R, size_t tsize) {
-  const int mp = R / 2 + 1;
-  const size_t tcount = (size_t)R * (R + 1) + (size_t)R * ((R + 3) / 4 * 4) + 2 * mp + 2 + 16 / tsize;
-  return sizeof(double) * (5 * (size_t)R + 33) + tsize * tcount + sizeof(int) * (R + 100 + mp) + 64;
-}
 static size_t reorth_smem_bytes(int R) { return sizeof(double) * (2 * R * R + R + 32); }
 
 template <typename T>
@@ -545,8 +705,12 @@ static ng_status dalloc(T** p, size_t count) {
 static ng_status set_kernel_attrs() {
   static bool done = false;
   if (done) return NG_OK;
-  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)refresh_smem_bytes(kMaxRank, sizeof(double))));
+  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<REFRESH_INPLACE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)refresh_plan(kMaxRank, REFRESH_INPLACE).total_bytes));
+  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<REFRESH_PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)refresh_plan(kJacobiPPMax, REFRESH_PP).total_bytes));
+  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<REFRESH_CLUSTER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)refresh_plan(kJacobiPPMax, REFRESH_CLUSTER).total_bytes));
   NG_CUDA_TRY(cudaFuncSetAttribute(reorth_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)reorth_smem_bytes(kMaxRank)));
   NG_CUDA_TRY(cudaFuncSetAttribute(apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -586,7 +750,7 @@ ng_status ngsgd_create_impl(int dim, int max_rows, const ngsgd_config* cfg, cuda
     h->kl_splits = std::max(h->kl_splits, kTcMaxSplits);
     l_splits = std::max(l_splits, kTcMaxSplits);
   }
-  h->ctiles = ceil_div(dim, kApplyCols);
+  h->ctiles = ceil_div(dim, 32);   // partial-norm slots for the narrowest column tiling
   ng_status s = NG_OK;
 #define ALLOC(ptr, cnt) if (s == NG_OK) s = dalloc(&(ptr), (size_t)(cnt))
   ALLOC(h->W[0], (size_t)R * h->ldw);
@@ -735,8 +899,38 @@ static ng_status launch_refresh_chain(ngsgd_ctx* h, int n, double eta) {
     // FP32 solve leaves R_{t+1} non-orthonormal beyond 1e-3 and B.3.1 repairs would fire on
     // most updates (measured on the config-3 network).
     static const int dbg = getenv("NG_PROFILE_JACOBI_MASK") ? atoi(getenv("NG_PROFILE_JACOBI_MASK")) : 0;
-    refresh_kernel<double><<<1, 1024, refresh_smem_bytes(R, sizeof(double)), ss>>>(
-        R, D, n, eta, a_, e_, h->KL, h->dstate, h->sums, h->Amat, h->svec, h->flags, dbg);
+    // Solver choice: the cluster split for R >= 48 (where the eigenvector update dominates
+    // the shared-memory traffic), the one-CTA permuted solver below, the in-place solver
+    // beyond kJacobiPPMax.  NG_TUNE_EIG_MODE = 0/1/2 forces one (comparisons only).
+    static const int force = tune_int("NG_TUNE_EIG_MODE", -1);
+    int mode = R > kJacobiPPMax || R < 2 ? REFRESH_INPLACE : (R >= 48 ? REFRESH_CLUSTER : REFRESH_PP);
+    if (force >= 0 && (force == REFRESH_INPLACE || R <= kJacobiPPMax) && (force != REFRESH_CLUSTER || R >= 8))
+      mode = force;
+    const RefreshSmem plan = refresh_plan(R, mode);
+    if (mode == REFRESH_CLUSTER) {
+      cudaLaunchConfig_t lc;
+      std::memset(&lc, 0, sizeof(lc));
+      lc.gridDim = dim3(1 + plan.nv, 1, 1);
+      lc.blockDim = dim3(1024, 1, 1);
+      lc.dynamicSmemBytes = plan.total_bytes;
+      lc.stream = ss;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 1 + plan.nv;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      NG_CUDA_TRY(cudaLaunchKernelEx(&lc, refresh_kernel<REFRESH_CLUSTER>, R, D, n, eta, a_, e_,
+                                     (const float*)h->KL, h->dstate, (const double*)h->sums, h->Amat, h->svec,
+                                     h->flags, dbg));
+    } else if (mode == REFRESH_PP) {
+      refresh_kernel<REFRESH_PP><<<1, 1024, plan.total_bytes, ss>>>(R, D, n, eta, a_, e_, h->KL, h->dstate,
+                                                                    h->sums, h->Amat, h->svec, h->flags, dbg);
+    } else {
+      refresh_kernel<REFRESH_INPLACE><<<1, 1024, plan.total_bytes, ss>>>(R, D, n, eta, a_, e_, h->KL, h->dstate,
+                                                                         h->sums, h->Amat, h->svec, h->flags, dbg);
+    }
     NG_TRY(check_launch("refresh_kernel"));
   }
   ProfScope ps(NG_PROF_NG_REFRESH, ss, 2.0 * (double)R * R * D + 2.0 * R * D, 4.0 * (4.0 * R * D));
@@ -881,17 +1075,19 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
   // X_hat = X - H W in place, with partial row norms
   {
     ProfScope ps(NG_PROF_NG_APPLY, st, 2.0 * nRD, 4.0 * (2.0 * n * D + (double)R * D));
+    int tiles = ceil_div(D, kApplyCols);
     if (tc) {
       TcEpilogue e;
       e.kind = TC_EPI_NGAPPLY; e.C = x; e.ldc = ld; e.xx = h->xxpart; e.pp = h->ppart; e.part_ld = h->max_rows;
-      NG_TRY(tc_gemm_tf32(st, n, D, R, h->H, R, true, W, h->ldw, false, e, 128, 1));
+      NG_TRY(tc_gemm_tf32(st, n, D, R, h->H, R, true, W, h->ldw, false, e, apply_bn(), 1));
+      tiles = ceil_div(D, apply_bn());
     } else {
       dim3 grid(ceil_div(n, kApplyRows), ceil_div(D, kApplyCols));
       const size_t smem = sizeof(float) * (kApplyRows * R + R * kApplyCols);
       apply_kernel<<<grid, 256, smem, st>>>(n, D, R, x, ld, h->H, W, h->ldw, h->xxpart, h->ppart, h->max_rows);
       NG_TRY(check_launch("apply_kernel"));
     }
-    finalize_kernel<<<1, 512, 0, st>>>(n, h->ctiles, h->xxpart, h->ppart, h->max_rows, h->p, p_out, h->sums,
+    finalize_kernel<<<1, 512, 0, st>>>(n, tiles, h->xxpart, h->ppart, h->max_rows, h->p, p_out, h->sums,
                                        h->gamma, gamma_out, h->flags);
     NG_TRY(check_launch("finalize_kernel"));
   }
@@ -1115,12 +1311,12 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
       q.epi.kind = TC_EPI_NGAPPLY; q.epi.C = c.x; q.epi.ldc = c.ld; q.epi.xx = h->xxpart; q.epi.pp = h->ppart;
       q.epi.part_ld = h->max_rows;
       q.splits_used = nullptr;
-      fg.n[g] = c.n; fg.tiles[g] = h->ctiles; fg.xxpart[g] = h->xxpart; fg.ppart[g] = h->ppart;
+      fg.n[g] = c.n; fg.tiles[g] = ceil_div(D, apply_bn()); fg.xxpart[g] = h->xxpart; fg.ppart[g] = h->ppart;
       fg.part_ld[g] = h->max_rows; fg.p_int[g] = h->p; fg.p_out[g] = c.p_out; fg.sums[g] = h->sums;
       fg.gamma_int[g] = h->gamma; fg.gamma_out[g] = c.gamma_out; fg.flags[g] = h->flags;
     }
     ProfScope ps(NG_PROF_NG_APPLY, st, flops, bytes);
-    NG_TRY(tc_gemm_tf32_grouped(st, d.data(), G, true, false, TC_EPI_NGAPPLY, 128));
+    NG_TRY(tc_gemm_tf32_grouped(st, d.data(), G, true, false, TC_EPI_NGAPPLY, apply_bn()));
     finalize_group_kernel<<<G, 512, 0, st>>>(fg);
     NG_TRY(check_launch("finalize_group_kernel"));
   }

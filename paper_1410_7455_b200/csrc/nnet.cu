@@ -24,6 +24,7 @@
 
 using namespace ng;
 
+constexpr int kMaxRowWidth = 50000;   // widest activation row staged in shared memory
 constexpr int kBwdSplits = 6;   // split-K of the TF32 backward-data GEMM (K = 3000..5000)
 
 struct nnet_ctx {
@@ -100,36 +101,53 @@ __global__ void input_kernel(int n, int din, const float* __restrict__ f, int64_
   }
 }
 
+// One row of Z staged in shared memory with 16-byte loads (rows are 16B aligned: ld % 8 == 0).
+__device__ __forceinline__ void stage_row(float* __restrict__ dst, const float* __restrict__ src, int cnt) {
+  const int c4 = cnt >> 2;
+  for (int i = threadIdx.x; i < c4; i += blockDim.x)
+    reinterpret_cast<float4*>(dst)[i] = __ldg(reinterpret_cast<const float4*>(src) + i);
+  for (int i = (c4 << 2) + threadIdx.x; i < cnt; i += blockDim.x) dst[i] = __ldg(src + i);
+}
+
 // p-norm, p = 2: a_j = sqrt(sum_{k in group j} z_k^2); Y_next = [a, 1].
-__global__ void pnorm_kernel(int n, int dout, int ldz, int G, const float* __restrict__ Z, float* __restrict__ Yn,
-                             int ldy) {
-  const int dp = dout / G;
-  const int64_t total = (int64_t)n * ldy;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(i / ldy), c = (int)(i % ldy);
+// One CTA per row; the row of Z is read once, coalesced, into shared memory.
+__global__ void __launch_bounds__(256)
+pnorm_kernel(int n, int dout, int ldz, int G, const float* __restrict__ Z, float* __restrict__ Yn, int ldy) {
+  extern __shared__ __align__(16) unsigned char nn_smem[];
+  float* zs = reinterpret_cast<float*>(nn_smem);
+  const int r = blockIdx.x, dp = dout / G;
+  stage_row(zs, Z + (int64_t)r * ldz, dout);
+  __syncthreads();
+  float* y = Yn + (int64_t)r * ldy;
+  for (int c = threadIdx.x; c < ldy; c += blockDim.x) {
     float v = 0.f;
     if (c < dp) {
-      const float* z = Z + (int64_t)r * ldz + (int64_t)c * G;
       float s = 0.f;
-      for (int k = 0; k < G; ++k) s = fmaf(z[k], z[k], s);
+      for (int k = 0; k < G; ++k) s = fmaf(zs[c * G + k], zs[c * G + k], s);
       v = sqrtf(s);
-    } else if (c == dp) v = 1.f;
-    Yn[i] = v;
+    } else if (c == dp) {
+      v = 1.f;
+    }
+    y[c] = v;
   }
 }
 
-// log p(y|x) = z_y - logsumexp(z); X_L = onehot(y) - softmax(z); one CTA per row.
+// log p(y|x) = z_y - logsumexp(z); X_L = onehot(y) - softmax(z); one CTA per row,
+// the row staged once in shared memory.
 __global__ void __launch_bounds__(256)
 softmax_kernel(int n, int C, int ld, const float* __restrict__ Z, const int32_t* __restrict__ labels,
                float* __restrict__ X, double* __restrict__ objrows, int* eflags) {
+  extern __shared__ __align__(16) unsigned char nn_smem[];
   __shared__ float sc[32];
+  float* zs = reinterpret_cast<float*>(nn_smem);
   const int r = blockIdx.x;
-  const float* z = Z + (int64_t)r * ld;
+  stage_row(zs, Z + (int64_t)r * ld, C);
+  __syncthreads();
   float m = -INFINITY;
-  for (int j = threadIdx.x; j < C; j += blockDim.x) m = fmaxf(m, z[j]);
+  for (int j = threadIdx.x; j < C; j += blockDim.x) m = fmaxf(m, zs[j]);
   m = block_max(m, sc);
   float s = 0.f;
-  for (int j = threadIdx.x; j < C; j += blockDim.x) s += expf(z[j] - m);
+  for (int j = threadIdx.x; j < C; j += blockDim.x) s += expf(zs[j] - m);
   s = block_sum(s, sc);
   const float lse = m + logf(s);
   int y = labels[r];
@@ -138,9 +156,17 @@ softmax_kernel(int n, int C, int ld, const float* __restrict__ Z, const int32_t*
     y = -1;
   }
   float* x = X + (int64_t)r * ld;
-  for (int j = threadIdx.x; j < C; j += blockDim.x) x[j] = (j == y ? 1.f : 0.f) - expf(z[j] - lse);
+  const int c4 = C >> 2;
+  for (int i = threadIdx.x; i < c4; i += blockDim.x) {
+    const float4 z = reinterpret_cast<const float4*>(zs)[i];
+    const int j = i << 2;
+    reinterpret_cast<float4*>(x)[i] =
+        make_float4((j == y ? 1.f : 0.f) - expf(z.x - lse), (j + 1 == y ? 1.f : 0.f) - expf(z.y - lse),
+                    (j + 2 == y ? 1.f : 0.f) - expf(z.z - lse), (j + 3 == y ? 1.f : 0.f) - expf(z.w - lse));
+  }
+  for (int j = (c4 << 2) + threadIdx.x; j < C; j += blockDim.x) x[j] = (j == y ? 1.f : 0.f) - expf(zs[j] - lse);
   if (threadIdx.x == 0) {
-    objrows[r] = (y >= 0) ? (double)(z[y] - lse) : 0.0;
+    objrows[r] = (y >= 0) ? (double)(zs[y] - lse) : 0.0;
     if (!isfinite(lse)) atomicOr(reinterpret_cast<unsigned*>(eflags), kErrNonFinite);
   }
 }
@@ -171,19 +197,34 @@ struct EpiPnormBack {
 };
 
 // TF32 path: g = sum_z partial_z (fixed order), then the p-norm backward of EpiPnormBack.
-__global__ void pnorm_back_kernel(const float* __restrict__ part, int splits, int n, int din, const float* __restrict__ Zp,
-                                  const float* __restrict__ Yl, float* __restrict__ Xp, int ldx, int ldy, int G) {
+// One CTA per row: g / a_j for the row's din groups into shared memory, then the row of
+// X_{l-1} = (g/a) z with 16-byte coalesced loads of Z and stores of X.
+__global__ void __launch_bounds__(256)
+pnorm_back_kernel(const float* __restrict__ part, int splits, int n, int din, const float* __restrict__ Zp,
+                  const float* __restrict__ Yl, float* __restrict__ Xp, int ldx, int ldy, int G) {
+  extern __shared__ __align__(16) unsigned char nn_smem[];
+  float* ga = reinterpret_cast<float*>(nn_smem);
+  const int r = blockIdx.x;
   const int64_t total = (int64_t)n * din;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int j = threadIdx.x; j < din; j += blockDim.x) {
+    const int64_t i = (int64_t)r * din + j;
     float g = 0.f;
     for (int z = 0; z < splits; ++z) g += part[(int64_t)z * total + i];
-    const int r = (int)(i / din), j = (int)(i % din);
     const float a = Yl[(int64_t)r * ldy + j];
-    const float* zz = Zp + (int64_t)r * ldx + (int64_t)j * G;
-    float* xo = Xp + (int64_t)r * ldx + (int64_t)j * G;
-    const float ga = a > 0.f ? g / a : 0.f;
-    for (int q = 0; q < G; ++q) xo[q] = ga * zz[q];
+    ga[j] = a > 0.f ? g / a : 0.f;
   }
+  __syncthreads();
+  const int dout = din * G;
+  const float* zr = Zp + (int64_t)r * ldx;
+  float* xr = Xp + (int64_t)r * ldx;
+  const int c4 = dout >> 2;
+  for (int i = threadIdx.x; i < c4; i += blockDim.x) {
+    const float4 z = __ldg(reinterpret_cast<const float4*>(zr) + i);
+    const int k = i << 2;
+    reinterpret_cast<float4*>(xr)[i] =
+        make_float4(ga[k / G] * z.x, ga[(k + 1) / G] * z.y, ga[(k + 2) / G] * z.z, ga[(k + 3) / G] * z.w);
+  }
+  for (int k = (c4 << 2) + threadIdx.x; k < dout; k += blockDim.x) xr[k] = ga[k / G] * zr[k];
 }
 
 // plain SGD (precond = 0): p_i = ||row_i||^2, gamma = 1
@@ -289,6 +330,18 @@ ng_status nnet_create(const nnet_config* cfg, void* cuda_stream, nnet_t* out) {
   NG_REQUIRE(cfg->precision == NG_FP32 || cfg->precision == NG_TF32, NG_EINVAL,
              "precision must be NG_FP32 or NG_TF32 (NG_BF16 is reserved)");
   NG_REQUIRE(cfg->num_hidden + 1 <= 16, NG_EINVAL, "at most 16 weight matrices");
+  NG_REQUIRE(cfg->hidden_dim <= kMaxRowWidth && cfg->num_classes <= kMaxRowWidth, NG_ESHAPE,
+             "hidden_dim and num_classes must be <= 50000 (one row staged in shared memory)");
+  {
+    static bool attr = false;
+    if (!attr) {
+      const int b = (int)(sizeof(float) * kMaxRowWidth);
+      NG_CUDA_TRY(cudaFuncSetAttribute(pnorm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+      NG_CUDA_TRY(cudaFuncSetAttribute(softmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+      NG_CUDA_TRY(cudaFuncSetAttribute(pnorm_back_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, b));
+      attr = true;
+    }
+  }
   nnet_ctx* h = new nnet_ctx();
   h->cfg = *cfg;
   h->st = (cudaStream_t)cuda_stream;
@@ -404,19 +457,21 @@ ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const
     if (tc) {
       TcEpilogue e;
       e.kind = TC_EPI_STORE; e.C = h->Z[l]; e.ldc = h->ldr[l];
-      NG_TRY(tc_gemm_tf32(st, n, h->rows[l], h->cols[l], h->Y[l], h->ldp[l], true, W, h->ldp[l], true, e, 128, 1));
+      static const int bn = tune_int("NG_TUNE_FWD_BN", 128);
+      NG_TRY(tc_gemm_tf32(st, n, h->rows[l], h->cols[l], h->Y[l], h->ldp[l], true, W, h->ldp[l], true, e, bn, 1));
     } else {
       NG_TRY((gemm_simt<float, true, true>(st, n, h->rows[l], h->cols[l], h->Y[l], h->ldp[l], W, h->ldp[l],
                                            EpiStore<float>{h->Z[l], h->ldr[l], 1.f})));
     }
     if (l < L - 1) {
       const int64_t tot = (int64_t)n * h->ldp[l + 1];
-      pnorm_kernel<<<std::min(4096, ceil_div(tot, 256)), 256, 0, st>>>(n, h->rows[l], h->ldr[l], G, h->Z[l],
-                                                                       h->Y[l + 1], h->ldp[l + 1]);
+      (void)tot;
+      pnorm_kernel<<<n, 256, sizeof(float) * h->rows[l], st>>>(n, h->rows[l], h->ldr[l], G, h->Z[l], h->Y[l + 1],
+                                                               h->ldp[l + 1]);
       NG_TRY(check_launch("pnorm_kernel"));
     }
   }
-  softmax_kernel<<<n, 256, 0, st>>>(n, h->rows[L - 1], h->ldr[L - 1], h->Z[L - 1], labels, h->X[L - 1], h->objrows,
+  softmax_kernel<<<n, 256, sizeof(float) * h->rows[L - 1], st>>>(n, h->rows[L - 1], h->ldr[L - 1], h->Z[L - 1], labels, h->X[L - 1], h->objrows,
                                     h->eflags);
   NG_TRY(check_launch("softmax_kernel"));
   // backward with the pre-update weights (reading R21)
@@ -430,10 +485,13 @@ ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const
       TcEpilogue e;
       e.kind = TC_EPI_PARTIAL; e.C = h->gpart; e.ldc = din; e.zstride = (int64_t)n * din;
       int sp = 1;
-      NG_TRY(tc_gemm_tf32(st, n, din, h->rows[l], h->X[l], h->ldr[l], true, W, h->ldp[l], false, e, 64, kBwdSplits,
+      static const int bn = tune_int("NG_TUNE_BWD_BN", 64);
+      static const int splits = std::min(kBwdSplits, std::max(1, tune_int("NG_TUNE_BWD_SPLITS", kBwdSplits)));
+      NG_TRY(tc_gemm_tf32(st, n, din, h->rows[l], h->X[l], h->ldr[l], true, W, h->ldp[l], false, e, bn, splits,
                           &sp));
       const int64_t tot = (int64_t)n * din;
-      pnorm_back_kernel<<<std::min(4096, ceil_div(tot, 256)), 256, 0, st>>>(h->gpart, sp, n, din, h->Z[l - 1], h->Y[l],
+      (void)tot;
+      pnorm_back_kernel<<<n, 256, sizeof(float) * din, st>>>(h->gpart, sp, n, din, h->Z[l - 1], h->Y[l],
                                                                             h->X[l - 1], h->ldr[l - 1], h->ldp[l], G);
       NG_TRY(check_launch("pnorm_back_kernel"));
     } else {
@@ -491,7 +549,8 @@ ng_status nnet_update(nnet_t h, float lr, float max_change_per_sample, nnet_upda
     if (tc) {
       TcEpilogue e;
       e.kind = TC_EPI_AXPY; e.C = W; e.ldc = h->ldp[l]; e.scale = h->scale + l;
-      NG_TRY(tc_gemm_tf32(st, h->rows[l], h->cols[l], n, h->X[l], h->ldr[l], false, h->Y[l], h->ldp[l], false, e, 64,
+      static const int bn = tune_int("NG_TUNE_UPD_BN", 64);
+      NG_TRY(tc_gemm_tf32(st, h->rows[l], h->cols[l], n, h->X[l], h->ldr[l], false, h->Y[l], h->ldp[l], false, e, bn,
                           1));
     } else {
       NG_TRY((gemm_simt<float, false, false>(st, h->rows[l], h->cols[l], n, h->X[l], h->ldr[l], h->Y[l], h->ldp[l],
