@@ -261,6 +261,15 @@ ng_status ng_debug_gemm_tf32(int32_t M, int32_t N, int32_t K, const float* A, in
                              const float* B, int64_t ldb, int32_t b_kmajor, float* C, int64_t ldc,
                              int32_t bn, int32_t splits, void* cuda_stream);
 
+/* Eigensolver round timing, accumulated over every refresh since the last call and reset
+ * by it (SM clock cycles; only recorded while NG_PROFILE_JACOBI_MASK has bit 64 set):
+ *   out[0] rounds timed, out[1] angle thread: round start -> inputs loaded,
+ *   out[2] inputs -> rotation computed, out[3] rotation -> hand-off issued,
+ *   out[4] block thread: round start -> inputs loaded, out[5] inputs -> stores issued,
+ *   out[6] round start -> barrier passed (thread 0), out[7] reserved.
+ * out: host array of 8.  Synchronises the device. */
+ng_status ng_debug_eig_clocks(uint64_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -86,6 +86,7 @@ SIGNATURES = {
     "ng_kernel_launches": (ctypes.c_int64, []),
     "ng_debug_gemm_tf32": (c_int32, [c_int32, c_int32, c_int32, c_void_p, c_int64, c_int32, c_void_p, c_int64,
                                      c_int32, c_void_p, c_int64, c_int32, c_int32, c_void_p]),
+    "ng_debug_eig_clocks": (c_int32, [ctypes.POINTER(ctypes.c_uint64)]),
 }
 
 

@@ -437,14 +437,16 @@ __device__ __forceinline__ void mb_init(uint32_t bar, uint32_t count) {
 __device__ __forceinline__ void mb_arm(uint32_t bar, uint32_t bytes) {   // local arrive + expect_tx
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+// (default .release.cta semantics, as CUTLASS's cluster pipelines: a cluster-scope release
+// would put a MEMBAR.GPU on every round)
 __device__ __forceinline__ void mb_arrive_remote(uint32_t cluster_bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
 __device__ __forceinline__ void mb_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAITC_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@!P1 bra WAITC_%=;\n\t}" ::"r"(bar),
       "r"(parity)
       : "memory");
@@ -475,6 +477,9 @@ __device__ __forceinline__ int ld_cluster_i(uint32_t cluster_addr) {
 // 1..nv): a ring of `ring` rounds; slot s holds the m rotations of one round plus a
 // command word (CONTINUE / STOP).  All addresses are local shared addresses of the
 // same-offset arrays (identical layout in every CTA of the cluster).
+// round timing (ng_debug_eig_clocks), recorded when dbg & 64
+__device__ unsigned long long g_eig_clk[8];
+
 struct PPCluster {
   int nv, ring;
   uint32_t cs_ring;    // V CTAs: ring x m double2
@@ -629,18 +634,29 @@ __device__ __forceinline__ int jacobi_pp(JacobiPPBuf b, int n, int max_sweeps, d
   __syncthreads();
   int sweep = 0, g = 0;
   const uint32_t csd = 16u * m;
+  const bool timing = (dbg & 64) != 0;
+  unsigned long long ck[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const bool t_angle = timing && is_angle && kk == 0, t_blk = timing && tid == m + 1, t_zero = timing && tid == 0;
   for (; sweep < max_sweeps; ++sweep) {
     for (int round = 0; round < rounds; ++round, ++g) {
       const bool odd = g & 1;
+      long long c0 = 0;
+      if (timing) c0 = clock64();
       const uint32_t zc = zb + (odd ? zd : 0u), zn = zb + (odd ? 0u : zd);
       const uint32_t vc = vb + (odd ? vd : 0u), vn = vb + (odd ? 0u : vd);
       const uint32_t cc_ = odd ? csd : 0u;
-      if (is_off) {
+      if (is_off && !(dbg & 16)) {
         const double2 r1 = lds_d2(ca + cc_), r2 = lds_d2(cbk + cc_);
         const double2 u = lds_d2(zc + boff);          // (2ka, 2kb), (2ka+1, 2kb)
         const double2 w = lds_d2(zc + boff + 16u);    // (2ka, 2kb+1), (2ka+1, 2kb+1)
         const double c1 = r1.x, s1 = r1.y, c2 = r2.x, s2 = r2.y;
         const double m00 = u.x, m10 = u.y, m01 = w.x, m11 = w.y;
+        long long c1t = 0;
+        if (t_blk) {
+          asm volatile("" ::"d"(m00), "d"(m11), "d"(c1), "d"(s2));
+          c1t = clock64();
+          ck[4] += c1t - c0;
+        }
         const double t00 = c1 * m00 - s1 * m10, t01 = c1 * m01 - s1 * m11;
         const double t10 = s1 * m00 + c1 * m10, t11 = s1 * m01 + c1 * m11;
         const double r00 = c2 * t00 - s2 * t01, r01 = s2 * t00 + c2 * t01;
@@ -649,13 +665,14 @@ __device__ __forceinline__ int jacobi_pp(JacobiPPBuf b, int n, int max_sweeps, d
         sts_d(zn + w01, r01);
         sts_d(zn + w10, r10);
         sts_d(zn + w11, r11);
+        if (t_blk) ck[5] += clock64() - c1t;
         if (dup) {
           if (dup & 1) sts_d(zn + x00, r00);
           if (dup & 2) sts_d(zn + x01, r01);
           if (dup & 4) sts_d(zn + x10, r10);
           if (dup & 8) sts_d(zn + x11, r11);
         }
-      } else if (is_diag) {
+      } else if (is_diag && !(dbg & 16)) {
         const double2 r1 = lds_d2(ca + cc_);
         const double2 u = lds_d2(zc + boff);
         const double2 w = lds_d2(zc + boff + 16u);
@@ -695,16 +712,35 @@ __device__ __forceinline__ int jacobi_pp(JacobiPPBuf b, int n, int max_sweeps, d
         const double m10 = mtr ? zm1.x : zm0.y, m01 = mtr ? zm0.y : zm1.x;
         const double apq = xu0 * (m00 * xv0 + m01 * xv1) + xu1 * (m10 * xv0 + m11 * xv1);
         const bool wrap = round + 1 == rounds;
-        const double2 rn =
-            wrap ? angle(app, aqq, apq, rot_next, off_next) : angle(app, aqq, apq, rot_cur, off_cur);
+        long long a1t = 0;
+        if (t_angle) {
+          asm volatile("" ::"d"(zu0.x), "d"(zv1.y), "d"(zm0.x), "d"(zm1.y), "d"(rP.x), "d"(rQ.y));
+          a1t = clock64();
+          ck[1] += a1t - c0;
+        }
+        double2 rn;
+        if (dbg & 32) {   // profiling: fixed rotation, no angle chain
+          rn.x = 0.8;
+          rn.y = 0.6;
+        } else {
+          rn = wrap ? angle(app, aqq, apq, rot_next, off_next) : angle(app, aqq, apq, rot_cur, off_cur);
+        }
+        long long a2t = 0;
+        if (t_angle) {
+          asm volatile("" ::"d"(rn.x), "d"(rn.y));
+          a2t = clock64();
+          ck[2] += a2t - a1t;
+        }
         sts_d2(csb + (odd ? 0u : csd) + 16u * kk, rn);
         if (!VLOCAL) {
           pp_push_cs(cl, m, g + 1, kk, rn);
           if (kk == 0 && !wrap) pp_push_cmd(cl, g + 1, kPPContinue);
         }
+        if (t_angle) { ck[3] += clock64() - a2t; ck[0] += 1; }
       }
       if (tid == 0 && *phantom >= 0) *phantom = pp_sigma(*phantom, m);
       __syncthreads();
+      if (t_zero) ck[6] += clock64() - c0;
     }
     int my_rot = warp_sum(rot_cur);
     float my_off = warp_max(off_cur);
@@ -719,6 +755,11 @@ __device__ __forceinline__ int jacobi_pp(JacobiPPBuf b, int n, int max_sweeps, d
     // the next round's rotations were already pushed; its command decides
     if (!VLOCAL && is_angle && kk == 0) pp_push_cmd(cl, g, stop ? kPPStop : kPPContinue);
     if (stop) { ++sweep; break; }
+  }
+  if (timing) {
+    if (t_angle) for (int i = 0; i < 4; ++i) atomicAdd(&g_eig_clk[i], ck[i]);
+    if (t_blk) { atomicAdd(&g_eig_clk[4], ck[4]); atomicAdd(&g_eig_clk[5], ck[5]); }
+    if (t_zero) atomicAdd(&g_eig_clk[6], ck[6]);
   }
   *fb = g & 1;
   return sweep;

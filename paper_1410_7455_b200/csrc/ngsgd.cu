@@ -1461,4 +1461,15 @@ ng_status ngsgd_set_state(ngsgd_t h, const ngsgd_state_host* in) {
   return NG_OK;
 }
 
+ng_status ng_debug_eig_clocks(uint64_t* out) {
+  NG_REQUIRE(out != nullptr, NG_EINVAL, "NULL argument");
+  NG_CUDA_TRY(cudaDeviceSynchronize());
+  unsigned long long v[8];
+  NG_CUDA_TRY(cudaMemcpyFromSymbol(v, g_eig_clk, sizeof(v)));
+  for (int i = 0; i < 8; ++i) out[i] = v[i];
+  std::memset(v, 0, sizeof(v));
+  NG_CUDA_TRY(cudaMemcpyToSymbol(g_eig_clk, v, sizeof(v)));
+  return NG_OK;
+}
+
 }  // extern "C"
