@@ -80,7 +80,9 @@ typedef struct ngsgd_ctx* ngsgd_t;
  * `max_rows` bounds the minibatch size N of later calls (workspaces are sized here so
  * the hot path never allocates).  `cuda_stream` is a cudaStream_t (NULL = legacy default
  * stream).  The state is uninitialised until the first minibatch with tr(X^T X) > 0
- * (B.3.2; reading R7).  Owns all its device memory. */
+ * (B.3.2; reading R7); earlier minibatches pass through unchanged
+ * but are counted in t (the update schedule is per minibatch).  Owns all its
+ * device memory. */
 ng_status ngsgd_create(int32_t dim, int32_t max_rows, const ngsgd_config* cfg,
                        void* cuda_stream, ngsgd_t* out);
 ng_status ngsgd_destroy(ngsgd_t h);

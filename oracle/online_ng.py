@@ -145,8 +145,7 @@ def init_state(state: OnlineNgState, X0: np.ndarray) -> None:
     state.rho = rho0
     state.d = d0
     state.W = np.sqrt(e0)[:, None] * R0                        # eqn:wt:def
-    state.t = 0
-    state.initialized = True
+    state.initialized = True                                   # (t is not reset: reading R7)
 
 
 # --------------------------------------------------------------------------------------
@@ -169,9 +168,11 @@ def precondition(state: OnlineNgState, X: np.ndarray, update: bool | None = None
 
     # Reading R7: defer initialisation until the first minibatch with tr(X^T X) > 0
     # (zero-initialised softmax makes hidden-layer derivatives exactly 0 at step 0,
-    # P:1697-1698; eigenvectors of S_0 = 0 are arbitrary).
+    # P:1697-1698; eigenvectors of S_0 = 0 are arbitrary).  t still counts the minibatch:
+    # the update schedule is per minibatch of the process.
     if not state.initialized:
         if float(np.sum(X * X)) == 0.0:
+            state.t += 1
             return PrecondOutput(X.copy(), 1.0, np.zeros(N), tr_xxt=0.0)
         init_state(state, X)
 
@@ -322,6 +323,7 @@ def precondition_naive(state: OnlineNgState, X: np.ndarray, update: bool | None 
     N, D = X.shape
     if not state.initialized:
         if float(np.sum(X * X)) == 0.0:
+            state.t += 1                                       # reading R7
             return PrecondOutput(X.copy(), 1.0, np.zeros(N))
         init_state(state, X)
     if update is None:

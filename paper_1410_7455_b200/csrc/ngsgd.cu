@@ -74,6 +74,21 @@ ng_status status_from_flags(uint32_t f, const char* where) {
 }
 
 constexpr int kApplyRows = 16, kApplyCols = 128;
+int rr_chunks(int D);
+// The refresh chain (side stream) only gates the state's next call; give its small,
+// dependent kernels the highest stream priority so that they are not queued behind the
+// main stream's full-GPU GEMMs (NG_TUNE_SIDE_PRIORITY=0 keeps the default priority).
+inline int refresh_priority() {
+  static int v = 1;
+  static bool done = false;
+  if (!done) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    v = tune_int("NG_TUNE_SIDE_PRIORITY", 1) ? hi : lo;
+    done = true;
+  }
+  return v;
+}
 // Column tile of the tensor-core NG apply (NG_TUNE_APPLY_BN: 32, 64 or 128).
 inline int apply_bn() {
   static const int v = tune_int("NG_TUNE_APPLY_BN", 128);
@@ -509,15 +524,14 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
 
 // B.3.1 (reading R5): O = E^{-1/2} (W W^T) E^{-1/2} for the NEW state; if
 // max |O - I| > 1e-3: O = C C^T, M = E^{1/2} C^{-1} E^{-1/2} (flags[2] = 1).
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 reorth_check_kernel(int R, const float* __restrict__ WW, const double* __restrict__ dstate,
-                    float* __restrict__ Mmat, int* __restrict__ flags) {
+                    double* __restrict__ Cfac, int* __restrict__ flags) {
   if (flags[1] == 0) return;
   extern __shared__ __align__(16) unsigned char ng_smem[];
   double* sm = reinterpret_cast<double*>(ng_smem);
   double* O = sm;             // R*R
-  double* Li = O + R * R;     // R*R  (C^{-1})
-  double* eh = Li + R * R;    // R    e^{1/2}
+  double* eh = O + R * R;     // R    e^{1/2}
   double* red = eh + R;       // 32
   __shared__ int fail;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -534,43 +548,68 @@ reorth_check_kernel(int R, const float* __restrict__ WW, const double* __restric
   }
   dev = block_max(dev, red);
   if (dev <= 1e-3) { if (tid == 0) flags[2] = 0; return; }
-  // Cholesky (lower), right-looking
+  // Cholesky O = C C^T (lower), right-looking; column k is scaled by every thread from the
+  // pivot it reads itself (one barrier per column for the pivot, one for the update)
   for (int k = 0; k < R; ++k) {
-    if (tid == 0) {
-      const double okk = O[k * R + k];
-      if (!(okk > 0.0)) fail = 1; else O[k * R + k] = sqrt(okk);
-    }
-    __syncthreads();
-    if (fail) break;
-    const double ckk = O[k * R + k];
-    for (int i = k + 1 + tid; i < R; i += nt) O[i * R + k] /= ckk;
-    __syncthreads();
+    const double okk = O[k * R + k];
+    if (!(okk > 0.0)) { fail = 1; break; }   // uniform: every thread reads the same pivot
+    const double ckk = sqrt(okk);
+    const double inv = 1.0 / ckk;
     const int m = R - k - 1;
+    // rank-1 update of the trailing lower triangle with the scaled column
     for (int idx = tid; idx < m * m; idx += nt) {
       const int i = k + 1 + idx / m, j = k + 1 + idx % m;
-      if (j <= i) O[i * R + j] -= O[i * R + k] * O[j * R + k];
+      if (j <= i) O[i * R + j] -= (O[i * R + k] * inv) * (O[j * R + k] * inv);
     }
+    __syncthreads();
+    for (int i = k + 1 + tid; i < R; i += nt) O[i * R + k] *= inv;
+    if (tid == 0) O[k * R + k] = ckk;
     __syncthreads();
   }
   if (fail) {
     if (tid == 0) { flags[2] = 0; atomicOr(reinterpret_cast<unsigned*>(flags + 3), kErrNotPD); }
     return;
   }
-  // C^{-1} by forward substitution, one column per thread
-  for (int j = tid; j < R; j += nt) {
-    for (int i = 0; i < R; ++i) {
-      if (i < j) { Li[i * R + j] = 0.0; continue; }
-      double s = (i == j) ? 1.0 : 0.0;
-      for (int k = j; k < i; ++k) s -= O[i * R + k] * Li[k * R + j];
-      Li[i * R + j] = s / O[i * R + i];
-    }
-  }
-  __syncthreads();
   for (int idx = tid; idx < R * R; idx += nt) {
     const int i = idx / R, j = idx % R;
-    Mmat[idx] = (float)(eh[i] * Li[idx] / eh[j]);
+    Cfac[idx] = (j <= i) ? O[idx] : 0.0;
   }
   if (tid == 0) flags[2] = 1;
+}
+
+// B.3.1 repair W' <- M W' with M = E'^{1/2} C^{-1} E'^{-1/2} (reading R5), as an
+// FP64 forward substitution per column of W' (no explicit C^{-1}): column j of W' is
+// y = C^{-1} (E'^{-1/2} w_j), then w_j <- E'^{1/2} y.  In place, gated on flags[2].
+// 128 columns per CTA; the factor and the 128 right-hand sides live in shared memory.
+constexpr int kTrsmCols = 128;
+__global__ void __launch_bounds__(kTrsmCols)
+reorth_trsm_kernel(int R, int D, float* __restrict__ W, int64_t ldw, const double* __restrict__ Cfac,
+                   const double* __restrict__ dstate, const int* __restrict__ flag) {
+  if (*flag == 0) return;
+  extern __shared__ __align__(16) unsigned char ng_smem[];
+  double* C = reinterpret_cast<double*>(ng_smem);    // R*R
+  double* eh = C + R * R;                            // R
+  double* Y = eh + R;                                // R x kTrsmCols
+  const int tid = threadIdx.x;
+  for (int i = tid; i < R * R; i += blockDim.x) C[i] = Cfac[i];
+  for (int i = tid; i < R; i += blockDim.x) eh[i] = sqrt(dstate[1 + R + i]);
+  __syncthreads();
+  const int j = blockIdx.x * kTrsmCols + tid;
+  if (j >= D) return;
+  for (int i = 0; i < R; ++i) {
+    const double* ci = C + i * R;
+    double s0 = (double)W[(int64_t)i * ldw + j] / eh[i], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int k = 0;
+    for (; k + 4 <= i; k += 4) {
+      s0 -= ci[k] * Y[k * kTrsmCols + tid];
+      s1 -= ci[k + 1] * Y[(k + 1) * kTrsmCols + tid];
+      s2 -= ci[k + 2] * Y[(k + 2) * kTrsmCols + tid];
+      s3 -= ci[k + 3] * Y[(k + 3) * kTrsmCols + tid];
+    }
+    for (; k < i; ++k) s0 -= ci[k] * Y[k * kTrsmCols + tid];
+    Y[i * kTrsmCols + tid] = ((s0 + s1) + (s2 + s3)) / ci[i];
+  }
+  for (int i = 0; i < R; ++i) W[(int64_t)i * ldw + j] = (float)(eh[i] * Y[i * kTrsmCols + tid]);
 }
 
 // ------------------------------------------------------------------------------------
@@ -692,7 +731,8 @@ __global__ void passthrough_kernel(int n, float* p, float* p_out, float* g, floa
 // host side
 // ------------------------------------------------------------------------------------
 
-static size_t reorth_smem_bytes(int R) { return sizeof(double) * (2 * R * R + R + 32); }
+static size_t reorth_smem_bytes(int R) { return sizeof(double) * (R * R + R + 32); }
+static size_t trsm_smem_bytes(int R) { return sizeof(double) * ((size_t)R * R + R + (size_t)R * kTrsmCols); }
 
 template <typename T>
 static ng_status dalloc(T** p, size_t count) {
@@ -713,6 +753,8 @@ static ng_status set_kernel_attrs() {
                                    (int)refresh_plan(kJacobiPPMax, REFRESH_CLUSTER).total_bytes));
   NG_CUDA_TRY(cudaFuncSetAttribute(reorth_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)reorth_smem_bytes(kMaxRank)));
+  NG_CUDA_TRY(cudaFuncSetAttribute(reorth_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)trsm_smem_bytes(kMaxRank)));
   NG_CUDA_TRY(cudaFuncSetAttribute(apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(sizeof(float) * (kApplyRows * kMaxRank + kMaxRank * kApplyCols))));
   done = true;
@@ -759,13 +801,14 @@ ng_status ngsgd_create_impl(int dim, int max_rows, const ngsgd_config* cfg, cuda
   ALLOC(h->Hpart, std::max((size_t)h->h_splits * max_rows * R, (size_t)kTcJSplits * R * h->ldw));
   ALLOC(h->H, (size_t)max_rows * R);
   ALLOC(h->J, (size_t)R * h->ldw);
-  ALLOC(h->Kpart, (size_t)h->kl_splits * R * R);
-  ALLOC(h->Lpart, (size_t)l_splits * R * R);
+  ALLOC(h->Kpart, (size_t)std::max(h->kl_splits, rr_chunks(dim)) * R * R);
+  ALLOC(h->Lpart, (size_t)std::max(l_splits, rr_chunks(dim)) * R * R);
   ALLOC(h->KL, 2 * R * R);
   ALLOC(h->WWpart, (size_t)h->kl_splits * R * R);
   ALLOC(h->WW, R * R);
   ALLOC(h->Amat, R * R);
   ALLOC(h->Mmat, R * R);
+  ALLOC(h->Cfac, R * R);
   ALLOC(h->svec, R);
   ALLOC(h->xxpart, (size_t)h->ctiles * max_rows);
   ALLOC(h->ppart, (size_t)h->ctiles * max_rows);
@@ -775,7 +818,7 @@ ng_status ngsgd_create_impl(int dim, int max_rows, const ngsgd_config* cfg, cuda
   ALLOC(h->flags, 8);
 #undef ALLOC
   if (s == NG_OK && cudaMallocHost((void**)&h->h_scalar, 4 * sizeof(double)) != cudaSuccess) s = NG_ENOMEM;
-  if (s == NG_OK && (cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking) != cudaSuccess ||
+  if (s == NG_OK && (cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, refresh_priority()) != cudaSuccess ||
                      cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
                      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess)) {
     set_error("ngsgd_create: stream/event creation failed");
@@ -800,6 +843,7 @@ void ngsgd_destroy_impl(ngsgd_ctx* h) {
                  h->Amat, h->Mmat, h->svec, h->xxpart, h->ppart, h->p, h->gamma};
   for (float* p : fp) if (p) cudaFree(p);
   if (h->dstate) cudaFree(h->dstate);
+  if (h->Cfac) cudaFree(h->Cfac);
   if (h->sums) cudaFree(h->sums);
   if (h->flags) cudaFree(h->flags);
   if (h->h_scalar) cudaFreeHost(h->h_scalar);
@@ -857,7 +901,7 @@ static ng_status ngsgd_init(ngsgd_ctx* h, int n, const float* x, int64_t ld, dou
     if (e != cudaSuccess) { set_error(std::string("ngsgd init: ") + cudaGetErrorString(e)); s = NG_ECUDA; }
   }
   cudaFree(X64); cudaFree(A); cudaFree(Vt); cudaFree(Vs); cudaFree(lam); cudaFree(R0); cudaFree(wsd); cudaFree(wsi);
-  if (s == NG_OK) { h->initialized = true; h->t = 0; }
+  if (s == NG_OK) h->initialized = true;   // t is not reset (reading R7)
   return s;
 }
 
@@ -946,12 +990,11 @@ static ng_status launch_refresh_chain(ngsgd_ctx* h, int n, double eta) {
                                        EpiStoreSplit<float>{h->WWpart, R, (int64_t)R * R}, ks, h->flags + 1)));
   reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, ss>>>(h->WW, h->WWpart, R * R, ks, R * R, h->flags + 1);
   NG_TRY(check_launch("reduce_splits(WW)"));
-  reorth_check_kernel<<<1, 256, reorth_smem_bytes(R), ss>>>(R, h->WW, h->dstate, h->Mmat, h->flags);
+  reorth_check_kernel<<<1, 1024, reorth_smem_bytes(R), ss>>>(R, h->WW, h->dstate, h->Cfac, h->flags);
   NG_TRY(check_launch("reorth_check_kernel"));
-  NG_TRY((gemm_simt<float, true, false>(ss, R, D, R, h->Mmat, R, Wn, h->ldw, EpiStore<float>{h->J, h->ldw, 1.f},
-                                        1, h->flags + 2)));
-  copy_gated_kernel<<<std::min(1024, ceil_div((int64_t)R * D, 256)), 256, 0, ss>>>(R, D, Wn, h->J, h->ldw, h->flags + 2);
-  NG_TRY(check_launch("copy_gated_kernel"));
+  reorth_trsm_kernel<<<ceil_div(D, kTrsmCols), kTrsmCols, trsm_smem_bytes(R), ss>>>(R, D, Wn, h->ldw, h->Cfac,
+                                                                                   h->dstate, h->flags + 2);
+  NG_TRY(check_launch("reorth_trsm_kernel"));
   NG_CUDA_TRY(cudaEventRecord(h->ev_join, ss));
   h->pending = true;
   h->cur = nxt;
@@ -977,6 +1020,8 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
     const double trXX = h->h_scalar[0];
     NG_REQUIRE(std::isfinite(trXX), NG_ENONFINITE, "non-finite input");
     if (trXX == 0.0) {
+      // t still counts the minibatch: the update schedule is per minibatch
+      h->t += 1;
       passthrough_kernel<<<1, 256, 0, st>>>(n, h->p, p_out, h->gamma, gamma_out);
       return check_launch("passthrough_kernel");
     }
@@ -1178,6 +1223,106 @@ static ng_status launch_seg_reduce(cudaStream_t st, SegReduce& sr) {
   return check_launch("seg_reduce_kernel");
 }
 
+// ---- K_t = J J^T and L_t = W J^T of every updating state in one launch.
+// One CTA = the whole R x R product over one 256-wide chunk of the D axis (FP32 FMA, the
+// chunk's partial written to part[chunk]); the fixed-order segmented reduction sums the
+// chunks.  FP32 in both precision modes (the refresh needs them accurate).
+constexpr int kRRMax = 32, kRRChunk = 256, kRRSub = 64;
+struct RRProb {
+  const float* A;
+  const float* B;
+  float* part;
+  int64_t lda, ldb, zstride;
+  int R, D, tile_begin, pad_;
+};
+struct RRGroup {
+  RRProb p[kRRMax];
+  int count;
+};
+
+template <int TM>
+__global__ void __launch_bounds__(256) rr_gemm_kernel(const __grid_constant__ RRGroup grp) {
+  constexpr int SUB = TM <= 5 ? kRRSub : kRRSub / 2;   // static shared memory <= 48 KB
+  __shared__ float As[SUB][16 * TM + 1];
+  __shared__ float Bs[SUB][16 * TM + 1];
+  int g = 0;
+  while (g + 1 < grp.count && (int)blockIdx.x >= grp.p[g + 1].tile_begin) ++g;
+  const RRProb& P = grp.p[g];
+  const int chunk = (int)blockIdx.x - P.tile_begin;
+  const int R = P.R, k0 = chunk * kRRChunk, k1 = min(P.D, k0 + kRRChunk);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float acc[TM][TM];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TM; ++j) acc[i][j] = 0.f;
+  for (int kb = k0; kb < k1; kb += SUB) {
+    const int kn = min(SUB, k1 - kb);
+    for (int idx = threadIdx.x; idx < 16 * TM * SUB; idx += 256) {
+      const int i = idx / SUB, k = idx - (idx / SUB) * SUB;
+      const bool ok = i < R && k < kn;
+      As[k][i] = ok ? __ldg(P.A + (int64_t)i * P.lda + kb + k) : 0.f;
+      Bs[k][i] = ok ? __ldg(P.B + (int64_t)i * P.ldb + kb + k) : 0.f;
+    }
+    __syncthreads();
+    for (int k = 0; k < kn; ++k) {
+      float a[TM], b[TM];
+#pragma unroll
+      for (int t = 0; t < TM; ++t) { a[t] = As[k][ty * TM + t]; b[t] = Bs[k][tx * TM + t]; }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TM; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  float* out = P.part + (int64_t)chunk * P.zstride;
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TM; ++j) {
+      const int r = ty * TM + i, c = tx * TM + j;
+      if (r < R && c < R) out[r * R + c] = acc[i][j];
+    }
+}
+
+int rr_chunks(int D) { return ceil_div(D, kRRChunk); }
+
+// K and L partials of the states `which` (indices into grp), all with rank <= 16 TM.
+template <int TM>
+static ng_status launch_rr(cudaStream_t st, NgCall* calls, const std::vector<int>& grp, const std::vector<int>& which) {
+  RRGroup gr;
+  std::memset(&gr, 0, sizeof(gr));
+  int tiles = 0;
+  auto flush = [&]() -> ng_status {
+    if (gr.count == 0) return NG_OK;
+    rr_gemm_kernel<TM><<<tiles, 256, 0, st>>>(gr);
+    NG_TRY(check_launch("rr_gemm_kernel"));
+    std::memset(&gr, 0, sizeof(gr));
+    tiles = 0;
+    return NG_OK;
+  };
+  for (int g : which) {
+    ngsgd_ctx* h = calls[grp[g]].h;
+    const int R = h->rank, D = h->dim, nc = rr_chunks(D);
+    for (int w = 0; w < 2; ++w) {
+      if (gr.count == kRRMax) NG_TRY(flush());
+      RRProb& q = gr.p[gr.count++];
+      q.A = w ? h->W[h->cur] : h->J;
+      q.B = h->J;
+      q.lda = h->ldw;
+      q.ldb = h->ldw;
+      q.part = w ? h->Lpart : h->Kpart;
+      q.zstride = (int64_t)R * R;
+      q.R = R;
+      q.D = D;
+      q.tile_begin = tiles;
+      tiles += nc;
+    }
+  }
+  return flush();
+}
+
 ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
   NG_REQUIRE(calls != nullptr && count >= 0, NG_EINVAL, "NULL argument");
   std::vector<int> grp;          // indices of tensor-core group members
@@ -1268,21 +1413,22 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
       sr.zstride[u] = (int64_t)h->rank * h->ldw; sr.rows[u] = h->rank; sr.cols[u] = h->dim; sr.splits[u] = sp[u];
     }
     NG_TRY(launch_seg_reduce(st, sr));
-    for (int g : ug) {
-      ngsgd_ctx* h = calls[grp[g]].h;
-      const int R = h->rank, D = h->dim;
-      const int ks = gemm_simt_splits(D, h->kl_splits);
-      NG_TRY((gemm_simt<float, true, true>(st, R, R, D, h->J, h->ldw, h->J, h->ldw,
-                                           EpiStoreSplit<float>{h->Kpart, R, (int64_t)R * R}, ks)));
-      NG_TRY((gemm_simt<float, true, true>(st, R, R, D, h->W[h->cur], h->ldw, h->J, h->ldw,
-                                           EpiStoreSplit<float>{h->Lpart, R, (int64_t)R * R}, ks)));
+    {
+      std::vector<int> small, mid, big;   // by micro-tile: R <= 32, <= 80, <= 128
+      for (int g : ug) {
+        const int R = calls[grp[g]].h->rank;
+        (R <= 32 ? small : (R <= 80 ? mid : big)).push_back(g);
+      }
+      if (!small.empty()) NG_TRY(launch_rr<2>(st, calls, grp, small));
+      if (!mid.empty()) NG_TRY(launch_rr<5>(st, calls, grp, mid));
+      if (!big.empty()) NG_TRY(launch_rr<8>(st, calls, grp, big));
     }
     SegReduce kl;
     std::memset(&kl, 0, sizeof(kl));
     kl.count = 0;
     for (int g : ug) {
       ngsgd_ctx* h = calls[grp[g]].h;
-      const int R = h->rank, ks = gemm_simt_splits(h->dim, h->kl_splits);
+      const int R = h->rank, ks = rr_chunks(h->dim);
       for (int w = 0; w < 2; ++w) {
         if (kl.count == kSegMax) { NG_TRY(launch_seg_reduce(st, kl)); kl.count = 0; }
         const int k = kl.count++;

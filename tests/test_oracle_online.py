@@ -61,10 +61,11 @@ def test_init_trace_matching_random():
 
 
 def test_deferred_init_on_zero_input():
-    """Reading R7: an all-zero first minibatch passes through and leaves the state."""
+    """Reading R7: an all-zero first minibatch passes through and leaves the state
+    uninitialised; t counts it (the schedule is per minibatch)."""
     s = ong.OnlineNgState(6, _cfg(2))
     out = ong.precondition(s, np.zeros((5, 6)))
-    assert not s.initialized and s.t == 0 and out.gamma == 1.0
+    assert not s.initialized and s.t == 1 and out.gamma == 1.0
     assert np.all(out.x_hat == 0) and np.all(out.row_sq == 0)
 
 
