@@ -542,6 +542,26 @@ ng_status nnet_update(nnet_t h, float lr, float max_change_per_sample, nnet_upda
   maxchange_kernel<<<L, 256, 0, st>>>(n, N, lr, max_change_per_sample, h->gam, h->pbuf, h->scale, h->stats);
   NG_TRY(check_launch("maxchange_kernel"));
   const bool tc = h->cfg.precision == NG_TF32;
+  static const int upd_grouped = tune_int("NG_TUNE_UPD_GROUPED", 1);
+  if (tc && upd_grouped && L <= kTcGroupMax) {
+    // all L weight updates W_l += s_l X_l^T Y_l (eqn:add:w) in ONE tensor-core launch
+    std::vector<TcGroupDesc> d(L);
+    double flops = 0, bytes = 0;
+    for (int l = 0; l < L; ++l) {
+      const double R_ = h->rows[l], C_ = h->cols[l];
+      flops += 2.0 * n * R_ * C_;
+      bytes += 4.0 * (n * R_ + n * C_ + 2.0 * R_ * C_);
+      TcGroupDesc& q = d[l];
+      std::memset(&q, 0, sizeof(q));
+      q.M = h->rows[l]; q.N = h->cols[l]; q.K = n; q.splits = 1;
+      q.A = h->X[l]; q.lda = h->ldr[l]; q.B = h->Y[l]; q.ldb = h->ldp[l];
+      q.epi.kind = TC_EPI_AXPY; q.epi.C = h->arena + h->off[l]; q.epi.ldc = h->ldp[l]; q.epi.scale = h->scale + l;
+      q.splits_used = nullptr;
+    }
+    static const int bn = tune_int("NG_TUNE_UPD_BN", 64);
+    ProfScope ps(NG_PROF_UPD_GEMM, st, flops, bytes);
+    NG_TRY(tc_gemm_tf32_grouped(st, d.data(), L, false, false, TC_EPI_AXPY, bn));
+  } else
   for (int l = 0; l < L; ++l) {
     float* W = h->arena + h->off[l];
     const double R_ = h->rows[l], C_ = h->cols[l];
