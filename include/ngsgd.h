@@ -268,9 +268,17 @@ ng_status ng_debug_gemm_tf32(int32_t M, int32_t N, int32_t K, const float* A, in
  *   out[0] rounds timed, out[1] angle thread: round start -> inputs loaded,
  *   out[2] inputs -> rotation computed, out[3] rotation -> hand-off issued,
  *   out[4] block thread: round start -> inputs loaded, out[5] inputs -> stores issued,
- *   out[6] round start -> barrier passed (thread 0), out[7] reserved.
- * out: host array of 8.  Synchronises the device. */
+ *   out[6] round start -> barrier passed (thread 0), out[7] reserved;
+ * divide-and-conquer solver (always recorded): out[8] Householder, out[9] D&C, out[10]
+ * back-transformation cycles, out[11] solves, out[12 + l] merge level l (width 2^l).
+ * out: host array of 24.  Synchronises the device. */
 ng_status ng_debug_eig_clocks(uint64_t* out);
+
+/* The refresh's dense symmetric eigensolver (Householder + divide and conquer, FP64, one
+ * CTA; eqn:zt:eig) on its own, for unit tests: z device double[n*n] (row
+ * major, symmetric), lam device double[n] (ascending), vt device double[n*n] (row i = the
+ * unit eigenvector of lam[i]).  n in [1, 80]; asynchronous on `stream`. */
+ng_status ng_debug_eig_dc(const double* z, int32_t n, double* lam, double* vt, void* stream);
 
 #ifdef __cplusplus
 }

@@ -156,6 +156,32 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
 
+  // Read-modify-write epilogues: the old C tile does not depend on the MMA, so every
+  // thread loads its row of it now (registers) and the HBM latency overlaps the mainloop.
+  constexpr bool RMW = EPI == TC_EPI_AXPY || EPI == TC_EPI_NGAPPLY;
+  constexpr int CW = BN >= 32 ? 32 : 16;
+  const int row = m0 + warp * 32 + lane;
+  float* __restrict__ crow = epi.C + (EPI == TC_EPI_PARTIAL ? (int64_t)ztile * epi.zstride : 0) +
+                             (int64_t)row * epi.ldc;
+  float oldv[RMW ? BN : 1];
+  if (RMW) {
+#pragma unroll
+    for (int c = 0; c < BN / CW; ++c) {
+      const int nb = n0 + c * CW;
+      const bool full = row < M && (nb + CW <= N) && ((reinterpret_cast<uintptr_t>(crow + nb) & 15) == 0);
+      if (full) {
+#pragma unroll
+        for (int j = 0; j < CW; j += 4) {
+          const float4 o = *reinterpret_cast<const float4*>(crow + nb + j);
+          oldv[c * CW + j] = o.x; oldv[c * CW + j + 1] = o.y; oldv[c * CW + j + 2] = o.z; oldv[c * CW + j + 3] = o.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < CW; ++j) oldv[c * CW + j] = (row < M && nb + j < N) ? crow[nb + j] : 0.f;
+      }
+    }
+  }
+
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
     int s = 0;
@@ -209,13 +235,9 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
   mbar_wait(&accum_bar, 0);
   tc_fence_after();
   __syncwarp();
-  const int row = m0 + warp * 32 + lane;
   const float scale = (EPI == TC_EPI_AXPY) ? __ldg(epi.scale) : 0.f;
-  float* __restrict__ crow = epi.C + (EPI == TC_EPI_PARTIAL ? (int64_t)ztile * epi.zstride : 0) +
-                             (int64_t)row * epi.ldc;
   float xx = 0.f, pp = 0.f;   // TC_EPI_NGAPPLY row partial sums over this tile's columns
-  constexpr int CW = BN >= 32 ? 32 : 16;
-#pragma unroll 1
+#pragma unroll
   for (int c = 0; c < BN / CW; ++c) {
     float acc[CW];
     {
@@ -238,20 +260,12 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
           for (int j = 0; j < CW; j += 4)
             *reinterpret_cast<float4*>(crow + nb + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
         } else {
-          for (int j = 0; j < CW && nb + j < N; ++j) crow[nb + j] = acc[j];
+#pragma unroll
+          for (int j = 0; j < CW; ++j)
+            if (nb + j < N) crow[nb + j] = acc[j];
         }
       } else {
-        float old[CW];
-        if (full) {
-#pragma unroll
-          for (int j = 0; j < CW; j += 4) {
-            const float4 o = *reinterpret_cast<const float4*>(crow + nb + j);
-            old[j] = o.x; old[j + 1] = o.y; old[j + 2] = o.z; old[j + 3] = o.w;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < CW; ++j) old[j] = (nb + j < N) ? crow[nb + j] : 0.f;
-        }
+        const float* old = oldv + (RMW ? c * CW : 0);
 #pragma unroll
         for (int j = 0; j < CW; ++j) {
           if (EPI == TC_EPI_AXPY) {
@@ -268,7 +282,9 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
           for (int j = 0; j < CW; j += 4)
             *reinterpret_cast<float4*>(crow + nb + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
         } else {
-          for (int j = 0; j < CW && nb + j < N; ++j) crow[nb + j] = acc[j];
+#pragma unroll
+          for (int j = 0; j < CW; ++j)
+            if (nb + j < N) crow[nb + j] = acc[j];
         }
       }
     }

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "eig_jacobi.cuh"
+#include "eig_dc.cuh"
 #include "gemm_simt.cuh"
 #include "gemm_tc.cuh"
 #include "ngsgd_impl.cuh"
@@ -244,7 +245,7 @@ __global__ void copy_gated_kernel(int R, int D, float* __restrict__ dst, const f
 //                    1..nv keep column slices of the eigenvectors and apply each round's
 //                    rotations as they arrive (DSMEM ring, eig_jacobi.cuh); the shared-
 //                    memory traffic of the eigenvector update leaves the Z CTA (R <= 80)
-enum RefreshMode : int { REFRESH_INPLACE = 0, REFRESH_PP = 1, REFRESH_CLUSTER = 2 };
+enum RefreshMode : int { REFRESH_INPLACE = 0, REFRESH_PP = 1, REFRESH_CLUSTER = 2, REFRESH_DC = 3 };
 constexpr int kPPRing = 16;
 
 // Shared-memory plan (offsets in doubles from the 16-byte aligned dynamic base).
@@ -277,7 +278,14 @@ __host__ __device__ inline RefreshSmem refresh_plan(int R, int mode) {
   p.o_lam = o;  o += (size_t)p.npad + 2;               // eigenvalues (slot / index order)
   p.o_share = o; o += (size_t)R;                       // A_t row factors (cluster)
   o = (o + 1) & ~(size_t)1;                            // 16-byte alignment
-  if (mode == REFRESH_INPLACE) {
+  if (mode == REFRESH_DC) {   // eig_dc's plan; Z_t is built in its A region (ld R + 1)
+    const DCPlan dp = dc_plan(R);
+    p.o_ring = o;
+    p.o_z0 = o + dp.oA; p.o_z1 = p.o_z0;
+    p.o_v0 = o + dp.oV; p.o_v1 = p.o_v0;     // eigenvector rows come out here (ld R)
+    p.o_cs = o;
+    o += (dp.total + 15) / 8;
+  } else if (mode == REFRESH_INPLACE) {
     p.o_z0 = o; o += ((size_t)R * p.LD + 1) & ~(size_t)1;
     p.o_z1 = p.o_z0;
     p.o_v0 = o; o += (size_t)R * p.LDV;
@@ -375,7 +383,7 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   int* fbuf = phantom + 1;
   float* offmax = reinterpret_cast<float*>(fbuf + 1);  // 32 (per-warp max ratio)
   const int tid = threadIdx.x, nt = blockDim.x;
-  constexpr bool PPK = MODE != REFRESH_INPLACE;
+  constexpr bool PPK = MODE == REFRESH_PP || MODE == REFRESH_CLUSTER;
 
   const double rho = dstate[0];
   for (int i = tid; i < R; i += nt) d[i] = dstate[1 + i];
@@ -404,7 +412,7 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
     return z;
   };
   double* Z = sm + P.o_z0;
-  if (PPK) {
+  if (PPK && MODE != REFRESH_DC) {
     // slot-pair block layout, upper block triangle (eig_jacobi.cuh), zero padding row
     const int np = P.npad;
     for (int idx = tid; idx < np * np; idx += nt) {
@@ -427,7 +435,14 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   int sweeps;
   const double* V = nullptr;   // eigenvector rows (index / slot order), row stride ldv
   int ldv = 0, nlam;
-  if (PPK) {
+  if (MODE == REFRESH_DC) {
+    // Householder + divide and conquer (eig_dc.cuh); the eigenvector rows overwrite Z
+    eig_dc(sm + P.o_ring, dc_plan(R), Z, P.LD, lam, sm + P.o_v0, R);
+    sweeps = 0;
+    V = sm + P.o_v0;
+    ldv = R;
+    nlam = R;
+  } else if (PPK) {
     JacobiPPBuf jb{{sm + P.o_z0, sm + P.o_z1}, {sm + P.o_v0, sm + P.o_v1},
                    reinterpret_cast<double2*>(sm + P.o_cs), nrot, offmax};
     int fb_local = 0;
@@ -443,7 +458,7 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
     V = fb_local ? jb.V[1] : jb.V[0];
     ldv = P.npad;
     nlam = P.npad;
-  } else {
+  } else if (MODE == REFRESH_INPLACE) {
     JacobiSmem<double> scr{sm + P.o_cs, sm + P.o_cs + P.mp, nrot, offmax};
     double* Vt = sm + P.o_v0;
     sweeps = jacobi_eig_smem<double>(Z, P.LD, Vt, P.LDV, R, scr, 20, 1e-15 * zmax, 1e-7, dbg_mask);
@@ -751,6 +766,8 @@ static ng_status set_kernel_attrs() {
                                    (int)refresh_plan(kJacobiPPMax, REFRESH_PP).total_bytes));
   NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<REFRESH_CLUSTER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)refresh_plan(kJacobiPPMax, REFRESH_CLUSTER).total_bytes));
+  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<REFRESH_DC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)refresh_plan(kDCMax, REFRESH_DC).total_bytes));
   NG_CUDA_TRY(cudaFuncSetAttribute(reorth_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)reorth_smem_bytes(kMaxRank)));
   NG_CUDA_TRY(cudaFuncSetAttribute(reorth_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -948,7 +965,8 @@ static ng_status launch_refresh_chain(ngsgd_ctx* h, int n, double eta) {
     // beyond kJacobiPPMax.  NG_TUNE_EIG_MODE = 0/1/2 forces one (comparisons only).
     static const int force = tune_int("NG_TUNE_EIG_MODE", -1);
     int mode = R > kJacobiPPMax || R < 2 ? REFRESH_INPLACE : (R >= 48 ? REFRESH_CLUSTER : REFRESH_PP);
-    if (force >= 0 && (force == REFRESH_INPLACE || R <= kJacobiPPMax) && (force != REFRESH_CLUSTER || R >= 8))
+    if (force >= 0 && (force == REFRESH_INPLACE || R <= kJacobiPPMax) && (force != REFRESH_CLUSTER || R >= 8) &&
+        (force != REFRESH_DC || (R >= 2 && R <= kDCMax)))
       mode = force;
     const RefreshSmem plan = refresh_plan(R, mode);
     if (mode == REFRESH_CLUSTER) {
@@ -968,6 +986,9 @@ static ng_status launch_refresh_chain(ngsgd_ctx* h, int n, double eta) {
       NG_CUDA_TRY(cudaLaunchKernelEx(&lc, refresh_kernel<REFRESH_CLUSTER>, R, D, n, eta, a_, e_,
                                      (const float*)h->KL, h->dstate, (const double*)h->sums, h->Amat, h->svec,
                                      h->flags, dbg));
+    } else if (mode == REFRESH_DC) {
+      refresh_kernel<REFRESH_DC><<<1, 1024, plan.total_bytes, ss>>>(R, D, n, eta, a_, e_, h->KL, h->dstate,
+                                                                    h->sums, h->Amat, h->svec, h->flags, dbg);
     } else if (mode == REFRESH_PP) {
       refresh_kernel<REFRESH_PP><<<1, 1024, plan.total_bytes, ss>>>(R, D, n, eta, a_, e_, h->KL, h->dstate,
                                                                     h->sums, h->Amat, h->svec, h->flags, dbg);
@@ -1610,12 +1631,30 @@ ng_status ngsgd_set_state(ngsgd_t h, const ngsgd_state_host* in) {
 ng_status ng_debug_eig_clocks(uint64_t* out) {
   NG_REQUIRE(out != nullptr, NG_EINVAL, "NULL argument");
   NG_CUDA_TRY(cudaDeviceSynchronize());
-  unsigned long long v[8];
+  unsigned long long v[8], w[16];
   NG_CUDA_TRY(cudaMemcpyFromSymbol(v, g_eig_clk, sizeof(v)));
+  NG_CUDA_TRY(cudaMemcpyFromSymbol(w, g_dc_clk, sizeof(w)));
   for (int i = 0; i < 8; ++i) out[i] = v[i];
+  for (int i = 0; i < 16; ++i) out[8 + i] = w[i];
   std::memset(v, 0, sizeof(v));
+  std::memset(w, 0, sizeof(w));
   NG_CUDA_TRY(cudaMemcpyToSymbol(g_eig_clk, v, sizeof(v)));
+  NG_CUDA_TRY(cudaMemcpyToSymbol(g_dc_clk, w, sizeof(w)));
   return NG_OK;
+}
+
+__global__ void __launch_bounds__(1024) debug_eig_dc_kernel(const double* Z, int n, double* lam, double* vt) {
+  extern __shared__ __align__(16) unsigned char ng_smem[];
+  eig_dc(reinterpret_cast<double*>(ng_smem), dc_plan(n), Z, n, lam, vt, n);
+}
+
+ng_status ng_debug_eig_dc(const double* z, int32_t n, double* lam, double* vt, void* stream) {
+  NG_REQUIRE(z && lam && vt, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(n >= 1 && n <= kDCMax, NG_ESHAPE, "n must be in [1, 80]");
+  const size_t smem = dc_plan(n).total;
+  NG_CUDA_TRY(cudaFuncSetAttribute(debug_eig_dc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  debug_eig_dc_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(z, n, lam, vt);
+  return check_launch("debug_eig_dc_kernel");
 }
 
 }  // extern "C"
