@@ -826,11 +826,12 @@ ng_status ngsgd_create_impl(int dim, int max_rows, const ngsgd_config* cfg, cuda
   ALLOC(h->Amat, R * R);
   ALLOC(h->Mmat, R * R);
   ALLOC(h->Cfac, R * R);
+  ALLOC(h->trpart, 32);
   ALLOC(h->svec, R);
   ALLOC(h->xxpart, (size_t)h->ctiles * max_rows);
   ALLOC(h->ppart, (size_t)h->ctiles * max_rows);
   ALLOC(h->p, max_rows);
-  ALLOC(h->sums, 2);
+  ALLOC(h->sums, 4);   // [0] tr(XX^T) (apply), [1] sum p, [2] tr(XX^T) for the early refresh launch, [3] spare
   ALLOC(h->gamma, 1);
   ALLOC(h->flags, 8);
 #undef ALLOC
@@ -861,6 +862,7 @@ void ngsgd_destroy_impl(ngsgd_ctx* h) {
   for (float* p : fp) if (p) cudaFree(p);
   if (h->dstate) cudaFree(h->dstate);
   if (h->Cfac) cudaFree(h->Cfac);
+  if (h->trpart) cudaFree(h->trpart);
   if (h->sums) cudaFree(h->sums);
   if (h->flags) cudaFree(h->flags);
   if (h->h_scalar) cudaFreeHost(h->h_scalar);
@@ -944,7 +946,7 @@ static bool skip_refresh_knob() {
   return v == 1;
 }
 
-static ng_status launch_refresh_chain(ngsgd_ctx* h, int n, double eta) {
+static ng_status launch_refresh_chain(ngsgd_ctx* h, int n, double eta, const double* trx) {
   if (skip_refresh_knob()) return NG_OK;
   const int D = h->dim, R = h->rank;
   cudaStream_t st = h->st;
@@ -984,17 +986,17 @@ static ng_status launch_refresh_chain(ngsgd_ctx* h, int n, double eta) {
       lc.attrs = at;
       lc.numAttrs = 1;
       NG_CUDA_TRY(cudaLaunchKernelEx(&lc, refresh_kernel<REFRESH_CLUSTER>, R, D, n, eta, a_, e_,
-                                     (const float*)h->KL, h->dstate, (const double*)h->sums, h->Amat, h->svec,
+                                     (const float*)h->KL, h->dstate, trx, h->Amat, h->svec,
                                      h->flags, dbg));
     } else if (mode == REFRESH_DC) {
       refresh_kernel<REFRESH_DC><<<1, 1024, plan.total_bytes, ss>>>(R, D, n, eta, a_, e_, h->KL, h->dstate,
-                                                                    h->sums, h->Amat, h->svec, h->flags, dbg);
+                                                                    trx, h->Amat, h->svec, h->flags, dbg);
     } else if (mode == REFRESH_PP) {
       refresh_kernel<REFRESH_PP><<<1, 1024, plan.total_bytes, ss>>>(R, D, n, eta, a_, e_, h->KL, h->dstate,
-                                                                    h->sums, h->Amat, h->svec, h->flags, dbg);
+                                                                    trx, h->Amat, h->svec, h->flags, dbg);
     } else {
       refresh_kernel<REFRESH_INPLACE><<<1, 1024, plan.total_bytes, ss>>>(R, D, n, eta, a_, e_, h->KL, h->dstate,
-                                                                         h->sums, h->Amat, h->svec, h->flags, dbg);
+                                                                         trx, h->Amat, h->svec, h->flags, dbg);
     }
     NG_TRY(check_launch("refresh_kernel"));
   }
@@ -1157,7 +1159,7 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
                                        h->gamma, gamma_out, h->flags);
     NG_TRY(check_launch("finalize_kernel"));
   }
-  if (upd) NG_TRY(launch_refresh_chain(h, n, eta));
+  if (upd) NG_TRY(launch_refresh_chain(h, n, eta, h->sums));
   h->t += 1;
   h->last_updated = upd ? 1 : 0;
   if (updated_out) *updated_out = upd ? 1 : 0;
@@ -1190,6 +1192,39 @@ __global__ void __launch_bounds__(256) seg_reduce_kernel(const __grid_constant__
     for (int z = 0; z < sp; ++z) acc += src[(int64_t)z * sr.zstride[g]];
     sr.out[g][r * sr.ldo[g] + c] = acc;
   }
+}
+
+// tr(X X^T) of every updating state, computed before the apply so the refresh chains can
+// be launched right after K_t, L_t (phase B): sums[2] = sum_i ||x_i||^2 in FP64, partial
+// sums of kTrBlocks row slices reduced in a fixed order.
+constexpr int kTrBlocks = 32;
+struct TraceGroup {
+  const float* x[kSegMax];
+  int64_t ld[kSegMax];
+  int n[kSegMax], D[kSegMax];
+  double* out[kSegMax];
+  double* part[kSegMax];   // kTrBlocks each
+  int count;
+};
+__global__ void __launch_bounds__(256) trace_part_kernel(const __grid_constant__ TraceGroup tg) {
+  __shared__ double sc[32];
+  const int g = blockIdx.y, b = blockIdx.x;
+  const int n = tg.n[g], D = tg.D[g];
+  const int r0 = (int)((int64_t)n * b / kTrBlocks), r1 = (int)((int64_t)n * (b + 1) / kTrBlocks);
+  double acc = 0.0;
+  for (int r = r0; r < r1; ++r) {
+    const float* xr = tg.x[g] + (int64_t)r * tg.ld[g];
+    for (int j = threadIdx.x; j < D; j += blockDim.x) { const double v = xr[j]; acc += v * v; }
+  }
+  acc = block_sum(acc, sc);
+  if (threadIdx.x == 0) tg.part[g][b] = acc;
+}
+__global__ void trace_final_kernel(const __grid_constant__ TraceGroup tg) {
+  const int g = threadIdx.x;
+  if (g >= tg.count) return;
+  double acc = 0.0;
+  for (int b = 0; b < kTrBlocks; ++b) acc += tg.part[g][b];
+  *tg.out[g] = acc;
 }
 
 struct FinalizeGroup {
@@ -1459,6 +1494,29 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
     }
     if (kl.count) NG_TRY(launch_seg_reduce(st, kl));
   }
+  // ---- tr(X X^T) of the updating states, then their refresh chains start right away (they
+  // need J, K, L and the trace only); phase C keeps using the pre-refresh W_t
+  std::vector<float*> Wold(G);
+  for (int g = 0; g < G; ++g) Wold[g] = calls[grp[g]].h->W[calls[grp[g]].h->cur];
+  if (!ug.empty()) {
+    TraceGroup tr;
+    std::memset(&tr, 0, sizeof(tr));
+    tr.count = (int)ug.size();
+    for (size_t u = 0; u < ug.size(); ++u) {
+      NgCall& c = calls[grp[ug[u]]];
+      tr.x[u] = c.x; tr.ld[u] = c.ld; tr.n[u] = c.n; tr.D[u] = c.h->dim;
+      tr.out[u] = c.h->sums + 2; tr.part[u] = c.h->trpart;
+    }
+    trace_part_kernel<<<dim3(kTrBlocks, tr.count), 256, 0, st>>>(tr);
+    NG_TRY(check_launch("trace_part_kernel"));
+    trace_final_kernel<<<1, 32, 0, st>>>(tr);
+    NG_TRY(check_launch("trace_final_kernel"));
+    for (int g : ug) {
+      NgCall& c = calls[grp[g]];
+      const double eta = 1.0 - exp(-(double)c.n / (double)c.h->cfg.s_samples);   // eqn:eta:ns
+      NG_TRY(launch_refresh_chain(c.h, c.n, eta, c.h->sums + 2));
+    }
+  }
   // ---- phase C: X_hat = X - H W with fused row norms (one launch), finalize (one launch)
   {
     double flops = 0, bytes = 0;
@@ -1474,7 +1532,7 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
       bytes += 4.0 * (2.0 * c.n * D + (double)R * D);
       TcGroupDesc& q = d[g];
       q.M = c.n; q.N = D; q.K = R; q.splits = 1;
-      q.A = h->H; q.lda = R; q.B = h->W[h->cur]; q.ldb = h->ldw;
+      q.A = h->H; q.lda = R; q.B = Wold[g]; q.ldb = h->ldw;
       q.epi.kind = TC_EPI_NGAPPLY; q.epi.C = c.x; q.epi.ldc = c.ld; q.epi.xx = h->xxpart; q.epi.pp = h->ppart;
       q.epi.part_ld = h->max_rows;
       q.splits_used = nullptr;
@@ -1491,10 +1549,6 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
   for (int g = 0; g < G; ++g) {
     NgCall& c = calls[grp[g]];
     ngsgd_ctx* h = c.h;
-    if (upd[grp[g]]) {
-      const double eta = 1.0 - exp(-(double)c.n / (double)h->cfg.s_samples);   // eqn:eta:ns
-      NG_TRY(launch_refresh_chain(h, c.n, eta));
-    }
     h->t += 1;
     h->last_updated = upd[grp[g]] ? 1 : 0;
     if (c.updated_out) *c.updated_out = upd[grp[g]] ? 1 : 0;
