@@ -826,7 +826,7 @@ ng_status ngsgd_create_impl(int dim, int max_rows, const ngsgd_config* cfg, cuda
   ALLOC(h->Amat, R * R);
   ALLOC(h->Mmat, R * R);
   ALLOC(h->Cfac, R * R);
-  ALLOC(h->trpart, 32);
+  ALLOC(h->trpart, max_rows);
   ALLOC(h->svec, R);
   ALLOC(h->xxpart, (size_t)h->ctiles * max_rows);
   ALLOC(h->ppart, (size_t)h->ctiles * max_rows);
@@ -1195,36 +1195,43 @@ __global__ void __launch_bounds__(256) seg_reduce_kernel(const __grid_constant__
 }
 
 // tr(X X^T) of every updating state, computed before the apply so the refresh chains can
-// be launched right after K_t, L_t (phase B): sums[2] = sum_i ||x_i||^2 in FP64, partial
-// sums of kTrBlocks row slices reduced in a fixed order.
-constexpr int kTrBlocks = 32;
+// be launched right after K_t, L_t (phase B): sums[2] = sum_i ||x_i||^2 in FP64; one CTA
+// per row (row sums), then a fixed-order sum over the rows.
 struct TraceGroup {
   const float* x[kSegMax];
   int64_t ld[kSegMax];
   int n[kSegMax], D[kSegMax];
   double* out[kSegMax];
-  double* part[kSegMax];   // kTrBlocks each
+  double* part[kSegMax];   // n row sums each
   int count;
 };
-__global__ void __launch_bounds__(256) trace_part_kernel(const __grid_constant__ TraceGroup tg) {
+__global__ void __launch_bounds__(128) trace_part_kernel(const __grid_constant__ TraceGroup tg) {
   __shared__ double sc[32];
-  const int g = blockIdx.y, b = blockIdx.x;
-  const int n = tg.n[g], D = tg.D[g];
-  const int r0 = (int)((int64_t)n * b / kTrBlocks), r1 = (int)((int64_t)n * (b + 1) / kTrBlocks);
+  const int g = blockIdx.y, r = blockIdx.x;
+  if (r >= tg.n[g]) return;
+  const int D = tg.D[g];
+  const float* xr = tg.x[g] + (int64_t)r * tg.ld[g];
   double acc = 0.0;
-  for (int r = r0; r < r1; ++r) {
-    const float* xr = tg.x[g] + (int64_t)r * tg.ld[g];
+  if ((reinterpret_cast<uintptr_t>(xr) & 15) == 0) {
+    const int d4 = D >> 2;
+    for (int j = threadIdx.x; j < d4; j += blockDim.x) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(xr) + j);
+      acc += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+    }
+    for (int j = (d4 << 2) + threadIdx.x; j < D; j += blockDim.x) { const double v = xr[j]; acc += v * v; }
+  } else {
     for (int j = threadIdx.x; j < D; j += blockDim.x) { const double v = xr[j]; acc += v * v; }
   }
   acc = block_sum(acc, sc);
-  if (threadIdx.x == 0) tg.part[g][b] = acc;
+  if (threadIdx.x == 0) tg.part[g][r] = acc;
 }
-__global__ void trace_final_kernel(const __grid_constant__ TraceGroup tg) {
-  const int g = threadIdx.x;
-  if (g >= tg.count) return;
+__global__ void __launch_bounds__(256) trace_final_kernel(const __grid_constant__ TraceGroup tg) {
+  __shared__ double sc[32];
+  const int g = blockIdx.x;
   double acc = 0.0;
-  for (int b = 0; b < kTrBlocks; ++b) acc += tg.part[g][b];
-  *tg.out[g] = acc;
+  for (int r = threadIdx.x; r < tg.n[g]; r += blockDim.x) acc += tg.part[g][r];
+  acc = block_sum(acc, sc);
+  if (threadIdx.x == 0) *tg.out[g] = acc;
 }
 
 struct FinalizeGroup {
@@ -1507,9 +1514,11 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
       tr.x[u] = c.x; tr.ld[u] = c.ld; tr.n[u] = c.n; tr.D[u] = c.h->dim;
       tr.out[u] = c.h->sums + 2; tr.part[u] = c.h->trpart;
     }
-    trace_part_kernel<<<dim3(kTrBlocks, tr.count), 256, 0, st>>>(tr);
+    int nmax = 1;
+    for (int u = 0; u < tr.count; ++u) nmax = std::max(nmax, tr.n[u]);
+    trace_part_kernel<<<dim3(nmax, tr.count), 128, 0, st>>>(tr);
     NG_TRY(check_launch("trace_part_kernel"));
-    trace_final_kernel<<<1, 32, 0, st>>>(tr);
+    trace_final_kernel<<<tr.count, 256, 0, st>>>(tr);
     NG_TRY(check_launch("trace_final_kernel"));
     for (int g : ug) {
       NgCall& c = calls[grp[g]];

@@ -30,7 +30,7 @@ struct ngsgd_ctx {
   float* Amat = nullptr;    // R x R  A_t; also M of B.3.1
   float* Mmat = nullptr;    // R x R (unused by the repair since the triangular-solve form)
   double* Cfac = nullptr;   // R x R lower Cholesky factor of O (B.3.1 repair)
-  double* trpart = nullptr; // kTrBlocks partial sums of tr(X X^T)
+  double* trpart = nullptr; // max_rows row sums of ||x_i||^2 (early tr(X X^T))
   float* svec = nullptr;    // R:  N(1-eta)/eta (d_i + rho)  (row scale of B_t)
   float* xxpart = nullptr;  // ctiles x max_rows: partial ||x_i||^2
   float* ppart = nullptr;   // ctiles x max_rows: partial ||x_hat_i||^2
