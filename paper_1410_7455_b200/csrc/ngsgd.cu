@@ -1287,10 +1287,10 @@ static ng_status launch_seg_reduce(cudaStream_t st, SegReduce& sr) {
 }
 
 // ---- K_t = J J^T and L_t = W J^T of every updating state in one launch.
-// One CTA = the whole R x R product over one 256-wide chunk of the D axis (FP32 FMA, the
+// One CTA = the whole R x R product over one 64-wide chunk of the D axis (FP32 FMA, the
 // chunk's partial written to part[chunk]); the fixed-order segmented reduction sums the
 // chunks.  FP32 in both precision modes (the refresh needs them accurate).
-constexpr int kRRMax = 32, kRRChunk = 256, kRRSub = 64;
+constexpr int kRRMax = 32, kRRChunk = 64, kRRSub = 64;
 struct RRProb {
   const float* A;
   const float* B;
