@@ -128,7 +128,7 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
                                         int kb0, int nkb, int ntile, int ztile, const TcEpilogue& epi,
                                         int nstages) {
   constexpr uint32_t A_BYTES = kBM * kBK * 4, B_BYTES = BN * kBK * 4, STAGE = A_BYTES + B_BYTES;
-  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));   // power of 2
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned ring (SWIZZLE_128B atoms); pointer arithmetic keeps the shared space
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -235,6 +235,44 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
   mbar_wait(&accum_bar, 0);
   tc_fence_after();
   __syncwarp();
+  if constexpr (EPI == TC_EPI_PNORM) {
+    // Z row (80 columns = 8 groups of 10) and the group 2-norms
+    static_assert(BN == 80, "p-norm epilogue: 80-column tiles");
+    float acc[80];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      uint32_t v[16];
+      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * 16), v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[c * 16 + j] = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
+    }
+    if (row < M) {
+      const bool full = n0 + 80 <= N && ((reinterpret_cast<uintptr_t>(crow + n0) & 15) == 0);
+      if (full) {
+#pragma unroll
+        for (int j = 0; j < 80; j += 4)
+          *reinterpret_cast<float4*>(crow + n0 + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 80; ++j)
+          if (n0 + j < N) crow[n0 + j] = acc[j];
+      }
+      float* yrow = epi.y + (int64_t)row * epi.ldy;
+      const int g0 = n0 / 10;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        float sq = 0.f;
+#pragma unroll
+        for (int q = 0; q < 10; ++q) sq = fmaf(acc[g * 10 + q], acc[g * 10 + q], sq);
+        if (n0 + g * 10 + 10 <= N) yrow[g0 + g] = sqrtf(sq);
+      }
+      if (n0 + 80 >= N) {   // last column tile: bias input and the zero padding
+        const int dp = N / 10;
+        yrow[dp] = 1.f;
+        for (int c = dp + 1; c < epi.ldy; ++c) yrow[c] = 0.f;
+      }
+    }
+  } else {
   const float scale = (EPI == TC_EPI_AXPY) ? __ldg(epi.scale) : 0.f;
   float xx = 0.f, pp = 0.f;   // TC_EPI_NGAPPLY row partial sums over this tile's columns
 #pragma unroll
@@ -293,6 +331,7 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
     epi.xx[(int64_t)ntile * epi.part_ld + row] = xx;
     epi.pp[(int64_t)ntile * epi.part_ld + row] = pp;
   }
+  }   // EPI != TC_EPI_PNORM
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -452,6 +491,22 @@ ng_status tc_gemm_tf32(cudaStream_t st, int M, int N, int K, const float* A, int
   if (bn == 32) return dispatch_major<32>(st, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
   if (bn == 64) return dispatch_major<64>(st, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
   return dispatch_major<128>(st, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
+}
+
+ng_status tc_gemm_tf32_pnorm(cudaStream_t st, int M, int N, int K, const float* A, int64_t lda, const float* B,
+                                  int64_t ldb, float* Z, int64_t ldz, float* Ynext, int64_t ldy) {
+  NG_REQUIRE(M >= 1 && N >= 10 && K >= 1 && N % 10 == 0 && ldy >= N / 10 + 1, NG_ESHAPE, "tc_gemm_tf32_pnorm: shape");
+  const int kb = ceil_div(K, kBK);
+  CUtensorMap ta, tb;
+  NG_TRY(make_tmap(&ta, A, K, M, lda, kBM, false));
+  NG_TRY(make_tmap(&tb, B, K, N, ldb, 80, false));
+  TcEpilogue e;
+  e.kind = TC_EPI_PNORM;
+  e.C = Z;
+  e.ldc = ldz;
+  e.y = Ynext;
+  e.ldy = ldy;
+  return launch<80, true, true, TC_EPI_PNORM>(st, ta, tb, M, N, K, kb, 1, e);
 }
 
 template <int BN, bool AK, bool BKM, int EPI>

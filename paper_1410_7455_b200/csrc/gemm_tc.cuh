@@ -22,6 +22,9 @@ enum TcEpiKind : int {
   TC_EPI_PARTIAL = 2,   // C[z][m][n] = acc                    (split-K partials)
   TC_EPI_NGAPPLY = 3,   // C[m][n] -= acc, with per-row partial sums of old^2 / new^2 of this
                         // column tile in xx / pp [blockIdx.x * part_ld + m]  (NG apply)
+  TC_EPI_PNORM = 4,     // C[m][n] = acc and the p-norm of each group of 10 columns:
+                        // y[m][n/10] = sqrt(sum z^2); the last column tile also writes y[m][N/10]
+                        // = 1 (bias input of the next layer) and zeros up to ldy (BN = 80 only)
 };
 
 struct TcEpilogue {
@@ -33,6 +36,8 @@ struct TcEpilogue {
   float* xx = nullptr;        // TC_EPI_NGAPPLY partial ||x_i||^2
   float* pp = nullptr;        // TC_EPI_NGAPPLY partial ||x_hat_i||^2
   int64_t part_ld = 0;
+  float* y = nullptr;         // TC_EPI_PNORM next-layer input [a, 1, 0...], row stride ldy
+  int64_t ldy = 0;
 };
 
 // Launch one GEMM on `st`.  bn in {32, 64, 128}; splits >= 1 (K split evenly over 32-wide
@@ -69,6 +74,12 @@ struct TcGroup {
 
 ng_status tc_gemm_tf32_grouped(cudaStream_t st, const TcGroupDesc* desc, int count, bool a_kmajor, bool b_kmajor,
                                int epi_kind, int bn);
+
+// Forward affine layer fused with the p-norm (G = 10): Z = Y W^T (both K-major,
+// Z row stride ldz) and Ynext = [pnorm(Z), 1, 0 ...] (row stride ldy >= N/10 + 1).  N must be
+// a multiple of 10.  80-column tiles (8 whole groups each).
+ng_status tc_gemm_tf32_pnorm(cudaStream_t st, int M, int N, int K, const float* A, int64_t lda, const float* B,
+                             int64_t ldb, float* Z, int64_t ldz, float* Ynext, int64_t ldy);
 
 // Split count actually used for a requested split count.
 int tc_splits(int K, int splits);

@@ -454,7 +454,13 @@ ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const
     const float* W = h->arena + h->off[l];
     const double R_ = h->rows[l], C_ = h->cols[l];
     ProfScope ps(NG_PROF_FWD_GEMM, st, 2.0 * n * R_ * C_, 4.0 * (n * C_ + R_ * C_ + n * R_));
-    if (tc) {
+    static const int fuse_pnorm = tune_int("NG_TUNE_FWD_PNORM", 1);
+    const bool fused = tc && fuse_pnorm && l < L - 1 && G == 10 && h->rows[l] % 10 == 0;
+    if (fused) {
+      // affine + p-norm in one tensor-core launch (80-column tiles = 8 whole groups)
+      NG_TRY(tc_gemm_tf32_pnorm(st, n, h->rows[l], h->cols[l], h->Y[l], h->ldp[l], W, h->ldp[l], h->Z[l], h->ldr[l],
+                                h->Y[l + 1], h->ldp[l + 1]));
+    } else if (tc) {
       TcEpilogue e;
       e.kind = TC_EPI_STORE; e.C = h->Z[l]; e.ldc = h->ldr[l];
       static const int bn = tune_int("NG_TUNE_FWD_BN", 128);
@@ -463,7 +469,7 @@ ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const
       NG_TRY((gemm_simt<float, true, true>(st, n, h->rows[l], h->cols[l], h->Y[l], h->ldp[l], W, h->ldp[l],
                                            EpiStore<float>{h->Z[l], h->ldr[l], 1.f})));
     }
-    if (l < L - 1) {
+    if (l < L - 1 && !fused) {
       const int64_t tot = (int64_t)n * h->ldp[l + 1];
       (void)tot;
       pnorm_kernel<<<n, 256, sizeof(float) * h->rows[l], st>>>(n, h->rows[l], h->ldr[l], G, h->Z[l], h->Y[l + 1],
