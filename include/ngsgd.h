@@ -280,6 +280,15 @@ ng_status ng_debug_eig_clocks(uint64_t* out);
  * unit eigenvector of lam[i]).  n in [1, 80]; asynchronous on `stream`. */
 ng_status ng_debug_eig_dc(const double* z, int32_t n, double* lam, double* vt, void* stream);
 
+/* The refresh's default eigensolver (Householder + relatively robust representation +
+ * twisted-factorisation eigenvectors, FP64, one CTA; eqn:zt:eig) on its own,
+ * for unit tests: same arguments as ng_debug_eig_dc except that lam / vt come out UNORDERED
+ * (vt row i = unit eigenvector of lam[i]); ok device int[4]: ok[0] = 1 when the solve passed
+ * its orthogonality check (0 = the refresh would fall back to Jacobi; lam / vt undefined),
+ * ok[1] = cycles spent (clock64, whole solve), ok[2..5] = cycles of the phases
+ * (tridiagonalisation, eigenvalues + vectors of T, orthogonality check, V = X Q^T); ok: int[8].  n in [1, 80]; asynchronous on `stream`. */
+ng_status ng_debug_eig_tri(const double* z, int32_t n, double* lam, double* vt, int32_t* ok, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,737 @@
+// eig_tri.cuh -- dense symmetric eigendecomposition for the R x R refresh (eqn:zt:eig:repeat,
+// P:1382-1384): Z = U C U^T.  FP64, ONE CTA (1024 threads), n <= kTriMax.
+//
+//   1. Householder tridiagonalisation Z = Q T Q^T (LAPACK dsytd2 'L' order).  One CTA pass
+//      per column both applies the previous reflector's rank-2 update and forms the next
+//      product A_22 v; the same pass applies the previous reflector to Q and forms Q v, so Q
+//      is accumulated with no extra barriers.  Between passes one warp forms w, updates the
+//      next column and builds the next reflector.  2 barriers per column.
+//   2. T is split where an off-diagonal is negligible (relative to its diagonal neighbours,
+//      or to eps ||T||).  Each block gets a positive definite root representation
+//      L D L^T = T_b - sigma_b I (sigma_b = 0 when T_b factors with D > 0, which Z = Y Y^T
+//      makes the usual case), which determines its eigenvalues to high RELATIVE accuracy
+//      (Demmel-Kahan).  One thread per eigenvalue: bisection on the stationary-qd negcount
+//      until the eigenvalue is isolated, then Rayleigh-quotient steps from the twisted
+//      factorisation (stationary top-down + progressive bottom-up qd, twist r = argmin
+//      |gamma_r|), safeguarded by the bisection bracket.  The eigenvector is the twisted
+//      solve z_r = 1 at the converged shift (Dhillon-Parlett "getvec"); its error is
+//      O(n eps / relgap), so the graded tails of Z_t (eigenvalues over 8-20 decades, tiny
+//      absolute but large relative gaps) come out orthogonal without any Gram-Schmidt.
+//   3. Safety net: X X^T is formed and the solve reports failure when max |X X^T - I| >
+//      kTriOrthTol (tight relative clusters, noise-level eigenvalues of a numerically
+//      indefinite block); the caller then runs the cyclic Jacobi solver instead.
+//   4. The eigenvectors of Z are V = X Q^T (rows), an n x n x n FP64 product.
+//
+// This replaces 8-13 Jacobi sweeps (79 barrier rounds each at R = 80) with ~2n barriers and
+// per-thread qd recurrences.  scratch/ prototypes: tools/tri_proto.py.
+#pragma once
+
+#include "eig_dc.cuh"   // frcp / fdiv / fsqrt (MUFU approximations + Newton steps)
+#include "ng_common.cuh"
+
+namespace ng {
+
+constexpr int kTriMax = 80;
+constexpr int kTriChunks = 5;   // column chunks of the Householder pass
+constexpr double kTriOrthTol = 1e-8;
+constexpr int kTriCoarse = 64;        // coarse negcount points per block (ratio 8 apart)
+constexpr int kTriCoarseBlocks = 16;  // blocks of >= kTriCoarseMin indices that get them
+constexpr int kTriCoarseMin = 8;
+constexpr double kTriClusterTol = 1e-5;   // relative gap below which twisted vectors are redone
+__device__ long long g_tri_clk[8];
+__device__ int g_tri_maxit;   // thread 0's phase stamps of the last solve (ng_debug_eig_tri)
+
+// Shared-memory plan (offsets in doubles from a 16-byte aligned base), n <= kTriMax.
+struct TriPlan {
+  int n, lda;
+  size_t oA, oQ, oX, od, oe, oD, oL, oDL, oDL2, ogu, osig, olam, omu, ov, ow, opb, oqb, otau, ored, oint, total;
+};
+__host__ __device__ inline TriPlan tri_plan(int n) {
+  TriPlan p;
+  p.n = n;
+  p.lda = n + 1;   // odd row stride: column walks across lanes stay conflict-free
+  size_t o = 0;
+  p.oA = o; o += (size_t)n * p.lda;   // Householder work; then per-eigenvalue qd scratch; then V
+  p.oQ = o; o += (size_t)n * p.lda;   // accumulated reflectors
+  p.oX = o; o += (size_t)n * p.lda;   // eigenvectors of T (rows)
+  p.od = o; o += n;                   // diag(T)
+  p.oe = o; o += n;                   // offdiag(T)
+  p.oD = o; o += n;                   // root representation D (per block)
+  p.oL = o; o += n;                   // root representation L
+  p.oDL = o; o += n;                  // D_i L_i
+  p.oDL2 = o; o += n;                 // D_i L_i^2
+  p.ogu = o; o += n;                  // Gershgorin upper bound of the block's L D L^T, per index
+  p.osig = o; o += n;                 // block shift sigma, per index
+  p.olam = o; o += n;                 // eigenvalues (index order, unscaled)
+  p.omu = o; o += n;                  // eigenvalues of the block representations
+  p.ov = o; o += 3 * (size_t)n;       // reflector vectors (triple buffer)
+  p.ow = o; o += 2 * (size_t)n;       // w vectors (double buffer)
+  p.opb = o; o += (size_t)kTriChunks * n;       // partial sums of A_22 v
+  p.oqb = o; o += 2 * (size_t)kTriChunks * n;   // partial sums of Q v (double buffer)
+  p.otau = o; o += 4;                 // tau (triple buffer)
+  p.ored = o; o += 64;
+  p.oint = o;   // ints: bstart[n], bend[n], crow[n], cpos[n], status[4], blo[kTriCoarseBlocks], coarse counts
+  p.total = sizeof(double) * o + sizeof(int) * (4 * (size_t)n + 4 + kTriCoarseBlocks * (kTriCoarse + 1));
+  return p;
+}
+
+// Register layout of an n-vector inside a warp: index i lives in lane (i & 31), slot i >> 5.
+__device__ __forceinline__ double tri_bcast(const double (&r)[3], int i) {   // i warp-uniform
+  const int c = i >> 5;
+  const double x = (c == 0) ? r[0] : (c == 1 ? r[1] : r[2]);
+  return __shfl_sync(0xffffffffu, x, i & 31);
+}
+
+
+// Reflector from the (already updated) column c held in registers (col[i], i >= c), LAPACK
+// dlarfg on rows c+1..n-1: H = I - tau v v^T, H x = beta e_1, v_{c+1} = 1.  One warp;
+// writes v (smem), tau, d[c] = col_c, e[c] = beta.
+__device__ __forceinline__ void tri_reflect(const double (&col)[3], int c, int n, double* __restrict__ vout,
+                                            double* __restrict__ tau_out, double* __restrict__ d,
+                                            double* __restrict__ e, int lane) {
+  const double alpha = tri_bcast(col, c + 1);
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int i = lane + 32 * q;
+    if (i >= c + 2 && i < n) s = fma(col[q], col[q], s);
+  }
+  s = warp_sum(s);
+  double beta, scal, tau;
+  if (s == 0.0) {
+    beta = alpha; tau = 0.0; scal = 0.0;
+  } else {
+    beta = -copysign(fsqrt(fma(alpha, alpha, s)), alpha);
+    tau = fdiv(beta - alpha, beta);
+    scal = frcp(alpha - beta);
+  }
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int i = lane + 32 * q;
+    if (i < n) vout[i] = (i >= c + 2) ? col[q] * scal : (i == c + 1 ? 1.0 : 0.0);
+  }
+  const double dc = tri_bcast(col, c);
+  if (lane == 0) { d[c] = dc; e[c] = beta; *tau_out = tau; }
+}
+
+// Step 1: A (n x n symmetric, ld lda, scaled) -> d, e; Q = H_0 ... H_{n-3} accumulated.
+// Per column k, two barriers.  The pass (30 warps: 3 row groups x kTriChunks column chunks
+// for A_22 and the same for Q; lanes run over ROWS, so each thread walks a short run of
+// columns with no shuffles) applies update k-1 (rank 2) to A_22 and forms partial sums of
+// p = A_22 v_k, applies H_{k-1} to Q and forms partial sums of Q v_k.  Then warp 0 adds the
+// partials, forms w_k, the updated column k+1 and reflector k+1.
+__device__ __forceinline__ void tri_reduce(const TriPlan& P, double* __restrict__ sm) {
+  const int n = P.n, lda = P.lda, tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  double* A = sm + P.oA;
+  double* Q = sm + P.oQ;
+  double* d = sm + P.od;
+  double* e = sm + P.oe;
+  double* vb = sm + P.ov;       // v by parity of the reflector index
+  double* wb = sm + P.ow;       // w by parity
+  double* pA = sm + P.opb;      // [kTriChunks][n] partial sums of A_22 v
+  double* pQ = sm + P.oqb;      // [2][kTriChunks][n] partial sums of Q v (parity)
+  double* tauv = sm + P.otau;
+  for (int idx = tid; idx < n * n; idx += nt) {
+    const int i = idx / n, j = idx - i * n;
+    Q[i * lda + j] = (i == j) ? 1.0 : 0.0;
+  }
+  if (n <= 2) {
+    if (tid == 0) {
+      d[0] = A[0];
+      if (n == 2) { d[1] = A[lda + 1]; e[0] = A[lda]; }
+    }
+    __syncthreads();
+    return;
+  }
+  if (warp == 0) {
+    double col[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int i = lane + 32 * q;
+      col[q] = (i < n) ? A[i * lda] : 0.0;
+    }
+    tri_reflect(col, 0, n, vb, tauv, d, e, lane);
+  }
+  __syncthreads();
+  // warps 0-14: A_22 (3 row groups x kTriChunks column chunks); warps 15-29: Q (same split);
+  // warps 30-31 idle.  The Q warps only need v_k, v_{k-1}, tau_{k-1} and Q v_{k-1}, all
+  // known when step k starts, so they run while warp 0 forms reflector k+1 (named barrier 1
+  // joins only the A warps before it; barrier 0 closes the step for everyone).
+  const bool qwarp = warp >= 3 * kTriChunks;
+  const int wl = qwarp ? warp - 3 * kTriChunks : warp;
+  const int rg = wl % 3, ch = wl / 3;
+  unsigned t_pass = 0, t_ser = 0, t0 = clock();
+  for (int k = 0; k + 2 < n; ++k) {
+    const int cur = k & 1, prv = cur ^ 1;
+    const int k3 = k % 3, p3 = (k + 2) % 3;
+    const double* v = vb + k3 * n;
+    const double* vp = vb + p3 * n;
+    const double* wp = wb + prv * n;
+    if (!qwarp) {
+      const int m = n - k - 1, L = (m + kTriChunks - 1) / kTriChunks;
+      const int i = k + 1 + 32 * rg + lane;
+      const int j0 = k + 1 + ch * L, j1 = min(n, j0 + L);
+      if (i < n) {
+        double acc = 0.0;
+        double* Ai = A + i * lda;
+        if (k > 0) {
+          const double vpi = vp[i], wpi = wp[i];
+#pragma unroll 4
+          for (int j = j0; j < j1; ++j) {
+            const double a = fma(-vpi, wp[j], fma(-wpi, vp[j], Ai[j]));
+            Ai[j] = a;
+            acc = fma(a, v[j], acc);
+          }
+        } else {
+#pragma unroll 4
+          for (int j = j0; j < j1; ++j) acc = fma(Ai[j], v[j], acc);
+        }
+        pA[ch * n + i] = acc;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(3 * kTriChunks * 32) : "memory");
+    } else if (ch < kTriChunks) {
+      const int L = (n - k + kTriChunks - 1) / kTriChunks;
+      const int r = 32 * rg + lane;
+      const int j0 = k + ch * L, j1 = min(n, j0 + L);   // H_{k-1} acts on columns k..n-1
+      if (r < n) {
+        double acc = 0.0;
+        double* Qr = Q + r * lda;
+        if (k > 0) {
+          double qv = 0.0;
+#pragma unroll
+          for (int c2 = 0; c2 < kTriChunks; ++c2) qv += pQ[(prv * kTriChunks + c2) * n + r];
+          const double sq = tauv[p3] * qv;
+#pragma unroll 4
+          for (int j = j0; j < j1; ++j) {
+            const double x = fma(-sq, vp[j], Qr[j]);
+            Qr[j] = x;
+            acc = fma(x, v[j], acc);   // v_k[k] = 0: column k adds nothing
+          }
+        } else {
+#pragma unroll 4
+          for (int j = j0; j < j1; ++j) acc = fma(Qr[j], v[j], acc);
+        }
+        pQ[(cur * kTriChunks + ch) * n + r] = acc;
+      }
+    }
+    if (warp == 0) { const unsigned t1 = clock(); t_pass += t1 - t0; t0 = t1; }
+    if (warp == 0) {
+      // w_k = tau (p - (tau/2)(p.v) v), column c = k+1 after update k, reflector c
+      const int c = k + 1;
+      const double tau = tauv[k3];
+      double pr[3], vr[3], w[3], col[3];
+      double dot = 0.0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int i = lane + 32 * q;
+        const bool in = i >= c && i < n;
+        double s = 0.0;
+        if (in) {
+#pragma unroll
+          for (int c2 = 0; c2 < kTriChunks; ++c2) s += pA[c2 * n + i];
+        }
+        pr[q] = s;
+        vr[q] = in ? v[i] : 0.0;
+        col[q] = in ? A[i * lda + c] : 0.0;
+        dot = fma(s, vr[q], dot);
+      }
+      dot = warp_sum(dot);
+      const double hk = 0.5 * tau * dot;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        w[q] = tau * fma(-hk, vr[q], pr[q]);
+        const int i = lane + 32 * q;
+        if (i < n) wb[cur * n + i] = w[q];
+      }
+      const double vc = tri_bcast(vr, c), wc = tri_bcast(w, c);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) col[q] = fma(-vr[q], wc, fma(-w[q], vc, col[q]));
+      if (c + 2 < n) {
+        tri_reflect(col, c, n, vb + ((k + 1) % 3) * n, tauv + (k + 1) % 3, d, e, lane);
+      } else {
+        const int l = n - 1;
+        const double dc = tri_bcast(col, c), el = tri_bcast(col, l);
+        const double vl = tri_bcast(vr, l), wl = tri_bcast(w, l);
+        if (lane == 0) {
+          d[c] = dc;
+          e[c] = el;
+          d[l] = fma(-2.0 * vl, wl, A[l * lda + l]);
+        }
+      }
+    }
+    __syncthreads();
+    if (warp == 0) { const unsigned t1 = clock(); t_ser += t1 - t0; t0 = t1; }
+  }
+  if (tid == 0) { g_tri_clk[6] = t_pass; g_tri_clk[7] = t_ser; }
+  // the last reflector (n-3) on Q columns n-2, n-1
+  {
+    const int k = n - 3, cur = k & 1;
+    const double* v = vb + (k % 3) * n;
+    for (int idx = tid; idx < 2 * n; idx += nt) {
+      const int r = idx >> 1, j = n - 2 + (idx & 1);
+      double qv = 0.0;
+#pragma unroll
+      for (int c2 = 0; c2 < kTriChunks; ++c2) qv += pQ[(cur * kTriChunks + c2) * n + r];
+      Q[r * lda + j] = fma(-tauv[k % 3] * qv, v[j], Q[r * lda + j]);
+    }
+  }
+  __syncthreads();
+}
+
+// Reciprocal from MUFU.RCP64H plus one Newton step (relative error ~2^-44): the negcount
+// only needs the signs of the D+_i, and a 2^-44 relative perturbation of each ratio is a
+// tiny relative perturbation of the representation's entries (Demmel-Kahan), so the count
+// stays that of a representation relatively close to L D L^T.
+__device__ __forceinline__ double rcp1(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return fma(r, fma(-x, r, 1.0), r);
+}
+
+// Stationary qd (dstqds) negcount of L D L^T - lam on block [lo, hi): the number of
+// eigenvalues of the block's representation below lam.  DL2_i = D_i L_i^2.
+__device__ __forceinline__ int tri_negcount(const double* __restrict__ D, const double* __restrict__ DL2, int lo, int hi,
+                                            double lam, double pivmin) {
+  int neg = 0;
+  double s = -lam;
+  for (int i = lo; i < hi - 1; ++i) {
+    double dp = D[i] + s;
+    if (fabs(dp) < pivmin) dp = -pivmin;
+    neg += dp < 0.0;
+    s = fma(DL2[i] * rcp1(dp), s, -lam);
+  }
+  double dp = D[hi - 1] + s;
+  if (fabs(dp) < pivmin) dp = -pivmin;
+  return neg + (dp < 0.0);
+}
+
+// Twisted factorisation of L D L^T - lam on [lo, hi) (Dhillon-Parlett): stationary qd
+// top-down (L+_i -> x[i], s_i -> sc[i]), progressive qd bottom-up (U-_i overwrites sc[i]
+// once gamma_i = s_i + p_i + lam is formed), twist r = argmin |gamma_i|; z_r = 1,
+// z_i = -L+_i z_{i+1} (i < r), z_{i+1} = -U-_i z_i (i >= r).  z -> x[lo..hi-1].  Returns the
+// negcount; gamma_r and ||z||^2 out.
+__device__ __forceinline__ int tri_twisted(const double* __restrict__ D, const double* __restrict__ L,
+                                           const double* __restrict__ DL, const double* __restrict__ DL2, int lo,
+                                           int hi, double lam, double pivmin, double* __restrict__ x,
+                                           double* __restrict__ sc, double* gamma_out, double* znorm2_out) {
+  int neg = 0;
+  double s = -lam;
+  for (int i = lo; i < hi - 1; ++i) {
+    sc[i] = s;
+    double dp = D[i] + s;
+    if (fabs(dp) < pivmin) dp = -pivmin;
+    neg += dp < 0.0;
+    const double lp = fdiv(DL[i], dp);
+    x[i] = lp;
+    s = fma(lp * L[i], s, -lam);
+  }
+  {
+    double dp = D[hi - 1] + s;
+    if (fabs(dp) < pivmin) dp = -pivmin;
+    neg += dp < 0.0;
+  }
+  double p = D[hi - 1] - lam;
+  int r = hi - 1;
+  double gbest = s + p + lam;
+  for (int i = hi - 2; i >= lo; --i) {
+    double dm = DL2[i] + p;
+    if (fabs(dm) < pivmin) dm = -pivmin;
+    const double rd = frcp(dm);
+    const double si = sc[i];
+    sc[i] = DL[i] * rd;                 // U-_i = D_i L_i / D-_{i+1}
+    p = fma(p, D[i] * rd, -lam);
+    const double g = si + p + lam;
+    if (fabs(g) < fabs(gbest)) { gbest = g; r = i; }
+  }
+  double nrm = 1.0, zn = 1.0, znn = 0.0;   // z_{i+1}, z_{i+2} on the upward walk
+  for (int i = r - 1; i >= lo; --i) {
+    double z = -x[i] * zn;
+    if (zn == 0.0 && i + 2 < hi) z = -fdiv(DL[i + 1], DL[i]) * znn;   // restart across a zero (dlar1v)
+    x[i] = z;
+    nrm = fma(z, z, nrm);
+    znn = zn;
+    zn = z;
+  }
+  x[r] = 1.0;
+  zn = 1.0;
+  znn = 0.0;
+  for (int i = r; i < hi - 1; ++i) {
+    double z = -sc[i] * zn;
+    if (zn == 0.0 && i > lo) z = -fdiv(DL[i - 1], DL[i]) * znn;
+    x[i + 1] = z;
+    nrm = fma(z, z, nrm);
+    znn = zn;
+    zn = z;
+  }
+  *gamma_out = gbest;
+  *znorm2_out = nrm;
+  return neg;
+}
+
+// C[i][j] = sum_k A[i][k] B[j][k] (n x n, FP64, shared memory, ld ldx), 4 x 4 per thread with
+// rows i = ti + g a, columns j = tj + g b (g = ceil(n / 4)).  Returns max |C - I| over the
+// block when `dev_only` (C not written), else writes C.
+__device__ __forceinline__ double tri_gemm_nt(const double* __restrict__ Am, const double* __restrict__ Bm, int n,
+                                              int ldx, double* __restrict__ C, int ldc, bool dev_only,
+                                              double* __restrict__ red) {
+  const int g = (n + 3) >> 2;
+  const int tid = threadIdx.x;
+  double dev = 0.0;
+  for (int t = tid; t < g * g; t += blockDim.x) {
+    const int ti = t / g, tj = t - ti * g;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    int ia[4], jb[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      ia[a] = min(ti + g * a, n - 1);
+      jb[a] = min(tj + g * a, n - 1);
+    }
+    for (int k = 0; k < n; ++k) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) { av[a] = Am[ia[a] * ldx + k]; bv[a] = Bm[jb[a] * ldx + k]; }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int i = ti + g * a;
+      if (i >= n) continue;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int j = tj + g * b;
+        if (j >= n) continue;
+        if (dev_only) {
+          const double x = acc[a][b] - (i == j ? 1.0 : 0.0);
+          dev = (x == x) ? fmax(dev, fabs(x)) : INFINITY;
+        } else {
+          C[i * ldc + j] = acc[a][b];
+        }
+      }
+    }
+  }
+  if (dev_only) return block_max(dev, red);
+  return 0.0;
+}
+
+// Full solve.  On entry A (= sm + P.oA, ld P.lda) holds the symmetric matrix.  On success
+// (return 1): lam[i] (sm + P.olam, unordered) and eigenvector rows V = sm + P.oA (ld P.lda).
+// Returns 0 when the orthogonality check fails (the caller falls back to Jacobi).
+__device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
+  const int n = P.n, lda = P.lda, tid = threadIdx.x, nt = blockDim.x;
+  double* A = sm + P.oA;
+  double* X = sm + P.oX;
+  double* d = sm + P.od;
+  double* e = sm + P.oe;
+  double* Dr = sm + P.oD;
+  double* Lr = sm + P.oL;
+  double* sig = sm + P.osig;
+  double* lam = sm + P.olam;
+  double* red = sm + P.ored;
+  int* bstart = reinterpret_cast<int*>(sm + P.oint);
+  int* bend = bstart + n;
+  int* crow = bend + n;                        // coarse row of the block starting here (-1: none)
+  int* cpos = crow + n;                        // position in a relative cluster (0: first / none)
+  int* status = cpos + n;                      // [0] ok, [1] max cluster position, [2] coarse rows
+  int* blo = status + 4;                       // block start of coarse row b
+  int* ccnt = blo + kTriCoarseBlocks;          // coarse counts [kTriCoarseBlocks][kTriCoarse]
+  constexpr double eps = 2.220446049250313e-16;
+  // scale to max |a_ij| ~ 1 by a power of two (exact)
+  double amax = 0.0;
+  for (int idx = tid; idx < n * n; idx += nt) {
+    const int i = idx / n, j = idx - i * n;
+    amax = fmax(amax, fabs(A[i * lda + j]));
+  }
+  amax = block_max(amax, red);
+  if (!(amax > 0.0) || !isfinite(amax)) {
+    if (!isfinite(amax)) return 0;
+    for (int i = tid; i < n; i += nt) lam[i] = 0.0;
+    for (int idx = tid; idx < n * n; idx += nt) {
+      const int i = idx / n, j = idx - i * n;
+      A[i * lda + j] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    return 1;
+  }
+  int ex;
+  frexp(amax, &ex);
+  const double scale = ldexp(1.0, -ex), unscale = ldexp(1.0, ex);
+  for (int idx = tid; idx < n * n; idx += nt) {
+    const int i = idx / n, j = idx - i * n;
+    A[i * lda + j] *= scale;
+  }
+  __syncthreads();
+  if (tid == 0) g_tri_clk[0] = clock64();
+  tri_reduce(P, sm);
+  if (tid == 0) g_tri_clk[1] = clock64();
+  // ||T|| and the split
+  double tn = 0.0;
+  for (int i = tid; i < n; i += nt) tn = fmax(tn, fmax(fabs(d[i]), i + 1 < n ? fabs(e[i]) : 0.0));
+  tn = block_max(tn, red);
+  if (tid == 0) {
+    int s0 = 0;
+    status[0] = 1;
+    status[2] = 0;
+    for (int i = 0; i < n; ++i) {
+      bool cut = (i == n - 1);
+      if (!cut) {
+        const double ei = fabs(e[i]);
+        cut = ei <= eps * sqrt(fabs(d[i])) * sqrt(fabs(d[i + 1])) || ei <= 2.0 * eps * tn;
+        if (cut) e[i] = 0.0;
+      }
+      if (cut) {
+        for (int k = s0; k <= i; ++k) { bstart[k] = s0; bend[k] = i + 1; }
+        crow[s0] = -1;
+        if (i + 1 - s0 >= kTriCoarseMin && status[2] < kTriCoarseBlocks) {
+          crow[s0] = status[2];
+          blo[status[2]++] = s0;
+        }
+        s0 = i + 1;
+      }
+    }
+  }
+  __syncthreads();
+  const double pivmin = 1e-290;
+  // root representation per block, L D L^T = T_b - sigma I positive definite
+  double* DL = sm + P.oDL;
+  double* DL2 = sm + P.oDL2;
+  double* gub = sm + P.ogu;
+  if (tid < n && bstart[tid] == tid) {
+    const int lo = tid, hi = bend[tid];
+    double sigma = 0.0;
+    bool ok = false;
+    for (int attempt = 0; attempt < 64 && !ok; ++attempt) {
+      ok = true;
+      double di = d[lo] - sigma;
+      for (int i = lo; i < hi - 1; ++i) {
+        if (!(di > 0.0)) { ok = false; break; }
+        Dr[i] = di;
+        const double li = fdiv(e[i], di);
+        Lr[i] = li;
+        DL[i] = e[i];                            // D_i L_i = e_i
+        DL2[i] = e[i] * li;
+        di = (d[i + 1] - sigma) - DL2[i];
+      }
+      if (ok && !(di > 0.0)) ok = false;
+      if (ok) Dr[hi - 1] = di;
+      else sigma = (sigma == 0.0) ? -4.0 * (hi - lo) * eps * tn : 2.0 * sigma;
+    }
+    if (!ok) status[0] = 0;
+    // Gershgorin upper bound of the representation (= of T_b - sigma)
+    double gu = 0.0;
+    for (int i = lo; i < hi; ++i) {
+      double rad = 0.0;
+      if (i > lo) rad += fabs(e[i - 1]);
+      if (i < hi - 1) rad += fabs(e[i]);
+      gu = fmax(gu, (d[i] - sigma) + rad);
+    }
+    gu *= 1.0 + 4.0 * (hi - lo) * eps;
+    for (int i = lo; i < hi; ++i) { sig[i] = sigma; gub[i] = gu; }
+  }
+  __syncthreads();
+  if (status[0] == 0) return 0;
+  // coarse pass: negcounts of each big block at gu 8^-k, k = 0..kTriCoarse-1 (a thread each)
+  {
+    const int b = tid / kTriCoarse, k = tid - b * kTriCoarse;
+    if (b < status[2]) {
+      const int lo = blo[b], hi = bend[lo];
+      ccnt[b * kTriCoarse + k] = (k == 0) ? (hi - lo) : tri_negcount(Dr, DL2, lo, hi, ldexp(gub[lo], -3 * k), pivmin);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) g_tri_clk[5] = clock64();
+  // eight threads per eigenvalue: eigenvalue jj (ascending) of the block containing index j.
+  // 9-section (8 negcounts per round, geometric spacing while the bracket spans > 2^9) until
+  // isolated and 1e-6 wide, then safeguarded RQI by the group's first thread (one Rayleigh
+  // correction from there is accurate to ~eps, the second twisted solve gives the vector).
+  {
+    const int j = tid >> 3, g8 = tid & 7;
+    const unsigned gmask = 0xffu << (tid & 24);
+    double a = 0.0, b = 0.0;
+    int na = 0, nbc = 0;
+    if (j < n) {
+      const int lo = bstart[j], hi = bend[j], nb = hi - lo, jj = j - lo;
+      double* x = X + j * lda;
+      for (int c = g8; c < n; c += 8) x[c] = 0.0;
+      __syncwarp(gmask);
+      if (nb == 1) {
+        if (g8 == 0) x[lo] = 1.0;
+      } else {
+        const double gu = gub[lo];
+        a = gu * 1e-300;
+        b = gu;
+        nbc = nb;
+        if (crow[lo] >= 0) {   // tightest coarse bracket of eigenvalue jj
+          const int* cc = ccnt + crow[lo] * kTriCoarse;
+          for (int k = 1; k < kTriCoarse; ++k) {
+            const int c = cc[k];
+            const double xk = ldexp(gu, -3 * k);
+            if (c <= jj) { a = xk; na = c; break; }
+            b = xk; nbc = c;
+          }
+        }
+        for (int it = 0; it < 64; ++it) {
+          const bool iso = (na == jj) && (nbc == jj + 1);
+          if (iso && (b - a) <= 1e-6 * a) break;
+          double xg;
+          const int ea = ilogb(a), eb = ilogb(b);
+          if (eb - ea >= 9) xg = ldexp(a, ((g8 + 1) * (eb - ea)) / 9);
+          else xg = fma((double)(g8 + 1) * (1.0 / 9.0), b - a, a);
+          if (!(xg > a && xg < b)) xg = 0.5 * (a + b);
+          const int cg = tri_negcount(Dr, DL2, lo, hi, xg, pivmin);
+          const unsigned bits = (__ballot_sync(gmask, cg <= jj) >> (tid & 24)) & 0xffu;
+          const int f = __ffs(~bits & 0x1ffu) - 1;   // first point with count > jj (8: none)
+          const int base = tid & 24;
+          const double xa = __shfl_sync(gmask, xg, base + max(f - 1, 0));
+          const int ca = __shfl_sync(gmask, cg, base + max(f - 1, 0));
+          const double xb = __shfl_sync(gmask, xg, base + min(f, 7));
+          const int cb = __shfl_sync(gmask, cg, base + min(f, 7));
+          if (f > 0) { a = xa; na = ca; }
+          if (f < 8) { b = xb; nbc = cb; }
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) g_tri_clk[6] = clock64();
+    if (j < n) {
+      const int lo = bstart[j], hi = bend[j], nb = hi - lo, jj = j - lo;
+      double* x = X + j * lda;
+      double lj = 0.0;
+      if (nb == 1) {
+        lj = Dr[lo];
+      } else {
+        if (g8 == 0) {
+          double lc = -1.0, lam_v = 0.0, gm = 0.0, nz = 1.0;
+          bool have_vec = false, conv = false;
+          double* ss = A + j * lda;
+          int it_used = 0, ntw = 0;
+          for (int it = 0; it < 400 && !conv; ++it) {
+            ++it_used;
+            const bool iso = (na == jj) && (nbc == jj + 1);
+            const bool rqi = iso && (b - a) <= 0.5 * a;
+            ntw += rqi;
+            double l;
+            if (rqi && lc > a && lc < b) l = lc;
+            else if (b > 4.0 * a) l = sqrt(a) * sqrt(b);
+            else l = 0.5 * (a + b);
+            int neg;
+            if (rqi) {
+              neg = tri_twisted(Dr, Lr, DL, DL2, lo, hi, l, pivmin, x, ss, &gm, &nz);
+              have_vec = true;
+              lam_v = l;
+            } else {
+              neg = tri_negcount(Dr, DL2, lo, hi, l, pivmin);
+            }
+            if (neg <= jj) { a = l; na = neg; } else { b = l; nbc = neg; }
+            if (rqi) {
+              const double dl = fdiv(gm, nz);
+              lc = l + dl;
+              if (fabs(dl) <= 4.0 * eps * l || (b - a) <= 4.0 * eps * a) conv = true;
+            } else if (iso && (b - a) <= 4.0 * eps * a) {
+              conv = true;
+            }
+          }
+          atomicMax(&g_tri_maxit, 1000 * it_used + ntw);
+          if (!have_vec || !conv) {
+            lam_v = have_vec ? lam_v : 0.5 * (a + b);
+            tri_twisted(Dr, Lr, DL, DL2, lo, hi, lam_v, pivmin, x, ss, &gm, &nz);
+            if (!conv) atomicAnd(status, 0);
+          }
+          lj = lam_v;
+          const double inv = rsqrt(nz);
+          for (int c = lo; c < hi; ++c) x[c] *= inv;
+        }
+      }
+      if (g8 == 0) {
+        lam[j] = (lj + sig[lo]) * unscale;
+        sm[P.omu + j] = lj;
+      }
+    }
+  }
+  __syncthreads();
+  // relative clusters (relgap < kTriClusterTol within a block): the twisted vectors of the
+  // members after the first are not reliable (error ~ n eps / relgap); redo them by inverse
+  // iteration from a fixed pseudo-random start, orthogonalised against the earlier members
+  // (dstein-style, one cluster position per round)
+  {
+    const double* mu = sm + P.omu;
+    if (tid == 0) {
+      int mx = 0;
+      for (int j = 0; j < n; ++j) {
+        int pos = 0;
+        if (j > bstart[j] && fabs(mu[j] - mu[j - 1]) <= kTriClusterTol * fabs(mu[j - 1])) pos = cpos[j - 1] + 1;
+        cpos[j] = pos;
+        mx = max(mx, pos);
+      }
+      status[1] = mx;
+    }
+    __syncthreads();
+    const int mx = status[1];
+    for (int pos = 1; pos <= mx; ++pos) {
+      if (tid < n && cpos[tid] == pos) {
+        const int j = tid, lo = bstart[j], hi = bend[j];
+        double* y = X + j * lda;
+        double* lp = A + j * lda;             // L+ of the stationary factorisation
+        const double l = mu[j];
+        uint32_t hsh = 0x9e3779b9u * (uint32_t)(j + 1);
+        for (int i = lo; i < hi; ++i) {
+          hsh ^= hsh << 13; hsh ^= hsh >> 17; hsh ^= hsh << 5;
+          y[i] = (double)(hsh & 0xffffu) * (1.0 / 65536.0) - 0.5;
+        }
+        for (int it = 0; it < 2; ++it) {
+          // (L D L^T - l I) y <- y via L+ D+ L+^T: the stationary factorisation and the
+          // forward substitution + diagonal scaling in one top-down walk, then backward
+          double sst = -l, yp = 0.0;
+          for (int i = lo; i < hi; ++i) {
+            double dp = Dr[i] + sst;
+            if (fabs(dp) < pivmin) dp = -pivmin;
+            const double yi = (i > lo) ? fma(-lp[i - 1], yp, y[i]) : y[i];
+            yp = yi;
+            y[i] = fdiv(yi, dp);
+            if (i < hi - 1) {
+              const double q = fdiv(DL[i], dp);
+              lp[i] = q;
+              sst = fma(q * Lr[i], sst, -l);
+            }
+          }
+          double ymax = fabs(y[hi - 1]);
+          for (int i = hi - 2; i >= lo; --i) { y[i] = fma(-lp[i], y[i + 1], y[i]); ymax = fmax(ymax, fabs(y[i])); }
+          const double isc = (ymax > 0.0 && isfinite(ymax)) ? 1.0 / ymax : 1.0;
+          for (int i = lo; i < hi; ++i) y[i] *= isc;
+          for (int rep = 0; rep < 2; ++rep)
+            for (int q = j - pos; q < j; ++q) {
+              const double* xq = X + q * lda;
+              double dt = 0.0;
+              for (int i = lo; i < hi; ++i) dt = fma(xq[i], y[i], dt);
+              for (int i = lo; i < hi; ++i) y[i] = fma(-dt, xq[i], y[i]);
+            }
+          double nr = 0.0;
+          for (int i = lo; i < hi; ++i) nr = fma(y[i], y[i], nr);
+          const double inr = nr > 0.0 ? 1.0 / sqrt(nr) : 0.0;
+          for (int i = lo; i < hi; ++i) y[i] *= inr;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) g_tri_clk[2] = clock64();
+  if (status[0] == 0) return 0;
+  // safety net: orthogonality of the eigenvectors of T
+  const double dev = tri_gemm_nt(X, X, n, lda, nullptr, 0, true, red);
+  if (tid == 0) g_tri_clk[3] = clock64();
+  if (!(dev <= kTriOrthTol)) return 0;
+  // V = X Q^T (rows = eigenvectors of Z), into the A region
+  tri_gemm_nt(X, sm + P.oQ, n, lda, A, lda, false, red);
+  __syncthreads();
+  if (tid == 0) g_tri_clk[4] = clock64();
+  return 1;
+}
+
+}  // namespace ng

@@ -21,6 +21,7 @@
 
 #include "eig_jacobi.cuh"
 #include "eig_dc.cuh"
+#include "eig_tri.cuh"
 #include "gemm_simt.cuh"
 #include "gemm_tc.cuh"
 #include "ngsgd_impl.cuh"
@@ -245,7 +246,11 @@ __global__ void copy_gated_kernel(int R, int D, float* __restrict__ dst, const f
 //                    1..nv keep column slices of the eigenvectors and apply each round's
 //                    rotations as they arrive (DSMEM ring, eig_jacobi.cuh); the shared-
 //                    memory traffic of the eigenvector update leaves the Z CTA (R <= 80)
-enum RefreshMode : int { REFRESH_INPLACE = 0, REFRESH_PP = 1, REFRESH_CLUSTER = 2, REFRESH_DC = 3 };
+//   REFRESH_DC       one CTA, Householder + divide and conquer (eig_dc.cuh)
+//   REFRESH_TRI      one CTA, Householder + relatively robust representation + twisted
+//                    factorisation eigenvectors (eig_tri.cuh), falling back to the in-place
+//                    Jacobi when its orthogonality check fails (default, 2 <= R <= 80)
+enum RefreshMode : int { REFRESH_INPLACE = 0, REFRESH_PP = 1, REFRESH_CLUSTER = 2, REFRESH_DC = 3, REFRESH_TRI = 4 };
 constexpr int kPPRing = 16;
 
 // Shared-memory plan (offsets in doubles from the 16-byte aligned dynamic base).
@@ -285,6 +290,13 @@ __host__ __device__ inline RefreshSmem refresh_plan(int R, int mode) {
     p.o_v0 = o + dp.oV; p.o_v1 = p.o_v0;     // eigenvector rows come out here (ld R)
     p.o_cs = o;
     o += (dp.total + 15) / 8;
+  } else if (mode == REFRESH_TRI) {   // eig_tri's plan; Z_t in its A region (ld R + 1)
+    const TriPlan tp = tri_plan(R);
+    p.o_ring = o;
+    p.o_z0 = o + tp.oA; p.o_z1 = p.o_z0;
+    p.o_v0 = o + tp.oX; p.o_v1 = p.o_v0;   // Jacobi fallback: eigenvector rows (ld LDV)
+    p.o_cs = o + tp.oQ;                    // Jacobi fallback: (c, s) scratch
+    o += ((tp.total + 15) / 16) * 2;
   } else if (mode == REFRESH_INPLACE) {
     p.o_z0 = o; o += ((size_t)R * p.LD + 1) & ~(size_t)1;
     p.o_z1 = p.o_z0;
@@ -435,7 +447,31 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   int sweeps;
   const double* V = nullptr;   // eigenvector rows (index / slot order), row stride ldv
   int ldv = 0, nlam;
-  if (MODE == REFRESH_DC) {
+  if (MODE == REFRESH_TRI) {
+    const TriPlan tp = tri_plan(R);
+    double* tb = sm + P.o_ring;
+    if (eig_tri(tp, tb)) {
+      for (int i = tid; i < R; i += nt) lam[i] = tb[tp.olam + i];
+      sweeps = 0;
+      V = tb + tp.oA;
+      ldv = tp.lda;
+    } else {
+      // fallback: Z_t again (the solve overwrote it), in-place cyclic Jacobi
+      __syncthreads();
+      for (int idx = tid; idx < R * R; idx += nt) {
+        const int i = idx / R, j = idx % R;
+        Z[i * P.LD + j] = zval(i, j);
+      }
+      __syncthreads();
+      JacobiSmem<double> scr{sm + P.o_cs, sm + P.o_cs + P.mp, nrot, offmax};
+      sweeps = jacobi_eig_smem<double>(Z, P.LD, sm + P.o_v0, P.LDV, R, scr, 20, 1e-15 * zmax, 1e-7, dbg_mask);
+      if (sweeps == 0) sweeps = 1;   // flags[4] > 0 marks the fallback
+      for (int i = tid; i < R; i += nt) lam[i] = Z[i * P.LD + i];
+      V = sm + P.o_v0;
+      ldv = P.LDV;
+    }
+    nlam = R;
+  } else if (MODE == REFRESH_DC) {
     // Householder + divide and conquer (eig_dc.cuh); the eigenvector rows overwrite Z
     eig_dc(sm + P.o_ring, dc_plan(R), Z, P.LD, lam, sm + P.o_v0, R);
     sweeps = 0;
@@ -768,6 +804,8 @@ static ng_status set_kernel_attrs() {
                                    (int)refresh_plan(kJacobiPPMax, REFRESH_CLUSTER).total_bytes));
   NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<REFRESH_DC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)refresh_plan(kDCMax, REFRESH_DC).total_bytes));
+  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<REFRESH_TRI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)refresh_plan(kTriMax, REFRESH_TRI).total_bytes));
   NG_CUDA_TRY(cudaFuncSetAttribute(reorth_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)reorth_smem_bytes(kMaxRank)));
   NG_CUDA_TRY(cudaFuncSetAttribute(reorth_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -962,13 +1000,13 @@ static ng_status launch_refresh_chain(ngsgd_ctx* h, int n, double eta, const dou
     // FP32 solve leaves R_{t+1} non-orthonormal beyond 1e-3 and B.3.1 repairs would fire on
     // most updates (measured on the config-3 network).
     static const int dbg = getenv("NG_PROFILE_JACOBI_MASK") ? atoi(getenv("NG_PROFILE_JACOBI_MASK")) : 0;
-    // Solver choice: the cluster split for R >= 48 (where the eigenvector update dominates
-    // the shared-memory traffic), the one-CTA permuted solver below, the in-place solver
-    // beyond kJacobiPPMax.  NG_TUNE_EIG_MODE = 0/1/2 forces one (comparisons only).
+    // Solver choice: Householder + RRR/twisted eigenvectors (eig_tri.cuh, Jacobi fallback
+    // inside) for 2 <= R <= kTriMax, the in-place Jacobi beyond.  NG_TUNE_EIG_MODE = 0..4
+    // forces one (comparisons only): 1/2 the permuted one-CTA / cluster Jacobi, 3 D&C.
     static const int force = tune_int("NG_TUNE_EIG_MODE", -1);
-    int mode = R > kJacobiPPMax || R < 2 ? REFRESH_INPLACE : (R >= 48 ? REFRESH_CLUSTER : REFRESH_PP);
+    int mode = (R >= 2 && R <= kTriMax) ? REFRESH_TRI : REFRESH_INPLACE;
     if (force >= 0 && (force == REFRESH_INPLACE || R <= kJacobiPPMax) && (force != REFRESH_CLUSTER || R >= 8) &&
-        (force != REFRESH_DC || (R >= 2 && R <= kDCMax)))
+        (force != REFRESH_DC || (R >= 2 && R <= kDCMax)) && (force != REFRESH_TRI || (R >= 2 && R <= kTriMax)))
       mode = force;
     const RefreshSmem plan = refresh_plan(R, mode);
     if (mode == REFRESH_CLUSTER) {
@@ -988,6 +1026,9 @@ static ng_status launch_refresh_chain(ngsgd_ctx* h, int n, double eta, const dou
       NG_CUDA_TRY(cudaLaunchKernelEx(&lc, refresh_kernel<REFRESH_CLUSTER>, R, D, n, eta, a_, e_,
                                      (const float*)h->KL, h->dstate, trx, h->Amat, h->svec,
                                      h->flags, dbg));
+    } else if (mode == REFRESH_TRI) {
+      refresh_kernel<REFRESH_TRI><<<1, 1024, plan.total_bytes, ss>>>(R, D, n, eta, a_, e_, h->KL, h->dstate,
+                                                                     trx, h->Amat, h->svec, h->flags, dbg);
     } else if (mode == REFRESH_DC) {
       refresh_kernel<REFRESH_DC><<<1, 1024, plan.total_bytes, ss>>>(R, D, n, eta, a_, e_, h->KL, h->dstate,
                                                                     trx, h->Amat, h->svec, h->flags, dbg);
@@ -1718,6 +1759,36 @@ ng_status ng_debug_eig_dc(const double* z, int32_t n, double* lam, double* vt, v
   NG_CUDA_TRY(cudaFuncSetAttribute(debug_eig_dc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   debug_eig_dc_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(z, n, lam, vt);
   return check_launch("debug_eig_dc_kernel");
+}
+
+__global__ void __launch_bounds__(1024) debug_eig_tri_kernel(const double* Z, int n, double* lam, double* vt, int* ok) {
+  extern __shared__ __align__(16) unsigned char ng_smem[];
+  double* sm = reinterpret_cast<double*>(ng_smem);
+  const TriPlan tp = tri_plan(n);
+  const long long t0 = clock64();
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) sm[tp.oA + (idx / n) * tp.lda + idx % n] = Z[idx];
+  __syncthreads();
+  const int r = eig_tri(tp, sm);
+  const long long t1 = clock64();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) lam[i] = sm[tp.olam + i];
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) vt[idx] = sm[tp.oA + (idx / n) * tp.lda + idx % n];
+  if (threadIdx.x == 0) {
+    ok[0] = r;
+    ok[1] = (int)min(t1 - t0, (long long)INT32_MAX);
+    for (int k = 0; k < 4; ++k) ok[2 + k] = r || k < 2 ? (int)(g_tri_clk[k + 1] - g_tri_clk[k]) : 0;
+    ok[5] = g_tri_maxit; g_tri_maxit = 0;
+    ok[6] = (int)(g_tri_clk[6] - g_tri_clk[5]);   // multisection
+    ok[7] = (int)(g_tri_clk[2] - g_tri_clk[6]);   // RQI + vectors + clusters
+  }
+}
+
+ng_status ng_debug_eig_tri(const double* z, int32_t n, double* lam, double* vt, int32_t* ok, void* stream) {
+  NG_REQUIRE(z && lam && vt && ok, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(n >= 1 && n <= kTriMax, NG_ESHAPE, "n must be in [1, 80]");
+  const size_t smem = tri_plan(n).total + 16;
+  NG_CUDA_TRY(cudaFuncSetAttribute(debug_eig_tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  debug_eig_tri_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(z, n, lam, vt, ok);
+  return check_launch("debug_eig_tri_kernel");
 }
 
 }  // extern "C"

@@ -1,14 +1,14 @@
 """NumPy prototype of the refresh eigensolver candidate: Householder tridiagonalisation +
 divide-and-conquer (Cuppen tearing, LAPACK-style deflation, secular equation solved for the
 offset from the nearer pole, Gu-Eisenstat eigenvectors).  Used to validate the numerics on
-the oracle's own Z_t matrices before the CUDA port (tools/jacobi_sweep_sim.py captures them).
+the oracle's own Z_t matrices before the CUDA port (tests/tools/jacobi_sweep_sim.py captures them).
 
     python tools/dc_proto.py
 """
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 
 EPS = np.finfo(np.float64).eps

@@ -10,7 +10,7 @@ G = U diag(sqrt(max(c, floor))) U^T.
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 
 from oracle import nnet as onn
