@@ -289,6 +289,14 @@ ng_status ng_debug_eig_dc(const double* z, int32_t n, double* lam, double* vt, v
  * (tridiagonalisation, eigenvalues + vectors of T, orthogonality check, V = X Q^T); ok: int[8].  n in [1, 80]; asynchronous on `stream`. */
 ng_status ng_debug_eig_tri(const double* z, int32_t n, double* lam, double* vt, int32_t* ok, void* stream);
 
+/* Diagnostics of the refresh's Jacobi fallback (eig_tri failed its checks): z_host double[80*80]
+ * gets the last such Z_t (row major, n x n with n = info_host[0]); info_host int[5] = {n, number
+ * of fallbacks so far, reason of the last one: 1 no positive definite root representation,
+ * 2 an eigenvalue did not converge, 3 orthogonality check; the largest relative-cluster
+ * position and 1000 x RQI-loop iterations + twisted solves of any eigenvalue since the last
+ * call (both reset)}.  Synchronises the device. */
+ng_status ng_debug_tri_fail(double* z_host, int32_t* info_host);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,13 +33,16 @@ namespace ng {
 
 constexpr int kTriMax = 80;
 constexpr int kTriChunks = 5;   // column chunks of the Householder pass
-constexpr double kTriOrthTol = 1e-8;
+constexpr double kTriOrthTol = 1e-6;   // ~ the Jacobi solver's 1e-7 rotation threshold; W is FP32
 constexpr int kTriCoarse = 64;        // coarse negcount points per block (ratio 8 apart)
 constexpr int kTriCoarseBlocks = 16;  // blocks of >= kTriCoarseMin indices that get them
 constexpr int kTriCoarseMin = 8;
-constexpr double kTriClusterTol = 1e-5;   // relative gap below which twisted vectors are redone
+constexpr double kTriClusterTol = 1e-7;   // relative gap below which twisted vectors are redone
+                                          // (above it their error n eps / relgap < 2e-7)
 __device__ long long g_tri_clk[8];
-__device__ int g_tri_maxit;   // thread 0's phase stamps of the last solve (ng_debug_eig_tri)
+__device__ int g_tri_maxit;
+__device__ double g_tri_fail_z[kTriMax * kTriMax];   // last Z_t whose solve fell back (ng_debug_tri_fail)
+__device__ int g_tri_fail_n, g_tri_fail_count, g_tri_fail_why, g_tri_maxpos;   // thread 0's phase stamps of the last solve (ng_debug_eig_tri)
 
 // Shared-memory plan (offsets in doubles from a 16-byte aligned base), n <= kTriMax.
 struct TriPlan {
@@ -523,7 +526,7 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
       if (ok) Dr[hi - 1] = di;
       else sigma = (sigma == 0.0) ? -4.0 * (hi - lo) * eps * tn : 2.0 * sigma;
     }
-    if (!ok) status[0] = 0;
+    if (!ok) { status[0] = 0; g_tri_fail_why = 1; }
     // Gershgorin upper bound of the representation (= of T_b - sigma)
     double gu = 0.0;
     for (int i = lo; i < hi; ++i) {
@@ -642,7 +645,7 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
           if (!have_vec || !conv) {
             lam_v = have_vec ? lam_v : 0.5 * (a + b);
             tri_twisted(Dr, Lr, DL, DL2, lo, hi, lam_v, pivmin, x, ss, &gm, &nz);
-            if (!conv) atomicAnd(status, 0);
+            if (!conv) { atomicAnd(status, 0); g_tri_fail_why = 2; }
           }
           lj = lam_v;
           const double inv = rsqrt(nz);
@@ -657,9 +660,10 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
   }
   __syncthreads();
   // relative clusters (relgap < kTriClusterTol within a block): the twisted vectors of the
-  // members after the first are not reliable (error ~ n eps / relgap); redo them by inverse
-  // iteration from a fixed pseudo-random start, orthogonalised against the earlier members
-  // (dstein-style, one cluster position per round)
+  // members are not reliable (error ~ n eps / relgap).  Every member redoes its vector by two
+  // steps of inverse iteration from its own pseudo-random start (in parallel), then each
+  // cluster is orthonormalised by modified Gram-Schmidt run twice, one member per step
+  // (every later member projects out the current one; one barrier per step).
   {
     const double* mu = sm + P.omu;
     if (tid == 0) {
@@ -670,12 +674,16 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
         cpos[j] = pos;
         mx = max(mx, pos);
       }
+      // a cluster's first member (pos 0 followed by pos 1) is redone too: mark it -1
+      for (int j = 0; j + 1 < n; ++j)
+        if (cpos[j] == 0 && cpos[j + 1] == 1) cpos[j] = -1;
       status[1] = mx;
+      atomicMax(&g_tri_maxpos, mx);
     }
     __syncthreads();
     const int mx = status[1];
-    for (int pos = 1; pos <= mx; ++pos) {
-      if (tid < n && cpos[tid] == pos) {
+    if (mx > 0) {
+      if (tid < n && cpos[tid] != 0) {
         const int j = tid, lo = bstart[j], hi = bend[j];
         double* y = X + j * lda;
         double* lp = A + j * lda;             // L+ of the stationary factorisation
@@ -705,20 +713,39 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
           for (int i = hi - 2; i >= lo; --i) { y[i] = fma(-lp[i], y[i + 1], y[i]); ymax = fmax(ymax, fabs(y[i])); }
           const double isc = (ymax > 0.0 && isfinite(ymax)) ? 1.0 / ymax : 1.0;
           for (int i = lo; i < hi; ++i) y[i] *= isc;
-          for (int rep = 0; rep < 2; ++rep)
-            for (int q = j - pos; q < j; ++q) {
-              const double* xq = X + q * lda;
+        }
+      }
+      __syncthreads();
+      // MGS twice over cluster positions: at step p the member at position p-1 of every
+      // cluster is final (normalised); the members after it project it out
+      for (int rep = 0; rep < 2; ++rep) {
+        for (int p = 0; p <= mx; ++p) {
+          if (tid < n && cpos[tid] != 0) {
+            const int j = tid, lo = bstart[j], hi = bend[j];
+            const int pj = cpos[j] < 0 ? 0 : cpos[j];
+            double* y = X + j * lda;
+            if (pj == p) {
+              double nr = 0.0;
+              for (int i = lo; i < hi; ++i) nr = fma(y[i], y[i], nr);
+              const double inr = nr > 0.0 ? rsqrt(nr) : 0.0;
+              for (int i = lo; i < hi; ++i) y[i] *= inr;
+            }
+          }
+          __syncthreads();
+          if (tid < n && cpos[tid] != 0) {
+            const int j = tid, lo = bstart[j], hi = bend[j];
+            const int pj = cpos[j] < 0 ? 0 : cpos[j];
+            if (pj > p) {
+              const double* xq = X + (j - (pj - p)) * lda;   // the member at position p
+              double* y = X + j * lda;
               double dt = 0.0;
               for (int i = lo; i < hi; ++i) dt = fma(xq[i], y[i], dt);
               for (int i = lo; i < hi; ++i) y[i] = fma(-dt, xq[i], y[i]);
             }
-          double nr = 0.0;
-          for (int i = lo; i < hi; ++i) nr = fma(y[i], y[i], nr);
-          const double inr = nr > 0.0 ? 1.0 / sqrt(nr) : 0.0;
-          for (int i = lo; i < hi; ++i) y[i] *= inr;
+          }
+          __syncthreads();
         }
       }
-      __syncthreads();
     }
   }
   if (tid == 0) g_tri_clk[2] = clock64();
@@ -726,7 +753,7 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
   // safety net: orthogonality of the eigenvectors of T
   const double dev = tri_gemm_nt(X, X, n, lda, nullptr, 0, true, red);
   if (tid == 0) g_tri_clk[3] = clock64();
-  if (!(dev <= kTriOrthTol)) return 0;
+  if (!(dev <= kTriOrthTol)) { if (tid == 0) g_tri_fail_why = 3; return 0; }
   // V = X Q^T (rows = eigenvectors of Z), into the A region
   tri_gemm_nt(X, sm + P.oQ, n, lda, A, lda, false, red);
   __syncthreads();

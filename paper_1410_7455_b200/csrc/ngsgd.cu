@@ -461,7 +461,9 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
       for (int idx = tid; idx < R * R; idx += nt) {
         const int i = idx / R, j = idx % R;
         Z[i * P.LD + j] = zval(i, j);
+        g_tri_fail_z[idx] = Z[i * P.LD + j];
       }
+      if (tid == 0) { g_tri_fail_n = R; atomicAdd(&g_tri_fail_count, 1); }
       __syncthreads();
       JacobiSmem<double> scr{sm + P.o_cs, sm + P.o_cs + P.mp, nrot, offmax};
       sweeps = jacobi_eig_smem<double>(Z, P.LD, sm + P.o_v0, P.LDV, R, scr, 20, 1e-15 * zmax, 1e-7, dbg_mask);
@@ -1780,6 +1782,23 @@ __global__ void __launch_bounds__(1024) debug_eig_tri_kernel(const double* Z, in
     ok[6] = (int)(g_tri_clk[6] - g_tri_clk[5]);   // multisection
     ok[7] = (int)(g_tri_clk[2] - g_tri_clk[6]);   // RQI + vectors + clusters
   }
+}
+
+ng_status ng_debug_tri_fail(double* z_host, int32_t* info_host) {
+  NG_REQUIRE(z_host && info_host, NG_EINVAL, "NULL argument");
+  NG_CUDA_TRY(cudaDeviceSynchronize());
+  int v[5];
+  NG_CUDA_TRY(cudaMemcpyFromSymbol(&v[3], g_tri_maxpos, sizeof(int)));
+  NG_CUDA_TRY(cudaMemcpyFromSymbol(&v[4], g_tri_maxit, sizeof(int)));
+  const int zero = 0;
+  NG_CUDA_TRY(cudaMemcpyToSymbol(g_tri_maxpos, &zero, sizeof(int)));
+  NG_CUDA_TRY(cudaMemcpyToSymbol(g_tri_maxit, &zero, sizeof(int)));
+  NG_CUDA_TRY(cudaMemcpyFromSymbol(&v[0], g_tri_fail_n, sizeof(int)));
+  NG_CUDA_TRY(cudaMemcpyFromSymbol(&v[1], g_tri_fail_count, sizeof(int)));
+  NG_CUDA_TRY(cudaMemcpyFromSymbol(&v[2], g_tri_fail_why, sizeof(int)));
+  NG_CUDA_TRY(cudaMemcpyFromSymbol(z_host, g_tri_fail_z, sizeof(double) * kTriMax * kTriMax));
+  for (int i = 0; i < 5; ++i) info_host[i] = v[i];
+  return NG_OK;
 }
 
 ng_status ng_debug_eig_tri(const double* z, int32_t n, double* lam, double* vt, int32_t* ok, void* stream) {
