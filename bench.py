@@ -31,6 +31,10 @@ import sys
 import threading
 import time
 
+# one hardware work queue per NG refresh stream (paper_1410_7455_b200/__init__.py); set
+# before torch creates the CUDA context
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 

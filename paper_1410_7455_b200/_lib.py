@@ -90,6 +90,7 @@ SIGNATURES = {
     "ng_debug_eig_dc": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     "ng_debug_eig_tri": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ng_debug_tri_fail": (c_int32, [c_void_p, c_void_p]),
+    "ng_debug_refresh_times": (c_int32, [c_void_p, c_void_p]),
 }
 
 

@@ -360,6 +360,9 @@ __device__ void refresh_vrank(const RefreshSmem& P, uint32_t rank, double* sm, f
   cl_sync();   // (2) rank 0's shared memory is no longer read
 }
 
+__device__ unsigned long long g_ref_t[256][3];   // refresh timing (ng_debug_refresh_times): R, start, end ns
+__device__ unsigned int g_ref_n;
+
 template <int MODE>
 __global__ void __launch_bounds__(1024)
 refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
@@ -368,6 +371,8 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
                float* __restrict__ svec, int* __restrict__ flags, int dbg_mask) {
   extern __shared__ __align__(16) unsigned char ng_smem[];
   double* sm = reinterpret_cast<double*>(ng_smem);
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   const RefreshSmem P = refresh_plan(R, MODE);
   PPCluster cl{};
   if constexpr (MODE == REFRESH_CLUSTER) {
@@ -573,6 +578,14 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
     if (!isfinite(rho_new) || !isfinite(sdn)) atomicOr(reinterpret_cast<unsigned*>(flags + 3), kErrNonFinite);
   }
   if (MODE == REFRESH_CLUSTER) cl_sync();   // (2) the V ranks are done with this CTA's shared memory
+  if (tid == 0) {
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    const unsigned slot = atomicAdd(&g_ref_n, 1u) & 255u;
+    g_ref_t[slot][0] = (unsigned long long)R | ((unsigned long long)D << 16);
+    g_ref_t[slot][1] = t_start;
+    g_ref_t[slot][2] = t_end;
+  }
 }
 
 // B.3.1 (reading R5): O = E^{-1/2} (W W^T) E^{-1/2} for the NEW state; if
@@ -1782,6 +1795,16 @@ __global__ void __launch_bounds__(1024) debug_eig_tri_kernel(const double* Z, in
     ok[6] = (int)(g_tri_clk[6] - g_tri_clk[5]);   // multisection
     ok[7] = (int)(g_tri_clk[2] - g_tri_clk[6]);   // RQI + vectors + clusters
   }
+}
+
+ng_status ng_debug_refresh_times(uint64_t* out, int32_t* count) {
+  NG_REQUIRE(out && count, NG_EINVAL, "NULL argument");
+  NG_CUDA_TRY(cudaDeviceSynchronize());
+  unsigned int n = 0;
+  NG_CUDA_TRY(cudaMemcpyFromSymbol(&n, g_ref_n, sizeof(n)));
+  NG_CUDA_TRY(cudaMemcpyFromSymbol(out, g_ref_t, sizeof(unsigned long long) * 256 * 3));
+  *count = (int32_t)n;
+  return NG_OK;
 }
 
 ng_status ng_debug_tri_fail(double* z_host, int32_t* info_host) {
