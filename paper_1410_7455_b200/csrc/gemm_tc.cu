@@ -155,6 +155,8 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
+  pdl_trigger();
+  pdl_wait();   // operands and the RMW tile may come from the previous kernel on the stream
 
   // Read-modify-write epilogues: the old C tile does not depend on the MMA, so every
   // thread loads its row of it now (registers) and the HBM latency overlaps the mainloop.
@@ -440,7 +442,8 @@ ng_status launch(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, 
   // co-resident CTAs per SM.
   const int ns = std::max(1, std::min(ring_stages(BN), kbps));
   dim3 grid(ceil_div(N, BN), ceil_div(M, kBM), splits);
-  tc_gemm_tf32_kernel<BN, AK, BKM, EPI><<<grid, 128, ring_smem(BN, ns), st>>>(ta, tb, M, N, K, kbps, epi, ns);
+  NG_CUDA_TRY(launch_pdl(tc_gemm_tf32_kernel<BN, AK, BKM, EPI>, grid, dim3(128), ring_smem(BN, ns), st, ta, tb, M, N,
+                         K, kbps, epi, ns));
   return check_launch("tc_gemm_tf32_kernel");
 }
 
@@ -517,7 +520,8 @@ ng_status launch_grouped(cudaStream_t st, const TcGroup& grp, int tiles) {
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_smem(BN, ring_stages(BN))));
     attr = true;
   }
-  tc_gemm_tf32_grouped_kernel<BN, AK, BKM, EPI><<<tiles, 128, ring_smem(BN, grp.nstages), st>>>(grp);
+  NG_CUDA_TRY(launch_pdl(tc_gemm_tf32_grouped_kernel<BN, AK, BKM, EPI>, dim3(tiles), dim3(128),
+                         ring_smem(BN, grp.nstages), st, grp));
   return check_launch("tc_gemm_tf32_grouped_kernel");
 }
 

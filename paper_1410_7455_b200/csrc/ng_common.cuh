@@ -7,6 +7,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <cstring>
 #include <string>
 
 #include "../../include/ngsgd.h"
@@ -74,6 +75,36 @@ inline ng_status check_launch(const char* what) {
 inline int tune_int(const char* name, int def) {
   const char* e = getenv(name);
   return e ? atoi(e) : def;
+}
+
+// Programmatic dependent launch (PDL) on the main stream's kernel chain: a kernel launched
+// with launch_pdl may be scheduled while its predecessor is still running; it runs its
+// prologue (barrier init, TMEM alloc, tensor-map prefetch), then pdl_wait() blocks until the
+// predecessor grid has completed and its writes are visible.  Every kernel launched with
+// launch_pdl calls pdl_wait() before touching global memory the stream produced; kernels
+// call pdl_trigger() early so their successor's prologue overlaps their own work.
+// NG_TUNE_PDL=0 turns the attribute off (A/B measurements).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+inline bool pdl_enabled() {
+  static const int v = tune_int("NG_TUNE_PDL", 1);
+  return v != 0;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }

@@ -1236,6 +1236,8 @@ struct SegReduce {            // out[i*ldo + j] = sum_z src[z*zstride + i*lds + 
 };
 
 __global__ void __launch_bounds__(256) seg_reduce_kernel(const __grid_constant__ SegReduce sr) {
+  pdl_trigger();
+  pdl_wait();   // launched with launch_pdl
   int g = 0;
   while (g + 1 < sr.count && (int)blockIdx.x >= sr.block_begin[g + 1]) ++g;
   const int64_t total = (int64_t)sr.rows[g] * sr.cols[g];
@@ -1306,6 +1308,8 @@ struct FinalizeGroup {
 
 // One CTA per state: identical arithmetic to finalize_kernel.
 __global__ void __launch_bounds__(512) finalize_group_kernel(const __grid_constant__ FinalizeGroup fg) {
+  pdl_trigger();
+  pdl_wait();   // launched with launch_pdl
   const int g = blockIdx.x;
   __shared__ double sc[32];
   const int n = fg.n[g], tiles = fg.tiles[g];
@@ -1338,7 +1342,7 @@ static ng_status launch_seg_reduce(cudaStream_t st, SegReduce& sr) {
     blocks += std::max(1, std::min(64, ceil_div((int64_t)sr.rows[g] * sr.cols[g], 256)));
   }
   sr.block_begin[sr.count] = blocks;
-  seg_reduce_kernel<<<blocks, 256, 0, st>>>(sr);
+  NG_CUDA_TRY(launch_pdl(seg_reduce_kernel, dim3(blocks), dim3(256), 0, st, sr));
   return check_launch("seg_reduce_kernel");
 }
 
@@ -1607,7 +1611,7 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
     }
     ProfScope ps(NG_PROF_NG_APPLY, st, flops, bytes);
     NG_TRY(tc_gemm_tf32_grouped(st, d.data(), G, true, false, TC_EPI_NGAPPLY, apply_bn()));
-    finalize_group_kernel<<<G, 512, 0, st>>>(fg);
+    NG_CUDA_TRY(launch_pdl(finalize_group_kernel, dim3(G), dim3(512), 0, st, fg));
     NG_TRY(check_launch("finalize_group_kernel"));
   }
   // ---- phase D: refresh chains on the side streams; bookkeeping

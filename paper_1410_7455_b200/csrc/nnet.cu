@@ -89,6 +89,8 @@ __global__ void init_weights_kernel(float* W, int rows, int cols, int ld, uint64
 // Y_1 = [frames, 1], zero padding columns.
 __global__ void input_kernel(int n, int din, const float* __restrict__ f, int64_t ldf, float* __restrict__ Y,
                              int ldy, int* eflags) {
+  pdl_trigger();
+  pdl_wait();   // launched with launch_pdl: inputs come from the previous kernel
   const int64_t total = (int64_t)n * ldy;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(i / ldy), c = (int)(i % ldy);
@@ -137,6 +139,8 @@ pnorm_kernel(int n, int dout, int ldz, int G, const float* __restrict__ Z, float
 __global__ void __launch_bounds__(256)
 softmax_kernel(int n, int C, int ld, const float* __restrict__ Z, const int32_t* __restrict__ labels,
                float* __restrict__ X, double* __restrict__ objrows, int* eflags) {
+  pdl_trigger();
+  pdl_wait();   // launched with launch_pdl: inputs come from the previous kernel
   extern __shared__ __align__(16) unsigned char nn_smem[];
   __shared__ float sc[32];
   float* zs = reinterpret_cast<float*>(nn_smem);
@@ -172,6 +176,8 @@ softmax_kernel(int n, int C, int ld, const float* __restrict__ Z, const int32_t*
 }
 
 __global__ void objsum_kernel(int n, const double* __restrict__ rows, double* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();   // launched with launch_pdl: inputs come from the previous kernel
   __shared__ double sc[32];
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += rows[i];
@@ -202,6 +208,8 @@ struct EpiPnormBack {
 __global__ void __launch_bounds__(256)
 pnorm_back_kernel(const float* __restrict__ part, int splits, int n, int din, const float* __restrict__ Zp,
                   const float* __restrict__ Yl, float* __restrict__ Xp, int ldx, int ldy, int G) {
+  pdl_trigger();
+  pdl_wait();   // launched with launch_pdl: inputs come from the previous kernel
   extern __shared__ __align__(16) unsigned char nn_smem[];
   float* ga = reinterpret_cast<float*>(nn_smem);
   const int r = blockIdx.x;
@@ -244,6 +252,8 @@ __global__ void rowsq_kernel(int n, int D, const float* __restrict__ X, int64_t 
 __global__ void __launch_bounds__(256)
 maxchange_kernel(int n, int maxmb, float lr, float mc, const float* __restrict__ gam, const float* __restrict__ pbuf,
                  float* __restrict__ scale, float* __restrict__ stats) {
+  pdl_trigger();
+  pdl_wait();   // launched with launch_pdl: inputs come from the previous kernel
   __shared__ double sc[32];
   const int l = blockIdx.x;
   const float gy = gam[2 * l], gx = gam[2 * l + 1];
@@ -445,8 +455,8 @@ ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const
   const bool tc = h->cfg.precision == NG_TF32;
   {
     const int64_t tot = (int64_t)n * h->ldp[0];
-    input_kernel<<<std::min(4096, ceil_div(tot, 256)), 256, 0, st>>>(n, h->cfg.input_dim, frames, ld, h->Y[0],
-                                                                      h->ldp[0], h->eflags);
+    NG_CUDA_TRY(launch_pdl(input_kernel, dim3(std::min(4096, ceil_div(tot, 256))), dim3(256), 0, st, n,
+                           h->cfg.input_dim, frames, ld, h->Y[0], h->ldp[0], h->eflags));
     NG_TRY(check_launch("input_kernel"));
   }
   // forward
@@ -477,8 +487,8 @@ ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const
       NG_TRY(check_launch("pnorm_kernel"));
     }
   }
-  softmax_kernel<<<n, 256, sizeof(float) * h->rows[L - 1], st>>>(n, h->rows[L - 1], h->ldr[L - 1], h->Z[L - 1], labels, h->X[L - 1], h->objrows,
-                                    h->eflags);
+  NG_CUDA_TRY(launch_pdl(softmax_kernel, dim3(n), dim3(256), sizeof(float) * h->rows[L - 1], st, n, h->rows[L - 1],
+                         h->ldr[L - 1], (const float*)h->Z[L - 1], labels, h->X[L - 1], h->objrows, h->eflags));
   NG_TRY(check_launch("softmax_kernel"));
   // backward with the pre-update weights (reading R21)
   for (int l = L - 1; l >= 1; --l) {
@@ -497,8 +507,9 @@ ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const
                           &sp));
       const int64_t tot = (int64_t)n * din;
       (void)tot;
-      pnorm_back_kernel<<<n, 256, sizeof(float) * din, st>>>(h->gpart, sp, n, din, h->Z[l - 1], h->Y[l],
-                                                                            h->X[l - 1], h->ldr[l - 1], h->ldp[l], G);
+      NG_CUDA_TRY(launch_pdl(pnorm_back_kernel, dim3(n), dim3(256), sizeof(float) * din, st, (const float*)h->gpart, sp,
+                             n, din, (const float*)h->Z[l - 1], (const float*)h->Y[l], h->X[l - 1], h->ldr[l - 1],
+                             h->ldp[l], G));
       NG_TRY(check_launch("pnorm_back_kernel"));
     } else {
       NG_TRY((gemm_simt<float, true, false>(st, n, h->cols[l] - 1, h->rows[l], h->X[l], h->ldr[l], W, h->ldp[l],
@@ -508,7 +519,7 @@ ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const
   h->n_last = n;
   h->have_fb = true;
   if (objective_out) {
-    objsum_kernel<<<1, 512, 0, st>>>(n, h->objrows, h->obj);
+    NG_CUDA_TRY(launch_pdl(objsum_kernel, dim3(1), dim3(512), 0, st, n, (const double*)h->objrows, h->obj));
     NG_TRY(check_launch("objsum_kernel"));
     NG_CUDA_TRY(cudaMemcpyAsync(objective_out, h->obj, sizeof(double), cudaMemcpyDeviceToHost, st));
     NG_CUDA_TRY(cudaStreamSynchronize(st));
@@ -545,7 +556,8 @@ ng_status nnet_update(nnet_t h, float lr, float max_change_per_sample, nnet_upda
       NG_TRY(check_launch("rowsq_kernel"));
     }
   }
-  maxchange_kernel<<<L, 256, 0, st>>>(n, N, lr, max_change_per_sample, h->gam, h->pbuf, h->scale, h->stats);
+  NG_CUDA_TRY(launch_pdl(maxchange_kernel, dim3(L), dim3(256), 0, st, n, N, lr, max_change_per_sample,
+                         (const float*)h->gam, (const float*)h->pbuf, h->scale, h->stats));
   NG_TRY(check_launch("maxchange_kernel"));
   const bool tc = h->cfg.precision == NG_TF32;
   static const int upd_grouped = tune_int("NG_TUNE_UPD_GROUPED", 1);
