@@ -189,7 +189,7 @@ def run_reference(args, rank: int, world: int):
     val, dt = oracle_steps(args.steps, args.warmup, n)
     thr, api_ = blas_threads()
     sample = (f"each step = one float64 oracle train step (forward, backward, online NG-SGD on 10 factors, "
-              f"update) of config 3 on a {n}-frame minibatch (paper CPU minibatch, P:1438-1443); "
+              f"update) of {WORKLOAD.split(":")[0]} on a {n}-frame minibatch (paper CPU minibatch, P:1438-1443); "
               f"steady-state NG states injected")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
@@ -433,7 +433,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         val, dt = oracle_steps(args.cpu_steps, 1, n)
         thr, api_ = blas_threads()
         cpu = {"value": val, "unit": "frames/s", "cores": thr, "kind": "oracle",
-               "sample": f"{args.cpu_steps} float64 oracle steps of config 3 on {n}-frame minibatches "
+               "sample": f"{args.cpu_steps} float64 oracle steps of {WORKLOAD.split(":")[0]} on {n}-frame minibatches "
                          f"(steady-state NG states injected), {dt:.1f} s", "blas": api_, "host_cores": cpu_cores()}
 
     if dist:
@@ -468,8 +468,17 @@ def main():
     ap.add_argument("--no-precond-bench", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=100)
     ap.add_argument("--update-period", type=int, default=4, help="NG J (P:1295-1297); experiments only")
+    ap.add_argument("--workload", choices=["config3", "config5"], default="config3",
+                    help="config3 (default, the metric's workload) or BASELINE.json configs[4] (wide DNN)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.workload == "config5":
+        global WORKLOAD
+        CFG3.update(num_hidden=6, hidden_dim=5000, num_classes=8000)
+        WORKLOAD = ("config5: wide p-norm DNN 360 -> 6x[5000 -> p-norm 500] -> 8000 softmax, N=512, "
+                    "online NG-SGD R_in=20/R_out=80 on all 14 Fisher factors, max-change 0.075")
+        if args.cpu_steps == 100:
+            args.cpu_steps = 30
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -201,7 +201,7 @@ def inject_states(net, states, seed):
             net.ngsgd(l, side).set_state(s.rho, s.d, s.W.astype(np.float32), s.t)
 
 
-@pytest.mark.parametrize("shape", ["tiny", "config3"])
+@pytest.mark.parametrize("shape", ["tiny", "config3", "config5"])
 def test_tf32_tensor_core_step(api, shape):
     """NG_TF32: the DNN GEMMs on tcgen05 (TF32 inputs, FP32 accumulate).  Bar (north
     star, reduced-precision tensor-core inputs): the preconditioned update
@@ -211,8 +211,11 @@ def test_tf32_tensor_core_step(api, shape):
     if shape == "tiny":
         cfg = onn.NnetConfig(input_dim=40, num_hidden=2, hidden_dim=200, pnorm_group=10, num_classes=16)
         N, rin, rout = 128, 4, 8
-    else:
+    elif shape == "config3":
         cfg = onn.NnetConfig(input_dim=360, num_hidden=4, hidden_dim=3000, pnorm_group=10, num_classes=5000)
+        N, rin, rout = 512, 20, 80
+    else:   # BASELINE.json configs[4]: 6 p-norm hidden layers 5000 -> 500, 8000-state softmax (14 NG states)
+        cfg = onn.NnetConfig(input_dim=360, num_hidden=6, hidden_dim=5000, pnorm_group=10, num_classes=8000)
         N, rin, rout = 512, 20, 80
     net, params, states = make_pair(api, cfg, True, 91, rin, rout, N, random_softmax=True, precision="tf32")
     inject_states(net, states, 3)
