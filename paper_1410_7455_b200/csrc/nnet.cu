@@ -214,12 +214,34 @@ pnorm_back_kernel(const float* __restrict__ part, int splits, int n, int din, co
   float* ga = reinterpret_cast<float*>(nn_smem);
   const int r = blockIdx.x;
   const int64_t total = (int64_t)n * din;
-  for (int j = threadIdx.x; j < din; j += blockDim.x) {
-    const int64_t i = (int64_t)r * din + j;
-    float g = 0.f;
-    for (int z = 0; z < splits; ++z) g += part[(int64_t)z * total + i];
-    const float a = Yl[(int64_t)r * ldy + j];
-    ga[j] = a > 0.f ? g / a : 0.f;
+  if ((din & 3) == 0 && (total & 3) == 0 && splits <= 8) {
+    // 16-byte loads of the split-K partials, all splits issued before the fixed-order sum
+    const int d4 = din >> 2;
+    for (int j4 = threadIdx.x; j4 < d4; j4 += blockDim.x) {
+      const int64_t i4 = ((int64_t)r * din >> 2) + j4;
+      float4 pv[8];
+#pragma unroll
+      for (int z = 0; z < 8; ++z)
+        if (z < splits) pv[z] = __ldg(reinterpret_cast<const float4*>(part + (int64_t)z * total) + i4);
+      float4 g = pv[0];
+#pragma unroll
+      for (int z = 1; z < 8; ++z)
+        if (z < splits) { g.x += pv[z].x; g.y += pv[z].y; g.z += pv[z].z; g.w += pv[z].w; }
+      const float* ar = Yl + (int64_t)r * ldy + 4 * j4;
+      const float a0 = ar[0], a1 = ar[1], a2 = ar[2], a3 = ar[3];
+      ga[4 * j4 + 0] = a0 > 0.f ? g.x / a0 : 0.f;
+      ga[4 * j4 + 1] = a1 > 0.f ? g.y / a1 : 0.f;
+      ga[4 * j4 + 2] = a2 > 0.f ? g.z / a2 : 0.f;
+      ga[4 * j4 + 3] = a3 > 0.f ? g.w / a3 : 0.f;
+    }
+  } else {
+    for (int j = threadIdx.x; j < din; j += blockDim.x) {
+      const int64_t i = (int64_t)r * din + j;
+      float g = 0.f;
+      for (int z = 0; z < splits; ++z) g += part[(int64_t)z * total + i];
+      const float a = Yl[(int64_t)r * ldy + j];
+      ga[j] = a > 0.f ? g / a : 0.f;
+    }
   }
   __syncthreads();
   const int dout = din * G;
