@@ -523,7 +523,7 @@ ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const
       TcEpilogue e;
       e.kind = TC_EPI_PARTIAL; e.C = h->gpart; e.ldc = din; e.zstride = (int64_t)n * din;
       int sp = 1;
-      static const int bn = tune_int("NG_TUNE_BWD_BN", 64);
+      static const int bn = tune_int("NG_TUNE_BWD_BN", 128);   // measured +2% over 64 (tools/tune_sweep3.sh)
       static const int splits = std::min(kBwdSplits, std::max(1, tune_int("NG_TUNE_BWD_SPLITS", kBwdSplits)));
       NG_TRY(tc_gemm_tf32(st, n, din, h->rows[l], h->X[l], h->ldr[l], true, W, h->ldp[l], false, e, bn, splits,
                           &sp));
@@ -598,7 +598,7 @@ ng_status nnet_update(nnet_t h, float lr, float max_change_per_sample, nnet_upda
       q.epi.kind = TC_EPI_AXPY; q.epi.C = h->arena + h->off[l]; q.epi.ldc = h->ldp[l]; q.epi.scale = h->scale + l;
       q.splits_used = nullptr;
     }
-    static const int bn = tune_int("NG_TUNE_UPD_BN", 64);
+    static const int bn = tune_int("NG_TUNE_UPD_BN", 128);   // with BWD_BN 128: +3.7% (tools/tune_sweep3.sh)
     ProfScope ps(NG_PROF_UPD_GEMM, st, flops, bytes);
     NG_TRY(tc_gemm_tf32_grouped(st, d.data(), L, false, false, TC_EPI_AXPY, bn));
   } else
@@ -609,7 +609,7 @@ ng_status nnet_update(nnet_t h, float lr, float max_change_per_sample, nnet_upda
     if (tc) {
       TcEpilogue e;
       e.kind = TC_EPI_AXPY; e.C = W; e.ldc = h->ldp[l]; e.scale = h->scale + l;
-      static const int bn = tune_int("NG_TUNE_UPD_BN", 64);
+      static const int bn = tune_int("NG_TUNE_UPD_BN", 128);   // with BWD_BN 128: +3.7% (tools/tune_sweep3.sh)
       NG_TRY(tc_gemm_tf32(st, h->rows[l], h->cols[l], n, h->X[l], h->ldr[l], false, h->Y[l], h->ldp[l], false, e, bn,
                           1));
     } else {
