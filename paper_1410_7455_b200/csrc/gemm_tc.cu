@@ -238,40 +238,44 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
   tc_fence_after();
   __syncwarp();
   if constexpr (EPI == TC_EPI_PNORM) {
-    // Z row (80 columns = 8 groups of 10) and the group 2-norms
-    static_assert(BN == 80, "p-norm epilogue: 80-column tiles");
-    float acc[80];
+    // Z row in 80-column halves (8 groups of 10 each) and the group 2-norms
+    static_assert(BN % 80 == 0, "p-norm epilogue: tiles of whole 80-column blocks");
+    float* yrow = epi.y + (int64_t)row * epi.ldy;
+#pragma unroll 1
+    for (int hh = 0; hh < BN / 80; ++hh) {
+      const int nh = n0 + hh * 80;
+      float acc[80];
 #pragma unroll
-    for (int c = 0; c < 5; ++c) {
-      uint32_t v[16];
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * 16), v);
+      for (int c = 0; c < 5; ++c) {
+        uint32_t v[16];
+        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(hh * 80 + c * 16), v);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) acc[c * 16 + j] = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
-    }
-    if (row < M) {
-      const bool full = n0 + 80 <= N && ((reinterpret_cast<uintptr_t>(crow + n0) & 15) == 0);
-      if (full) {
-#pragma unroll
-        for (int j = 0; j < 80; j += 4)
-          *reinterpret_cast<float4*>(crow + n0 + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 80; ++j)
-          if (n0 + j < N) crow[n0 + j] = acc[j];
+        for (int j = 0; j < 16; ++j) acc[c * 16 + j] = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
       }
-      float* yrow = epi.y + (int64_t)row * epi.ldy;
-      const int g0 = n0 / 10;
+      if (row < M && nh < N) {
+        const bool full = nh + 80 <= N && ((reinterpret_cast<uintptr_t>(crow + nh) & 15) == 0);
+        if (full) {
 #pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        float sq = 0.f;
+          for (int j = 0; j < 80; j += 4)
+            *reinterpret_cast<float4*>(crow + nh + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        } else {
 #pragma unroll
-        for (int q = 0; q < 10; ++q) sq = fmaf(acc[g * 10 + q], acc[g * 10 + q], sq);
-        if (n0 + g * 10 + 10 <= N) yrow[g0 + g] = sqrtf(sq);
-      }
-      if (n0 + 80 >= N) {   // last column tile: bias input and the zero padding
-        const int dp = N / 10;
-        yrow[dp] = 1.f;
-        for (int c = dp + 1; c < epi.ldy; ++c) yrow[c] = 0.f;
+          for (int j = 0; j < 80; ++j)
+            if (nh + j < N) crow[nh + j] = acc[j];
+        }
+        const int g0 = nh / 10;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          float sq = 0.f;
+#pragma unroll
+          for (int q = 0; q < 10; ++q) sq = fmaf(acc[g * 10 + q], acc[g * 10 + q], sq);
+          if (nh + g * 10 + 10 <= N) yrow[g0 + g] = sqrtf(sq);
+        }
+        if (nh + 80 >= N) {   // last column block: bias input and the zero padding
+          const int dp = N / 10;
+          yrow[dp] = 1.f;
+          for (int c = dp + 1; c < epi.ldy; ++c) yrow[c] = 0.f;
+        }
       }
     }
   } else {
@@ -502,13 +506,16 @@ ng_status tc_gemm_tf32_pnorm(cudaStream_t st, int M, int N, int K, const float* 
   const int kb = ceil_div(K, kBK);
   CUtensorMap ta, tb;
   NG_TRY(make_tmap(&ta, A, K, M, lda, kBM, false));
-  NG_TRY(make_tmap(&tb, B, K, N, ldb, 80, false));
+  // 80 or 160 columns (8 or 16 whole groups) per tile (NG_TUNE_FWD_PNORM_BN)
+  static const int bn = tune_int("NG_TUNE_FWD_PNORM_BN", 80) == 160 ? 160 : 80;
+  NG_TRY(make_tmap(&tb, B, K, N, ldb, bn, false));
   TcEpilogue e;
   e.kind = TC_EPI_PNORM;
   e.C = Z;
   e.ldc = ldz;
   e.y = Ynext;
   e.ldy = ldy;
+  if (bn == 160) return launch<160, true, true, TC_EPI_PNORM>(st, ta, tb, M, N, K, kb, 1, e);
   return launch<80, true, true, TC_EPI_PNORM>(st, ta, tb, M, N, K, kb, 1, e);
 }
 
