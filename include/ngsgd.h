@@ -166,6 +166,14 @@ ng_status nnet_destroy(nnet_t h);
 ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld,
                                 const int32_t* labels, int32_t n, double* objective_out);
 
+/* The objective of the last nnet_forward_backward, without synchronising: enqueues the
+ * fixed-order sum over the minibatch's rows (same value as objective_out above) and an
+ * asynchronous device-to-host copy into `host_out` (host double*, should be pinned) on the
+ * handle's stream.  The value is valid once the stream reaches this point (e.g. after a
+ * cudaEventSynchronize on an event recorded after the call); lets a caller overlap the next
+ * step's input copy and launches with the readback of this step's result. */
+ng_status nnet_objective_async(nnet_t h, double* host_out);
+
 typedef struct {
   float alpha_t[16];      /* max-change scale per weight matrix (C.3)        */
   float gamma_in[16];     /* gamma of the input side (eqn:gammat)                        */

@@ -71,6 +71,7 @@ SIGNATURES = {
     "nnet_create": (c_int32, [ctypes.POINTER(NnetConfig), c_void_p, ctypes.POINTER(c_void_p)]),
     "nnet_destroy": (c_int32, [c_void_p]),
     "nnet_forward_backward": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_int32, ctypes.POINTER(c_double)]),
+    "nnet_objective_async": (c_int32, [c_void_p, c_void_p]),
     "nnet_update": (c_int32, [c_void_p, c_float, c_float, ctypes.POINTER(NnetUpdateStats)]),
     "nnet_num_layers": (c_int32, [c_void_p, ctypes.POINTER(c_int32)]),
     "nnet_layer_shape": (c_int32, [c_void_p, c_int32, ctypes.POINTER(c_int32), ctypes.POINTER(c_int32)]),

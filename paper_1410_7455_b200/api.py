@@ -170,6 +170,13 @@ class Nnet:
                                         ctypes.byref(out) if objective else None))
         return out.value if objective else None
 
+    def objective_async(self, host_out: torch.Tensor) -> None:
+        """Enqueue the readback of the last forward_backward's objective into a pinned CPU
+        float64 tensor (nnet_objective_async); valid once the net's stream gets there."""
+        if host_out.is_cuda or host_out.dtype != torch.float64 or host_out.numel() < 1:
+            raise ValueError("host_out must be a CPU float64 tensor (pinned)")
+        check(lib.nnet_objective_async(self._h, ctypes.c_void_p(host_out.data_ptr())))
+
     def update(self, lr: float, max_change_per_sample: float = 0.075, stats: bool = False):
         st = _lib.NnetUpdateStats() if stats else None
         check(lib.nnet_update(self._h, float(lr), float(max_change_per_sample), ctypes.byref(st) if stats else None))

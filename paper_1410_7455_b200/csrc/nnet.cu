@@ -446,6 +446,16 @@ ng_status nnet_destroy(nnet_t h) {
   return NG_OK;
 }
 
+ng_status nnet_objective_async(nnet_t h, double* host_out) {
+  NG_REQUIRE(h != nullptr && host_out != nullptr, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(h->have_fb, NG_ESTATE, "nnet_objective_async before nnet_forward_backward");
+  cudaStream_t st = h->st;
+  NG_CUDA_TRY(launch_pdl(objsum_kernel, dim3(1), dim3(512), 0, st, h->n_last, (const double*)h->objrows, h->obj));
+  NG_TRY(check_launch("objsum_kernel"));
+  NG_CUDA_TRY(cudaMemcpyAsync(host_out, h->obj, sizeof(double), cudaMemcpyDeviceToHost, st));
+  return NG_OK;
+}
+
 ng_status nnet_join(nnet_t h) {
   NG_REQUIRE(h != nullptr, NG_EINVAL, "NULL argument");
   for (auto* p : h->ng_in) NG_TRY(ngsgd_join_impl(p));
