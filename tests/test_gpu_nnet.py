@@ -234,3 +234,18 @@ def test_tf32_tensor_core_step(api, shape):
             d_gpu = net.get_params(l).astype(np.float64) - before[l]
             d_ref = ref[l] - before[l]
             assert normwise(d_gpu, d_ref) <= 2e-2, (k, l, normwise(d_gpu, d_ref))
+
+
+def test_objective_async_matches_sync(api):
+    """nnet_objective_async (used by bench.py's pipelined e2e loop) reads back exactly the
+    objective nnet_forward_backward(objective_out) returns, without a host sync."""
+    cfg = onn.NnetConfig(input_dim=40, num_hidden=1, hidden_dim=200, pnorm_group=10, num_classes=16)
+    net, params, _ = make_pair(api, cfg, False, 5, 4, 4, 128, random_softmax=True)
+    frames, labels = spliced_frames(9, 128, context=0, num_classes=16)
+    f, y = to_dev(frames, labels)
+    obj = net.forward_backward(f, y, objective=True)
+    out = torch.zeros(1, dtype=torch.float64).pin_memory()
+    net.forward_backward(f, y)
+    net.objective_async(out)
+    torch.cuda.synchronize()
+    assert float(out[0]) == obj
