@@ -402,7 +402,7 @@ __device__ void refresh_vrank(const RefreshSmem& P, uint32_t rank, double* sm, d
   cl_sync();   // (2) rank 0's shared memory is no longer read
 }
 
-__device__ unsigned long long g_ref_t[256][3];   // refresh timing (ng_debug_refresh_times): R, start, end ns
+__device__ unsigned long long g_ref_t[256][5];   // refresh timing (ng_debug_refresh_times): R, start, end ns
 __device__ unsigned int g_ref_n;
 
 template <int MODE>
@@ -494,6 +494,8 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   int sweeps;
   const double* V = nullptr;   // eigenvector rows (index / slot order), row stride ldv
   int ldv = 0, nlam;
+  unsigned long long t_eig0 = 0, t_eig1 = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_eig0));
   if (MODE == REFRESH_TRI) {
     const TriPlan tp = tri_plan(R);
     double* tb = sm + P.o_ring;
@@ -520,6 +522,7 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
       ldv = P.LDV;
     }
     nlam = R;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_eig1));
   } else if (MODE == REFRESH_DC) {
     // Householder + divide and conquer (eig_dc.cuh); the eigenvector rows overwrite Z
     eig_dc(sm + P.o_ring, dc_plan(R), Z, P.LD, lam, sm + P.o_v0, R);
@@ -627,6 +630,8 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
     g_ref_t[slot][0] = (unsigned long long)R | ((unsigned long long)D << 16);
     g_ref_t[slot][1] = t_start;
     g_ref_t[slot][2] = t_end;
+    g_ref_t[slot][3] = t_eig0;
+    g_ref_t[slot][4] = t_eig1;
   }
 }
 
@@ -1859,7 +1864,7 @@ ng_status ng_debug_refresh_times(uint64_t* out, int32_t* count) {
   NG_CUDA_TRY(cudaDeviceSynchronize());
   unsigned int n = 0;
   NG_CUDA_TRY(cudaMemcpyFromSymbol(&n, g_ref_n, sizeof(n)));
-  NG_CUDA_TRY(cudaMemcpyFromSymbol(out, g_ref_t, sizeof(unsigned long long) * 256 * 3));
+  NG_CUDA_TRY(cudaMemcpyFromSymbol(out, g_ref_t, sizeof(unsigned long long) * 256 * 5));
   *count = (int32_t)n;
   return NG_OK;
 }
