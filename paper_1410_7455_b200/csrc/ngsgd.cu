@@ -225,48 +225,6 @@ __global__ void bscale_kernel(int R, int D, float* __restrict__ J, const float* 
   }
 }
 
-// W_{t+1} = A_t B_t (eqn:wt1) with B_t = J_t + diag(s) W_t formed on
-// the fly, FP64 products and accumulation from the FP64 A_t of the refresh and the FP32 J, W:
-// the rows of A_t are scaled by C^{-1/2} (cond(C) up to 1e17 on config 3), and an FP32
-// product left R_{t+1} non-orthonormal beyond the B.3.1 threshold on many updates.  One CTA
-// per 32 columns: A_t and the CTA's 32 columns of B_t in shared memory, lane = column,
-// warp = rows r = warp, warp + 8, ...
-constexpr int kWnCols = 32, kWnRowsPerThread = 16;   // R <= 8 * 16 = 128
-__global__ void __launch_bounds__(256)
-wnext_kernel(int R, int D, const double* __restrict__ A, const float* __restrict__ J, const float* __restrict__ W,
-             int64_t ldw, const double* __restrict__ s, float* __restrict__ Wn) {
-  extern __shared__ __align__(16) unsigned char ng_smem[];
-  double* As = reinterpret_cast<double*>(ng_smem);   // R x R
-  double* Bs = As + R * R;                           // R x kWnCols
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int c0 = blockIdx.x * kWnCols;
-  for (int i = tid; i < R * R; i += blockDim.x) As[i] = A[i];
-  for (int i = tid; i < R * kWnCols; i += blockDim.x) {
-    const int k = i / kWnCols, c = c0 + i % kWnCols;
-    Bs[i] = (c < D) ? fma(s[k], (double)W[(int64_t)k * ldw + c], (double)J[(int64_t)k * ldw + c]) : 0.0;
-  }
-  __syncthreads();
-  double acc[kWnRowsPerThread];
-#pragma unroll
-  for (int q = 0; q < kWnRowsPerThread; ++q) acc[q] = 0.0;
-  for (int k = 0; k < R; ++k) {
-    const double b = Bs[k * kWnCols + lane];
-#pragma unroll
-    for (int q = 0; q < kWnRowsPerThread; ++q) {
-      const int r = warp + 8 * q;
-      if (r < R) acc[q] = fma(As[r * R + k], b, acc[q]);
-    }
-  }
-  const int c = c0 + lane;
-  if (c < D) {
-#pragma unroll
-    for (int q = 0; q < kWnRowsPerThread; ++q) {
-      const int r = warp + 8 * q;
-      if (r < R) Wn[(int64_t)r * ldw + c] = (float)acc[q];
-    }
-  }
-}
-
 __global__ void copy_gated_kernel(int R, int D, float* __restrict__ dst, const float* __restrict__ src,
                                   int64_t ld, const int* gate) {
   if (gate && *gate == 0) return;
@@ -368,7 +326,7 @@ __host__ __device__ inline RefreshSmem refresh_plan(int R, int mode) {
 
 // V ranks of the cluster refresh: rotate the eigenvector slice, then write their columns
 // of A_t from the row factors / permutation rank 0 publishes.
-__device__ void refresh_vrank(const RefreshSmem& P, uint32_t rank, double* sm, double* __restrict__ Amat) {
+__device__ void refresh_vrank(const RefreshSmem& P, uint32_t rank, double* sm, float* __restrict__ Amat) {
   const int R = P.R, tid = threadIdx.x, nt = blockDim.x;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + P.o_bar);
   uint32_t* cmd = reinterpret_cast<uint32_t*>(sm + P.o_cmd);
@@ -397,7 +355,7 @@ __device__ void refresh_vrank(const RefreshSmem& P, uint32_t rank, double* sm, d
   const int jn = min(R, j0 + P.w) - j0;
   for (int idx = tid; idx < R * (jn > 0 ? jn : 0); idx += nt) {
     const int r = idx / jn, jj = idx - r * jn, j = j0 + jj;
-    Amat[r * R + j] = fr[r] * Vf[perm[r] * P.w + jj] * emh[j];
+    Amat[r * R + j] = (float)(fr[r] * Vf[perm[r] * P.w + jj] * emh[j]);
   }
   cl_sync();   // (2) rank 0's shared memory is no longer read
 }
@@ -409,8 +367,8 @@ template <int MODE>
 __global__ void __launch_bounds__(1024)
 refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
                const float* __restrict__ KL, double* __restrict__ dstate,
-               const double* __restrict__ sums, double* __restrict__ Amat,
-               double* __restrict__ svec, int* __restrict__ flags, int dbg_mask) {
+               const double* __restrict__ sums, float* __restrict__ Amat,
+               float* __restrict__ svec, int* __restrict__ flags, int dbg_mask) {
   extern __shared__ __align__(16) unsigned char ng_smem[];
   double* sm = reinterpret_cast<double*>(ng_smem);
   unsigned long long t_start;
@@ -598,11 +556,11 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
     for (int idx = tid; idx < R * R; idx += nt) {
       const int r = idx / R, j = idx % R;
       const double en = 1.0 / (beta_new / dn[r] + 1.0);
-      Amat[idx] = (eta / N) * sqrt(en) / sqrt(c[r]) * V[perm[r] * ldv + j] * emh[j];
+      Amat[idx] = (float)((eta / N) * sqrt(en) / sqrt(c[r]) * V[perm[r] * ldv + j] * emh[j]);
     }
   }
   // row scale of B_t with the OLD d, rho
-  for (int k = tid; k < R; k += nt) svec[k] = (N * (1.0 - eta) / eta) * dr[k];
+  for (int k = tid; k < R; k += nt) svec[k] = (float)((N * (1.0 - eta) / eta) * dr[k]);
   double cmax = 0.0, cmin = 1e300;
   for (int r = tid; r < R; r += nt) { cmax = fmax(cmax, c[r]); cmin = fmin(cmin, c[r]); }
   cmax = block_max(cmax, red);
@@ -958,10 +916,8 @@ ng_status ngsgd_create_impl(int dim, int max_rows, const ngsgd_config* cfg, cuda
 void ngsgd_destroy_impl(ngsgd_ctx* h) {
   if (!h) return;
   float* fp[] = {h->W[0], h->W[1], h->Hpart, h->H, h->J, h->Kpart, h->Lpart, h->KL, h->WWpart, h->WW,
-                 h->Mmat, h->xxpart, h->ppart, h->p, h->gamma};
+                 h->Amat, h->Mmat, h->svec, h->xxpart, h->ppart, h->p, h->gamma};
   for (float* p : fp) if (p) cudaFree(p);
-  if (h->Amat) cudaFree(h->Amat);
-  if (h->svec) cudaFree(h->svec);
   if (h->dstate) cudaFree(h->dstate);
   if (h->Cfac) cudaFree(h->Cfac);
   if (h->trpart) cudaFree(h->trpart);
@@ -1106,21 +1062,12 @@ static ng_status launch_refresh_chain(ngsgd_ctx* h, int n, double eta, const dou
     NG_TRY(check_launch("refresh_kernel"));
   }
   ProfScope ps(NG_PROF_NG_REFRESH, ss, 2.0 * (double)R * R * D + 2.0 * R * D, 4.0 * (4.0 * R * D));
+  bscale_kernel<<<std::min(1024, ceil_div((int64_t)R * D, 256)), 256, 0, ss>>>(R, D, h->J, W, h->ldw, h->svec);
+  NG_TRY(check_launch("bscale_kernel"));
   const int nxt = 1 - h->cur;
   float* Wn = h->W[nxt];
-  // W_{t+1} = A_t (J + diag(s) W_t) (eqn:wt1), FP64 products in both modes
-  {
-    const size_t smem = sizeof(double) * ((size_t)R * R + (size_t)R * kWnCols);
-    static bool attr = false;
-    if (!attr) {
-      NG_CUDA_TRY(cudaFuncSetAttribute(wnext_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(sizeof(double) * ((size_t)kMaxRank * kMaxRank + (size_t)kMaxRank * kWnCols))));
-      attr = true;
-    }
-    NG_REQUIRE(R <= 8 * kWnRowsPerThread, NG_ESHAPE, "rank too large for wnext_kernel");
-    wnext_kernel<<<ceil_div(D, kWnCols), 256, smem, ss>>>(R, D, h->Amat, h->J, W, h->ldw, h->svec, Wn);
-    NG_TRY(check_launch("wnext_kernel"));
-  }
+  // W_{t+1} = A_t B_t (eqn:wt1), FP32 in both modes (orthonormality of R_{t+1})
+  NG_TRY((gemm_simt<float, true, false>(ss, R, D, R, h->Amat, R, h->J, h->ldw, EpiStore<float>{Wn, h->ldw, 1.f})));
   // B.3.1, gated on the device flag (no host synchronisation)
   const int ks = gemm_simt_splits(D, h->kl_splits);
   NG_TRY((gemm_simt<float, true, true>(ss, R, R, D, Wn, h->ldw, Wn, h->ldw,

@@ -27,11 +27,11 @@ struct ngsgd_ctx {
   float* KL = nullptr;      // 2 x R x R  (K_t then L_t)
   float* WWpart = nullptr;  // kl_splits x R x R (re-orthogonalisation, B.3.1)
   float* WW = nullptr;      // R x R
-  double* Amat = nullptr;      // R x R  A_t; also M of B.3.1
+  float* Amat = nullptr;    // R x R  A_t; also M of B.3.1
   float* Mmat = nullptr;    // R x R (unused by the repair since the triangular-solve form)
   double* Cfac = nullptr;   // R x R lower Cholesky factor of O (B.3.1 repair)
   double* trpart = nullptr; // max_rows row sums of ||x_i||^2 (early tr(X X^T))
-  double* svec = nullptr;      // R:  N(1-eta)/eta (d_i + rho)  (row scale of B_t)
+  float* svec = nullptr;    // R:  N(1-eta)/eta (d_i + rho)  (row scale of B_t)
   float* xxpart = nullptr;  // ctiles x max_rows: partial ||x_i||^2
   float* ppart = nullptr;   // ctiles x max_rows: partial ||x_hat_i||^2
   float* p = nullptr;       // max_rows
