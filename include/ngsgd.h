@@ -214,7 +214,10 @@ int32_t nnet_comm_id_bytes(void);
 /* Create an NCCL unique id into host buffer `id_out` (nnet_comm_id_bytes() bytes), to
  * be broadcast by the caller (e.g. torch.distributed) to all ranks. */
 ng_status nnet_comm_get_unique_id(void* id_out);
-/* Join the communicator of `nranks` jobs as `rank` (one process per GPU). */
+/* Join the communicator of `nranks` jobs as `rank` (one process per GPU), 1 <= nranks <= 64
+ * (any count, e.g. the paper's 6 jobs).  The arena is split into nranks shards of
+ * ceil(count / nranks) floats rounded up to 64; the last shard(s) are ragged.  Allocates two
+ * device staging buffers of nranks x shard floats. */
 ng_status nnet_comm_init(nnet_t h, const void* nccl_unique_id, int32_t rank, int32_t nranks);
 /* In-place average of all parameters over the ranks (3.1): W <- (sum_r W^r)/n
  * with the sum taken in a fixed pairwise-tree order over rank index (R18), so
@@ -224,6 +227,12 @@ ng_status nnet_comm_init(nnet_t h, const void* nccl_unique_id, int32_t rank, int
  * then scale (speed reference; order not fixed).  Synchronises the stream. */
 ng_status nnet_average(nnet_t h, int32_t mode);
 
+
+/* The fixed-order sum kernel of nnet_average on its own, for bit-exact tests on one GPU:
+ * out[i] = (sum over r of in[r * count + i]) * (1.0f / nr), summed in the pairwise tree order
+ * of DESIGN.md R18 (oracle/training.py tree_sum).  in: device float[nr * count]; out: device
+ * float[count]; 1 <= nr <= 64; asynchronous on `stream`. */
+ng_status ng_debug_tree_avg(int32_t nr, int64_t count, const float* in, float* out, void* cuda_stream);
 
 /* ------------------------------------------------ instrumentation (bench.py) ---- */
 

@@ -82,6 +82,7 @@ SIGNATURES = {
     "nnet_comm_get_unique_id": (c_int32, [c_void_p]),
     "nnet_comm_init": (c_int32, [c_void_p, c_void_p, c_int32, c_int32]),
     "nnet_average": (c_int32, [c_void_p, c_int32]),
+    "ng_debug_tree_avg": (c_int32, [c_int32, c_int64, c_void_p, c_void_p, c_void_p]),
     "ng_profile_enable": (c_int32, [ctypes.c_uint32]),
     "ng_profile_read": (c_int32, [ctypes.POINTER(ProfileStats)]),
     "ng_kernel_launches": (ctypes.c_int64, []),

@@ -25,7 +25,8 @@
 using namespace ng;
 
 constexpr int kMaxRowWidth = 50000;   // widest activation row staged in shared memory
-constexpr int kBwdSplits = 6;   // split-K of the TF32 backward-data GEMM (K = 3000..5000)
+constexpr int kBwdSplits = 6;
+constexpr int kMaxRanks = 64;      // nnet_average: jobs per communicator   // split-K of the TF32 backward-data GEMM (K = 3000..5000)
 
 struct nnet_ctx {
   nnet_config cfg{};
@@ -53,7 +54,8 @@ struct nnet_ctx {
   // NCCL
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
-  float* recvbuf = nullptr;
+  float* recvbuf = nullptr;     // nranks x shard: shard `rank` of every rank
+  float* gatherbuf = nullptr;   // nranks x shard: averaged shards (all-gather target)
   size_t shard = 0;
 };
 
@@ -296,15 +298,57 @@ maxchange_kernel(int n, int maxmb, float lr, float mc, const float* __restrict__
   }
 }
 
-// Deterministic average: out = tree_sum(recv[0..n-1]) * inv  (R18).
-__global__ void tree_avg_kernel(int nr, size_t shard, const float* __restrict__ recv, float* __restrict__ out, float inv) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < shard; i += (size_t)gridDim.x * blockDim.x) {
-    float v[64];
-    for (int r = 0; r < nr; ++r) v[r] = recv[(size_t)r * shard + i];
-    for (int w = 1; w < nr; w *= 2)
-      for (int k = 0; k + w < nr; k += 2 * w) v[k] = v[k] + v[k + w];
-    out[i] = v[0] * inv;
+// Deterministic average of one shard (R18): out[i] = tree_sum_r(recv[r*stride + i])
+// * inv over r = 0..nr-1 in the oracle's fixed pairwise order (level by level, an unpaired
+// last element carried up; oracle/training.py tree_sum).  That order equals complete
+// binary trees over the blocks given by the binary digits of nr (largest block first),
+// folded right to left: e.g. nr = 7 = 4+2+1 -> (((0+1)+(2+3)) + ((4+5) + 6)).  Each block
+// is a compile-time recursion, so every partial sum stays in registers (nr <= 127).
+template <int K>
+__device__ __forceinline__ float tree_block(const float* __restrict__ p, size_t stride) {
+  if constexpr (K == 0) {
+    return __ldg(p);
+  } else {
+    const float a = tree_block<K - 1>(p, stride);
+    const float b = tree_block<K - 1>(p + ((size_t)1 << (K - 1)) * stride, stride);
+    return a + b;
   }
+}
+
+__device__ __forceinline__ float tree_block_dyn(int k, const float* __restrict__ p, size_t stride) {
+  switch (k) {
+    case 0: return tree_block<0>(p, stride);
+    case 1: return tree_block<1>(p, stride);
+    case 2: return tree_block<2>(p, stride);
+    case 3: return tree_block<3>(p, stride);
+    case 4: return tree_block<4>(p, stride);
+    case 5: return tree_block<5>(p, stride);
+    default: return tree_block<6>(p, stride);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+tree_avg_kernel(int nr, size_t count, size_t stride, const float* __restrict__ recv, float* __restrict__ out,
+                float inv) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    bool have = false;
+    for (int k = 0; k < 7; ++k) {            // blocks from the right end (lowest binary digit)
+      if (!((nr >> k) & 1)) continue;
+      const size_t start = (size_t)(nr & ~((2 << k) - 1));
+      const float b = tree_block_dyn(k, recv + start * stride + i, stride);
+      acc = have ? b + acc : b;
+      have = true;
+    }
+    out[i] = acc * inv;
+  }
+}
+
+static ng_status launch_tree_avg(cudaStream_t st, int nr, size_t count, size_t stride, const float* recv, float* out) {
+  if (count == 0) return NG_OK;
+  const int blocks = (int)std::min<size_t>(4 * 148, (count + 255) / 256);
+  tree_avg_kernel<<<blocks, 256, 0, st>>>(nr, count, stride, recv, out, 1.0f / (float)nr);
+  return check_launch("tree_avg_kernel");
 }
 
 __global__ void scale_kernel(float* x, size_t n, float s) {
@@ -331,6 +375,7 @@ static void nnet_free(nnet_ctx* h) {
   if (h->obj) cudaFree(h->obj);
   if (h->eflags) cudaFree(h->eflags);
   if (h->recvbuf) cudaFree(h->recvbuf);
+  if (h->gatherbuf) cudaFree(h->gatherbuf);
   if (h->comm) ncclCommDestroy(h->comm);
   if (h->gpart) cudaFree(h->gpart);
   delete h;
@@ -687,7 +732,8 @@ ng_status nnet_comm_get_unique_id(void* id_out) {
 
 ng_status nnet_comm_init(nnet_t h, const void* nccl_unique_id, int32_t rank, int32_t nranks) {
   NG_REQUIRE(h && nccl_unique_id, NG_EINVAL, "NULL argument");
-  NG_REQUIRE(nranks >= 1 && nranks <= 64 && rank >= 0 && rank < nranks, NG_EINVAL, "bad rank/nranks");
+  NG_REQUIRE(nranks >= 1 && nranks <= kMaxRanks && rank >= 0 && rank < nranks, NG_EINVAL,
+             "bad rank/nranks (1 <= nranks <= 64)");
   NG_REQUIRE(h->comm == nullptr, NG_ESTATE, "communicator already initialised");
   ncclUniqueId id;
   std::memcpy(&id, nccl_unique_id, sizeof(id));
@@ -695,9 +741,12 @@ ng_status nnet_comm_init(nnet_t h, const void* nccl_unique_id, int32_t rank, int
   if (r != ncclSuccess) { set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r)); h->comm = nullptr; return NG_ENCCL; }
   h->rank = rank;
   h->nranks = nranks;
-  h->shard = h->arena_count / nranks;   // arena_count is a multiple of 512 >= 8 * 64
-  if (h->arena_count % nranks != 0) h->shard = (h->arena_count + nranks - 1) / nranks;
+  // any nranks: equal shards of ceil(count / n) rounded up to 64 floats; the last shard(s)
+  // are ragged (possibly empty) in the arena and padded in the gather buffer
+  h->shard = (size_t)round_up((int64_t)((h->arena_count + nranks - 1) / nranks), 64);
   NG_TRY(nalloc(&h->recvbuf, h->shard * nranks));
+  NG_TRY(nalloc(&h->gatherbuf, h->shard * nranks));
+  NG_CUDA_TRY(cudaMemsetAsync(h->gatherbuf, 0, sizeof(float) * h->shard * nranks, h->st));
   return NG_OK;
 }
 
@@ -706,23 +755,30 @@ ng_status nnet_average(nnet_t h, int32_t mode) {
   NG_REQUIRE(h->comm != nullptr, NG_ENCCL, "nnet_comm_init not called");
   cudaStream_t st = h->st;
   const int nr = h->nranks;
-  NG_REQUIRE(h->shard * nr == h->arena_count, NG_ESTATE, "arena not divisible by nranks");
   ncclResult_t r = ncclSuccess;
   ProfScope ps(NG_PROF_AVERAGE, st, 0.0, 4.0 * 2.0 * h->arena_count);
   if (mode == 0) {
+    // shard p of every rank goes to rank p (all-to-all), rank p sums it in the fixed tree
+    // order, then an in-place all-gather of the padded shards and one copy back
+    auto len = [&](int p) -> size_t {
+      const size_t lo = (size_t)p * h->shard;
+      return lo >= h->arena_count ? 0 : std::min(h->shard, h->arena_count - lo);
+    };
+    const size_t mine = len(h->rank);
     r = ncclGroupStart();
     for (int p = 0; p < nr && r == ncclSuccess; ++p) {
-      r = ncclSend(h->arena + (size_t)p * h->shard, h->shard, ncclFloat, p, h->comm, st);
-      if (r == ncclSuccess) r = ncclRecv(h->recvbuf + (size_t)p * h->shard, h->shard, ncclFloat, p, h->comm, st);
+      if (len(p) > 0) r = ncclSend(h->arena + (size_t)p * h->shard, len(p), ncclFloat, p, h->comm, st);
+      if (r == ncclSuccess && mine > 0)
+        r = ncclRecv(h->recvbuf + (size_t)p * h->shard, mine, ncclFloat, p, h->comm, st);
     }
     ncclResult_t r2 = ncclGroupEnd();
     if (r == ncclSuccess) r = r2;
     if (r == ncclSuccess) {
-      tree_avg_kernel<<<std::min<size_t>(4096, (h->shard + 255) / 256), 256, 0, st>>>(
-          nr, h->shard, h->recvbuf, h->arena + (size_t)h->rank * h->shard, 1.0f / (float)nr);
-      NG_TRY(check_launch("tree_avg_kernel"));
-      r = ncclAllGather(h->arena + (size_t)h->rank * h->shard, h->arena, h->shard, ncclFloat, h->comm, st);
+      NG_TRY(launch_tree_avg(st, nr, mine, h->shard, h->recvbuf, h->gatherbuf + (size_t)h->rank * h->shard));
+      r = ncclAllGather(h->gatherbuf + (size_t)h->rank * h->shard, h->gatherbuf, h->shard, ncclFloat, h->comm, st);
     }
+    if (r == ncclSuccess)
+      NG_CUDA_TRY(cudaMemcpyAsync(h->arena, h->gatherbuf, sizeof(float) * h->arena_count, cudaMemcpyDeviceToDevice, st));
   } else {
     r = ncclAllReduce(h->arena, h->arena, h->arena_count, ncclFloat, ncclSum, h->comm, st);
     if (r == ncclSuccess) {
@@ -734,6 +790,12 @@ ng_status nnet_average(nnet_t h, int32_t mode) {
   if (r != ncclSuccess) { set_error(std::string("nnet_average: ") + ncclGetErrorString(r)); return NG_ENCCL; }
   NG_CUDA_TRY(cudaStreamSynchronize(st));
   return read_eflags(h, "nnet_average");
+}
+
+ng_status ng_debug_tree_avg(int32_t nr, int64_t count, const float* in, float* out, void* stream) {
+  NG_REQUIRE(in && out, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(nr >= 1 && nr <= kMaxRanks && count >= 0, NG_EINVAL, "bad nr / count");
+  return launch_tree_avg((cudaStream_t)stream, nr, (size_t)count, (size_t)count, in, out);
 }
 
 }  // extern "C"

@@ -34,13 +34,18 @@ def rank_seed(rank: int, base: int = 1410) -> int:
     return base + 7455 * int(rank)
 
 
+def shard_size(count: int, nranks: int) -> int:
+    """Shard length of nnet_comm_init: ceil(count / nranks) rounded up to 64 floats."""
+    s = -(-count // nranks)
+    return -(-s // 64) * 64
+
+
 def shard_bounds(count: int, nranks: int, rank: int):
-    """The slice of the flat parameter arena rank `rank` reduces in the deterministic
-    average (all arenas are padded to a multiple of nranks)."""
-    if count % nranks:
-        raise ValueError("arena must be padded to a multiple of nranks")
-    s = count // nranks
-    return rank * s, (rank + 1) * s
+    """The slice [lo, hi) of the flat parameter arena that rank `rank` reduces in the
+    deterministic average (nnet_average); the last shards are ragged, possibly empty."""
+    s = shard_size(count, nranks)
+    lo = min(count, rank * s)
+    return lo, min(count, lo + s)
 
 
 def tree_order(n: int) -> list:

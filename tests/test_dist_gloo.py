@@ -33,17 +33,20 @@ def _worker(rank, world, port, q):
         out["max"] = driver.max_over_ranks(float(rank + 3))
         # every job starts from the same model, trains on its own shard (seed per rank)
         rng = np.random.default_rng(driver.rank_seed(rank))
-        count = 8 * 64 * world
+        count = 5_297_000 // 1000 + 17            # not a multiple of world or 64: ragged shards
         arena = rng.normal(size=count).astype(np.float32)
         # deterministic average: rank r reduces shard r of every rank in tree order
         gathered = [torch.zeros(count) for _ in range(world)]
         dist.all_gather(gathered, torch.from_numpy(arena))
         lo, hi = driver.shard_bounds(count, world, rank)
+        shard = driver.shard_size(count, world)
         shards = [g.numpy()[lo:hi].astype(np.float32) for g in gathered]
-        mine = (driver.tree_reduce_stride(shards) * np.float32(1.0 / world)).astype(np.float32)
-        pieces = [torch.zeros(hi - lo) for _ in range(world)]
+        mine = np.zeros(shard, dtype=np.float32)            # padded shard (gather buffer layout)
+        if hi > lo:
+            mine[:hi - lo] = (driver.tree_reduce_stride(shards) * np.float32(1.0 / world)).astype(np.float32)
+        pieces = [torch.zeros(shard) for _ in range(world)]
         dist.all_gather(pieces, torch.from_numpy(mine))
-        out["avg"] = np.concatenate([p.numpy() for p in pieces]).astype(np.float32)
+        out["avg"] = np.concatenate([p.numpy() for p in pieces]).astype(np.float32)[:count]
         out["all"] = [g.numpy().astype(np.float32) for g in gathered]
         out["lr"] = driver.job_learning_rate(0, 1, world)
         q.put((rank, out))
@@ -51,8 +54,8 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_rank_average_and_helpers():
-    world = 2
+@pytest.mark.parametrize("world", [2, 3])
+def test_multi_rank_average_and_helpers(world):
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -63,12 +66,12 @@ def test_two_rank_average_and_helpers():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert res[0]["uid"] == res[1]["uid"] == bytes(range(128))
-    assert res[0]["max"] == res[1]["max"] == 4.0
-    assert np.array_equal(res[0]["avg"], res[1]["avg"])            # identical on every rank
+    assert all(res[r]["uid"] == bytes(range(128)) for r in range(world))
+    assert all(res[r]["max"] == world + 2.0 for r in range(world))
     ref = otr.average_models([[a] for a in res[0]["all"]], dtype=np.float32)[0]
-    assert np.array_equal(res[0]["avg"], ref)                       # bit-exact vs oracle tree
-    assert res[0]["lr"] == pytest.approx(0.01 * 2 / 6)              # lr x n_jobs / 6
+    for r in range(world):
+        assert np.array_equal(res[r]["avg"], ref)                   # bit-exact vs oracle tree, every rank
+    assert res[0]["lr"] == pytest.approx(0.01 * world / 6)          # lr x n_jobs / 6
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 8])
@@ -84,3 +87,8 @@ def test_outer_iteration_sizes():
     assert driver.rank_seed(0) != driver.rank_seed(1)
     lo, hi = driver.shard_bounds(1024, 4, 3)
     assert (lo, hi) == (768, 1024)
+    # the paper's 6 jobs on the config-3 arena (5 360 128 floats): ragged, covers everything
+    count = 5_360_128
+    b = [driver.shard_bounds(count, 6, r) for r in range(6)]
+    assert b[0][0] == 0 and b[-1][1] == count and all(b[r][1] == b[r + 1][0] for r in range(5))
+    assert driver.shard_size(count, 6) % 64 == 0
