@@ -5,7 +5,11 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 Problem (section 2): frames x in R^D, labels y, maximise sum_i log p(y_i|x_i).
 Affine layers carry the bias as the last column of W with a 1 appended to the input
 (P:281-283).  Hidden nonlinearity: p-norm with p = 2 over contiguous groups of G
-(reading R19, no renormalisation layer).  Gradients are summed
+(reading R19).  Optionally (``renorm=True``, reading R32) each
+p-norm layer is followed by the renormalisation layer the paper's networks carry
+("renormalization layers that follow each p-norm layer"): y = s a with
+s = sqrt(D / ||a||^2), i.e. every row rescaled to unit root-mean-square (s = 0 for an
+all-zero row).  Gradients are summed
 over the minibatch, not averaged.  Backprop of all layers uses
 the pre-update weights, then every layer is updated (reading R21).
 """
@@ -26,6 +30,7 @@ class NnetConfig:
     hidden_dim: int          # p-norm input dimension (e.g. 3000)
     pnorm_group: int         # G (e.g. 10): p-norm output dimension = hidden_dim / G
     num_classes: int
+    renorm: bool = False     # renormalisation layer after each p-norm layer (R32)
 
     @property
     def pnorm_dim(self) -> int:
@@ -67,6 +72,14 @@ def pnorm(z: np.ndarray, group: int) -> np.ndarray:
     return np.sqrt(np.sum((z * z).reshape(n, d // group, group), axis=2))
 
 
+def renorm_scale(a: np.ndarray) -> np.ndarray:
+    """Per-row scale of the renormalisation layer (reading R32):
+    s = sqrt(D / ||a||^2) so that y = s a has unit root-mean-square; s = 0 if a = 0."""
+    ss = np.sum(a * a, axis=1, keepdims=True)
+    with np.errstate(divide="ignore"):
+        return np.where(ss > 0.0, np.sqrt(a.shape[1] / np.where(ss > 0.0, ss, 1.0)), 0.0)
+
+
 def log_softmax(z: np.ndarray) -> np.ndarray:
     """log p(y|x) = z_y - log sum_k exp z_k."""
     m = np.max(z, axis=1, keepdims=True)
@@ -76,6 +89,7 @@ def log_softmax(z: np.ndarray) -> np.ndarray:
 @dataclasses.dataclass
 class ForwardBackward:
     Y: List[np.ndarray]        # per weight matrix: input with the 1-column, N x (D_in + 1)
+    S: List[np.ndarray]        # per hidden layer: renormalisation scale s (N x 1), or None
     Z: List[np.ndarray]        # per weight matrix: output, N x D_out
     X: List[np.ndarray]        # per weight matrix: derivative of objective w.r.t. Z
     objective: float
@@ -83,8 +97,8 @@ class ForwardBackward:
 
 
 def forward(params: Sequence[np.ndarray], cfg: NnetConfig, frames: np.ndarray):
-    """Forward pass; returns (Y list, Z list, log-probs)."""
-    Y, Z = [], []
+    """Forward pass; returns (Y list, Z list, S list, log-probs)."""
+    Y, Z, S = [], [], []
     a = np.asarray(frames, dtype=np.float64)
     for l, W in enumerate(params):
         y = append_one(a)
@@ -93,7 +107,13 @@ def forward(params: Sequence[np.ndarray], cfg: NnetConfig, frames: np.ndarray):
         Z.append(z)
         if l < len(params) - 1:
             a = pnorm(z, cfg.pnorm_group)
-    return Y, Z, log_softmax(Z[-1])
+            if cfg.renorm:
+                s = renorm_scale(a)
+                a = s * a                                      # unit-RMS rows
+                S.append(s)
+            else:
+                S.append(None)
+    return Y, Z, S, log_softmax(Z[-1])
 
 
 def forward_backward(params: Sequence[np.ndarray], cfg: NnetConfig, frames: np.ndarray,
@@ -101,7 +121,7 @@ def forward_backward(params: Sequence[np.ndarray], cfg: NnetConfig, frames: np.n
     """Objective sum_i log p(y_i|x_i) and, for every weight matrix, the
     derivative X_i w.r.t. its output and its input Y_i."""
     labels = np.asarray(labels)
-    Y, Z, logp = forward(params, cfg, frames)
+    Y, Z, S, logp = forward(params, cfg, frames)
     N = logp.shape[0]
     if np.any(labels < 0) or np.any(labels >= cfg.num_classes):
         raise ValueError("label out of range")
@@ -117,11 +137,18 @@ def forward_backward(params: Sequence[np.ndarray], cfg: NnetConfig, frames: np.n
         g = X[l] @ W[:, :-1]                                   # d obj / d a_{l-1} (bias col excluded)
         z = Z[l - 1]
         a = Y[l][:, :-1]
+        s = S[l - 1]
+        if s is not None:
+            # renormalisation backward: y = s a, s = sqrt(D/||a||^2) =>
+            # d obj / d a = s (g - y (y^T g) / D)
+            g = s * (g - a * np.sum(a * g, axis=1, keepdims=True) / a.shape[1])
+            with np.errstate(divide="ignore", invalid="ignore"):
+                a = np.where(s > 0.0, a / np.where(s > 0.0, s, 1.0), 0.0)   # the p-norm output
         a_rep = np.repeat(a, G, axis=1)
         g_rep = np.repeat(g, G, axis=1)
         with np.errstate(divide="ignore", invalid="ignore"):
             X[l - 1] = np.where(a_rep > 0.0, g_rep * z / a_rep, 0.0)   # d a_j / d z_k = z_k / a_j
-    return ForwardBackward(Y, Z, X, objective, logp)
+    return ForwardBackward(Y, S, Z, X, objective, logp)
 
 
 @dataclasses.dataclass
@@ -132,6 +159,10 @@ class LayerStats:
     bound: float
     updated_in: bool
     updated_out: bool
+    flags_in: tuple = (False, False, False)    # (floored, reorth_checked, reorthogonalized), B.3.1
+    flags_out: tuple = (False, False, False)
+    margins_in: tuple = (0.0, 0.0)             # (floor_margin, cond_c) of the update, if any
+    margins_out: tuple = (0.0, 0.0)
 
 
 def make_states(cfg: NnetConfig, ng_in: online_ng.OnlineNgConfig, ng_out: online_ng.OnlineNgConfig):
@@ -157,6 +188,8 @@ def update(params: List[np.ndarray], fb: ForwardBackward, lr: float, states=None
         X, Y = fb.X[l], fb.Y[l]
         N = X.shape[0]
         upd_in = upd_out = False
+        fl_in = fl_out = (False, False, False)
+        mg_in = mg_out = (0.0, 0.0)
         if precond == "online":
             s_in, s_out = states[l]
             ox = online_ng.precondition(s_out, X)
@@ -164,6 +197,9 @@ def update(params: List[np.ndarray], fb: ForwardBackward, lr: float, states=None
             x_hat, gx, px = ox.x_hat, ox.gamma, ox.row_sq / (ox.gamma ** 2)
             y_hat, gy, py = oy.x_hat, oy.gamma, oy.row_sq / (oy.gamma ** 2)
             upd_in, upd_out = oy.updated, ox.updated
+            fl_in = (oy.floored, oy.reorth_checked, oy.reorthogonalized)
+            fl_out = (ox.floored, ox.reorth_checked, ox.reorthogonalized)
+            mg_in, mg_out = (oy.floor_margin, oy.cond_c), (ox.floor_margin, ox.cond_c)
         elif precond == "simple":
             x_hat, gx, _ = simple_ng.precondition_simple(X)
             y_hat, gy, _ = simple_ng.precondition_simple(Y)
@@ -177,7 +213,7 @@ def update(params: List[np.ndarray], fb: ForwardBackward, lr: float, states=None
         bound = training.max_change_bound(lr, gx, gy, px, py)
         alpha_t = training.max_change_scale(bound, N, max_change_per_sample)
         params[l] += (alpha_t * lr * gx * gy) * (x_hat.T @ y_hat)
-        stats.append(LayerStats(alpha_t, gy, gx, bound, upd_in, upd_out))
+        stats.append(LayerStats(alpha_t, gy, gx, bound, upd_in, upd_out, fl_in, fl_out, mg_in, mg_out))
     return stats
 
 

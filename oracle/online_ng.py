@@ -76,6 +76,10 @@ class PrecondOutput:
     reorth_checked: bool = False
     reorthogonalized: bool = False
     tr_xxt: float = 0.0
+    # diagnostics of the update's threshold decisions (values the algorithm computes anyway;
+    # tests use them to tell a decided threshold from one inside rounding noise)
+    floor_margin: float = 0.0     # (min_i c_i - (1-eta)^2 rho^2) / max_i c_i, before flooring
+    cond_c: float = 0.0           # max c / min c after flooring (the B.3.1 trigger, > 1e6)
 
     @property
     def x_bar(self) -> np.ndarray:
@@ -226,6 +230,7 @@ def precondition(state: OnlineNgState, X: np.ndarray, update: bool | None = None
     c, U = _eigh_descending(Z)                                 # eqn:zt:eig:repeat
     c_floor = ((1.0 - eta) ** 2) * rho * rho                   # P:1125-1128 (reading R13: old rho)
     floored = bool(np.any(c < c_floor))
+    floor_margin = float((np.min(c) - c_floor) / np.max(c))
     c = np.maximum(c, c_floor)
 
     X_hat = X - H @ W
@@ -264,7 +269,7 @@ def precondition(state: OnlineNgState, X: np.ndarray, update: bool | None = None
     state.t += 1
     return PrecondOutput(X_hat, gamma, gamma * gamma * p, updated=True, floored=floored,
                          reorth_checked=reorth_checked, reorthogonalized=reorthogonalized,
-                         tr_xxt=tr_xxt)
+                         tr_xxt=tr_xxt, floor_margin=floor_margin, cond_c=cond)
 
 
 def _reorthogonalize(W: np.ndarray, e: np.ndarray, tol: float = 1e-3):

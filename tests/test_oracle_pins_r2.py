@@ -61,7 +61,7 @@ def test_online_step_equals_plain_sgd_in_span():
     bi, _ = _orthonormal(rng, Din1, R)
     X = rng.normal(size=(N, R)) @ bo
     Y = rng.normal(size=(N, R)) @ bi
-    fb = nnet.ForwardBackward(Y=[Y], Z=[None], X=[X], objective=0.0, logp=None)
+    fb = nnet.ForwardBackward(Y=[Y], S=[], Z=[None], X=[X], objective=0.0, logp=None)
     for lr, mc in ((1e-3, 0.075), (10.0, 0.075)):     # guard inactive / active
         w0 = rng.normal(size=(Dout, Din1))
         p_on, p_plain = [w0.copy()], [w0.copy()]

@@ -72,7 +72,7 @@ def test_pnorm_golden():
 def test_zero_net_uniform_logprob():
     """zero network -> log p = -log C for every class."""
     params = [np.zeros(s) for s in CFG_T.layer_shapes()]
-    _, _, logp = nnet.forward(params, CFG_T, gaussian_rows(0, 4, 6))
+    _, _, _, logp = nnet.forward(params, CFG_T, gaussian_rows(0, 4, 6))
     assert np.allclose(logp, -np.log(5.0))
 
 
