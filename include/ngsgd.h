@@ -65,10 +65,13 @@ typedef struct {
   int32_t update_period;       /* J = 4                             */
   int32_t always_update_first; /* 10: always update on the first 10 minibatches  */
   float epsilon;               /* floor of rho and d, 1e-10      */
-  int32_t precision;           /* ng_precision (below) of the NG projections: NG_FP32 = CUDA
-                                  cores in FP32 (default); NG_TF32 = H, J, K, L, X_hat, W_{t+1}
-                                  on tcgen05 tensor cores (needs ld % 4 == 0 and R % 4 == 0,
-                                  otherwise that call uses FP32).  The R x R math is FP64.   */
+  int32_t precision;           /* ng_precision (below).  NG_FP32 and NG_TF32: the projections
+                                  H = X W^T, J = H^T X and X_hat = X - H W on tcgen05 tensor
+                                  cores in 3xTF32 (FP32-grade: X_hat is a difference of nearly
+                                  equal terms when the subspace holds most of X's energy);
+                                  needs ld % 4 == 0 and R % 4 == 0, otherwise that call uses
+                                  CUDA cores.  NG_FP32_SIMT: CUDA cores in FP32 throughout.
+                                  K, L, A_t B_t are FP32 CUDA-core, the R x R math FP64.     */
 } ngsgd_config;
 
 void ngsgd_config_default(ngsgd_config* cfg, int32_t rank);
@@ -129,15 +132,21 @@ ng_status ngsgd_set_state(ngsgd_t h, const ngsgd_state_host* in);
 
 /* ---------------------------------------- p-norm / softmax DNN training step ---- */
 
-/* NG_FP32: every GEMM on CUDA cores in FP32 (paper-faithful; parity 1e-4).
+/* NG_FP32: FP32-grade (paper-faithful; parity 1e-4): every GEMM on tcgen05 tensor
+ *          cores in 3xTF32 (hi/lo split of both operands in shared memory, three MMAs
+ *          accumulated in FP32 TMEM).
  * NG_TF32: the DNN GEMMs (forward, backward-data, weight update) on tcgen05 tensor cores
  *          reading the FP32 buffers as TF32, FP32 accumulation (parity bar 2e-2 of the
- *          north star for reduced-precision tensor-core inputs).  NG-SGD stays FP32.
+ *          north star for reduced-precision tensor-core inputs); NG projections 3xTF32.
+ * NG_FP32_SIMT: every GEMM on FP32 CUDA cores (the round-1 reference path).
  * NG_BF16: reserved. */
-typedef enum { NG_FP32 = 0, NG_BF16 = 1, NG_TF32 = 2 } ng_precision;
+typedef enum { NG_FP32 = 0, NG_BF16 = 1, NG_TF32 = 2, NG_FP32_SIMT = 3 } ng_precision;
 
-/* Network: input_dim -> num_hidden x [affine hidden_dim -> p-norm /pnorm_group] ->
- * affine num_classes -> softmax (p = 2, R19). */
+/* Network: input_dim -> num_hidden x [affine hidden_dim -> p-norm /pnorm_group
+ * (-> renormalisation)] -> affine num_classes -> softmax (p = 2,
+ * DESIGN.md R19).  renorm != 0 adds the renormalisation layer that follows each p-norm
+ * layer in the paper's networks (R32): y = s a, s = sqrt(D/||a||^2)
+ * per row (unit root-mean-square; s = 0 for an all-zero row). */
 typedef struct {
   int32_t input_dim, num_hidden, hidden_dim, pnorm_group, num_classes;
   int32_t max_minibatch;        /* N bound; 512 on GPU              */
@@ -145,6 +154,7 @@ typedef struct {
   ngsgd_config ng_in, ng_out;   /* R_in = 20, R_out = 80                    */
   int32_t precision;            /* ng_precision of the DNN GEMMs                          */
   uint64_t seed;                /* weight-init seed (C.6)                    */
+  int32_t renorm;               /* 1: renormalisation layer after each p-norm (R32)       */
 } nnet_config;
 
 typedef struct nnet_ctx* nnet_t;
@@ -279,6 +289,12 @@ int64_t ng_kernel_launches(void);
 ng_status ng_debug_gemm_tf32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda, int32_t a_kmajor,
                              const float* B, int64_t ldb, int32_t b_kmajor, float* C, int64_t ldc,
                              int32_t bn, int32_t splits, void* cuda_stream);
+/* The same with split3 != 0 selecting 3xTF32 (each operand split in shared memory into a
+ * TF32 hi part and the exact remainder, A_lo B_hi + A_hi B_lo + A_hi B_hi accumulated in
+ * TMEM): the FP32-grade tensor-core GEMM of the NG_FP32 mode and of the NG projections. */
+ng_status ng_debug_gemm_tc(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda, int32_t a_kmajor,
+                           const float* B, int64_t ldb, int32_t b_kmajor, float* C, int64_t ldc,
+                           int32_t bn, int32_t splits, int32_t split3, void* cuda_stream);
 
 /* Eigensolver round timing, accumulated over every refresh since the last call and reset
  * by it (SM clock cycles; only recorded while NG_PROFILE_JACOBI_MASK has bit 64 set):

@@ -40,7 +40,7 @@ class NgsgdStateHost(ctypes.Structure):
 class NnetConfig(ctypes.Structure):
     _fields_ = [("input_dim", c_int32), ("num_hidden", c_int32), ("hidden_dim", c_int32), ("pnorm_group", c_int32),
                 ("num_classes", c_int32), ("max_minibatch", c_int32), ("precond", c_int32), ("ng_in", NgsgdConfig),
-                ("ng_out", NgsgdConfig), ("precision", c_int32), ("seed", ctypes.c_uint64)]
+                ("ng_out", NgsgdConfig), ("precision", c_int32), ("seed", ctypes.c_uint64), ("renorm", c_int32)]
 
 
 class NnetUpdateStats(ctypes.Structure):
@@ -88,6 +88,8 @@ SIGNATURES = {
     "ng_kernel_launches": (ctypes.c_int64, []),
     "ng_debug_gemm_tf32": (c_int32, [c_int32, c_int32, c_int32, c_void_p, c_int64, c_int32, c_void_p, c_int64,
                                      c_int32, c_void_p, c_int64, c_int32, c_int32, c_void_p]),
+    "ng_debug_gemm_tc": (c_int32, [c_int32, c_int32, c_int32, c_void_p, c_int64, c_int32, c_void_p, c_int64,
+                                   c_int32, c_void_p, c_int64, c_int32, c_int32, c_int32, c_void_p]),
     "ng_debug_eig_clocks": (c_int32, [ctypes.POINTER(ctypes.c_uint64)]),
     "ng_debug_eig_dc": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     "ng_debug_eig_tri": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),

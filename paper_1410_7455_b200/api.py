@@ -56,7 +56,7 @@ class OnlinePreconditioner:
         if _borrowed is not None:
             self._h = ctypes.c_void_p(_borrowed)
             return
-        cfg = default_ng_config(rank, precision={"fp32": 0, "tf32": 2}[precision], **cfg_overrides)
+        cfg = default_ng_config(rank, precision={"fp32": 0, "tf32": 2, "fp32_simt": 3}[precision], **cfg_overrides)
         h = ctypes.c_void_p()
         check(lib.ngsgd_create(int(dim), int(max_rows), ctypes.byref(cfg), _stream_handle(stream), ctypes.byref(h)))
         self._h = h
@@ -127,16 +127,17 @@ class Nnet:
     def __init__(self, input_dim: int, num_hidden: int, hidden_dim: int, pnorm_group: int, num_classes: int,
                  max_minibatch: int = 512, precond: bool = True, rank_in: int = 20, rank_out: int = 80,
                  precision: str = "fp32", seed: int = 0, stream: Optional[torch.cuda.Stream] = None,
-                 ng_overrides: Optional[dict] = None):
+                 ng_overrides: Optional[dict] = None, renorm: bool = False):
         cfg = _lib.NnetConfig()
         cfg.input_dim, cfg.num_hidden, cfg.hidden_dim = input_dim, num_hidden, hidden_dim
         cfg.pnorm_group, cfg.num_classes, cfg.max_minibatch = pnorm_group, num_classes, max_minibatch
         cfg.precond = 1 if precond else 0
-        prec = {"fp32": 0, "bf16": 1, "tf32": 2}[precision]
+        prec = {"fp32": 0, "bf16": 1, "tf32": 2, "fp32_simt": 3}[precision]
         cfg.ng_in = default_ng_config(rank_in, **dict({"precision": prec}, **(ng_overrides or {})))
         cfg.ng_out = default_ng_config(rank_out, **dict({"precision": prec}, **(ng_overrides or {})))
         cfg.precision = prec
         cfg.seed = int(seed)
+        cfg.renorm = 1 if renorm else 0
         h = ctypes.c_void_p()
         check(lib.nnet_create(ctypes.byref(cfg), _stream_handle(stream), ctypes.byref(h)))
         self._h = h

@@ -4,6 +4,11 @@
 //   warp 0 lane 0 : TMA producer   (cp.async.bulk.tensor -> S-stage smem ring, mbarrier tx)
 //   warp 1 lane 0 : MMA issuer     (tcgen05.mma.kind::tf32, 4 x K=8 per 32-wide k-block,
 //                                    tcgen05.commit -> frees the smem stage)
+//   warps 2..3    : (3xTF32 only) split each landed stage in place into hi = x rounded to
+//                   the nearest TF32 value and lo = (x - hi) rounded to TF32 in a second
+//                   buffer, fence.proxy.async, arrive; the MMA thread then issues
+//                   A_lo B_hi + A_hi B_lo + A_hi B_hi per k-slice (FP32-grade products: the
+//                   dropped A_lo B_lo and the rounding of lo are <= ~2^-23 |a||b| each)
 //   warps 0..3    : epilogue       (tcgen05.ld 32x32b: warp w owns TMEM lanes 32w..32w+31,
 //                                    i.e. tile rows; functor applied per element)
 // Shared-memory layouts are the canonical UMMA SWIZZLE_128B layouts produced directly by
@@ -46,6 +51,18 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Round to the nearest TF32 value (cvt.rna: 10 explicit mantissa bits, low 13 bits zero), so
+// the tensor core reads it exactly: hi = rna(x), lo = rna(x - hi) (x - hi is exact).
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
 }
 
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -123,17 +140,20 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 
 // One 128 x BN output tile: rows m0.., columns n0.., k-blocks kb0 .. kb0+nkb-1.  ntile /
 // ztile are the column-tile and split indices used by the NGAPPLY / PARTIAL epilogues.
-template <int BN, bool AK, bool BKM, int EPI>
+template <int BN, bool AK, bool BKM, int EPI, bool S3>
 __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int m0, int n0,
                                         int kb0, int nkb, int ntile, int ztile, const TcEpilogue& epi,
                                         int nstages) {
-  constexpr uint32_t A_BYTES = kBM * kBK * 4, B_BYTES = BN * kBK * 4, STAGE = A_BYTES + B_BYTES;
+  // S3: 3xTF32 -- each stage holds [A | B] as landed (then hi parts) and [A_lo | B_lo]
+  constexpr uint32_t A_BYTES = kBM * kBK * 4, B_BYTES = BN * kBK * 4, HALF = A_BYTES + B_BYTES;
+  constexpr uint32_t STAGE = S3 ? 2 * HALF : HALF;
   constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));   // power of 2
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned ring (SWIZZLE_128B atoms); pointer arithmetic keeps the shared space
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ __align__(8) uint64_t full_bar[kStages];
   __shared__ __align__(8) uint64_t empty_bar[kStages];
+  __shared__ __align__(8) uint64_t split_bar[S3 ? kStages : 1];
   __shared__ __align__(8) uint64_t accum_bar;
   __shared__ uint32_t tmem_base_sh;
 
@@ -142,7 +162,11 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmB)) : "memory");
-    for (int s = 0; s < nstages; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+    for (int s = 0; s < nstages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+      if (S3) mbar_init(&split_bar[s], 64);
+    }
     mbar_init(&accum_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -192,7 +216,7 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
       mbar_wait(&empty_bar[s], ph ^ 1u);
       uint8_t* sa = smem + s * STAGE;
       uint8_t* sb = sa + A_BYTES;
-      mbar_expect_tx(&full_bar[s], STAGE);
+      mbar_expect_tx(&full_bar[s], HALF);
       const int kc = (kb0 + i) * kBK;
       if (AK) {
         tma_load_2d(sa, tmA, kc, m0, &full_bar[s]);
@@ -214,19 +238,47 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
     int s = 0;
     uint32_t ph = 0;
     for (int i = 0; i < nkb; ++i) {
-      mbar_wait(&full_bar[s], ph);
+      mbar_wait(S3 ? &split_bar[s] : &full_bar[s], ph);
       tc_fence_after();
       const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
 #pragma unroll
       for (int k = 0; k < kBK / 8; ++k) {
         const uint64_t da = AK ? desc_kmajor(sa, k) : desc_mnmajor(sa, k);
         const uint64_t db = BKM ? desc_kmajor(sb, k) : desc_mnmajor(sb, k);
-        mma_tf32(tmem, da, db, idesc, (i > 0 || k > 0) ? 1u : 0u);
+        if (S3) {
+          const uint64_t dal = AK ? desc_kmajor(sa + HALF, k) : desc_mnmajor(sa + HALF, k);
+          const uint64_t dbl = BKM ? desc_kmajor(sb + HALF, k) : desc_mnmajor(sb + HALF, k);
+          mma_tf32(tmem, dal, db, idesc, (i > 0 || k > 0) ? 1u : 0u);   // small terms first
+          mma_tf32(tmem, da, dbl, idesc, 1u);
+          mma_tf32(tmem, da, db, idesc, 1u);
+        } else {
+          mma_tf32(tmem, da, db, idesc, (i > 0 || k > 0) ? 1u : 0u);
+        }
       }
       umma_commit(&empty_bar[s]);
       if (++s == nstages) { s = 0; ph ^= 1u; }
     }
     umma_commit(&accum_bar);
+  } else if (S3 && warp >= 2) {
+    // ---------------- 3xTF32 split (warps 2-3): hi in place, lo = x - hi beside it
+    const int t = threadIdx.x - 64;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < nkb; ++i) {
+      mbar_wait(&full_bar[s], ph);
+      float4* hi = reinterpret_cast<float4*>(smem + s * STAGE);
+      float4* lo = reinterpret_cast<float4*>(smem + s * STAGE + HALF);
+#pragma unroll 4
+      for (int q = t; q < (int)(HALF / 16); q += 64) {
+        const float4 x = hi[q];
+        const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
+        hi[q] = h;
+        lo[q] = make_float4(tf32_rna(x.x - h.x), tf32_rna(x.y - h.y), tf32_rna(x.z - h.z), tf32_rna(x.w - h.w));
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+      mbar_arrive(&split_bar[s]);
+      if (++s == nstages) { s = 0; ph ^= 1u; }
+    }
   }
   __syncwarp();
 
@@ -345,20 +397,20 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
   }
 }
 
-template <int BN, bool AK, bool BKM, int EPI>
+template <int BN, bool AK, bool BKM, int EPI, bool S3>
 __global__ void __launch_bounds__(128)
 tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                     int K, int kb_per_split, TcEpilogue epi, int nstages) {
   const int kb_total = (K + kBK - 1) / kBK;
   const int kb0 = blockIdx.z * kb_per_split;
   const int nkb = max(0, min(kb_total, kb0 + kb_per_split) - kb0);
-  tc_tile<BN, AK, BKM, EPI>(&tmA, &tmB, M, N, blockIdx.y * kBM, blockIdx.x * BN, kb0, nkb, blockIdx.x, blockIdx.z,
-                            epi, nstages);
+  tc_tile<BN, AK, BKM, EPI, S3>(&tmA, &tmB, M, N, blockIdx.y * kBM, blockIdx.x * BN, kb0, nkb, blockIdx.x,
+                                blockIdx.z, epi, nstages);
 }
 
 // Grouped launch: problem g owns tiles [tile_begin, tile_begin + mt*nt*splits); each tile
 // (z, m, n) of it is one CTA.  Problems share BN, operand majors and epilogue kind.
-template <int BN, bool AK, bool BKM, int EPI>
+template <int BN, bool AK, bool BKM, int EPI, bool S3>
 __global__ void __launch_bounds__(128) tc_gemm_tf32_grouped_kernel(const __grid_constant__ TcGroup grp) {
   int g = 0;
   while (g + 1 < grp.count && (int)blockIdx.x >= grp.p[g + 1].tile_begin) ++g;
@@ -369,8 +421,8 @@ __global__ void __launch_bounds__(128) tc_gemm_tf32_grouped_kernel(const __grid_
   const int kb_total = (P.K + kBK - 1) / kBK;
   const int kb0 = z * P.kbps;
   const int nkb = max(0, min(kb_total, kb0 + P.kbps) - kb0);
-  tc_tile<BN, AK, BKM, EPI>(&P.tmA, &P.tmB, P.M, P.N, mtile * kBM, ntile * BN, kb0, nkb, ntile, z, P.epi,
-                            grp.nstages);
+  tc_tile<BN, AK, BKM, EPI, S3>(&P.tmA, &P.tmB, P.M, P.N, mtile * kBM, ntile * BN, kb0, nkb, ntile, z, P.epi,
+                                grp.nstages);
 }
 
 // ------------------------------------------------------------------ host side
@@ -425,50 +477,61 @@ ng_status make_tmap(CUtensorMap* out, const float* ptr, int64_t inner, int64_t o
   return NG_OK;
 }
 
-inline size_t ring_smem(int bn, int stages) { return (size_t)stages * (kBM * kBK * 4 + bn * kBK * 4) + 1024; }
+inline size_t ring_smem(int bn, int stages, bool s3) {
+  return (size_t)stages * (kBM * kBK * 4 + bn * kBK * 4) * (s3 ? 2 : 1) + 1024;
+}
 // Ring depth for BN, capped by the 227 KB dynamic shared memory limit.
-inline int ring_stages(int bn) {
+inline int ring_stages(int bn, bool s3) {
   int ns = tc_stages();
-  while (ns > 1 && ring_smem(bn, ns) > 227u * 1024u) --ns;
+  while (ns > 1 && ring_smem(bn, ns, s3) > 227u * 1024u) --ns;
   return ns;
 }
 
-template <int BN, bool AK, bool BKM, int EPI>
+template <int BN, bool AK, bool BKM, int EPI, bool S3>
 ng_status launch(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int kbps,
                  int splits, const TcEpilogue& epi) {
   static bool attr = false;
   if (!attr) {
-    NG_CUDA_TRY(cudaFuncSetAttribute(tc_gemm_tf32_kernel<BN, AK, BKM, EPI>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_smem(BN, ring_stages(BN))));
+    NG_CUDA_TRY(cudaFuncSetAttribute(tc_gemm_tf32_kernel<BN, AK, BKM, EPI, S3>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)ring_smem(BN, ring_stages(BN, S3), S3)));
     attr = true;
   }
   // Only as many ring stages as k-blocks per tile: short-K tiles leave room for more
   // co-resident CTAs per SM.
-  const int ns = std::max(1, std::min(ring_stages(BN), kbps));
+  const int ns = std::max(1, std::min(ring_stages(BN, S3), kbps));
   dim3 grid(ceil_div(N, BN), ceil_div(M, kBM), splits);
-  NG_CUDA_TRY(launch_pdl(tc_gemm_tf32_kernel<BN, AK, BKM, EPI>, grid, dim3(128), ring_smem(BN, ns), st, ta, tb, M, N,
-                         K, kbps, epi, ns));
+  NG_CUDA_TRY(launch_pdl(tc_gemm_tf32_kernel<BN, AK, BKM, EPI, S3>, grid, dim3(128), ring_smem(BN, ns, S3), st, ta,
+                         tb, M, N, K, kbps, epi, ns));
   return check_launch("tc_gemm_tf32_kernel");
 }
 
-template <int BN, bool AK, bool BKM>
+template <int BN, bool AK, bool BKM, bool S3>
 ng_status dispatch_epi(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int kbps,
                        int splits, const TcEpilogue& epi) {
   switch (epi.kind) {
-    case TC_EPI_STORE: return launch<BN, AK, BKM, TC_EPI_STORE>(st, ta, tb, M, N, K, kbps, splits, epi);
-    case TC_EPI_AXPY: return launch<BN, AK, BKM, TC_EPI_AXPY>(st, ta, tb, M, N, K, kbps, splits, epi);
-    case TC_EPI_NGAPPLY: return launch<BN, AK, BKM, TC_EPI_NGAPPLY>(st, ta, tb, M, N, K, kbps, splits, epi);
-    default: return launch<BN, AK, BKM, TC_EPI_PARTIAL>(st, ta, tb, M, N, K, kbps, splits, epi);
+    case TC_EPI_STORE: return launch<BN, AK, BKM, TC_EPI_STORE, S3>(st, ta, tb, M, N, K, kbps, splits, epi);
+    case TC_EPI_AXPY: return launch<BN, AK, BKM, TC_EPI_AXPY, S3>(st, ta, tb, M, N, K, kbps, splits, epi);
+    case TC_EPI_NGAPPLY: return launch<BN, AK, BKM, TC_EPI_NGAPPLY, S3>(st, ta, tb, M, N, K, kbps, splits, epi);
+    default: return launch<BN, AK, BKM, TC_EPI_PARTIAL, S3>(st, ta, tb, M, N, K, kbps, splits, epi);
   }
 }
 
-template <int BN>
+template <int BN, bool S3>
 ng_status dispatch_major(cudaStream_t st, bool ak, bool bk, const CUtensorMap& ta, const CUtensorMap& tb, int M,
                          int N, int K, int kbps, int splits, const TcEpilogue& epi) {
-  if (ak && bk) return dispatch_epi<BN, true, true>(st, ta, tb, M, N, K, kbps, splits, epi);
-  if (ak && !bk) return dispatch_epi<BN, true, false>(st, ta, tb, M, N, K, kbps, splits, epi);
-  if (!ak && bk) return dispatch_epi<BN, false, true>(st, ta, tb, M, N, K, kbps, splits, epi);
-  return dispatch_epi<BN, false, false>(st, ta, tb, M, N, K, kbps, splits, epi);
+  if (ak && bk) return dispatch_epi<BN, true, true, S3>(st, ta, tb, M, N, K, kbps, splits, epi);
+  if (ak && !bk) return dispatch_epi<BN, true, false, S3>(st, ta, tb, M, N, K, kbps, splits, epi);
+  if (!ak && bk) return dispatch_epi<BN, false, true, S3>(st, ta, tb, M, N, K, kbps, splits, epi);
+  return dispatch_epi<BN, false, false, S3>(st, ta, tb, M, N, K, kbps, splits, epi);
+}
+
+template <bool S3>
+ng_status dispatch_bn(cudaStream_t st, int bn, bool ak, bool bk, const CUtensorMap& ta, const CUtensorMap& tb, int M,
+                      int N, int K, int kbps, int splits, const TcEpilogue& epi) {
+  if (bn == 32) return dispatch_major<32, S3>(st, ak, bk, ta, tb, M, N, K, kbps, splits, epi);
+  if (bn == 64) return dispatch_major<64, S3>(st, ak, bk, ta, tb, M, N, K, kbps, splits, epi);
+  return dispatch_major<128, S3>(st, ak, bk, ta, tb, M, N, K, kbps, splits, epi);
 }
 
 }  // namespace
@@ -482,7 +545,7 @@ int tc_splits(int K, int splits) {
 
 ng_status tc_gemm_tf32(cudaStream_t st, int M, int N, int K, const float* A, int64_t lda, bool a_kmajor,
                        const float* B, int64_t ldb, bool b_kmajor, const TcEpilogue& epi, int bn, int splits,
-                       int* splits_used) {
+                       int* splits_used, bool split3) {
   NG_REQUIRE(M >= 1 && N >= 1 && K >= 1, NG_ESHAPE, "tc_gemm_tf32: empty problem");
   NG_REQUIRE(bn == 32 || bn == 64 || bn == 128, NG_EINVAL, "tc_gemm_tf32: bn must be 32, 64 or 128");
   const int kb = ceil_div(K, kBK);
@@ -495,13 +558,12 @@ ng_status tc_gemm_tf32(cudaStream_t st, int M, int N, int K, const float* A, int
   else NG_TRY(make_tmap(&ta, A, M, K, lda, 32, true));                // [K][M]
   if (b_kmajor) NG_TRY(make_tmap(&tb, B, K, N, ldb, bn, false));      // [N][K]
   else NG_TRY(make_tmap(&tb, B, N, K, ldb, 32, true));                // [K][N]
-  if (bn == 32) return dispatch_major<32>(st, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
-  if (bn == 64) return dispatch_major<64>(st, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
-  return dispatch_major<128>(st, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
+  if (split3) return dispatch_bn<true>(st, bn, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
+  return dispatch_bn<false>(st, bn, a_kmajor, b_kmajor, ta, tb, M, N, K, kbps, splits, epi);
 }
 
 ng_status tc_gemm_tf32_pnorm(cudaStream_t st, int M, int N, int K, const float* A, int64_t lda, const float* B,
-                                  int64_t ldb, float* Z, int64_t ldz, float* Ynext, int64_t ldy) {
+                                  int64_t ldb, float* Z, int64_t ldz, float* Ynext, int64_t ldy, bool split3) {
   NG_REQUIRE(M >= 1 && N >= 10 && K >= 1 && N % 10 == 0 && ldy >= N / 10 + 1, NG_ESHAPE, "tc_gemm_tf32_pnorm: shape");
   const int kb = ceil_div(K, kBK);
   CUtensorMap ta, tb;
@@ -515,25 +577,31 @@ ng_status tc_gemm_tf32_pnorm(cudaStream_t st, int M, int N, int K, const float* 
   e.ldc = ldz;
   e.y = Ynext;
   e.ldy = ldy;
-  if (bn == 160) return launch<160, true, true, TC_EPI_PNORM>(st, ta, tb, M, N, K, kb, 1, e);
-  return launch<80, true, true, TC_EPI_PNORM>(st, ta, tb, M, N, K, kb, 1, e);
+  if (split3) return launch<80, true, true, TC_EPI_PNORM, true>(st, ta, tb, M, N, K, kb, 1, e);
+  if (bn == 160) return launch<160, true, true, TC_EPI_PNORM, false>(st, ta, tb, M, N, K, kb, 1, e);
+  return launch<80, true, true, TC_EPI_PNORM, false>(st, ta, tb, M, N, K, kb, 1, e);
 }
 
-template <int BN, bool AK, bool BKM, int EPI>
+template <int BN, bool AK, bool BKM, int EPI, bool S3>
 ng_status launch_grouped(cudaStream_t st, const TcGroup& grp, int tiles) {
   static bool attr = false;
   if (!attr) {
-    NG_CUDA_TRY(cudaFuncSetAttribute(tc_gemm_tf32_grouped_kernel<BN, AK, BKM, EPI>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring_smem(BN, ring_stages(BN))));
+    NG_CUDA_TRY(cudaFuncSetAttribute(tc_gemm_tf32_grouped_kernel<BN, AK, BKM, EPI, S3>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)ring_smem(BN, ring_stages(BN, S3), S3)));
     attr = true;
   }
-  NG_CUDA_TRY(launch_pdl(tc_gemm_tf32_grouped_kernel<BN, AK, BKM, EPI>, dim3(tiles), dim3(128),
-                         ring_smem(BN, grp.nstages), st, grp));
+  NG_CUDA_TRY(launch_pdl(tc_gemm_tf32_grouped_kernel<BN, AK, BKM, EPI, S3>, dim3(tiles), dim3(128),
+                         ring_smem(BN, grp.nstages, S3), st, grp));
   return check_launch("tc_gemm_tf32_grouped_kernel");
 }
 
+template <bool S3>
+ng_status grouped_dispatch(cudaStream_t st, const TcGroup& grp, int tiles, bool a_kmajor, bool b_kmajor, int epi_kind,
+                           int bn);
+
 ng_status tc_gemm_tf32_grouped(cudaStream_t st, const TcGroupDesc* desc, int count, bool a_kmajor, bool b_kmajor,
-                               int epi_kind, int bn) {
+                               int epi_kind, int bn, bool split3) {
   NG_REQUIRE(count >= 1 && count <= kTcGroupMax, NG_EINVAL, "tc_gemm_tf32_grouped: bad problem count");
   NG_REQUIRE(bn == 32 || bn == 64 || bn == 128, NG_EINVAL, "tc_gemm_tf32_grouped: bad bn");
   TcGroup grp;
@@ -559,8 +627,15 @@ ng_status tc_gemm_tf32_grouped(cudaStream_t st, const TcGroupDesc* desc, int cou
     if (d.splits_used) *d.splits_used = sp;
     tiles += ceil_div(d.M, kBM) * ceil_div(d.N, bn) * sp;
   }
-  grp.nstages = std::min(ring_stages(bn), kbps_max);
-#define NG_GRP(BN_, AK_, BK_, E_) return launch_grouped<BN_, AK_, BK_, E_>(st, grp, tiles)
+  grp.nstages = std::min(ring_stages(bn, split3), kbps_max);
+  if (split3) return grouped_dispatch<true>(st, grp, tiles, a_kmajor, b_kmajor, epi_kind, bn);
+  return grouped_dispatch<false>(st, grp, tiles, a_kmajor, b_kmajor, epi_kind, bn);
+}
+
+template <bool S3>
+ng_status grouped_dispatch(cudaStream_t st, const TcGroup& grp, int tiles, bool a_kmajor, bool b_kmajor, int epi_kind,
+                           int bn) {
+#define NG_GRP(BN_, AK_, BK_, E_) return launch_grouped<BN_, AK_, BK_, E_, S3>(st, grp, tiles)
 #define NG_GRP_E(BN_, AK_, BK_)                                         \
   switch (epi_kind) {                                                  \
     case TC_EPI_STORE: NG_GRP(BN_, AK_, BK_, TC_EPI_STORE);            \
@@ -604,6 +679,12 @@ ng_status reduce_partials_2d(cudaStream_t st, float* C, int64_t ldc, const float
 extern "C" ng_status ng_debug_gemm_tf32(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda, int32_t a_kmajor,
                                         const float* B, int64_t ldb, int32_t b_kmajor, float* C, int64_t ldc,
                                         int32_t bn, int32_t splits, void* stream) {
+  return ng_debug_gemm_tc(M, N, K, A, lda, a_kmajor, B, ldb, b_kmajor, C, ldc, bn, splits, 0, stream);
+}
+
+extern "C" ng_status ng_debug_gemm_tc(int32_t M, int32_t N, int32_t K, const float* A, int64_t lda, int32_t a_kmajor,
+                                      const float* B, int64_t ldb, int32_t b_kmajor, float* C, int64_t ldc,
+                                      int32_t bn, int32_t splits, int32_t split3, void* stream) {
   using namespace ng;
   NG_REQUIRE(A && B && C, NG_EINVAL, "NULL argument");
   cudaStream_t st = (cudaStream_t)stream;
@@ -612,7 +693,7 @@ extern "C" ng_status ng_debug_gemm_tf32(int32_t M, int32_t N, int32_t K, const f
     e.kind = TC_EPI_STORE;
     e.C = C;
     e.ldc = ldc;
-    return tc_gemm_tf32(st, M, N, K, A, lda, a_kmajor != 0, B, ldb, b_kmajor != 0, e, bn, 1);
+    return tc_gemm_tf32(st, M, N, K, A, lda, a_kmajor != 0, B, ldb, b_kmajor != 0, e, bn, 1, nullptr, split3 != 0);
   }
   const int sp = tc_splits(K, splits);
   float* part = nullptr;
@@ -621,7 +702,7 @@ extern "C" ng_status ng_debug_gemm_tf32(int32_t M, int32_t N, int32_t K, const f
   e.C = part;
   e.ldc = N;
   e.zstride = (int64_t)M * N;
-  ng_status s = tc_gemm_tf32(st, M, N, K, A, lda, a_kmajor != 0, B, ldb, b_kmajor != 0, e, bn, sp);
+  ng_status s = tc_gemm_tf32(st, M, N, K, A, lda, a_kmajor != 0, B, ldb, b_kmajor != 0, e, bn, sp, nullptr, split3 != 0);
   if (s == NG_OK) s = reduce_partials_2d(st, C, ldc, part, M, N, sp);
   cudaFreeAsync(part, st);
   return s;

@@ -7,7 +7,9 @@
 //
 // Operands are FP32 in HBM and are consumed by the tensor core as TF32 (kind::tf32,
 // FP32 accumulation): no conversion pass and no shadow copies; the same FP32 buffers feed
-// the NG-SGD kernels.  This is the "TF32 tensor-core" precision mode.
+// the NG-SGD kernels.  split3 = 3xTF32: every landed stage is split in shared memory into
+// hi (TF32) + lo (the rest) and A_lo B_hi + A_hi B_lo + A_hi B_hi accumulate in TMEM --
+// FP32-grade products on the tensor cores at 3x the MMA work.
 #pragma once
 
 #include <cuda.h>
@@ -46,7 +48,7 @@ struct TcEpilogue {
 // *splits_used (may be smaller than requested).
 ng_status tc_gemm_tf32(cudaStream_t st, int M, int N, int K, const float* A, int64_t lda, bool a_kmajor,
                        const float* B, int64_t ldb, bool b_kmajor, const TcEpilogue& epi, int bn = 128,
-                       int splits = 1, int* splits_used = nullptr);
+                       int splits = 1, int* splits_used = nullptr, bool split3 = false);
 
 // ---- grouped launch: several independent problems (same majors / epilogue kind / BN)
 // in ONE kernel launch; each CTA finds its problem from the tile index.
@@ -73,13 +75,13 @@ struct TcGroup {
 };
 
 ng_status tc_gemm_tf32_grouped(cudaStream_t st, const TcGroupDesc* desc, int count, bool a_kmajor, bool b_kmajor,
-                               int epi_kind, int bn);
+                               int epi_kind, int bn, bool split3 = false);
 
 // Forward affine layer fused with the p-norm (G = 10): Z = Y W^T (both K-major,
 // Z row stride ldz) and Ynext = [pnorm(Z), 1, 0 ...] (row stride ldy >= N/10 + 1).  N must be
 // a multiple of 10.  80-column tiles (8 whole groups each).
 ng_status tc_gemm_tf32_pnorm(cudaStream_t st, int M, int N, int K, const float* A, int64_t lda, const float* B,
-                             int64_t ldb, float* Z, int64_t ldz, float* Ynext, int64_t ldy);
+                             int64_t ldb, float* Z, int64_t ldz, float* Ynext, int64_t ldy, bool split3 = false);
 
 // Split count actually used for a requested split count.
 int tc_splits(int K, int splits);

@@ -841,7 +841,7 @@ ng_status ngsgd_create_impl(int dim, int max_rows, const ngsgd_config* cfg, cuda
   NG_REQUIRE(dim >= 1 && max_rows >= 1, NG_ESHAPE, "dim and max_rows must be >= 1");
   NG_REQUIRE(cfg->rank >= 0 && cfg->alpha >= 0.f && cfg->s_samples > 0.f && cfg->update_period >= 1 &&
                  cfg->always_update_first >= 0 && cfg->epsilon > 0.f &&
-                 (cfg->precision == NG_FP32 || cfg->precision == NG_TF32),
+                 (cfg->precision == NG_FP32 || cfg->precision == NG_TF32 || cfg->precision == NG_FP32_SIMT),
              NG_EINVAL, "invalid ngsgd_config");
   NG_TRY(set_kernel_attrs());
   ngsgd_ctx* h = new ngsgd_ctx();
@@ -862,7 +862,7 @@ ng_status ngsgd_create_impl(int dim, int max_rows, const ngsgd_config* cfg, cuda
   h->kl_splits = std::max(1, std::min(32, ceil_div(dim, 256)));
   h->kl_splits = gemm_simt_splits(dim, h->kl_splits);
   int l_splits = std::max(h->kl_splits, gemm_simt_splits(max_rows, std::max(1, max_rows / 128)));
-  if (cfg->precision == NG_TF32) {   // split-K capacities of the tensor-core path
+  if (cfg->precision != NG_FP32_SIMT) {   // split-K capacities of the tensor-core path
     h->h_splits = std::max(h->h_splits, kTcMaxSplits);
     h->kl_splits = std::max(h->kl_splits, kTcMaxSplits);
     l_splits = std::max(l_splits, kTcMaxSplits);
@@ -1132,7 +1132,7 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
   float* W = h->W[h->cur];
   const double nRD = (double)n * R * D;
   // Tensor-core (TF32) projections when requested and the operands satisfy TMA alignment.
-  const bool tc = h->cfg.precision == NG_TF32 && (ld % 4) == 0 && (R % 4) == 0 &&
+  const bool tc = h->cfg.precision != NG_FP32_SIMT && (ld % 4) == 0 && (R % 4) == 0 &&
                   (reinterpret_cast<uintptr_t>(x) & 15) == 0;
   const int bnR = R <= 32 ? 32 : (R <= 64 ? 64 : 128);
   const int m_tiles = ceil_div(n, 128);
@@ -1144,7 +1144,7 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
       TcEpilogue e;
       e.kind = TC_EPI_PARTIAL; e.C = h->Hpart; e.ldc = R; e.zstride = (int64_t)n * R;
       const int want = std::min(kTcMaxSplits, std::max(1, 148 / (m_tiles * ceil_div(R, bnR))));
-      NG_TRY(tc_gemm_tf32(st, n, R, D, x, ld, true, W, h->ldw, true, e, bnR, want, &hs));
+      NG_TRY(tc_gemm_tf32(st, n, R, D, x, ld, true, W, h->ldw, true, e, bnR, want, &hs, true));
     } else {
       NG_TRY((gemm_simt<float, true, true>(st, n, R, D, x, ld, W, h->ldw,
                                            EpiStoreSplit<float>{h->Hpart, R, (int64_t)n * R}, h->h_splits)));
@@ -1162,7 +1162,7 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
       TcEpilogue e;
       e.kind = TC_EPI_PARTIAL; e.C = h->Hpart; e.ldc = h->ldw; e.zstride = (int64_t)R * h->ldw;
       int js = 1;
-      NG_TRY(tc_gemm_tf32(st, R, D, n, h->H, R, false, x, ld, false, e, 128, kTcJSplits, &js));
+      NG_TRY(tc_gemm_tf32(st, R, D, n, h->H, R, false, x, ld, false, e, 128, kTcJSplits, &js, true));
       reduce_rows_kernel<<<std::min(1024, ceil_div((int64_t)R * D, 256)), 256, 0, st>>>(
           h->J, h->ldw, h->Hpart, (int64_t)R * h->ldw, js, R, D);
       NG_TRY(check_launch("reduce_rows(J)"));
@@ -1208,7 +1208,7 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
     if (tc) {
       TcEpilogue e;
       e.kind = TC_EPI_NGAPPLY; e.C = x; e.ldc = ld; e.xx = h->xxpart; e.pp = h->ppart; e.part_ld = h->max_rows;
-      NG_TRY(tc_gemm_tf32(st, n, D, R, h->H, R, true, W, h->ldw, false, e, apply_bn(), 1));
+      NG_TRY(tc_gemm_tf32(st, n, D, R, h->H, R, true, W, h->ldw, false, e, apply_bn(), 1, nullptr, true));
       tiles = ceil_div(D, apply_bn());
     } else {
       dim3 grid(ceil_div(n, kApplyRows), ceil_div(D, kApplyCols));
@@ -1460,7 +1460,7 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
     NgCall& c = calls[i];
     ngsgd_ctx* h = c.h;
     NG_REQUIRE(h != nullptr && c.x != nullptr, NG_EINVAL, "NULL argument");
-    const bool eligible = h->initialized && h->rank > 0 && h->rank <= 128 && h->cfg.precision == NG_TF32 &&
+    const bool eligible = h->initialized && h->rank > 0 && h->rank <= 128 && h->cfg.precision != NG_FP32_SIMT &&
                           (c.ld % 4) == 0 && (h->rank % 4) == 0 && (reinterpret_cast<uintptr_t>(c.x) & 15) == 0 &&
                           c.n >= 1 && c.n <= h->max_rows && c.ld >= h->dim && (int)grp.size() < kTcGroupMax &&
                           (grp.empty() || h->st == st);
@@ -1499,7 +1499,7 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
       q.splits_used = &sp[g];
     }
     ProfScope ps(NG_PROF_NG_PROJ, st, flops, bytes);
-    NG_TRY(tc_gemm_tf32_grouped(st, d.data(), G, true, true, TC_EPI_PARTIAL, 128));
+    NG_TRY(tc_gemm_tf32_grouped(st, d.data(), G, true, true, TC_EPI_PARTIAL, 128, true));
     SegReduce sr;
     std::memset(&sr, 0, sizeof(sr));
     sr.count = G;
@@ -1531,7 +1531,7 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
       q.splits_used = &sp[u];
     }
     ProfScope ps(NG_PROF_NG_REFRESH, st, flops, bytes);
-    NG_TRY(tc_gemm_tf32_grouped(st, d.data(), (int)ug.size(), false, false, TC_EPI_PARTIAL, 128));
+    NG_TRY(tc_gemm_tf32_grouped(st, d.data(), (int)ug.size(), false, false, TC_EPI_PARTIAL, 128, true));
     SegReduce sr;
     std::memset(&sr, 0, sizeof(sr));
     sr.count = (int)ug.size();
@@ -1615,7 +1615,7 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
       fg.gamma_int[g] = h->gamma; fg.gamma_out[g] = c.gamma_out; fg.flags[g] = h->flags;
     }
     ProfScope ps(NG_PROF_NG_APPLY, st, flops, bytes);
-    NG_TRY(tc_gemm_tf32_grouped(st, d.data(), G, true, false, TC_EPI_NGAPPLY, apply_bn()));
+    NG_TRY(tc_gemm_tf32_grouped(st, d.data(), G, true, false, TC_EPI_NGAPPLY, apply_bn(), true));
     NG_CUDA_TRY(launch_pdl(finalize_group_kernel, dim3(G), dim3(512), 0, st, fg));
     NG_TRY(check_launch("finalize_group_kernel"));
   }

@@ -2,9 +2,11 @@
 // the every-K parameter average (section 3.1), on sm_100a.
 //
 //   forward:   Y_1 = [frames, 1];  Z_l = Y_l W_l^T;  Y_{l+1} = [pnorm(Z_l), 1]
-//              (P:281-283);  output log-softmax, objective, X_L = onehot - p
+//              (P:281-283), optionally renormalised to unit-RMS rows
+//              (R32);  output log-softmax, objective, X_L = onehot - p
 //
-//   backward:  g = X_l W_l[:, :D_in];  X_{l-1} = g[k/G] z_k / a_{k/G}
+//   backward:  g = X_l W_l[:, :D_in];  (renorm: g <- s (g - y y^T g / D));
+//              X_{l-1} = g[k/G] z_k / a_{k/G}
 //   update:    X_hat, gamma_x = NG_out(X_l); Y_hat, gamma_y = NG_in(Y_l);
 //              alpha_t = min(1, N max_change / (lr gamma_x gamma_y sum_i sqrt(p_i^x p_i^y)))
 //              (C.3);  W_l += alpha_t lr gamma_x gamma_y X_hat^T Y_hat
@@ -43,6 +45,7 @@ struct nnet_ctx {
   float* scale = nullptr;     // L: alpha_t lr gamma_x gamma_y
   float* stats = nullptr;     // L x 4: alpha_t, gamma_in, gamma_out, bound
   double* objrows = nullptr;  // max_minibatch
+  float* rscale = nullptr;    // (L-1) x max_minibatch: renormalisation scale s per hidden layer row
   double* obj = nullptr;      // 1
   int* eflags = nullptr;      // sticky error bits
   int n_last = 0;
@@ -136,6 +139,37 @@ pnorm_kernel(int n, int dout, int ldz, int G, const float* __restrict__ Z, float
   }
 }
 
+// Renormalisation layer after a p-norm layer (reading R32): row i of
+// Y[:, :D] is scaled in place by s_i = sqrt(D / ||a_i||^2) (0 for an all-zero row) and s_i
+// is kept for the backward pass.  One warp per row, 16-byte accesses when aligned, FP64
+// sum of squares.
+__global__ void __launch_bounds__(256)
+renorm_kernel(int n, int D, float* __restrict__ Y, int ldy, float* __restrict__ rs) {
+  pdl_trigger();
+  pdl_wait();   // launched with launch_pdl: Y comes from the previous kernel
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= n) return;
+  float* y = Y + (int64_t)r * ldy;
+  const bool vec = ((ldy & 3) == 0) && ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
+  const int d4 = vec ? (D >> 2) : 0;
+  double ss = 0.0;
+  for (int i = lane; i < d4; i += 32) {
+    const float4 v = reinterpret_cast<const float4*>(y)[i];
+    ss += (double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w;
+  }
+  for (int j = 4 * d4 + lane; j < D; j += 32) ss += (double)y[j] * y[j];
+  ss = warp_sum(ss);
+  const float s = ss > 0.0 ? (float)sqrt((double)D / ss) : 0.f;
+  for (int i = lane; i < d4; i += 32) {
+    float4 v = reinterpret_cast<const float4*>(y)[i];
+    v.x *= s; v.y *= s; v.z *= s; v.w *= s;
+    reinterpret_cast<float4*>(y)[i] = v;
+  }
+  for (int j = 4 * d4 + lane; j < D; j += 32) y[j] *= s;
+  if (lane == 0) rs[r] = s;
+}
+
 // log p(y|x) = z_y - logsumexp(z); X_L = onehot(y) - softmax(z); one CTA per row,
 // the row staged once in shared memory.
 __global__ void __launch_bounds__(256)
@@ -209,14 +243,35 @@ struct EpiPnormBack {
 // X_{l-1} = (g/a) z with 16-byte coalesced loads of Z and stores of X.
 __global__ void __launch_bounds__(256)
 pnorm_back_kernel(const float* __restrict__ part, int splits, int n, int din, const float* __restrict__ Zp,
-                  const float* __restrict__ Yl, float* __restrict__ Xp, int ldx, int ldy, int G) {
+                  const float* __restrict__ Yl, float* __restrict__ Xp, int ldx, int ldy, int G,
+                  const float* __restrict__ rs) {
   pdl_trigger();
   pdl_wait();   // launched with launch_pdl: inputs come from the previous kernel
   extern __shared__ __align__(16) unsigned char nn_smem[];
   float* ga = reinterpret_cast<float*>(nn_smem);
   const int r = blockIdx.x;
   const int64_t total = (int64_t)n * din;
-  if ((din & 3) == 0 && (total & 3) == 0 && splits <= 8) {
+  if (rs != nullptr) {
+    // renormalisation layer between: y = s a (R32).  g_a = s (g - y (y^T g) / D), then the
+    // p-norm derivative divides by a = y / s (0 where a = 0)
+    __shared__ double sc[32];
+    double dot = 0.0;
+    for (int j = threadIdx.x; j < din; j += blockDim.x) {
+      const int64_t i = (int64_t)r * din + j;
+      float g = 0.f;
+      for (int z = 0; z < splits; ++z) g += part[(int64_t)z * total + i];
+      ga[j] = g;
+      dot += (double)Yl[(int64_t)r * ldy + j] * g;
+    }
+    dot = block_sum(dot, sc);   // (contains the barrier that publishes ga)
+    const float s = rs[r];
+    const float yg = (float)(dot / (double)din);
+    for (int j = threadIdx.x; j < din; j += blockDim.x) {
+      const float y = Yl[(int64_t)r * ldy + j];
+      const float a = s > 0.f ? y / s : 0.f;
+      ga[j] = a > 0.f ? (s * (ga[j] - y * yg)) / a : 0.f;
+    }
+  } else if ((din & 3) == 0 && (total & 3) == 0 && splits <= 8) {
     // 16-byte loads of the split-K partials, all splits issued before the fixed-order sum
     const int d4 = din >> 2;
     for (int j4 = threadIdx.x; j4 < d4; j4 += blockDim.x) {
@@ -372,6 +427,7 @@ static void nnet_free(nnet_ctx* h) {
   if (h->scale) cudaFree(h->scale);
   if (h->stats) cudaFree(h->stats);
   if (h->objrows) cudaFree(h->objrows);
+  if (h->rscale) cudaFree(h->rscale);
   if (h->obj) cudaFree(h->obj);
   if (h->eflags) cudaFree(h->eflags);
   if (h->recvbuf) cudaFree(h->recvbuf);
@@ -404,8 +460,8 @@ ng_status nnet_create(const nnet_config* cfg, void* cuda_stream, nnet_t* out) {
   NG_REQUIRE(cfg->num_hidden == 0 || (cfg->pnorm_group >= 1 && cfg->hidden_dim >= cfg->pnorm_group &&
                                       cfg->hidden_dim % cfg->pnorm_group == 0),
              NG_ESHAPE, "hidden_dim must be a multiple of pnorm_group");
-  NG_REQUIRE(cfg->precision == NG_FP32 || cfg->precision == NG_TF32, NG_EINVAL,
-             "precision must be NG_FP32 or NG_TF32 (NG_BF16 is reserved)");
+  NG_REQUIRE(cfg->precision == NG_FP32 || cfg->precision == NG_TF32 || cfg->precision == NG_FP32_SIMT, NG_EINVAL,
+             "precision must be NG_FP32, NG_TF32 or NG_FP32_SIMT (NG_BF16 is reserved)");
   NG_REQUIRE(cfg->num_hidden + 1 <= 16, NG_EINVAL, "at most 16 weight matrices");
   NG_REQUIRE(cfg->hidden_dim <= kMaxRowWidth && cfg->num_classes <= kMaxRowWidth, NG_ESHAPE,
              "hidden_dim and num_classes must be <= 50000 (one row staged in shared memory)");
@@ -457,9 +513,10 @@ ng_status nnet_create(const nnet_config* cfg, void* cuda_stream, nnet_t* out) {
   if (s == NG_OK) s = nalloc(&h->scale, h->L);
   if (s == NG_OK) s = nalloc(&h->stats, 4 * h->L);
   if (s == NG_OK) s = nalloc(&h->objrows, N);
+  if (s == NG_OK && cfg->renorm) s = nalloc(&h->rscale, (size_t)std::max(1, h->L - 1) * N);
   if (s == NG_OK) s = nalloc(&h->obj, 1);
   if (s == NG_OK) s = nalloc(&h->eflags, 1);
-  if (s == NG_OK && cfg->precision == NG_TF32) {
+  if (s == NG_OK && (cfg->precision != NG_FP32_SIMT || cfg->renorm)) {
     size_t mx = 0;
     for (int l = 1; l < h->L; ++l) mx = std::max(mx, (size_t)kBwdSplits * N * (h->cols[l] - 1));
     h->gpart_count = mx;
@@ -529,7 +586,8 @@ ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const
   NG_REQUIRE(ld >= h->cfg.input_dim, NG_ESHAPE, "ld < input_dim");
   cudaStream_t st = h->st;
   const int L = h->L, G = h->cfg.pnorm_group;
-  const bool tc = h->cfg.precision == NG_TF32;
+  const bool tc = h->cfg.precision != NG_FP32_SIMT;   // tcgen05 (TF32, or 3xTF32 in NG_FP32)
+  const bool s3 = h->cfg.precision == NG_FP32;
   {
     const int64_t tot = (int64_t)n * h->ldp[0];
     NG_CUDA_TRY(launch_pdl(input_kernel, dim3(std::min(4096, ceil_div(tot, 256))), dim3(256), 0, st, n,
@@ -546,22 +604,26 @@ ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const
     if (fused) {
       // affine + p-norm in one tensor-core launch (80-column tiles = 8 whole groups)
       NG_TRY(tc_gemm_tf32_pnorm(st, n, h->rows[l], h->cols[l], h->Y[l], h->ldp[l], W, h->ldp[l], h->Z[l], h->ldr[l],
-                                h->Y[l + 1], h->ldp[l + 1]));
+                                h->Y[l + 1], h->ldp[l + 1], s3));
     } else if (tc) {
       TcEpilogue e;
       e.kind = TC_EPI_STORE; e.C = h->Z[l]; e.ldc = h->ldr[l];
       static const int bn = tune_int("NG_TUNE_FWD_BN", 128);
-      NG_TRY(tc_gemm_tf32(st, n, h->rows[l], h->cols[l], h->Y[l], h->ldp[l], true, W, h->ldp[l], true, e, bn, 1));
+      NG_TRY(tc_gemm_tf32(st, n, h->rows[l], h->cols[l], h->Y[l], h->ldp[l], true, W, h->ldp[l], true, e, bn, 1,
+                          nullptr, s3));
     } else {
       NG_TRY((gemm_simt<float, true, true>(st, n, h->rows[l], h->cols[l], h->Y[l], h->ldp[l], W, h->ldp[l],
                                            EpiStore<float>{h->Z[l], h->ldr[l], 1.f})));
     }
     if (l < L - 1 && !fused) {
-      const int64_t tot = (int64_t)n * h->ldp[l + 1];
-      (void)tot;
       pnorm_kernel<<<n, 256, sizeof(float) * h->rows[l], st>>>(n, h->rows[l], h->ldr[l], G, h->Z[l], h->Y[l + 1],
                                                                h->ldp[l + 1]);
       NG_TRY(check_launch("pnorm_kernel"));
+    }
+    if (l < L - 1 && h->cfg.renorm) {
+      NG_CUDA_TRY(launch_pdl(renorm_kernel, dim3(ceil_div(n, 8)), dim3(256), 0, st, n, h->cols[l + 1] - 1,
+                             h->Y[l + 1], h->ldp[l + 1], h->rscale + (size_t)l * h->cfg.max_minibatch));
+      NG_TRY(check_launch("renorm_kernel"));
     }
   }
   NG_CUDA_TRY(launch_pdl(softmax_kernel, dim3(n), dim3(256), sizeof(float) * h->rows[L - 1], st, n, h->rows[L - 1],
@@ -572,6 +634,7 @@ ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const
     const float* W = h->arena + h->off[l];
     EpiPnormBack epi{h->X[l - 1], h->Z[l - 1], h->Y[l], h->ldr[l - 1], h->ldp[l], G};
     const double R_ = h->rows[l], C_ = h->cols[l], Rp = h->rows[l - 1];
+    const float* rs = h->cfg.renorm ? h->rscale + (size_t)(l - 1) * h->cfg.max_minibatch : nullptr;
     ProfScope ps(NG_PROF_BWD_GEMM, st, 2.0 * n * R_ * (C_ - 1), 4.0 * (n * R_ + R_ * C_ + 2.0 * n * Rp + n * C_));
     if (tc) {
       const int din = h->cols[l] - 1;
@@ -581,12 +644,21 @@ ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const
       static const int bn = tune_int("NG_TUNE_BWD_BN", 128);   // measured +2% over 64 (tools/tune_sweep3.sh)
       static const int splits = std::min(kBwdSplits, std::max(1, tune_int("NG_TUNE_BWD_SPLITS", kBwdSplits)));
       NG_TRY(tc_gemm_tf32(st, n, din, h->rows[l], h->X[l], h->ldr[l], true, W, h->ldp[l], false, e, bn, splits,
-                          &sp));
+                          &sp, s3));
       const int64_t tot = (int64_t)n * din;
       (void)tot;
       NG_CUDA_TRY(launch_pdl(pnorm_back_kernel, dim3(n), dim3(256), sizeof(float) * din, st, (const float*)h->gpart, sp,
                              n, din, (const float*)h->Z[l - 1], (const float*)h->Y[l], h->X[l - 1], h->ldr[l - 1],
-                             h->ldp[l], G));
+                             h->ldp[l], G, rs));
+      NG_TRY(check_launch("pnorm_back_kernel"));
+    } else if (rs != nullptr) {
+      // FP32 with renormalisation: g to a buffer, then the renorm + p-norm backward per row
+      const int din = h->cols[l] - 1;
+      NG_TRY((gemm_simt<float, true, false>(st, n, din, h->rows[l], h->X[l], h->ldr[l], W, h->ldp[l],
+                                            EpiStore<float>{h->gpart, din, 1.f})));
+      NG_CUDA_TRY(launch_pdl(pnorm_back_kernel, dim3(n), dim3(256), sizeof(float) * din, st, (const float*)h->gpart, 1,
+                             n, din, (const float*)h->Z[l - 1], (const float*)h->Y[l], h->X[l - 1], h->ldr[l - 1],
+                             h->ldp[l], G, rs));
       NG_TRY(check_launch("pnorm_back_kernel"));
     } else {
       NG_TRY((gemm_simt<float, true, false>(st, n, h->cols[l] - 1, h->rows[l], h->X[l], h->ldr[l], W, h->ldp[l],
@@ -636,7 +708,8 @@ ng_status nnet_update(nnet_t h, float lr, float max_change_per_sample, nnet_upda
   NG_CUDA_TRY(launch_pdl(maxchange_kernel, dim3(L), dim3(256), 0, st, n, N, lr, max_change_per_sample,
                          (const float*)h->gam, (const float*)h->pbuf, h->scale, h->stats));
   NG_TRY(check_launch("maxchange_kernel"));
-  const bool tc = h->cfg.precision == NG_TF32;
+  const bool tc = h->cfg.precision != NG_FP32_SIMT;
+  const bool s3 = h->cfg.precision == NG_FP32;
   static const int upd_grouped = tune_int("NG_TUNE_UPD_GROUPED", 1);
   if (tc && upd_grouped && L <= kTcGroupMax) {
     // all L weight updates W_l += s_l X_l^T Y_l (eqn:add:w) in ONE tensor-core launch
@@ -655,7 +728,7 @@ ng_status nnet_update(nnet_t h, float lr, float max_change_per_sample, nnet_upda
     }
     static const int bn = tune_int("NG_TUNE_UPD_BN", 128);   // with BWD_BN 128: +3.7% (tools/tune_sweep3.sh)
     ProfScope ps(NG_PROF_UPD_GEMM, st, flops, bytes);
-    NG_TRY(tc_gemm_tf32_grouped(st, d.data(), L, false, false, TC_EPI_AXPY, bn));
+    NG_TRY(tc_gemm_tf32_grouped(st, d.data(), L, false, false, TC_EPI_AXPY, bn, s3));
   } else
   for (int l = 0; l < L; ++l) {
     float* W = h->arena + h->off[l];
@@ -666,7 +739,7 @@ ng_status nnet_update(nnet_t h, float lr, float max_change_per_sample, nnet_upda
       e.kind = TC_EPI_AXPY; e.C = W; e.ldc = h->ldp[l]; e.scale = h->scale + l;
       static const int bn = tune_int("NG_TUNE_UPD_BN", 128);   // with BWD_BN 128: +3.7% (tools/tune_sweep3.sh)
       NG_TRY(tc_gemm_tf32(st, h->rows[l], h->cols[l], n, h->X[l], h->ldr[l], false, h->Y[l], h->ldp[l], false, e, bn,
-                          1));
+                          1, nullptr, s3));
     } else {
       NG_TRY((gemm_simt<float, false, false>(st, h->rows[l], h->cols[l], n, h->X[l], h->ldr[l], h->Y[l], h->ldp[l],
                                              EpiAxpyDevScale{W, h->ldp[l], h->scale + l})));
