@@ -1,11 +1,11 @@
 // eig_tri.cuh -- dense symmetric eigendecomposition for the R x R refresh (eqn:zt:eig:repeat,
 // P:1382-1384): Z = U C U^T.  FP64, ONE CTA (1024 threads), n <= kTriMax.
 //
-//   1. Householder tridiagonalisation Z = Q T Q^T (LAPACK dsytd2 'L' order).  One CTA pass
-//      per column both applies the previous reflector's rank-2 update and forms the next
-//      product A_22 v; the same pass applies the previous reflector to Q and forms Q v, so Q
-//      is accumulated with no extra barriers.  Between passes one warp forms w, updates the
-//      next column and builds the next reflector.  2 barriers per column.
+//   1. Householder tridiagonalisation Z = Q T Q^T (LAPACK dsytd2 'L' order) with the
+//      trailing matrix resident in registers (tri_reduce_reg): one pass per column applies
+//      the previous reflector's rank-2 update and forms A_22 v; one warp then forms w, the
+//      next column and the next reflector.  2 barriers per column; the reflectors are kept
+//      and applied to the eigenvectors at the end (tri_backtransform_reg, barrier-free).
 //   2. T is split where an off-diagonal is negligible (relative to its diagonal neighbours,
 //      or to eps ||T||).  Each block gets a positive definite root representation
 //      L D L^T = T_b - sigma_b I (sigma_b = 0 when T_b factors with D > 0, which Z = Y Y^T
@@ -20,7 +20,8 @@
 //   3. Safety net: X X^T is formed and the solve reports failure when max |X X^T - I| >
 //      kTriOrthTol (tight relative clusters, noise-level eigenvalues of a numerically
 //      indefinite block); the caller then runs the cyclic Jacobi solver instead.
-//   4. The eigenvectors of Z are V = X Q^T (rows), an n x n x n FP64 product.
+//   4. The eigenvectors of Z are V = X Q^T (rows): the n-2 reflectors applied to the rows of
+//      X in registers.
 //
 // This replaces 8-13 Jacobi sweeps (79 barrier rounds each at R = 80) with ~2n barriers and
 // per-thread qd recurrences.  scratch/ prototypes: tools/tri_proto.py.
@@ -47,6 +48,7 @@ __device__ int g_tri_fail_n, g_tri_fail_count, g_tri_fail_why, g_tri_maxpos;   /
 // Shared-memory plan (offsets in doubles from a 16-byte aligned base), n <= kTriMax.
 struct TriPlan {
   int n, lda;
+  __host__ __device__ int ldq() const { return kTriMax; }   // reflector rows, zero-padded to 80
   size_t oA, oQ, oX, od, oe, oD, oL, oDL, oDL2, ogu, osig, olam, omu, ov, ow, opb, oqb, otau, ored, oint, total;
 };
 __host__ __device__ inline TriPlan tri_plan(int n) {
@@ -54,25 +56,26 @@ __host__ __device__ inline TriPlan tri_plan(int n) {
   p.n = n;
   p.lda = n + 1;   // odd row stride: column walks across lanes stay conflict-free
   size_t o = 0;
-  p.oA = o; o += (size_t)n * p.lda;   // Householder work; then per-eigenvalue qd scratch; then V
-  p.oQ = o; o += (size_t)n * p.lda;   // accumulated reflectors
-  p.oX = o; o += (size_t)n * p.lda;   // eigenvectors of T (rows)
-  p.od = o; o += n;                   // diag(T)
-  p.oe = o; o += n;                   // offdiag(T)
-  p.oD = o; o += n;                   // root representation D (per block)
-  p.oL = o; o += n;                   // root representation L
-  p.oDL = o; o += n;                  // D_i L_i
-  p.oDL2 = o; o += n;                 // D_i L_i^2
-  p.ogu = o; o += n;                  // Gershgorin upper bound of the block's L D L^T, per index
-  p.osig = o; o += n;                 // block shift sigma, per index
-  p.olam = o; o += n;                 // eigenvalues (index order, unscaled)
-  p.omu = o; o += n;                  // eigenvalues of the block representations
-  p.ov = o; o += 3 * (size_t)n;       // reflector vectors (triple buffer)
-  p.ow = o; o += 2 * (size_t)n;       // w vectors (double buffer)
-  p.opb = o; o += (size_t)kTriChunks * n;       // partial sums of A_22 v
-  p.oqb = o; o += 2 * (size_t)kTriChunks * n;   // partial sums of Q v (double buffer)
-  p.otau = o; o += 4;                 // tau (triple buffer)
-  p.ored = o; o += 64;
+  auto al = [&]() { o = (o + 1) & ~(size_t)1; };   // 16-byte aligned arrays
+  p.oA = o; o += (size_t)n * p.lda; al();   // Householder work; then per-eigenvalue qd scratch; then V
+  p.oQ = o; o += (size_t)n * p.ldq(); al();   // reflector rows v_k, zero-padded to kTriMax (16-byte rows)
+  p.oX = o; o += (size_t)n * p.lda; al();   // eigenvectors of T (rows)
+  p.od = o; o += n; al();                   // diag(T)
+  p.oe = o; o += n; al();                   // offdiag(T)
+  p.oD = o; o += n; al();                   // root representation D (per block)
+  p.oL = o; o += n; al();                   // root representation L
+  p.oDL = o; o += n; al();                  // D_i L_i
+  p.oDL2 = o; o += n; al();                 // D_i L_i^2
+  p.ogu = o; o += n; al();                  // Gershgorin upper bound of the block's L D L^T, per index
+  p.osig = o; o += n; al();                 // block shift sigma, per index
+  p.olam = o; o += n; al();                 // eigenvalues (index order, unscaled)
+  p.omu = o; o += n; al();                  // eigenvalues of the block representations
+  p.ov = o; o += 3 * (size_t)n; al();       // reflector vectors (triple buffer)
+  p.ow = o; o += 2 * (size_t)kTriMax; al();  // w vectors (double buffer, zero-padded to kTriMax)
+  p.opb = o; o += (size_t)kTriChunks * n; al();       // partial sums of A_22 v
+  p.oqb = o; o += 2 * (size_t)kTriChunks * n; al();   // partial sums of Q v (double buffer)
+  p.otau = o; o += kTriMax; al();           // tau_k of the kept reflectors
+  p.ored = o; o += 64; al();
   p.oint = o;   // ints: bstart[n], bend[n], crow[n], cpos[n], status[4], blo[kTriCoarseBlocks], coarse counts
   p.total = sizeof(double) * o + sizeof(int) * (4 * (size_t)n + 4 + kTriCoarseBlocks * (kTriCoarse + 1));
   return p;
@@ -117,28 +120,45 @@ __device__ __forceinline__ void tri_reflect(const double (&col)[3], int c, int n
   if (lane == 0) { d[c] = dc; e[c] = beta; *tau_out = tau; }
 }
 
-// Step 1: A (n x n symmetric, ld lda, scaled) -> d, e; Q = H_0 ... H_{n-3} accumulated.
-// Per column k, two barriers.  The pass (30 warps: 3 row groups x kTriChunks column chunks
-// for A_22 and the same for Q; lanes run over ROWS, so each thread walks a short run of
-// columns with no shuffles) applies update k-1 (rank 2) to A_22 and forms partial sums of
-// p = A_22 v_k, applies H_{k-1} to Q and forms partial sums of Q v_k.  Then warp 0 adds the
-// partials, forms w_k, the updated column k+1 and reflector k+1.
-__device__ __forceinline__ void tri_reduce(const TriPlan& P, double* __restrict__ sm) {
+// Register layout of tri_reduce_reg / tri_backtransform_reg: lane = 8a + b; thread (warp w,
+// a, b) owns row i = 4w + a (tri_reduce_reg: 4(w - 1) + a, warp 0 being the serial warp),
+// columns j = 10b .. 10b + 9 (n <= 80: 20 warps hold rows).
+// A row reduction is then a 3-level shuffle inside an 8-lane group, and every thread reads
+// its ten entries of a column vector with five 16-byte shared-memory loads.
+constexpr int kTrCols = 10;
+
+__device__ __forceinline__ double tr_rowsum(double x) {   // sum over the 8 lanes of a row group
+  x += __shfl_xor_sync(0xffffffffu, x, 1);
+  x += __shfl_xor_sync(0xffffffffu, x, 2);
+  x += __shfl_xor_sync(0xffffffffu, x, 4);
+  return x;
+}
+
+// Step 1 (register-resident): A (n x n symmetric, ld lda, scaled, in shared memory) ->
+// d, e; the reflectors are kept, not accumulated: v_k in row k of the Q region (v_k[i] at
+// Q[k kTriMax + i], v_k[k+1] = 1, zero elsewhere up to kTriMax), tau_k at taus[k].  The
+// trailing matrix lives in registers for the whole reduction (layout above), so it never
+// touches shared memory; every column vector is zero-padded to kTriMax so the pass is
+// branch-free 16-byte loads.  Per column k, ONE pass applies update k-1 (A -= v w^T + w v^T)
+// and forms p = A v_k, and the owner of column k+1 publishes it; then warp 0 (which holds
+// no rows) forms w_k = tau (p - (tau/2)(p.v) v), updates column k+1 by it and builds
+// reflector k+1.  Two barriers per column (LAPACK dsytd2 'L' order).
+__device__ __forceinline__ void tri_reduce_reg(const TriPlan& P, double* __restrict__ sm) {
   const int n = P.n, lda = P.lda, tid = threadIdx.x, nt = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  double* A = sm + P.oA;
-  double* Q = sm + P.oQ;
+  constexpr int ldq = kTriMax;
+  const int lane = tid & 31, warp = tid >> 5, ra = lane >> 3, cb = lane & 7;
+  // warp 0 runs the serial part and holds no rows (its registers go to the reflector)
+  const int row = 4 * (warp - 1) + ra, j0 = kTrCols * cb;
+  const bool rwarp = warp >= 1 && 4 * (warp - 1) < n;
+  const double* A = sm + P.oA;
+  double* Q = sm + P.oQ;        // reflector rows
+  double* taus = sm + P.otau;
   double* d = sm + P.od;
   double* e = sm + P.oe;
-  double* vb = sm + P.ov;       // v by parity of the reflector index
   double* wb = sm + P.ow;       // w by parity
-  double* pA = sm + P.opb;      // [kTriChunks][n] partial sums of A_22 v
-  double* pQ = sm + P.oqb;      // [2][kTriChunks][n] partial sums of Q v (parity)
-  double* tauv = sm + P.otau;
-  for (int idx = tid; idx < n * n; idx += nt) {
-    const int i = idx / n, j = idx - i * n;
-    Q[i * lda + j] = (i == j) ? 1.0 : 0.0;
-  }
+  double* pA = sm + P.opb;      // p = A_22 v_k
+  double* colb = sm + P.oqb;    // column k+1 after updates 0..k-1
+  double* ann = sm + P.ored;    // A[n-1][n-1] after updates 0..k-1
   if (n <= 2) {
     if (tid == 0) {
       d[0] = A[0];
@@ -147,6 +167,13 @@ __device__ __forceinline__ void tri_reduce(const TriPlan& P, double* __restrict_
     __syncthreads();
     return;
   }
+  for (int i = tid; i < n * ldq; i += nt) Q[i] = 0.0;
+  for (int i = tid; i < 2 * ldq; i += nt) wb[i] = 0.0;
+  const bool own = rwarp && row < n;
+  double M[kTrCols];
+#pragma unroll
+  for (int g = 0; g < kTrCols; ++g) M[g] = (own && j0 + g < n) ? A[row * lda + j0 + g] : 0.0;
+  __syncthreads();
   if (warp == 0) {
     double col[3];
 #pragma unroll
@@ -154,90 +181,63 @@ __device__ __forceinline__ void tri_reduce(const TriPlan& P, double* __restrict_
       const int i = lane + 32 * q;
       col[q] = (i < n) ? A[i * lda] : 0.0;
     }
-    tri_reflect(col, 0, n, vb, tauv, d, e, lane);
+    tri_reflect(col, 0, n, Q, taus, d, e, lane);
   }
   __syncthreads();
-  // warps 0-14: A_22 (3 row groups x kTriChunks column chunks); warps 15-29: Q (same split);
-  // warps 30-31 idle.  The Q warps only need v_k, v_{k-1}, tau_{k-1} and Q v_{k-1}, all
-  // known when step k starts, so they run while warp 0 forms reflector k+1 (named barrier 1
-  // joins only the A warps before it; barrier 0 closes the step for everyone).
-  const bool qwarp = warp >= 3 * kTriChunks;
-  const int wl = qwarp ? warp - 3 * kTriChunks : warp;
-  const int rg = wl % 3, ch = wl / 3;
-  unsigned t_pass = 0, t_ser = 0, t0 = clock();
   for (int k = 0; k + 2 < n; ++k) {
     const int cur = k & 1, prv = cur ^ 1;
-    const int k3 = k % 3, p3 = (k + 2) % 3;
-    const double* v = vb + k3 * n;
-    const double* vp = vb + p3 * n;
-    const double* wp = wb + prv * n;
-    if (!qwarp) {
-      const int m = n - k - 1, L = (m + kTriChunks - 1) / kTriChunks;
-      const int i = k + 1 + 32 * rg + lane;
-      const int j0 = k + 1 + ch * L, j1 = min(n, j0 + L);
-      if (i < n) {
-        double acc = 0.0;
-        double* Ai = A + i * lda;
-        if (k > 0) {
-          const double vpi = vp[i], wpi = wp[i];
-#pragma unroll 4
-          for (int j = j0; j < j1; ++j) {
-            const double a = fma(-vpi, wp[j], fma(-wpi, vp[j], Ai[j]));
-            Ai[j] = a;
-            acc = fma(a, v[j], acc);
-          }
-        } else {
-#pragma unroll 4
-          for (int j = j0; j < j1; ++j) acc = fma(Ai[j], v[j], acc);
-        }
-        pA[ch * n + i] = acc;
-      }
-      asm volatile("bar.sync 1, %0;" ::"r"(3 * kTriChunks * 32) : "memory");
-    } else if (ch < kTriChunks) {
-      const int L = (n - k + kTriChunks - 1) / kTriChunks;
-      const int r = 32 * rg + lane;
-      const int j0 = k + ch * L, j1 = min(n, j0 + L);   // H_{k-1} acts on columns k..n-1
-      if (r < n) {
-        double acc = 0.0;
-        double* Qr = Q + r * lda;
-        if (k > 0) {
-          double qv = 0.0;
+    const double* v = Q + k * ldq;
+    if (rwarp) {   // warp-uniform: the row-group shuffles need every lane of the warp
+      // column vectors streamed from shared memory two entries at a time (holding them
+      // would need 60 more registers than a 1024-thread CTA allows)
+      const double2* v2 = reinterpret_cast<const double2*>(v + j0);
+      const double2* vp2 = reinterpret_cast<const double2*>(Q + (k > 0 ? k - 1 : 0) * ldq + j0);
+      const double2* wp2 = reinterpret_cast<const double2*>(wb + prv * ldq + j0);
+      // (at k = 0 both w buffers are still zero, so the update is a no-op)
+      const double vr = own ? Q[(k > 0 ? k - 1 : 0) * ldq + row] : 0.0;
+      const double wr = own ? wb[prv * ldq + row] : 0.0;
+      double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
-          for (int c2 = 0; c2 < kTriChunks; ++c2) qv += pQ[(prv * kTriChunks + c2) * n + r];
-          const double sq = tauv[p3] * qv;
-#pragma unroll 4
-          for (int j = j0; j < j1; ++j) {
-            const double x = fma(-sq, vp[j], Qr[j]);
-            Qr[j] = x;
-            acc = fma(x, v[j], acc);   // v_k[k] = 0: column k adds nothing
-          }
-        } else {
-#pragma unroll 4
-          for (int j = j0; j < j1; ++j) acc = fma(Qr[j], v[j], acc);
-        }
-        pQ[(cur * kTriChunks + ch) * n + r] = acc;
+      for (int q = 0; q < kTrCols / 2; ++q) {
+        const double2 x = v2[q], y = vp2[q], z = wp2[q];
+        M[2 * q] = fma(-vr, z.x, fma(-wr, y.x, M[2 * q]));
+        M[2 * q + 1] = fma(-vr, z.y, fma(-wr, y.y, M[2 * q + 1]));
+        acc0 = fma(M[2 * q], x.x, acc0);
+        acc1 = fma(M[2 * q + 1], x.y, acc1);
+      }
+      const double acc = tr_rowsum(acc0 + acc1);
+      if (own && cb == 0) pA[row] = acc;
+      // publish column k+1 (slot selected with compile-time indices: a runtime M[g] would
+      // move M to local memory) and A[n-1][n-1]
+      const int c = k + 1;
+      if (own && c / kTrCols == cb) {
+        double x = 0.0;
+#pragma unroll
+        for (int g = 0; g < kTrCols; ++g) if (j0 + g == c) x = M[g];
+        colb[row] = x;
+      }
+      if (row == n - 1 && (n - 1) / kTrCols == cb) {
+        double x = 0.0;
+#pragma unroll
+        for (int g = 0; g < kTrCols; ++g) if (j0 + g == n - 1) x = M[g];
+        *ann = x;
       }
     }
-    if (warp == 0) { const unsigned t1 = clock(); t_pass += t1 - t0; t0 = t1; }
+    __syncthreads();
     if (warp == 0) {
       // w_k = tau (p - (tau/2)(p.v) v), column c = k+1 after update k, reflector c
       const int c = k + 1;
-      const double tau = tauv[k3];
+      const double tau = taus[k];
       double pr[3], vr[3], w[3], col[3];
       double dot = 0.0;
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         const int i = lane + 32 * q;
         const bool in = i >= c && i < n;
-        double s = 0.0;
-        if (in) {
-#pragma unroll
-          for (int c2 = 0; c2 < kTriChunks; ++c2) s += pA[c2 * n + i];
-        }
-        pr[q] = s;
+        pr[q] = in ? pA[i] : 0.0;
         vr[q] = in ? v[i] : 0.0;
-        col[q] = in ? A[i * lda + c] : 0.0;
-        dot = fma(s, vr[q], dot);
+        col[q] = in ? colb[i] : 0.0;
+        dot = fma(pr[q], vr[q], dot);
       }
       dot = warp_sum(dot);
       const double hk = 0.5 * tau * dot;
@@ -245,13 +245,13 @@ __device__ __forceinline__ void tri_reduce(const TriPlan& P, double* __restrict_
       for (int q = 0; q < 3; ++q) {
         w[q] = tau * fma(-hk, vr[q], pr[q]);
         const int i = lane + 32 * q;
-        if (i < n) wb[cur * n + i] = w[q];
+        if (i < n) wb[cur * ldq + i] = w[q];
       }
       const double vc = tri_bcast(vr, c), wc = tri_bcast(w, c);
 #pragma unroll
       for (int q = 0; q < 3; ++q) col[q] = fma(-vr[q], wc, fma(-w[q], vc, col[q]));
       if (c + 2 < n) {
-        tri_reflect(col, c, n, vb + ((k + 1) % 3) * n, tauv + (k + 1) % 3, d, e, lane);
+        tri_reflect(col, c, n, Q + c * ldq, taus + c, d, e, lane);
       } else {
         const int l = n - 1;
         const double dc = tri_bcast(col, c), el = tri_bcast(col, l);
@@ -259,27 +259,51 @@ __device__ __forceinline__ void tri_reduce(const TriPlan& P, double* __restrict_
         if (lane == 0) {
           d[c] = dc;
           e[c] = el;
-          d[l] = fma(-2.0 * vl, wl, A[l * lda + l]);
+          d[l] = fma(-2.0 * vl, wl, *ann);
         }
       }
     }
     __syncthreads();
-    if (warp == 0) { const unsigned t1 = clock(); t_ser += t1 - t0; t0 = t1; }
   }
-  if (tid == 0) { g_tri_clk[6] = t_pass; g_tri_clk[7] = t_ser; }
-  // the last reflector (n-3) on Q columns n-2, n-1
-  {
-    const int k = n - 3, cur = k & 1;
-    const double* v = vb + (k % 3) * n;
-    for (int idx = tid; idx < 2 * n; idx += nt) {
-      const int r = idx >> 1, j = n - 2 + (idx & 1);
-      double qv = 0.0;
+}
+
+// V = X Q^T with Q = H_0 H_1 ... H_{n-3} (the reflectors tri_reduce_reg keeps): row i of
+// V is the i-th eigenvector of Z.  Rows of X in registers (layout above); V <- V H_k for
+// k = n-3 .. 0.  Every row reduction stays inside an 8-lane group: no barrier at all.
+// Writes V into `out` (ld lda).
+__device__ __forceinline__ void tri_backtransform_reg(const TriPlan& P, const double* __restrict__ sm,
+                                                      const double* __restrict__ X, double* __restrict__ out) {
+  const int n = P.n, lda = P.lda, tid = threadIdx.x;
+  constexpr int ldq = kTriMax;
+  const int lane = tid & 31, warp = tid >> 5, ra = lane >> 3, cb = lane & 7;
+  const int row = 4 * warp + ra, j0 = kTrCols * cb;
+  const double* Q = sm + P.oQ;
+  const double* taus = sm + P.otau;
+  if (4 * warp >= n) return;   // warp-uniform: the row-group shuffles need every lane
+  const bool own = row < n;
+  double M[kTrCols];
 #pragma unroll
-      for (int c2 = 0; c2 < kTriChunks; ++c2) qv += pQ[(cur * kTriChunks + c2) * n + r];
-      Q[r * lda + j] = fma(-tauv[k % 3] * qv, v[j], Q[r * lda + j]);
+  for (int g = 0; g < kTrCols; ++g) M[g] = (own && j0 + g < n) ? X[row * lda + j0 + g] : 0.0;
+  for (int k = n - 3; k >= 0; --k) {
+    const double2* v2 = reinterpret_cast<const double2*>(Q + k * ldq + j0);
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < kTrCols / 2; ++q) {
+      const double2 x = v2[q];
+      s0 = fma(M[2 * q], x.x, s0);
+      s1 = fma(M[2 * q + 1], x.y, s1);
+    }
+    const double s = -taus[k] * tr_rowsum(s0 + s1);
+#pragma unroll
+    for (int q = 0; q < kTrCols / 2; ++q) {
+      const double2 x = v2[q];
+      M[2 * q] = fma(s, x.x, M[2 * q]);
+      M[2 * q + 1] = fma(s, x.y, M[2 * q + 1]);
     }
   }
-  __syncthreads();
+#pragma unroll
+  for (int g = 0; g < kTrCols; ++g)
+    if (own && j0 + g < n) out[row * lda + j0 + g] = M[g];
 }
 
 // Reciprocal from MUFU.RCP64H plus one Newton step (relative error ~2^-44): the negcount
@@ -472,7 +496,7 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
   }
   __syncthreads();
   if (tid == 0) g_tri_clk[0] = clock64();
-  tri_reduce(P, sm);
+  tri_reduce_reg(P, sm);
   if (tid == 0) g_tri_clk[1] = clock64();
   // ||T|| and the split
   double tn = 0.0;
@@ -758,7 +782,7 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
   if (tid == 0) g_tri_clk[3] = clock64();
   if (!(dev <= kTriOrthTol)) { if (tid == 0) g_tri_fail_why = 3; return 0; }
   // V = X Q^T (rows = eigenvectors of Z), into the A region
-  tri_gemm_nt(X, sm + P.oQ, n, lda, A, lda, false, red);
+  tri_backtransform_reg(P, sm, X, A);
   __syncthreads();
   if (tid == 0) g_tri_clk[4] = clock64();
   return 1;
