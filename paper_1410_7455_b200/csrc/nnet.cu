@@ -253,21 +253,42 @@ pnorm_back_kernel(const float* __restrict__ part, int splits, int n, int din, co
   const int64_t total = (int64_t)n * din;
   if (rs != nullptr) {
     // renormalisation layer between: y = s a (R32).  g_a = s (g - y (y^T g) / D), then the
-    // p-norm derivative divides by a = y / s (0 where a = 0)
+    // p-norm derivative divides by a = y / s (0 where a = 0).  g (the fixed-order sum of
+    // the split-K partials) is staged in shared memory with 16-byte loads, y^T g reduced in
+    // FP64.
     __shared__ double sc[32];
     double dot = 0.0;
-    for (int j = threadIdx.x; j < din; j += blockDim.x) {
-      const int64_t i = (int64_t)r * din + j;
-      float g = 0.f;
-      for (int z = 0; z < splits; ++z) g += part[(int64_t)z * total + i];
-      ga[j] = g;
-      dot += (double)Yl[(int64_t)r * ldy + j] * g;
+    const float* yrow = Yl + (int64_t)r * ldy;
+    if ((din & 3) == 0 && (total & 3) == 0 && (ldy & 3) == 0 && splits <= 8) {
+      const int d4 = din >> 2;
+      for (int j4 = threadIdx.x; j4 < d4; j4 += blockDim.x) {
+        const int64_t i4 = ((int64_t)r * din >> 2) + j4;
+        float4 pv[8];
+#pragma unroll
+        for (int z = 0; z < 8; ++z)
+          if (z < splits) pv[z] = __ldg(reinterpret_cast<const float4*>(part + (int64_t)z * total) + i4);
+        float4 g = pv[0];
+#pragma unroll
+        for (int z = 1; z < 8; ++z)
+          if (z < splits) { g.x += pv[z].x; g.y += pv[z].y; g.z += pv[z].z; g.w += pv[z].w; }
+        reinterpret_cast<float4*>(ga)[j4] = g;
+        const float4 y = __ldg(reinterpret_cast<const float4*>(yrow) + j4);
+        dot += (double)y.x * g.x + (double)y.y * g.y + (double)y.z * g.z + (double)y.w * g.w;
+      }
+    } else {
+      for (int j = threadIdx.x; j < din; j += blockDim.x) {
+        const int64_t i = (int64_t)r * din + j;
+        float g = 0.f;
+        for (int z = 0; z < splits; ++z) g += part[(int64_t)z * total + i];
+        ga[j] = g;
+        dot += (double)yrow[j] * g;
+      }
     }
     dot = block_sum(dot, sc);   // (contains the barrier that publishes ga)
     const float s = rs[r];
     const float yg = (float)(dot / (double)din);
     for (int j = threadIdx.x; j < din; j += blockDim.x) {
-      const float y = Yl[(int64_t)r * ldy + j];
+      const float y = yrow[j];
       const float a = s > 0.f ? y / s : 0.f;
       ga[j] = a > 0.f ? (s * (ga[j] - y * yg)) / a : 0.f;
     }

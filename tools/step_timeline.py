@@ -9,7 +9,7 @@ N = 512
 frames, labels = spliced_frames(1410, 64 * N, num_classes=5000)
 f = torch.from_numpy(frames).cuda(); y = torch.from_numpy(labels).cuda()
 net = api.Nnet(360, 4, 3000, 10, 5000, max_minibatch=N, precond=True, rank_in=20, rank_out=80,
-               precision=os.environ.get("NG_PREC", "tf32"), seed=1410)
+               precision=os.environ.get("NG_PREC", "tf32"), seed=1410, renorm=True)
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 40
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
 mid = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
@@ -18,7 +18,7 @@ for k in range(steps):
     ev[k].record()
     net.forward_backward(f[i * N:(i + 1) * N], y[i * N:(i + 1) * N])
     mid[k].record()
-    net.update(0.01 / 6, 0.075)
+    net.update(0.01 / 6 / 8, 0.075)
 ev[steps].record()
 torch.cuda.synchronize()
 for k in range(steps):
