@@ -1166,18 +1166,21 @@ ng_status ngsgd_precondition_impl(ngsgd_ctx* h, int n, float* x, int64_t ld, flo
       reduce_rows_kernel<<<std::min(1024, ceil_div((int64_t)R * D, 256)), 256, 0, st>>>(
           h->J, h->ldw, h->Hpart, (int64_t)R * h->ldw, js, R, D);
       NG_TRY(check_launch("reduce_rows(J)"));
-      // K = J J^T and L = W J^T stay FP32 (CUDA cores): Z_t must equal Y_t Y_t^T for the
+      // K = J J^T and L = W J^T in 3xTF32 (FP32-grade): Z_t must equal Y_t Y_t^T for the
       // STORED J to FP32 accuracy, otherwise R_{t+1} = C^{-1/2} U^T Y_t loses orthonormality
       // at the TF32 level (1e-3) and B.3.1 repairs fire.  L = W J^T is used for every N
       // (it equals H^T H only when J = H^T X exactly).
-      const int ks = gemm_simt_splits(D, h->kl_splits);
-      NG_TRY((gemm_simt<float, true, true>(st, R, R, D, h->J, h->ldw, h->J, h->ldw,
-                                           EpiStoreSplit<float>{h->Kpart, R, (int64_t)R * R}, ks)));
+      const int want = std::max(1, std::min(kTcMaxSplits, 64));
+      int ks = 1, ls = 1;
+      TcEpilogue ek;
+      ek.kind = TC_EPI_PARTIAL; ek.C = h->Kpart; ek.ldc = R; ek.zstride = (int64_t)R * R;
+      NG_TRY(tc_gemm_tf32(st, R, R, D, h->J, h->ldw, true, h->J, h->ldw, true, ek, 128, want, &ks, true));
       reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->KL, h->Kpart, R * R, ks, R * R, nullptr);
       NG_TRY(check_launch("reduce_splits(K)"));
-      NG_TRY((gemm_simt<float, true, true>(st, R, R, D, W, h->ldw, h->J, h->ldw,
-                                           EpiStoreSplit<float>{h->Lpart, R, (int64_t)R * R}, ks)));
-      reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->KL + R * R, h->Lpart, R * R, ks, R * R, nullptr);
+      TcEpilogue el = ek;
+      el.C = h->Lpart;
+      NG_TRY(tc_gemm_tf32(st, R, R, D, W, h->ldw, true, h->J, h->ldw, true, el, 128, want, &ls, true));
+      reduce_splits_kernel<<<ceil_div(R * R, 256), 256, 0, st>>>(h->KL + R * R, h->Lpart, R * R, ls, R * R, nullptr);
       NG_TRY(check_launch("reduce_splits(L)"));
     } else {
       // J = H^T X -- before X is overwritten
@@ -1351,105 +1354,7 @@ static ng_status launch_seg_reduce(cudaStream_t st, SegReduce& sr) {
   return check_launch("seg_reduce_kernel");
 }
 
-// ---- K_t = J J^T and L_t = W J^T of every updating state in one launch.
-// One CTA = the whole R x R product over one 64-wide chunk of the D axis (FP32 FMA, the
-// chunk's partial written to part[chunk]); the fixed-order segmented reduction sums the
-// chunks.  FP32 in both precision modes (the refresh needs them accurate).
-constexpr int kRRMax = 32, kRRChunk = 64, kRRSub = 64;
-struct RRProb {
-  const float* A;
-  const float* B;
-  float* part;
-  int64_t lda, ldb, zstride;
-  int R, D, tile_begin, pad_;
-};
-struct RRGroup {
-  RRProb p[kRRMax];
-  int count;
-};
-
-template <int TM>
-__global__ void __launch_bounds__(256) rr_gemm_kernel(const __grid_constant__ RRGroup grp) {
-  constexpr int SUB = TM <= 5 ? kRRSub : kRRSub / 2;   // static shared memory <= 48 KB
-  __shared__ float As[SUB][16 * TM + 1];
-  __shared__ float Bs[SUB][16 * TM + 1];
-  int g = 0;
-  while (g + 1 < grp.count && (int)blockIdx.x >= grp.p[g + 1].tile_begin) ++g;
-  const RRProb& P = grp.p[g];
-  const int chunk = (int)blockIdx.x - P.tile_begin;
-  const int R = P.R, k0 = chunk * kRRChunk, k1 = min(P.D, k0 + kRRChunk);
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  float acc[TM][TM];
-#pragma unroll
-  for (int i = 0; i < TM; ++i)
-#pragma unroll
-    for (int j = 0; j < TM; ++j) acc[i][j] = 0.f;
-  for (int kb = k0; kb < k1; kb += SUB) {
-    const int kn = min(SUB, k1 - kb);
-    for (int idx = threadIdx.x; idx < 16 * TM * SUB; idx += 256) {
-      const int i = idx / SUB, k = idx - (idx / SUB) * SUB;
-      const bool ok = i < R && k < kn;
-      As[k][i] = ok ? __ldg(P.A + (int64_t)i * P.lda + kb + k) : 0.f;
-      Bs[k][i] = ok ? __ldg(P.B + (int64_t)i * P.ldb + kb + k) : 0.f;
-    }
-    __syncthreads();
-    for (int k = 0; k < kn; ++k) {
-      float a[TM], b[TM];
-#pragma unroll
-      for (int t = 0; t < TM; ++t) { a[t] = As[k][ty * TM + t]; b[t] = Bs[k][tx * TM + t]; }
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TM; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-    }
-    __syncthreads();
-  }
-  float* out = P.part + (int64_t)chunk * P.zstride;
-#pragma unroll
-  for (int i = 0; i < TM; ++i)
-#pragma unroll
-    for (int j = 0; j < TM; ++j) {
-      const int r = ty * TM + i, c = tx * TM + j;
-      if (r < R && c < R) out[r * R + c] = acc[i][j];
-    }
-}
-
-int rr_chunks(int D) { return ceil_div(D, kRRChunk); }
-
-// K and L partials of the states `which` (indices into grp), all with rank <= 16 TM.
-template <int TM>
-static ng_status launch_rr(cudaStream_t st, NgCall* calls, const std::vector<int>& grp, const std::vector<int>& which) {
-  RRGroup gr;
-  std::memset(&gr, 0, sizeof(gr));
-  int tiles = 0;
-  auto flush = [&]() -> ng_status {
-    if (gr.count == 0) return NG_OK;
-    rr_gemm_kernel<TM><<<tiles, 256, 0, st>>>(gr);
-    NG_TRY(check_launch("rr_gemm_kernel"));
-    std::memset(&gr, 0, sizeof(gr));
-    tiles = 0;
-    return NG_OK;
-  };
-  for (int g : which) {
-    ngsgd_ctx* h = calls[grp[g]].h;
-    const int R = h->rank, D = h->dim, nc = rr_chunks(D);
-    for (int w = 0; w < 2; ++w) {
-      if (gr.count == kRRMax) NG_TRY(flush());
-      RRProb& q = gr.p[gr.count++];
-      q.A = w ? h->W[h->cur] : h->J;
-      q.B = h->J;
-      q.lda = h->ldw;
-      q.ldb = h->ldw;
-      q.part = w ? h->Lpart : h->Kpart;
-      q.zstride = (int64_t)R * R;
-      q.R = R;
-      q.D = D;
-      q.tile_begin = tiles;
-      tiles += nc;
-    }
-  }
-  return flush();
-}
+int rr_chunks(int D) { return ceil_div(D, 64); }   // split capacity of the K / L partial buffers
 
 ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
   NG_REQUIRE(calls != nullptr && count >= 0, NG_EINVAL, "NULL argument");
@@ -1541,30 +1446,48 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
       sr.zstride[u] = (int64_t)h->rank * h->ldw; sr.rows[u] = h->rank; sr.cols[u] = h->dim; sr.splits[u] = sp[u];
     }
     NG_TRY(launch_seg_reduce(st, sr));
+    // K = J J^T and L = W J^T of every updating state: one grouped 3xTF32
+    // tensor-core launch per 16 problems (FP32-grade: Z_t must equal Y_t Y_t^T for the
+    // stored J to FP32 accuracy), split over D, then the fixed-order segmented reduction
     {
-      std::vector<int> small, mid, big;   // by micro-tile: R <= 32, <= 80, <= 128
-      for (int g : ug) {
-        const int R = calls[grp[g]].h->rank;
-        (R <= 32 ? small : (R <= 80 ? mid : big)).push_back(g);
+      std::vector<TcGroupDesc> d;
+      std::vector<int> spk(2 * ug.size());
+      const int nprob = 2 * (int)ug.size();
+      const int want = std::max(1, std::min(kTcMaxSplits, ceil_div(2 * 148, nprob)));
+      for (size_t u = 0; u < ug.size(); ++u) {
+        ngsgd_ctx* h = calls[grp[ug[u]]].h;
+        const int R = h->rank, D = h->dim;
+        for (int w = 0; w < 2; ++w) {
+          TcGroupDesc q;
+          std::memset(&q, 0, sizeof(q));
+          q.M = R; q.N = R; q.K = D; q.splits = want;
+          q.A = w ? h->W[h->cur] : h->J; q.lda = h->ldw;
+          q.B = h->J; q.ldb = h->ldw;
+          q.epi.kind = TC_EPI_PARTIAL; q.epi.C = w ? h->Lpart : h->Kpart; q.epi.ldc = R;
+          q.epi.zstride = (int64_t)R * R;
+          q.splits_used = &spk[2 * u + w];
+          d.push_back(q);
+        }
       }
-      if (!small.empty()) NG_TRY(launch_rr<2>(st, calls, grp, small));
-      if (!mid.empty()) NG_TRY(launch_rr<5>(st, calls, grp, mid));
-      if (!big.empty()) NG_TRY(launch_rr<8>(st, calls, grp, big));
-    }
-    SegReduce kl;
-    std::memset(&kl, 0, sizeof(kl));
-    kl.count = 0;
-    for (int g : ug) {
-      ngsgd_ctx* h = calls[grp[g]].h;
-      const int R = h->rank, ks = rr_chunks(h->dim);
-      for (int w = 0; w < 2; ++w) {
-        if (kl.count == kSegMax) { NG_TRY(launch_seg_reduce(st, kl)); kl.count = 0; }
-        const int k = kl.count++;
-        kl.out[k] = h->KL + w * R * R; kl.src[k] = w ? h->Lpart : h->Kpart; kl.ldo[k] = R; kl.lds[k] = R;
-        kl.zstride[k] = (int64_t)R * R; kl.rows[k] = R; kl.cols[k] = R; kl.splits[k] = ks;
+      for (size_t b = 0; b < d.size(); b += kTcGroupMax) {
+        const int cnt = (int)std::min<size_t>(kTcGroupMax, d.size() - b);
+        NG_TRY(tc_gemm_tf32_grouped(st, d.data() + b, cnt, true, true, TC_EPI_PARTIAL, 128, true));
       }
+      SegReduce kl;
+      std::memset(&kl, 0, sizeof(kl));
+      kl.count = 0;
+      for (size_t u = 0; u < ug.size(); ++u) {
+        ngsgd_ctx* h = calls[grp[ug[u]]].h;
+        const int R = h->rank;
+        for (int w = 0; w < 2; ++w) {
+          if (kl.count == kSegMax) { NG_TRY(launch_seg_reduce(st, kl)); kl.count = 0; }
+          const int k = kl.count++;
+          kl.out[k] = h->KL + w * R * R; kl.src[k] = w ? h->Lpart : h->Kpart; kl.ldo[k] = R; kl.lds[k] = R;
+          kl.zstride[k] = (int64_t)R * R; kl.rows[k] = R; kl.cols[k] = R; kl.splits[k] = spk[2 * u + w];
+        }
+      }
+      if (kl.count) NG_TRY(launch_seg_reduce(st, kl));
     }
-    if (kl.count) NG_TRY(launch_seg_reduce(st, kl));
   }
   // ---- tr(X X^T) of the updating states, then their refresh chains start right away (they
   // need J, K, L and the trace only); phase C keeps using the pre-refresh W_t
