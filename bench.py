@@ -31,10 +31,6 @@ import sys
 import threading
 import time
 
-# one hardware work queue per NG refresh stream (paper_1410_7455_b200/__init__.py); set
-# before torch creates the CUDA context
-os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
-
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -231,13 +227,17 @@ def roofline_for(group: str, prof: dict, precision: str, peaks: dict):
         pass
     is_gemm = group in ("fwd_gemm", "bwd_gemm", "upd_gemm")
     if group == "ng_eig":
-        # one CTA by design (FP64 Jacobi of the R x R matrix Z_t): peak = ONE SM's FP64 FMA rate
+        # one CTA per state by design (FP64 eigensolve of the R x R matrix Z_t; all updating
+        # states of a step in one grouped launch): peak = that many SMs' FP64 FMA rate (the
+        # library's accounting puts the CTA count of each launch in the "bytes" field)
         flops = g["flops"] / g["launches"]
+        ctas = max(1.0, g["bytes"] / g["launches"])
         achieved = flops / per_launch_s / 1e9
-        peak = FP64_SM_PEAK_GFLOPS
+        peak = FP64_SM_PEAK_GFLOPS * ctas
         return {"kernel": group, "bound": "alu", "achieved": achieved, "peak": peak, "unit": "GFLOP/s",
-                "frac": achieved / peak, "traffic": traffic,
-                "peak_source": "derived: one SM, 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md); algorithmic 9 R^3 flop",
+                "frac": achieved / peak, "traffic": traffic, "ctas_per_launch": ctas,
+                "peak_source": "derived: one SM per state (CTA), 64 FP64 FMA/clk x 2 x 1.965 GHz each (DESIGN.md); "
+                               "algorithmic 9 R^3 flop per state",
                 "algorithmic_per_launch": flops, "launch_ms": per_launch_s * 1e3}
     if is_gemm or group in ("ng_proj", "ng_refresh"):
         flops = g["flops"] / g["launches"]

@@ -364,11 +364,10 @@ __device__ unsigned long long g_ref_t[256][5];   // refresh timing (ng_debug_ref
 __device__ unsigned int g_ref_n;
 
 template <int MODE>
-__global__ void __launch_bounds__(1024)
-refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
-               const float* __restrict__ KL, double* __restrict__ dstate,
-               const double* __restrict__ sums, float* __restrict__ Amat,
-               float* __restrict__ svec, int* __restrict__ flags, int dbg_mask) {
+__device__ __forceinline__ void refresh_body(int R, int D, int N, double eta, double alpha, double eps,
+                                             const float* __restrict__ KL, double* __restrict__ dstate,
+                                             const double* __restrict__ sums, float* __restrict__ Amat,
+                                             float* __restrict__ svec, int* __restrict__ flags, int dbg_mask) {
   extern __shared__ __align__(16) unsigned char ng_smem[];
   double* sm = reinterpret_cast<double*>(ng_smem);
   unsigned long long t_start;
@@ -593,11 +592,59 @@ refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
   }
 }
 
+template <int MODE>
+__global__ void __launch_bounds__(1024)
+refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
+               const float* __restrict__ KL, double* __restrict__ dstate,
+               const double* __restrict__ sums, float* __restrict__ Amat,
+               float* __restrict__ svec, int* __restrict__ flags, int dbg_mask) {
+  refresh_body<MODE>(R, D, N, eta, alpha, eps, KL, dstate, sums, Amat, svec, flags, dbg_mask);
+}
+
+// Grouped refresh: every updating state of a step in ONE launch, one CTA per state
+// (Householder + RRR eigensolver, 2 <= R <= kTriMax), on one side stream.
+struct RefreshJob {
+  int R, D, N, pad_;
+  double eta, alpha, eps;
+  const float* KL;
+  double* dstate;
+  const double* sums;
+  float* Amat;
+  float* svec;
+  int* flags;
+};
+constexpr int kRefreshGroupMax = 16;
+struct RefreshGroup {
+  RefreshJob j[kRefreshGroupMax];
+  int count, dbg;
+};
+__global__ void __launch_bounds__(1024) refresh_group_kernel(const __grid_constant__ RefreshGroup g) {
+  const RefreshJob& J = g.j[blockIdx.x];
+  refresh_body<REFRESH_TRI>(J.R, J.D, J.N, J.eta, J.alpha, J.eps, J.KL, J.dstate, J.sums, J.Amat, J.svec, J.flags,
+                            g.dbg);
+}
+
+// B_t = J_t + (N(1-eta)/eta)(D_t + rho_t I) W_t of every job (blockIdx.y), in J's buffer.
+struct BscaleGroup {
+  float* J[kRefreshGroupMax];
+  const float* W[kRefreshGroupMax];
+  const float* s[kRefreshGroupMax];
+  int64_t ldw[kRefreshGroupMax];
+  int R[kRefreshGroupMax], D[kRefreshGroupMax];
+};
+__global__ void __launch_bounds__(256) bscale_group_kernel(const __grid_constant__ BscaleGroup g) {
+  const int q = blockIdx.y, R = g.R[q], D = g.D[q];
+  const int64_t total = (int64_t)R * D, ldw = g.ldw[q];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / D), j = (int)(i % D);
+    g.J[q][(int64_t)r * ldw + j] = fmaf(g.s[q][r], g.W[q][(int64_t)r * ldw + j], g.J[q][(int64_t)r * ldw + j]);
+  }
+}
+
 // B.3.1 (reading R5): O = E^{-1/2} (W W^T) E^{-1/2} for the NEW state; if
 // max |O - I| > 1e-3: O = C C^T, M = E^{1/2} C^{-1} E^{-1/2} (flags[2] = 1).
-__global__ void __launch_bounds__(1024)
-reorth_check_kernel(int R, const float* __restrict__ WW, const double* __restrict__ dstate,
-                    double* __restrict__ Cfac, int* __restrict__ flags) {
+__device__ __forceinline__ void reorth_check_body(int R, const float* __restrict__ WW, const double* __restrict__ dstate,
+                                                  double* __restrict__ Cfac, int* __restrict__ flags) {
   if (flags[1] == 0) return;
   extern __shared__ __align__(16) unsigned char ng_smem[];
   double* sm = reinterpret_cast<double*>(ng_smem);
@@ -653,9 +700,9 @@ reorth_check_kernel(int R, const float* __restrict__ WW, const double* __restric
 // y = C^{-1} (E'^{-1/2} w_j), then w_j <- E'^{1/2} y.  In place, gated on flags[2].
 // 128 columns per CTA; the factor and the 128 right-hand sides live in shared memory.
 constexpr int kTrsmCols = 128;
-__global__ void __launch_bounds__(kTrsmCols)
-reorth_trsm_kernel(int R, int D, float* __restrict__ W, int64_t ldw, const double* __restrict__ Cfac,
-                   const double* __restrict__ dstate, const int* __restrict__ flag) {
+__device__ __forceinline__ void reorth_trsm_body(int blk, int R, int D, float* __restrict__ W, int64_t ldw,
+                                                 const double* __restrict__ Cfac, const double* __restrict__ dstate,
+                                                 const int* __restrict__ flag) {
   if (*flag == 0) return;
   extern __shared__ __align__(16) unsigned char ng_smem[];
   double* C = reinterpret_cast<double*>(ng_smem);    // R*R
@@ -665,7 +712,7 @@ reorth_trsm_kernel(int R, int D, float* __restrict__ W, int64_t ldw, const doubl
   for (int i = tid; i < R * R; i += blockDim.x) C[i] = Cfac[i];
   for (int i = tid; i < R; i += blockDim.x) eh[i] = sqrt(dstate[1 + R + i]);
   __syncthreads();
-  const int j = blockIdx.x * kTrsmCols + tid;
+  const int j = blk * kTrsmCols + tid;
   if (j >= D) return;
   for (int i = 0; i < R; ++i) {
     const double* ci = C + i * R;
@@ -681,6 +728,39 @@ reorth_trsm_kernel(int R, int D, float* __restrict__ W, int64_t ldw, const doubl
     Y[i * kTrsmCols + tid] = ((s0 + s1) + (s2 + s3)) / ci[i];
   }
   for (int i = 0; i < R; ++i) W[(int64_t)i * ldw + j] = (float)(eh[i] * Y[i * kTrsmCols + tid]);
+}
+
+__global__ void __launch_bounds__(1024)
+reorth_check_kernel(int R, const float* __restrict__ WW, const double* __restrict__ dstate,
+                    double* __restrict__ Cfac, int* __restrict__ flags) {
+  reorth_check_body(R, WW, dstate, Cfac, flags);
+}
+__global__ void __launch_bounds__(kTrsmCols)
+reorth_trsm_kernel(int R, int D, float* __restrict__ W, int64_t ldw, const double* __restrict__ Cfac,
+                   const double* __restrict__ dstate, const int* __restrict__ flag) {
+  reorth_trsm_body(blockIdx.x, R, D, W, ldw, Cfac, dstate, flag);
+}
+
+// Grouped B.3.1 check (one CTA per job) and repair (the jobs' column blocks stacked).
+struct ReorthGroup {
+  const float* WW[kRefreshGroupMax];
+  const double* dstate[kRefreshGroupMax];
+  double* Cfac[kRefreshGroupMax];
+  int* flags[kRefreshGroupMax];
+  float* W[kRefreshGroupMax];
+  int64_t ldw[kRefreshGroupMax];
+  int R[kRefreshGroupMax], D[kRefreshGroupMax], blk_begin[kRefreshGroupMax + 1];
+  int count;
+};
+__global__ void __launch_bounds__(1024) reorth_check_group_kernel(const __grid_constant__ ReorthGroup g) {
+  const int q = blockIdx.x;
+  reorth_check_body(g.R[q], g.WW[q], g.dstate[q], g.Cfac[q], g.flags[q]);
+}
+__global__ void __launch_bounds__(kTrsmCols) reorth_trsm_group_kernel(const __grid_constant__ ReorthGroup g) {
+  int q = 0;
+  while (q + 1 < g.count && (int)blockIdx.x >= g.blk_begin[q + 1]) ++q;
+  reorth_trsm_body((int)blockIdx.x - g.blk_begin[q], g.R[q], g.D[q], g.W[q], g.ldw[q], g.Cfac[q], g.dstate[q],
+                   g.flags[q] + 2);
 }
 
 // ------------------------------------------------------------------------------------
@@ -826,6 +906,12 @@ static ng_status set_kernel_attrs() {
                                    (int)refresh_plan(kDCMax, REFRESH_DC).total_bytes));
   NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<REFRESH_TRI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)refresh_plan(kTriMax, REFRESH_TRI).total_bytes));
+  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)refresh_plan(kTriMax, REFRESH_TRI).total_bytes));
+  NG_CUDA_TRY(cudaFuncSetAttribute(reorth_check_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)reorth_smem_bytes(kMaxRank)));
+  NG_CUDA_TRY(cudaFuncSetAttribute(reorth_trsm_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)trsm_smem_bytes(kMaxRank)));
   NG_CUDA_TRY(cudaFuncSetAttribute(reorth_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)reorth_smem_bytes(kMaxRank)));
   NG_CUDA_TRY(cudaFuncSetAttribute(reorth_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1014,7 +1100,7 @@ static ng_status launch_refresh_chain(ngsgd_ctx* h, int n, double eta, const dou
   cudaStream_t ss = h->side;
   {
     // algorithmic work of a dense symmetric eigendecomposition with eigenvectors: ~9 R^3 flop
-    ProfScope pe(NG_PROF_NG_EIG, ss, 9.0 * (double)R * R * R, 8.0 * 2.0 * R * R);
+    ProfScope pe(NG_PROF_NG_EIG, ss, 9.0 * (double)R * R * R, 1.0);   // "bytes" = CTAs (one SM)
     const double a_ = (double)h->cfg.alpha, e_ = (double)h->cfg.epsilon;
     // FP64 eigensolve in both precision modes: with cond(C) > 1e6 (common) an
     // FP32 solve leaves R_{t+1} non-orthonormal beyond 1e-3 and B.3.1 repairs would fire on
@@ -1356,6 +1442,141 @@ static ng_status launch_seg_reduce(cudaStream_t st, SegReduce& sr) {
 
 int rr_chunks(int D) { return ceil_div(D, 64); }   // split capacity of the K / L partial buffers
 
+// The refresh chains of every updating state of a group as ONE chain of grouped launches on
+// ONE side stream (the first state's): the R x R refresh (one CTA per state), B_t, W_{t+1} =
+// A_t B_t and W_{t+1} W_{t+1}^T (3xTF32 tensor cores), the B.3.1 check and repair.  Every
+// state's join event is recorded at its end; the main stream waits for it before that
+// state's next call (the refresh only gates the next call).  Falls back to the
+// per-state chains for ranks the one-CTA Householder/RRR solver does not take.
+static ng_status launch_refresh_group(NgCall* calls, const std::vector<int>& grp, const std::vector<int>& ug,
+                                      cudaStream_t st) {
+  if (skip_refresh_knob() || ug.empty()) return NG_OK;
+  static const int force = tune_int("NG_TUNE_EIG_MODE", -1);
+  bool ok = force < 0 && (int)ug.size() <= kRefreshGroupMax;
+  int maxR = 0;
+  for (int g : ug) {
+    const int R = calls[grp[g]].h->rank;
+    ok = ok && R >= 2 && R <= kTriMax;
+    maxR = std::max(maxR, R);
+  }
+  if (!ok) {
+    for (int g : ug) {
+      NgCall& c = calls[grp[g]];
+      const double eta = 1.0 - exp(-(double)c.n / (double)c.h->cfg.s_samples);   // eqn:eta:ns
+      NG_TRY(launch_refresh_chain(c.h, c.n, eta, c.h->sums + 2));
+    }
+    return NG_OK;
+  }
+  const int G = (int)ug.size();
+  ngsgd_ctx* h0 = calls[grp[ug[0]]].h;
+  cudaStream_t ss = h0->side;
+  NG_CUDA_TRY(cudaEventRecord(h0->ev_fork, st));
+  NG_CUDA_TRY(cudaStreamWaitEvent(ss, h0->ev_fork, 0));
+  static const int dbg = getenv("NG_PROFILE_JACOBI_MASK") ? atoi(getenv("NG_PROFILE_JACOBI_MASK")) : 0;
+  {
+    RefreshGroup rg;
+    std::memset(&rg, 0, sizeof(rg));
+    rg.count = G;
+    rg.dbg = dbg;
+    double flops = 0.0;
+    for (int u = 0; u < G; ++u) {
+      NgCall& c = calls[grp[ug[u]]];
+      ngsgd_ctx* h = c.h;
+      RefreshJob& J = rg.j[u];
+      J.R = h->rank; J.D = h->dim; J.N = c.n;
+      J.eta = 1.0 - exp(-(double)c.n / (double)h->cfg.s_samples);   // eqn:eta:ns
+      J.alpha = h->cfg.alpha; J.eps = h->cfg.epsilon;
+      J.KL = h->KL; J.dstate = h->dstate; J.sums = h->sums + 2; J.Amat = h->Amat; J.svec = h->svec; J.flags = h->flags;
+      flops += 9.0 * (double)J.R * J.R * J.R;
+    }
+    // ng_eig: algorithmic work ~9 R^3 per state; "bytes" carries the CTA (state) count so the
+    // roofline is taken against that many SMs' FP64 rate
+    ProfScope pe(NG_PROF_NG_EIG, ss, flops, (double)G);
+    refresh_group_kernel<<<G, 1024, refresh_plan(maxR, REFRESH_TRI).total_bytes, ss>>>(rg);
+    NG_TRY(check_launch("refresh_group_kernel"));
+  }
+  double flops = 0.0, bytes = 0.0;
+  for (int g : ug) {
+    const ngsgd_ctx* h = calls[grp[g]].h;
+    flops += 4.0 * (double)h->rank * h->rank * h->dim;
+    bytes += 4.0 * 4.0 * h->rank * h->dim;
+  }
+  ProfScope ps(NG_PROF_NG_REFRESH, ss, flops, bytes);
+  {
+    BscaleGroup bg;
+    std::memset(&bg, 0, sizeof(bg));
+    int64_t mx = 1;
+    for (int u = 0; u < G; ++u) {
+      ngsgd_ctx* h = calls[grp[ug[u]]].h;
+      bg.J[u] = h->J; bg.W[u] = h->W[h->cur]; bg.s[u] = h->svec; bg.ldw[u] = h->ldw; bg.R[u] = h->rank;
+      bg.D[u] = h->dim;
+      mx = std::max<int64_t>(mx, (int64_t)h->rank * h->dim);
+    }
+    bscale_group_kernel<<<dim3(std::min(64, ceil_div(mx, 256)), G), 256, 0, ss>>>(bg);
+    NG_TRY(check_launch("bscale_group_kernel"));
+  }
+  // W_{t+1} = A_t B_t (eqn:wt1): M = R, N = D, K = R; A_t K-major, B_t = J MN-major
+  std::vector<TcGroupDesc> dw(G), dww(G);
+  std::vector<int> spw(G);
+  const int want = std::max(1, std::min(kTcMaxSplits, ceil_div(2 * 148, G)));
+  for (int u = 0; u < G; ++u) {
+    ngsgd_ctx* h = calls[grp[ug[u]]].h;
+    const int R = h->rank, D = h->dim;
+    float* Wn = h->W[1 - h->cur];
+    TcGroupDesc& q = dw[u];
+    std::memset(&q, 0, sizeof(q));
+    q.M = R; q.N = D; q.K = R; q.splits = 1;
+    q.A = h->Amat; q.lda = R; q.B = h->J; q.ldb = h->ldw;
+    q.epi.kind = TC_EPI_STORE; q.epi.C = Wn; q.epi.ldc = h->ldw;
+    TcGroupDesc& w = dww[u];
+    std::memset(&w, 0, sizeof(w));
+    w.M = R; w.N = R; w.K = D; w.splits = want;
+    w.A = Wn; w.lda = h->ldw; w.B = Wn; w.ldb = h->ldw;
+    w.epi.kind = TC_EPI_PARTIAL; w.epi.C = h->WWpart; w.epi.ldc = R; w.epi.zstride = (int64_t)R * R;
+    w.splits_used = &spw[u];
+  }
+  NG_TRY(tc_gemm_tf32_grouped(ss, dw.data(), G, true, false, TC_EPI_STORE, 128, true));
+  // B.3.1: W_{t+1} W_{t+1}^T (split over D, fixed-order reduction), check, repair
+  NG_TRY(tc_gemm_tf32_grouped(ss, dww.data(), G, true, true, TC_EPI_PARTIAL, 128, true));
+  {
+    SegReduce sr;
+    std::memset(&sr, 0, sizeof(sr));
+    sr.count = G;
+    for (int u = 0; u < G; ++u) {
+      ngsgd_ctx* h = calls[grp[ug[u]]].h;
+      const int R = h->rank;
+      sr.out[u] = h->WW; sr.src[u] = h->WWpart; sr.ldo[u] = R; sr.lds[u] = R; sr.zstride[u] = (int64_t)R * R;
+      sr.rows[u] = R; sr.cols[u] = R; sr.splits[u] = spw[u];
+    }
+    NG_TRY(launch_seg_reduce(ss, sr));
+  }
+  {
+    ReorthGroup rg;
+    std::memset(&rg, 0, sizeof(rg));
+    rg.count = G;
+    int blocks = 0;
+    for (int u = 0; u < G; ++u) {
+      ngsgd_ctx* h = calls[grp[ug[u]]].h;
+      rg.WW[u] = h->WW; rg.dstate[u] = h->dstate; rg.Cfac[u] = h->Cfac; rg.flags[u] = h->flags;
+      rg.W[u] = h->W[1 - h->cur]; rg.ldw[u] = h->ldw; rg.R[u] = h->rank; rg.D[u] = h->dim;
+      rg.blk_begin[u] = blocks;
+      blocks += ceil_div(h->dim, kTrsmCols);
+    }
+    rg.blk_begin[G] = blocks;
+    reorth_check_group_kernel<<<G, 1024, reorth_smem_bytes(maxR), ss>>>(rg);
+    NG_TRY(check_launch("reorth_check_group_kernel"));
+    reorth_trsm_group_kernel<<<blocks, kTrsmCols, trsm_smem_bytes(maxR), ss>>>(rg);
+    NG_TRY(check_launch("reorth_trsm_group_kernel"));
+  }
+  for (int g : ug) {
+    ngsgd_ctx* h = calls[grp[g]].h;
+    NG_CUDA_TRY(cudaEventRecord(h->ev_join, ss));
+    h->pending = true;
+    h->cur = 1 - h->cur;
+  }
+  return NG_OK;
+}
+
 ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
   NG_REQUIRE(calls != nullptr && count >= 0, NG_EINVAL, "NULL argument");
   std::vector<int> grp;          // indices of tensor-core group members
@@ -1508,11 +1729,7 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
     NG_TRY(check_launch("trace_part_kernel"));
     trace_final_kernel<<<tr.count, 256, 0, st>>>(tr);
     NG_TRY(check_launch("trace_final_kernel"));
-    for (int g : ug) {
-      NgCall& c = calls[grp[g]];
-      const double eta = 1.0 - exp(-(double)c.n / (double)c.h->cfg.s_samples);   // eqn:eta:ns
-      NG_TRY(launch_refresh_chain(c.h, c.n, eta, c.h->sums + 2));
-    }
+    NG_TRY(launch_refresh_group(calls, grp, ug, st));
   }
   // ---- phase C: X_hat = X - H W with fused row norms (one launch), finalize (one launch)
   {
