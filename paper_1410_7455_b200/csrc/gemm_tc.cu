@@ -4,13 +4,14 @@
 //   warp 0 lane 0 : TMA producer   (cp.async.bulk.tensor -> S-stage smem ring, mbarrier tx)
 //   warp 1 lane 0 : MMA issuer     (tcgen05.mma.kind::tf32, 4 x K=8 per 32-wide k-block,
 //                                    tcgen05.commit -> frees the smem stage)
-//   warps 2..3    : (3xTF32 only) split each landed stage in place into hi = x rounded to
+//   warps 2..5    : (3xTF32 only; the CTA then has 192 threads) split each landed stage in
+//                   place into hi = x rounded to
 //                   the nearest TF32 value and lo = (x - hi) rounded to TF32 in a second
 //                   buffer, fence.proxy.async, arrive; the MMA thread then issues
 //                   A_lo B_hi + A_hi B_lo + A_hi B_hi per k-slice (FP32-grade products: the
 //                   dropped A_lo B_lo and the rounding of lo are <= ~2^-23 |a||b| each)
-//   warps 0..3    : epilogue       (tcgen05.ld 32x32b: warp w owns TMEM lanes 32w..32w+31,
-//                                    i.e. tile rows; functor applied per element)
+//   warps 0..3    : epilogue       (tcgen05.ld 32x32b: warp w owns TMEM lanes 32(w%4)..+31,
+//   (3xTF32: 2..5)                   i.e. tile rows; functor applied per element)
 // Shared-memory layouts are the canonical UMMA SWIZZLE_128B layouts produced directly by
 // TMA with CU_TENSOR_MAP_SWIZZLE_128B:
 //   K-major  : [rows][128 B] (32 fp32 of K per row), 8-row atoms 1024 B apart (SBO)
@@ -158,6 +159,11 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // epilogue warps: 0..3, or 2..5 with 3xTF32 (warps 2..5 also split the stages); a warp
+  // reaches TMEM lanes 32 (warp % 4) .. + 31 only
+  constexpr int EW0 = S3 ? 2 : 0;
+  const bool epi_warp = warp >= EW0;
+  const int q4 = warp & 3;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmA)) : "memory");
@@ -165,7 +171,7 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
     for (int s = 0; s < nstages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
-      if (S3) mbar_init(&split_bar[s], 64);
+      if (S3) mbar_init(&split_bar[s], 128);
     }
     mbar_init(&accum_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -186,11 +192,11 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
   // thread loads its row of it now (registers) and the HBM latency overlaps the mainloop.
   constexpr bool RMW = EPI == TC_EPI_AXPY || EPI == TC_EPI_NGAPPLY;
   constexpr int CW = BN >= 32 ? 32 : 16;
-  const int row = m0 + warp * 32 + lane;
+  const int row = m0 + q4 * 32 + lane;
   float* __restrict__ crow = epi.C + (EPI == TC_EPI_PARTIAL ? (int64_t)ztile * epi.zstride : 0) +
                              (int64_t)row * epi.ldc;
   float oldv[RMW ? BN : 1];
-  if (RMW) {
+  if (RMW && epi_warp) {
 #pragma unroll
     for (int c = 0; c < BN / CW; ++c) {
       const int nb = n0 + c * CW;
@@ -260,7 +266,7 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
     }
     umma_commit(&accum_bar);
   } else if (S3 && warp >= 2) {
-    // ---------------- 3xTF32 split (warps 2-3): hi in place, lo = x - hi beside it
+    // ---------------- 3xTF32 split (warps 2-5): hi in place, lo = x - hi beside it
     const int t = threadIdx.x - 64;
     int s = 0;
     uint32_t ph = 0;
@@ -269,7 +275,7 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
       float4* hi = reinterpret_cast<float4*>(smem + s * STAGE);
       float4* lo = reinterpret_cast<float4*>(smem + s * STAGE + HALF);
 #pragma unroll 4
-      for (int q = t; q < (int)(HALF / 16); q += 64) {
+      for (int q = t; q < (int)(HALF / 16); q += 128) {
         const float4 x = hi[q];
         const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
         hi[q] = h;
@@ -286,6 +292,7 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
   // Warp w owns TMEM lanes (tile rows) 32w..32w+31.  Chunks of 32 columns (two tcgen05.ld):
   // each thread moves one full 128-byte line of its row per chunk with 8 independent
   // 16-byte accesses (all loads of a read-modify-write chunk are issued first).
+  if (epi_warp) {
   mbar_wait(&accum_bar, 0);
   tc_fence_after();
   __syncwarp();
@@ -300,7 +307,7 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
         uint32_t v[16];
-        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(hh * 80 + c * 16), v);
+        tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(hh * 80 + c * 16), v);
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[c * 16 + j] = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
       }
@@ -338,11 +345,11 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
     float acc[CW];
     {
       uint32_t v[16];
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * CW), v);
+      tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(c * CW), v);
 #pragma unroll
       for (int j = 0; j < 16; ++j) acc[j] = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
       if (CW == 32) {
-        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * CW + 16), v);
+        tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(c * CW + 16), v);
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[16 + j] = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
       }
@@ -390,6 +397,7 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
     epi.pp[(int64_t)ntile * epi.part_ld + row] = pp;
   }
   }   // EPI != TC_EPI_PNORM
+  }   // epi_warp
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -398,7 +406,7 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
 }
 
 template <int BN, bool AK, bool BKM, int EPI, bool S3>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(S3 ? 192 : 128)
 tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                     int K, int kb_per_split, TcEpilogue epi, int nstages) {
   const int kb_total = (K + kBK - 1) / kBK;
@@ -411,7 +419,7 @@ tc_gemm_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 // Grouped launch: problem g owns tiles [tile_begin, tile_begin + mt*nt*splits); each tile
 // (z, m, n) of it is one CTA.  Problems share BN, operand majors and epilogue kind.
 template <int BN, bool AK, bool BKM, int EPI, bool S3>
-__global__ void __launch_bounds__(128) tc_gemm_tf32_grouped_kernel(const __grid_constant__ TcGroup grp) {
+__global__ void __launch_bounds__(S3 ? 192 : 128) tc_gemm_tf32_grouped_kernel(const __grid_constant__ TcGroup grp) {
   int g = 0;
   while (g + 1 < grp.count && (int)blockIdx.x >= grp.p[g + 1].tile_begin) ++g;
   const TcProblem& P = grp.p[g];
@@ -501,7 +509,7 @@ ng_status launch(cudaStream_t st, const CUtensorMap& ta, const CUtensorMap& tb, 
   // co-resident CTAs per SM.
   const int ns = std::max(1, std::min(ring_stages(BN, S3), kbps));
   dim3 grid(ceil_div(N, BN), ceil_div(M, kBM), splits);
-  NG_CUDA_TRY(launch_pdl(tc_gemm_tf32_kernel<BN, AK, BKM, EPI, S3>, grid, dim3(128), ring_smem(BN, ns, S3), st, ta,
+  NG_CUDA_TRY(launch_pdl(tc_gemm_tf32_kernel<BN, AK, BKM, EPI, S3>, grid, dim3(S3 ? 192 : 128), ring_smem(BN, ns, S3), st, ta,
                          tb, M, N, K, kbps, epi, ns));
   return check_launch("tc_gemm_tf32_kernel");
 }
@@ -591,7 +599,7 @@ ng_status launch_grouped(cudaStream_t st, const TcGroup& grp, int tiles) {
                                      (int)ring_smem(BN, ring_stages(BN, S3), S3)));
     attr = true;
   }
-  NG_CUDA_TRY(launch_pdl(tc_gemm_tf32_grouped_kernel<BN, AK, BKM, EPI, S3>, dim3(tiles), dim3(128),
+  NG_CUDA_TRY(launch_pdl(tc_gemm_tf32_grouped_kernel<BN, AK, BKM, EPI, S3>, dim3(tiles), dim3(S3 ? 192 : 128),
                          ring_smem(BN, grp.nstages, S3), st, grp));
   return check_launch("tc_gemm_tf32_grouped_kernel");
 }
