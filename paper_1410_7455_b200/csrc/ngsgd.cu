@@ -906,8 +906,7 @@ static ng_status set_kernel_attrs() {
                                    (int)refresh_plan(kDCMax, REFRESH_DC).total_bytes));
   NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<REFRESH_TRI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)refresh_plan(kTriMax, REFRESH_TRI).total_bytes));
-  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)refresh_plan(kTriMax, REFRESH_TRI).total_bytes));
+  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   NG_CUDA_TRY(cudaFuncSetAttribute(reorth_check_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)reorth_smem_bytes(kMaxRank)));
   NG_CUDA_TRY(cudaFuncSetAttribute(reorth_trsm_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1492,7 +1491,11 @@ static ng_status launch_refresh_group(NgCall* calls, const std::vector<int>& grp
     // ng_eig: algorithmic work ~9 R^3 per state; "bytes" carries the CTA (state) count so the
     // roofline is taken against that many SMs' FP64 rate
     ProfScope pe(NG_PROF_NG_EIG, ss, flops, (double)G);
-    refresh_group_kernel<<<G, 1024, refresh_plan(maxR, REFRESH_TRI).total_bytes, ss>>>(rg);
+    // NG_TUNE_REFRESH_SMEM_KB pads the refresh CTA's shared memory so that no main-stream
+    // CTA can share its SM (measurement knob)
+    static const size_t pad = (size_t)std::max(0, tune_int("NG_TUNE_REFRESH_SMEM_KB", 0)) * 1024;
+    const size_t rsm = std::max(refresh_plan(maxR, REFRESH_TRI).total_bytes, pad);
+    refresh_group_kernel<<<G, 1024, rsm, ss>>>(rg);
     NG_TRY(check_launch("refresh_group_kernel"));
   }
   double flops = 0.0, bytes = 0.0;

@@ -21,14 +21,14 @@ frames, labels = spliced_frames(1410, 64 * N, num_classes=5000)
 f = torch.from_numpy(frames).cuda()
 y = torch.from_numpy(labels).cuda()
 net = api.Nnet(360, 4, 3000, 10, 5000, max_minibatch=N, precond=True, rank_in=20, rank_out=80,
-               precision=os.environ.get("NG_PREC", "tf32"), seed=1410)
+               precision=os.environ.get("NG_PREC", "tf32"), seed=1410, renorm=True)
 buf = np.zeros(256 * 5, dtype=np.uint64)
 cnt = np.zeros(1, dtype=np.int32)
 seen = 0
 for k in range(steps):
     i = k % 64
     net.forward_backward(f[i * N:(i + 1) * N], y[i * N:(i + 1) * N])
-    net.update(0.01 / 6, 0.075)
+    net.update(0.01 / 6 / 8, 0.075)
     if k >= 20:
         _lib.check(_lib.lib.ng_debug_refresh_times(buf.ctypes.data_as(ctypes.c_void_p), cnt.ctypes.data_as(ctypes.c_void_p)))
         c = int(cnt[0])
