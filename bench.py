@@ -242,10 +242,13 @@ def roofline_for(group: str, prof: dict, precision: str, peaks: dict):
     if is_gemm or group in ("ng_proj", "ng_refresh"):
         flops = g["flops"] / g["launches"]
         achieved = flops / per_launch_s / 1e12
-        if precision == "tf32" and is_gemm:
+        if is_gemm or group in ("ng_proj", "ng_refresh"):
+            # tcgen05 in every mode but fp32_simt: TF32 (1 MMA per product) or 3xTF32 (NG
+            # projections always, all GEMMs in fp32 mode: 3 MMAs per product, counted once)
             peak = peaks.get("bf16_tflops_sustained", 1378.9) * 0.5
             bound, src = "tensor", ("TF32 = MEASURED_PEAKS.json bf16_tflops_sustained x 0.5 (nominal dense "
-                                    "TF32/BF16 ratio 1.1/2.25 PF, B200_PROFILING.md)")
+                                    "TF32/BF16 ratio 1.1/2.25 PF, B200_PROFILING.md); algorithmic flops counted "
+                                    "once also where 3xTF32 issues three MMAs per product")
         else:
             peak = FP32_SIMT_PEAK_TFLOPS
             bound, src = "alu", "derived: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md)"
