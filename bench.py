@@ -348,8 +348,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     pool_mb = POOL_FRAMES // N
     log(f"[rank {rank}] synthetic pool {frames_np.nbytes / 1e6:.0f} MB in {time.time() - t_gen:.1f}s")
     net = api.Nnet(CFG3["input_dim"], CFG3["num_hidden"], CFG3["hidden_dim"], CFG3["pnorm_group"],
-                   CFG3["num_classes"], max_minibatch=N, precond=True, rank_in=CFG3["rank_in"],
-                   rank_out=CFG3["rank_out"], precision=precision, seed=1410, renorm=True,
+                   CFG3["num_classes"], max_minibatch=N, rank_in=CFG3["rank_in"],
+                   rank_out=CFG3["rank_out"], precision=precision, seed=1410, renorm=True, precond=args.precond,
                    ng_overrides=None if args.update_period == 4 else {"update_period": args.update_period})
     if world > 1:
         uid = api.comm_unique_id() if rank == 0 else None
@@ -560,6 +560,9 @@ def main():
     ap.add_argument("--no-precond-bench", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=100)
     ap.add_argument("--update-period", type=int, default=4, help="NG J (P:1295-1297); experiments only")
+    ap.add_argument("--precond", choices=["online", "simple", "none"], default="online",
+                    help="online NG-SGD (the metric; default), simple NG-SGD (Appendix A) or plain SGD: "
+                         "the paper's 93 / 208 / 88 s comparison (P:676-679)")
     ap.add_argument("--workload", choices=["config3", "config5"], default="config3",
                     help="config3 (default, the metric's workload) or BASELINE.json configs[4] (wide DNN)")
     args = ap.parse_args()
@@ -574,6 +577,13 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.precond != "online":
+        global METRIC
+        METRIC = {"simple": "train frames/sec (simple NG-SGD)", "none": "train frames/sec (plain SGD)"}[args.precond]
+        WORKLOAD = WORKLOAD.replace("online NG-SGD R_in=20/R_out=80 on all", "%s on all" % (
+            "simple NG-SGD (Appendix A)" if args.precond == "simple" else "no preconditioning (plain SGD) on")).replace(
+            " on all 10 Fisher factors", " on all 10 sides" if args.precond == "simple" else "")
+        globals()["WORKLOAD"] = WORKLOAD
     if args.impl == "reference":
         return run_reference(args, rank, world)
     return run_ours(args, rank, world, local_rank)

@@ -130,6 +130,30 @@ ng_status ngsgd_get_state(ngsgd_t h, ngsgd_state_host* out);
  * rank must equal the handle's effective rank; initialized != 0 marks it initialised. */
 ng_status ngsgd_set_state(ngsgd_t h, const ngsgd_state_host* in);
 
+/* ---------------------------------- simple NG-SGD preconditioner (Appendix A) ---- */
+
+/* The simple natural-gradient method (A.2), computed by its efficient form A.3
+ * (P:843-887): per minibatch X (n x dim) the Fisher estimate of every row is formed from
+ * the OTHER rows (held-out, reading R1), regularised by beta = alpha max(tr X^T X, 1e-20)
+ * / (n dim); Q = X (beta I + X^T X/(n-1))^{-1} if n > dim, else
+ * (beta I + X X^T/(n-1))^{-1} X (strict n > dim, reading R11);
+ * x_hat_i = (1 + a_i / (n-1-a_i)) q_i with a_i = x_i^T q_i;
+ * gamma = sqrt(tr X^T X / tr X_hat^T X_hat).  Stateless apart from its
+ * workspace (FP64 Gram / Cholesky factor of min(n, dim)^2 and dim x max_rows solves).
+ * Arithmetic: FP64 on the device (Gram, Cholesky, substitutions); I/O FP32. */
+typedef struct ngsimple_ctx* ngsimple_t;
+/* max_rows >= 2 (a held-out estimate needs another row); alpha > 0 (4). */
+ng_status ngsimple_create(int32_t dim, int32_t max_rows, float alpha, void* cuda_stream, ngsimple_t* out);
+ng_status ngsimple_destroy(ngsimple_t h);
+/* x: device, n x dim, leading dimension ld >= dim, 2 <= n <= max_rows.  In place:
+ * x <- X_hat (NOT scaled by gamma, as ngsgd_precondition); gamma_out: device float[1] or
+ * NULL; row_sq_out: device float[n] (||x_hat_i||^2) or NULL.  Asynchronous. */
+ng_status ngsimple_precondition(ngsimple_t h, int32_t n, float* x, int64_t ld, float* gamma_out,
+                                float* row_sq_out);
+/* Synchronise the handle's stream and report sticky device errors (non-positive pivot:
+ * NG_ENOTPD; non-finite data: NG_ENONFINITE). */
+ng_status ngsimple_read_flags(ngsimple_t h);
+
 /* ---------------------------------------- p-norm / softmax DNN training step ---- */
 
 /* NG_FP32: FP32-grade (paper-faithful; parity 1e-4): every GEMM on tcgen05 tensor
@@ -150,7 +174,8 @@ typedef enum { NG_FP32 = 0, NG_BF16 = 1, NG_TF32 = 2, NG_FP32_SIMT = 3 } ng_prec
 typedef struct {
   int32_t input_dim, num_hidden, hidden_dim, pnorm_group, num_classes;
   int32_t max_minibatch;        /* N bound; 512 on GPU              */
-  int32_t precond;              /* 0: plain SGD, 1: online NG-SGD (Appendix B)            */
+  int32_t precond;              /* 0: plain SGD, 1: online NG-SGD (Appendix B),
+                                   2: simple NG-SGD (Appendix A; ng_in.alpha is its alpha) */
   ngsgd_config ng_in, ng_out;   /* R_in = 20, R_out = 80                    */
   int32_t precision;            /* ng_precision of the DNN GEMMs                          */
   uint64_t seed;                /* weight-init seed (C.6)                    */

@@ -9,7 +9,7 @@ tensors (device memory and streams) into the C calls.  It never imports ``oracle
 The binding is loaded lazily so that ``python -m paper_1410_7455_b200.build`` works
 before the library exists; any use of the API without the built library raises.
 """
-_API = ("NgError", "Nnet", "NnetStats", "OnlinePreconditioner", "comm_unique_id", "default_ng_config",
+_API = ("NgError", "Nnet", "NnetStats", "OnlinePreconditioner", "SimplePreconditioner", "comm_unique_id", "default_ng_config",
         "library_path", "version", "profile_enable", "profile_read", "kernel_launches")
 
 

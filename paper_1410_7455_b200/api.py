@@ -47,6 +47,35 @@ def default_ng_config(rank: int, **overrides) -> _lib.NgsgdConfig:
     return cfg
 
 
+class SimplePreconditioner:
+    """Simple NG-SGD preconditioner (Appendix A; ngsimple_create / ngsimple_precondition)."""
+
+    def __init__(self, dim: int, max_rows: int, alpha: float = 4.0, stream: Optional[torch.cuda.Stream] = None):
+        h = ctypes.c_void_p()
+        check(lib.ngsimple_create(int(dim), int(max_rows), float(alpha), _stream_handle(stream), ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.ngsimple_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def precondition(self, x: torch.Tensor, gamma: Optional[torch.Tensor] = None,
+                     p: Optional[torch.Tensor] = None) -> None:
+        """In place: x <- X_hat; gamma[0] <- gamma; p[:n] <- ||x_hat_i||^2 (unscaled)."""
+        ld = _check_matrix(x)
+        check(lib.ngsimple_precondition(self._h, x.shape[0], _ptr(x), ld, _ptr(gamma), _ptr(p)))
+
+    def read_flags(self) -> None:
+        check(lib.ngsimple_read_flags(self._h))
+
+
 class OnlinePreconditioner:
     """One online NG-SGD state (Appendix B; ngsgd_create / ngsgd_precondition)."""
 
@@ -131,7 +160,7 @@ class Nnet:
         cfg = _lib.NnetConfig()
         cfg.input_dim, cfg.num_hidden, cfg.hidden_dim = input_dim, num_hidden, hidden_dim
         cfg.pnorm_group, cfg.num_classes, cfg.max_minibatch = pnorm_group, num_classes, max_minibatch
-        cfg.precond = 1 if precond else 0
+        cfg.precond = {False: 0, True: 1, "none": 0, "online": 1, "simple": 2}[precond]
         prec = {"fp32": 0, "bf16": 1, "tf32": 2, "fp32_simt": 3}[precision]
         cfg.ng_in = default_ng_config(rank_in, **dict({"precision": prec}, **(ng_overrides or {})))
         cfg.ng_out = default_ng_config(rank_out, **dict({"precision": prec}, **(ng_overrides or {})))

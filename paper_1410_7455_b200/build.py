@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libngsgd.so")
-SOURCES = ["ngsgd.cu", "nnet.cu", "gemm_tc.cu"]
+SOURCES = ["ngsgd.cu", "nnet.cu", "gemm_tc.cu", "simple_ng.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -23,6 +23,7 @@
 #include "gemm_simt.cuh"
 #include "gemm_tc.cuh"
 #include "ngsgd_impl.cuh"
+#include "simple_ng_impl.cuh"
 
 using namespace ng;
 
@@ -40,6 +41,7 @@ struct nnet_ctx {
   size_t arena_count = 0;
   std::vector<float*> Y, Z, X;               // per layer activations / derivatives
   std::vector<ngsgd_ctx*> ng_in, ng_out;
+  std::vector<ngsimple_ctx*> sn_in, sn_out;   // precond = 2: simple NG-SGD (Appendix A)
   float* gam = nullptr;       // 2L: gamma_in, gamma_out per layer
   float* pbuf = nullptr;      // 2L x max_minibatch: p_in, p_out per layer
   float* scale = nullptr;     // L: alpha_t lr gamma_x gamma_y
@@ -439,6 +441,8 @@ static void nnet_free(nnet_ctx* h) {
   if (!h) return;
   for (auto* p : h->ng_in) ngsgd_destroy_impl(p);
   for (auto* p : h->ng_out) ngsgd_destroy_impl(p);
+  for (auto* p : h->sn_in) ngsimple_destroy_impl(p);
+  for (auto* p : h->sn_out) ngsimple_destroy_impl(p);
   for (auto* p : h->Y) if (p) cudaFree(p);
   for (auto* p : h->Z) if (p) cudaFree(p);
   for (auto* p : h->X) if (p) cudaFree(p);
@@ -484,6 +488,8 @@ ng_status nnet_create(const nnet_config* cfg, void* cuda_stream, nnet_t* out) {
   NG_REQUIRE(cfg->precision == NG_FP32 || cfg->precision == NG_TF32 || cfg->precision == NG_FP32_SIMT, NG_EINVAL,
              "precision must be NG_FP32, NG_TF32 or NG_FP32_SIMT (NG_BF16 is reserved)");
   NG_REQUIRE(cfg->num_hidden + 1 <= 16, NG_EINVAL, "at most 16 weight matrices");
+  NG_REQUIRE(cfg->precond >= 0 && cfg->precond <= 2, NG_EINVAL, "precond must be 0 (none), 1 (online) or 2 (simple)");
+  NG_REQUIRE(cfg->precond != 2 || cfg->max_minibatch >= 2, NG_ESHAPE, "simple NG needs max_minibatch >= 2");
   NG_REQUIRE(cfg->hidden_dim <= kMaxRowWidth && cfg->num_classes <= kMaxRowWidth, NG_ESHAPE,
              "hidden_dim and num_classes must be <= 50000 (one row staged in shared memory)");
   {
@@ -522,7 +528,12 @@ ng_status nnet_create(const nnet_config* cfg, void* cuda_stream, nnet_t* out) {
     if (s == NG_OK) s = nalloc(&z, (size_t)N * h->ldr[l]);
     if (s == NG_OK) s = nalloc(&x, (size_t)N * h->ldr[l]);
     h->Y.push_back(y); h->Z.push_back(z); h->X.push_back(x);
-    if (s == NG_OK && cfg->precond) {
+    if (s == NG_OK && cfg->precond == 2) {
+      ngsimple_ctx *a = nullptr, *b = nullptr;
+      s = ngsimple_create_impl(h->cols[l], N, cfg->ng_in.alpha, h->st, &a);
+      if (s == NG_OK) s = ngsimple_create_impl(h->rows[l], N, cfg->ng_out.alpha, h->st, &b);
+      h->sn_in.push_back(a); h->sn_out.push_back(b);
+    } else if (s == NG_OK && cfg->precond) {
       ngsgd_ctx *a = nullptr, *b = nullptr;
       s = ngsgd_create_impl(h->cols[l], N, &cfg->ng_in, h->st, &a);
       if (s == NG_OK) s = ngsgd_create_impl(h->rows[l], N, &cfg->ng_out, h->st, &b);
@@ -704,7 +715,19 @@ ng_status nnet_update(nnet_t h, float lr, float max_change_per_sample, nnet_upda
   cudaStream_t st = h->st;
   const int L = h->L, n = h->n_last, N = h->cfg.max_minibatch;
   int upd_in[16] = {0}, upd_out[16] = {0};
-  if (h->cfg.precond) {
+  if (h->cfg.precond == 2) {
+    // simple NG-SGD (Appendix A) on both sides of every matrix: one launch per phase
+    NG_REQUIRE(n >= 2, NG_ESHAPE, "simple NG needs n >= 2 (held-out estimate, S:56)");
+    std::vector<SimpleCall> sc;
+    for (int l = 0; l < L; ++l) {
+      float* py = h->pbuf + (size_t)(2 * l) * N;
+      float* px = h->pbuf + (size_t)(2 * l + 1) * N;
+      sc.push_back(SimpleCall{h->sn_out[l], n, h->X[l], h->ldr[l], h->gam + 2 * l + 1, px});
+      sc.push_back(SimpleCall{h->sn_in[l], n, h->Y[l], h->ldp[l], h->gam + 2 * l, py});
+    }
+    ProfScope ps(NG_PROF_NG_APPLY, st, 0.0, 0.0);
+    NG_TRY(ngsimple_precondition_group_impl(sc.data(), (int)sc.size()));
+  } else if (h->cfg.precond) {
     // all 2I preconditioning calls of the step as one group: one launch per
     // NG phase for every tensor-core-eligible state
     std::vector<NgCall> calls;
@@ -807,7 +830,7 @@ ng_status nnet_set_params(nnet_t h, int32_t layer, const float* host, int64_t co
 
 ng_status nnet_get_ngsgd(nnet_t h, int32_t layer, int32_t side, ngsgd_t* out) {
   NG_REQUIRE(h && out, NG_EINVAL, "NULL argument");
-  NG_REQUIRE(h->cfg.precond != 0, NG_ESTATE, "network has no preconditioners");
+  NG_REQUIRE(h->cfg.precond == 1, NG_ESTATE, "network has no online NG-SGD preconditioners");
   NG_REQUIRE(layer >= 0 && layer < h->L && (side == 0 || side == 1), NG_EINVAL, "bad layer/side");
   *out = side == 0 ? h->ng_in[layer] : h->ng_out[layer];
   return NG_OK;

@@ -13,7 +13,7 @@ HEADER = os.path.join(ROOT, "include", "ngsgd.h")
 def _declared():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b((?:ng|ngsgd|nnet)_[a-z0-9_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b((?:ng|ngsgd|ngsimple|nnet)_[a-z0-9_]+)\s*\(", src)))
 
 
 def _lib_path():
