@@ -262,6 +262,21 @@ ng_status nnet_comm_init(nnet_t h, const void* nccl_unique_id, int32_t rank, int
  * then scale (speed reference; order not fixed).  Synchronises the stream. */
 ng_status nnet_average(nnet_t h, int32_t mode);
 
+/* Best-of-n in place of the average on an outer iteration that follows a random
+ * initialisation: every rank passes the objective of its job on the data it
+ * trained on (host double, e.g. the mean log-likelihood per frame of its last outer
+ * iteration); the objectives are all-gathered, the best one wins (ties: the lowest rank)
+ * and its parameters are broadcast to every rank (NCCL, in place).  NG states untouched.
+ * winner_out (host, may be NULL) receives the winning rank.  Synchronises. */
+ng_status nnet_select_best(nnet_t h, double objective, int32_t* winner_out);
+
+/* The n networks `nets` (same shapes, same device, n <= 64) all receive the average of
+ * their parameters, summed in the fixed pairwise tree order of nnet_average (bit-exact
+ * with it): the single-device form of the every-K average, for running several jobs on one
+ * GPU (experiments).  Stream-ordered on nets[0]'s stream after
+ * synchronising the others. */
+ng_status nnet_average_local(nnet_t* nets, int32_t n);
+
 
 /* The fixed-order sum kernel of nnet_average on its own, for bit-exact tests on one GPU:
  * out[i] = (sum over r of in[r * count + i]) * (1.0f / nr), summed in the pairwise tree order

@@ -90,6 +90,8 @@ SIGNATURES = {
                                      c_int32, c_void_p, c_int64, c_int32, c_int32, c_void_p]),
     "ng_debug_gemm_tc": (c_int32, [c_int32, c_int32, c_int32, c_void_p, c_int64, c_int32, c_void_p, c_int64,
                                    c_int32, c_void_p, c_int64, c_int32, c_int32, c_int32, c_void_p]),
+    "nnet_select_best": (c_int32, [c_void_p, c_double, ctypes.POINTER(c_int32)]),
+    "nnet_average_local": (c_int32, [ctypes.POINTER(c_void_p), c_int32]),
     "ngsimple_create": (c_int32, [c_int32, c_int32, c_float, c_void_p, ctypes.POINTER(c_void_p)]),
     "ngsimple_destroy": (c_int32, [c_void_p]),
     "ngsimple_precondition": (c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_void_p, c_void_p]),

@@ -244,6 +244,18 @@ class Nnet:
     def average(self, mode: int = 0) -> None:
         check(lib.nnet_average(self._h, int(mode)))
 
+    def select_best(self, objective: float) -> int:
+        """Best-of-n instead of the average after a random initialisation."""
+        w = ctypes.c_int32()
+        check(lib.nnet_select_best(self._h, float(objective), ctypes.byref(w)))
+        return w.value
+
+
+def average_local(nets) -> None:
+    """Average several networks living on the current device (nnet_average_local)."""
+    arr = (ctypes.c_void_p * len(nets))(*[n._h.value for n in nets])
+    check(lib.nnet_average_local(arr, len(nets)))
+
 
 def profile_enable(groups) -> None:
     """Time every launch of the named kernel groups with CUDA events (ng_profile_enable)."""

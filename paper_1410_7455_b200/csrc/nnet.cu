@@ -61,6 +61,8 @@ struct nnet_ctx {
   int rank = 0, nranks = 1;
   float* recvbuf = nullptr;     // nranks x shard: shard `rank` of every rank
   float* gatherbuf = nullptr;   // nranks x shard: averaged shards (all-gather target)
+  double* objbuf = nullptr;     // nranks: all-gathered objectives (nnet_select_best)
+  float* localsum = nullptr;    // nnet_average_local: the averaged arena
   size_t shard = 0;
 };
 
@@ -457,6 +459,8 @@ static void nnet_free(nnet_ctx* h) {
   if (h->eflags) cudaFree(h->eflags);
   if (h->recvbuf) cudaFree(h->recvbuf);
   if (h->gatherbuf) cudaFree(h->gatherbuf);
+  if (h->objbuf) cudaFree(h->objbuf);
+  if (h->localsum) cudaFree(h->localsum);
   if (h->comm) ncclCommDestroy(h->comm);
   if (h->gpart) cudaFree(h->gpart);
   delete h;
@@ -907,6 +911,58 @@ ng_status nnet_average(nnet_t h, int32_t mode) {
   if (r != ncclSuccess) { set_error(std::string("nnet_average: ") + ncclGetErrorString(r)); return NG_ENCCL; }
   NG_CUDA_TRY(cudaStreamSynchronize(st));
   return read_eflags(h, "nnet_average");
+}
+
+ng_status nnet_select_best(nnet_t h, double objective, int32_t* winner_out) {
+  NG_REQUIRE(h != nullptr, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(h->comm != nullptr, NG_ENCCL, "nnet_comm_init not called");
+  NG_REQUIRE(std::isfinite(objective), NG_EINVAL, "objective must be finite");
+  cudaStream_t st = h->st;
+  const int nr = h->nranks;
+  if (!h->objbuf) NG_TRY(nalloc(&h->objbuf, 2 * (size_t)nr));
+  NG_CUDA_TRY(cudaMemcpyAsync(h->objbuf + nr, &objective, sizeof(double), cudaMemcpyHostToDevice, st));
+  ncclResult_t r = ncclAllGather(h->objbuf + nr, h->objbuf, 1, ncclDouble, h->comm, st);
+  if (r != ncclSuccess) { set_error(std::string("nnet_select_best: ") + ncclGetErrorString(r)); return NG_ENCCL; }
+  std::vector<double> all(nr);
+  NG_CUDA_TRY(cudaMemcpyAsync(all.data(), h->objbuf, sizeof(double) * nr, cudaMemcpyDeviceToHost, st));
+  NG_CUDA_TRY(cudaStreamSynchronize(st));
+  int win = 0;                                  // the best objective; ties -> the lowest rank
+  for (int p = 1; p < nr; ++p)
+    if (all[p] > all[win]) win = p;
+  r = ncclBroadcast(h->arena, h->arena, h->arena_count, ncclFloat, win, h->comm, st);
+  if (r != ncclSuccess) { set_error(std::string("nnet_select_best: ") + ncclGetErrorString(r)); return NG_ENCCL; }
+  NG_CUDA_TRY(cudaStreamSynchronize(st));
+  if (winner_out) *winner_out = win;
+  return read_eflags(h, "nnet_select_best");
+}
+
+ng_status nnet_average_local(nnet_t* nets, int32_t n) {
+  NG_REQUIRE(nets != nullptr && n >= 1 && n <= kMaxRanks, NG_EINVAL, "bad network list (1 <= n <= 64)");
+  nnet_ctx* h0 = nets[0];
+  NG_REQUIRE(h0 != nullptr, NG_EINVAL, "NULL network");
+  for (int q = 1; q < n; ++q) {
+    NG_REQUIRE(nets[q] != nullptr && nets[q]->arena_count == h0->arena_count, NG_ESHAPE,
+               "nnet_average_local: networks of different shapes");
+    NG_TRY(nnet_join(nets[q]));
+    NG_CUDA_TRY(cudaStreamSynchronize(nets[q]->st));
+  }
+  NG_TRY(nnet_join(h0));
+  const size_t count = h0->arena_count;
+  cudaStream_t st = h0->st;
+  // stack the arenas (rank order) and sum them in the fixed tree of nnet_average
+  float* stack = nullptr;
+  NG_CUDA_TRY(cudaMallocAsync((void**)&stack, sizeof(float) * count * (n + 1), st));
+  for (int q = 0; q < n; ++q)
+    NG_CUDA_TRY(cudaMemcpyAsync(stack + (size_t)q * count, nets[q]->arena, sizeof(float) * count,
+                                cudaMemcpyDeviceToDevice, st));
+  ng_status s = launch_tree_avg(st, n, count, count, stack, stack + (size_t)n * count);
+  for (int q = 0; q < n && s == NG_OK; ++q)
+    if (cudaMemcpyAsync(nets[q]->arena, stack + (size_t)n * count, sizeof(float) * count, cudaMemcpyDeviceToDevice,
+                        st) != cudaSuccess) s = NG_ECUDA;
+  cudaFreeAsync(stack, st);
+  if (s != NG_OK) return s;
+  NG_CUDA_TRY(cudaStreamSynchronize(st));
+  return NG_OK;
 }
 
 ng_status ng_debug_tree_avg(int32_t nr, int64_t count, const float* in, float* out, void* stream) {

@@ -57,3 +57,34 @@ def test_comm_rejects_bad_nranks(lib):
         net.comm_init(api.comm_unique_id(), 0, 65)
     with pytest.raises(api.NgError):
         net.comm_init(api.comm_unique_id(), 3, 3)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 6])
+def test_average_local_bit_exact(lib, n):
+    """nnet_average_local (several jobs on one GPU; the f2 experiment's average): every
+    network gets the oracle's fixed-tree float32 mean of all of them, bit-exact."""
+    from paper_1410_7455_b200 import api
+    nets = [api.Nnet(40, 1, 200, 10, 16, max_minibatch=8, precond=False, seed=10 + q) for q in range(n)]
+    models = [[net.get_params(l) for l in range(2)] for net in nets]
+    rng = np.random.default_rng(n)
+    for q, net in enumerate(nets):          # non-zero softmax layers too
+        w = (rng.normal(size=models[q][1].shape) * 0.1).astype(np.float32)
+        net.set_params(1, w)
+        models[q][1] = w
+    api.average_local(nets)
+    ref = otr.average_models(models, dtype=np.float32)
+    for net in nets:
+        for l in range(2):
+            assert np.array_equal(net.get_params(l), ref[l])
+
+
+def test_select_best_single_rank(lib):
+    """nnet_select_best at nranks = 1: the only job wins and its parameters
+    are unchanged (the broadcast from itself is a no-op)."""
+    from paper_1410_7455_b200 import api
+    net = api.Nnet(40, 1, 200, 10, 16, max_minibatch=8, precond=False, seed=5)
+    before = [net.get_params(l) for l in range(2)]
+    net.comm_init(api.comm_unique_id(), 0, 1)
+    assert net.select_best(-3.25) == 0
+    for l in range(2):
+        assert np.array_equal(net.get_params(l), before[l])
