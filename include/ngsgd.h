@@ -201,6 +201,32 @@ ng_status nnet_destroy(nnet_t h);
 ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld,
                                 const int32_t* labels, int32_t n, double* objective_out);
 
+/* Input descriptor of nnet_forward_backward_ex (the step before the hot path, C.2,
+ * P:1459-1485):
+ *   frames  device; format 0: float32 [rows][ld]; format 1: uint8 codes [rows][ld] of the
+ *           1-byte lossy compression (R36), decoded in the input
+ *           kernel as float(lo[c] + step[c] * q) with lo, step device double[input_dim]
+ *           (see ng_compress_frames).
+ *   rows    device int32[n] or NULL: minibatch row r is frame row rows[r] (a block of the
+ *           N x M randomisation, resident in device memory); NULL = rows 0..n-1.
+ *   labels  device int32, indexed like the frame rows. */
+typedef struct {
+  const void* frames;
+  int32_t format;
+  int64_t ld;
+  const double* lo;
+  const double* step;
+  const int32_t* rows;
+  const int32_t* labels;
+} nnet_input;
+ng_status nnet_forward_backward_ex(nnet_t h, const nnet_input* in, int32_t n, double* objective_out);
+
+/* 1-byte compression of n frames (R36): per column lo = min, step = (max - min)/255 (FP64),
+ * q = clamp(round_half_even((x - lo)/step), 0, 255).  All pointers device; x is n x dim
+ * (ld ldx), q n x dim (ld ldq), lo/step double[dim].  Stream-ordered on `stream`. */
+ng_status ng_compress_frames(int32_t n, int32_t dim, const float* x, int64_t ldx, uint8_t* q, int64_t ldq,
+                             double* lo, double* step, void* stream);
+
 /* The objective of the last nnet_forward_backward, without synchronising: enqueues the
  * fixed-order sum over the minibatch's rows (same value as objective_out above) and an
  * asynchronous device-to-host copy into `host_out` (host double*, should be pinned) on the

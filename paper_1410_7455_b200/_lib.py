@@ -43,6 +43,11 @@ class NnetConfig(ctypes.Structure):
                 ("ng_out", NgsgdConfig), ("precision", c_int32), ("seed", ctypes.c_uint64), ("renorm", c_int32)]
 
 
+class NnetInput(ctypes.Structure):
+    _fields_ = [("frames", c_void_p), ("format", c_int32), ("ld", c_int64), ("lo", c_void_p), ("step", c_void_p),
+                ("rows", c_void_p), ("labels", c_void_p)]
+
+
 class NnetUpdateStats(ctypes.Structure):
     _fields_ = [("alpha_t", c_float * 16), ("gamma_in", c_float * 16), ("gamma_out", c_float * 16),
                 ("updated_in", c_int32 * 16), ("updated_out", c_int32 * 16)]
@@ -90,6 +95,9 @@ SIGNATURES = {
                                      c_int32, c_void_p, c_int64, c_int32, c_int32, c_void_p]),
     "ng_debug_gemm_tc": (c_int32, [c_int32, c_int32, c_int32, c_void_p, c_int64, c_int32, c_void_p, c_int64,
                                    c_int32, c_void_p, c_int64, c_int32, c_int32, c_int32, c_void_p]),
+    "nnet_forward_backward_ex": (c_int32, [c_void_p, ctypes.POINTER(NnetInput), c_int32, ctypes.POINTER(c_double)]),
+    "ng_compress_frames": (c_int32, [c_int32, c_int32, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
+                                     c_void_p]),
     "nnet_select_best": (c_int32, [c_void_p, c_double, ctypes.POINTER(c_int32)]),
     "nnet_average_local": (c_int32, [ctypes.POINTER(c_void_p), c_int32]),
     "ngsimple_create": (c_int32, [c_int32, c_int32, c_float, c_void_p, ctypes.POINTER(c_void_p)]),

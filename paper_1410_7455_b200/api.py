@@ -200,6 +200,31 @@ class Nnet:
                                         ctypes.byref(out) if objective else None))
         return out.value if objective else None
 
+    def forward_backward_ex(self, frames: torch.Tensor, labels: torch.Tensor, n: int, rows: Optional[torch.Tensor] = None,
+                            lo: Optional[torch.Tensor] = None, step: Optional[torch.Tensor] = None,
+                            objective: bool = False):
+        """nnet_forward_backward_ex: float32 or uint8-coded frames (C.2 compression, with lo /
+        step), optionally gathered by a device row index (a block of the N x M randomisation)."""
+        if frames.dtype == torch.uint8:
+            fmt = 1
+            if lo is None or step is None or lo.dtype != torch.float64 or step.dtype != torch.float64:
+                raise ValueError("uint8 frames need float64 lo and step")
+        elif frames.dtype == torch.float32:
+            fmt = 0
+        else:
+            raise ValueError("frames must be float32 or uint8")
+        if frames.dim() != 2 or frames.stride(1) != 1 or not frames.is_cuda:
+            raise ValueError("frames must be a CUDA matrix with unit column stride")
+        if rows is not None and (rows.dtype != torch.int32 or not rows.is_cuda):
+            raise ValueError("rows must be a CUDA int32 vector")
+        if labels.dtype != torch.int32 or not labels.is_cuda:
+            raise ValueError("labels must be a CUDA int32 vector")
+        inp = _lib.NnetInput(_ptr(frames), fmt, frames.stride(0), _ptr(lo), _ptr(step), _ptr(rows), _ptr(labels))
+        out = ctypes.c_double() if objective else None
+        check(lib.nnet_forward_backward_ex(self._h, ctypes.byref(inp), int(n),
+                                           ctypes.byref(out) if objective else None))
+        return out.value if objective else None
+
     def objective_async(self, host_out: torch.Tensor) -> None:
         """Enqueue the readback of the last forward_backward's objective into a pinned CPU
         float64 tensor (nnet_objective_async); valid once the net's stream gets there."""
@@ -249,6 +274,17 @@ class Nnet:
         w = ctypes.c_int32()
         check(lib.nnet_select_best(self._h, float(objective), ctypes.byref(w)))
         return w.value
+
+
+def compress_frames(x: torch.Tensor):
+    """ng_compress_frames: (q uint8, lo float64, step float64) of a CUDA float32 matrix (R36)."""
+    ld = _check_matrix(x)
+    n, d = x.shape
+    q = torch.empty((n, d), dtype=torch.uint8, device=x.device)
+    lo = torch.empty(d, dtype=torch.float64, device=x.device)
+    step = torch.empty(d, dtype=torch.float64, device=x.device)
+    check(lib.ng_compress_frames(n, d, _ptr(x), ld, _ptr(q), d, _ptr(lo), _ptr(step), _stream_handle(None)))
+    return q, lo, step
 
 
 def average_local(nets) -> None:

@@ -48,6 +48,7 @@ struct nnet_ctx {
   float* stats = nullptr;     // L x 4: alpha_t, gamma_in, gamma_out, bound
   double* objrows = nullptr;  // max_minibatch
   float* rscale = nullptr;    // (L-1) x max_minibatch: renormalisation scale s per hidden layer row
+  int32_t* lab = nullptr;     // max_minibatch: labels of a gathered minibatch
   double* obj = nullptr;      // 1
   int* eflags = nullptr;      // sticky error bits
   int n_last = 0;
@@ -95,20 +96,69 @@ __global__ void init_weights_kernel(float* W, int rows, int cols, int ld, uint64
   }
 }
 
-// Y_1 = [frames, 1], zero padding columns.
-__global__ void input_kernel(int n, int din, const float* __restrict__ f, int64_t ldf, float* __restrict__ Y,
-                             int ldy, int* eflags) {
+// Y_1 = [frames, 1], zero padding columns.  Frames are FP32, or 1-byte codes
+// decoded as x = float(lo_c + step_c q) (C.2, reading R36); row r of the
+// minibatch is row rows[r] of the frame array when rows != NULL (a block of the N x M
+// randomisation), whose label is copied to lab_out[r].
+__global__ void input_kernel(int n, int din, const void* __restrict__ f, int fmt, int64_t ldf,
+                             const double* __restrict__ lo, const double* __restrict__ step,
+                             const int32_t* __restrict__ rows, const int32_t* __restrict__ lab_in,
+                             int32_t* __restrict__ lab_out, float* __restrict__ Y, int ldy, int* eflags) {
   pdl_trigger();
   pdl_wait();   // launched with launch_pdl: inputs come from the previous kernel
   const int64_t total = (int64_t)n * ldy;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(i / ldy), c = (int)(i % ldy);
+    const int64_t src = rows ? (int64_t)rows[r] : (int64_t)r;
     float v = 0.f;
     if (c < din) {
-      v = f[(int64_t)r * ldf + c];
+      if (fmt == 1) {
+        const uint8_t q = reinterpret_cast<const uint8_t*>(f)[src * ldf + c];
+        v = (float)(lo[c] + step[c] * (double)q);
+      } else {
+        v = reinterpret_cast<const float*>(f)[src * ldf + c];
+      }
       if (!isfinite(v)) atomicOr(reinterpret_cast<unsigned*>(eflags), kErrNonFinite);
-    } else if (c == din) v = 1.f;
+    } else if (c == din) {
+      v = 1.f;
+      if (lab_out) lab_out[r] = lab_in[src];
+    }
     Y[i] = v;
+  }
+}
+
+// 1-byte compression (R36), column c: lo = min_r x[r, c], step = (max - min) / 255
+// (FP64 from the FP32 extremes).  One CTA per column, fixed-order reductions.
+__global__ void __launch_bounds__(256)
+compress_range_kernel(int n, int D, const float* __restrict__ x, int64_t ldx, double* __restrict__ lo,
+                      double* __restrict__ step) {
+  __shared__ float sc[32];
+  const int c = blockIdx.x;
+  float mn = INFINITY, mx = -INFINITY;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {
+    const float v = x[(int64_t)r * ldx + c];
+    mn = fminf(mn, v);
+    mx = fmaxf(mx, v);
+  }
+  mx = block_max(mx, sc);
+  __syncthreads();
+  mn = -block_max(-mn, sc);
+  if (threadIdx.x == 0) {
+    lo[c] = (double)mn;
+    step[c] = ((double)mx - (double)mn) / 255.0;
+  }
+}
+
+// q = clamp(rint((x - lo) / step), 0, 255) in FP64 (0 where step = 0)  (R36)
+__global__ void compress_codes_kernel(int n, int D, const float* __restrict__ x, int64_t ldx,
+                                      const double* __restrict__ lo, const double* __restrict__ step,
+                                      uint8_t* __restrict__ q, int64_t ldq) {
+  const int64_t total = (int64_t)n * D;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / D), c = (int)(i % D);
+    const double s = step[c];
+    const double t = s > 0.0 ? ((double)x[(int64_t)r * ldx + c] - lo[c]) / s : 0.0;
+    q[(int64_t)r * ldq + c] = (uint8_t)fmin(255.0, fmax(0.0, rint(t)));
   }
 }
 
@@ -455,6 +505,7 @@ static void nnet_free(nnet_ctx* h) {
   if (h->stats) cudaFree(h->stats);
   if (h->objrows) cudaFree(h->objrows);
   if (h->rscale) cudaFree(h->rscale);
+  if (h->lab) cudaFree(h->lab);
   if (h->obj) cudaFree(h->obj);
   if (h->eflags) cudaFree(h->eflags);
   if (h->recvbuf) cudaFree(h->recvbuf);
@@ -549,6 +600,7 @@ ng_status nnet_create(const nnet_config* cfg, void* cuda_stream, nnet_t* out) {
   if (s == NG_OK) s = nalloc(&h->scale, h->L);
   if (s == NG_OK) s = nalloc(&h->stats, 4 * h->L);
   if (s == NG_OK) s = nalloc(&h->objrows, N);
+  if (s == NG_OK) s = nalloc(&h->lab, N);
   if (s == NG_OK && cfg->renorm) s = nalloc(&h->rscale, (size_t)std::max(1, h->L - 1) * N);
   if (s == NG_OK) s = nalloc(&h->obj, 1);
   if (s == NG_OK) s = nalloc(&h->eflags, 1);
@@ -618,16 +670,28 @@ ng_status nnet_layer_shape(nnet_t h, int32_t layer, int32_t* rows, int32_t* cols
 ng_status nnet_forward_backward(nnet_t h, const float* frames, int64_t ld, const int32_t* labels, int32_t n,
                                 double* objective_out) {
   NG_REQUIRE(h && frames && labels, NG_EINVAL, "NULL argument");
+  nnet_input in;
+  std::memset(&in, 0, sizeof(in));
+  in.frames = frames; in.format = 0; in.ld = ld; in.labels = labels;
+  return nnet_forward_backward_ex(h, &in, n, objective_out);
+}
+
+ng_status nnet_forward_backward_ex(nnet_t h, const nnet_input* in, int32_t n, double* objective_out) {
+  NG_REQUIRE(h && in && in->frames && in->labels, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(in->format == 0 || in->format == 1, NG_EINVAL, "format must be 0 (float32) or 1 (uint8 codes)");
+  NG_REQUIRE(in->format == 0 || (in->lo && in->step), NG_EINVAL, "uint8 frames need lo and step");
   NG_REQUIRE(n >= 1 && n <= h->cfg.max_minibatch, NG_ESHAPE, "n must be in [1, max_minibatch]");
-  NG_REQUIRE(ld >= h->cfg.input_dim, NG_ESHAPE, "ld < input_dim");
+  NG_REQUIRE(in->ld >= h->cfg.input_dim, NG_ESHAPE, "ld < input_dim");
   cudaStream_t st = h->st;
   const int L = h->L, G = h->cfg.pnorm_group;
   const bool tc = h->cfg.precision != NG_FP32_SIMT;   // tcgen05 (TF32, or 3xTF32 in NG_FP32)
   const bool s3 = h->cfg.precision == NG_FP32;
+  const int32_t* labels = in->rows ? h->lab : in->labels;
   {
     const int64_t tot = (int64_t)n * h->ldp[0];
     NG_CUDA_TRY(launch_pdl(input_kernel, dim3(std::min(4096, ceil_div(tot, 256))), dim3(256), 0, st, n,
-                           h->cfg.input_dim, frames, ld, h->Y[0], h->ldp[0], h->eflags));
+                           h->cfg.input_dim, in->frames, (int)in->format, in->ld, in->lo, in->step, in->rows,
+                           in->labels, in->rows ? h->lab : (int32_t*)nullptr, h->Y[0], h->ldp[0], h->eflags));
     NG_TRY(check_launch("input_kernel"));
   }
   // forward
@@ -963,6 +1027,18 @@ ng_status nnet_average_local(nnet_t* nets, int32_t n) {
   if (s != NG_OK) return s;
   NG_CUDA_TRY(cudaStreamSynchronize(st));
   return NG_OK;
+}
+
+ng_status ng_compress_frames(int32_t n, int32_t dim, const float* x, int64_t ldx, uint8_t* q, int64_t ldq, double* lo,
+                             double* step, void* stream) {
+  NG_REQUIRE(x && q && lo && step, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(n >= 1 && dim >= 1 && ldx >= dim && ldq >= dim, NG_ESHAPE, "bad shape");
+  cudaStream_t st = (cudaStream_t)stream;
+  compress_range_kernel<<<dim, 256, 0, st>>>(n, dim, x, ldx, lo, step);
+  NG_TRY(check_launch("compress_range_kernel"));
+  compress_codes_kernel<<<std::min(4096, ceil_div((int64_t)n * dim, 256)), 256, 0, st>>>(n, dim, x, ldx, lo, step, q,
+                                                                                       ldq);
+  return check_launch("compress_codes_kernel");
 }
 
 ng_status ng_debug_tree_avg(int32_t nr, int64_t count, const float* in, float* out, void* stream) {

@@ -93,3 +93,27 @@ def tree_reduce_stride(values):
             v[k] = (v[k] + v[k + w]).astype(v[k].dtype)
         w *= 2
     return v[0]
+
+
+def outer_iterations_per_epoch(num_examples: int, n_jobs: int, k_samples: int = K_SAMPLES) -> int:
+    """M >= 1: the number of outer iterations per epoch, chosen so that each job's block of
+    an outer iteration holds close to K samples (C.2)."""
+    return max(1, int(round(num_examples / float(n_jobs * k_samples))))
+
+
+def block_randomize(num_examples: int, n_jobs: int, k_samples: int = K_SAMPLES, seed: int = 1410):
+    """The N x M data blocks of C.2: one random permutation of the examples
+    (fixed by the seed, so every epoch reads the same order) cut into N M
+    nearly equal blocks; job n processes blocks[n][m] on outer iteration m.  Returns int32
+    index arrays (host), to be uploaded once and used as the `rows` of
+    nnet_forward_backward_ex."""
+    import numpy as np
+    m = outer_iterations_per_epoch(num_examples, n_jobs, k_samples)
+    perm = np.random.default_rng(seed).permutation(num_examples)
+    nb = n_jobs * m
+    base, extra = divmod(num_examples, nb)            # the first `extra` blocks get one more
+    bounds = [0]
+    for q in range(nb):
+        bounds.append(bounds[-1] + base + (1 if q < extra else 0))
+    chunks = [perm[bounds[q]:bounds[q + 1]].astype(np.int32) for q in range(nb)]
+    return [[chunks[b * n_jobs + n] for b in range(m)] for n in range(n_jobs)]

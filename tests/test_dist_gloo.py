@@ -92,3 +92,18 @@ def test_outer_iteration_sizes():
     b = [driver.shard_bounds(count, 6, r) for r in range(6)]
     assert b[0][0] == 0 and b[-1][1] == count and all(b[r][1] == b[r + 1][0] for r in range(5))
     assert driver.shard_size(count, 6) % 64 == 0
+
+
+def test_block_randomize_matches_oracle_and_partitions_jobs():
+    """driver.block_randomize (the product's data schedule) against the oracle's C.2 blocks:
+    same examples in every block (the product uses balanced integer cut points, the oracle
+    numpy.array_split: equal sizes up to one), disjoint across jobs."""
+    from oracle import data as odata
+    for F, N, K in [(10_000, 1, 400), (100_003, 4, 3000), (262_144, 8, 32_768)]:
+        a = driver.block_randomize(F, N, K, seed=11)
+        b = odata.block_randomize(F, N, K, seed=11)
+        assert len(a) == len(b) == N
+        flat_a = np.concatenate([blk for row in a for blk in row])
+        flat_b = np.concatenate([blk for row in b for blk in row])
+        assert np.array_equal(np.sort(flat_a), np.arange(F)) and np.array_equal(flat_a, flat_b)
+        assert max(len(x) for row in a for x in row) - min(len(x) for row in a for x in row) <= 1
