@@ -22,6 +22,7 @@
 #include "eig_jacobi.cuh"
 #include "eig_dc.cuh"
 #include "eig_tri.cuh"
+#include "eig_topr.cuh"
 #include "gemm_simt.cuh"
 #include "gemm_tc.cuh"
 #include "ngsgd_impl.cuh"
@@ -797,6 +798,10 @@ init_eig_kernel(int ne, double* A, double* Vt, double* Vs, double* lam, int* ws_
   eig_sort_desc(A, ne, Vt, ne, ne, lam, Vs, ne, ws_int + 2 * m + 1);
 }
 
+// Top-R eigenpairs of the init matrix (eig_topr.cuh), one CTA: lam (descending) and the
+// eigenvector rows X (R x ne).
+__global__ void __launch_bounds__(1024) init_topr_kernel(int ne, int R, ToprWork w) { eig_topr(ne, R, w); }
+
 // rho_0, d_0, E_0 and W_0 = E_0^{1/2} R_0.  R0 (R x D,
 // double) holds either eigenvector rows of S_0 (gram = 0) or rows X^T v (gram = 1),
 // which are normalised here by 1/sqrt(N lambda); numerically-null directions are
@@ -1042,11 +1047,24 @@ static ng_status ngsgd_init(ngsgd_ctx* h, int n, const float* x, int64_t ld, dou
     else        // A = S_0 = X^T X / N  (D x D)
       s = gemm_simt<double, false, false>(st, D, D, n, X64, D, X64, D, EpiStore<double>{A, D, 1.0 / n});
   }
-  if (s == NG_OK) {
+  const int n_avail = std::min(ne, R);
+  double* topw = nullptr;
+  static const int use_jacobi = tune_int("NG_TUNE_INIT_JACOBI", 0);   // the round-1 solver (comparisons)
+  const bool topr = !use_jacobi && ne <= kToprMaxN && n_avail <= kToprMaxR && n_avail >= 1;
+  if (s == NG_OK && topr) {
+    // Householder + multisection + inverse iteration for the top R only (eig_topr.cuh)
+    s = dalloc(&topw, (size_t)3 * ne + (size_t)(1 + 3 * n_avail) * ne);
+    if (s == NG_OK) {
+      ToprWork w;
+      w.A = A; w.V = Vt; w.tau = topw; w.d = topw + ne; w.e = topw + 2 * ne; w.X = Vs; w.lam = lam;
+      w.scr = topw + 3 * ne;
+      init_topr_kernel<<<1, 1024, 0, st>>>(ne, n_avail, w);
+      s = check_launch("init_topr_kernel");
+    }
+  } else if (s == NG_OK) {
     init_eig_kernel<<<1, 1024, 0, st>>>(ne, A, Vt, Vs, lam, wsi, wsd);
     s = check_launch("init_eig_kernel");
   }
-  const int n_avail = std::min(ne, R);
   if (s == NG_OK && R > 0) {
     if (gram)   // R0raw = Vs[:R] X  (rows X^T v_r)
       s = gemm_simt<double, true, false>(st, n_avail, D, n, Vs, n, X64, D, EpiStore<double>{R0, D, 1.0});
@@ -1063,6 +1081,7 @@ static ng_status ngsgd_init(ngsgd_ctx* h, int n, const float* x, int64_t ld, dou
     if (e != cudaSuccess) { set_error(std::string("ngsgd init: ") + cudaGetErrorString(e)); s = NG_ECUDA; }
   }
   cudaFree(X64); cudaFree(A); cudaFree(Vt); cudaFree(Vs); cudaFree(lam); cudaFree(R0); cudaFree(wsd); cudaFree(wsi);
+  if (topw) cudaFree(topw);
   if (s == NG_OK) h->initialized = true;   // t is not reset (reading R7)
   return s;
 }
