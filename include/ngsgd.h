@@ -221,6 +221,21 @@ typedef struct {
 } nnet_input;
 ng_status nnet_forward_backward_ex(nnet_t h, const nnet_input* in, int32_t n, double* objective_out);
 
+/* ------------------------------------------ generalised model combination (C.4) ---- */
+/* The parameter arena (all W_l, FP32, layout of nnet_create) as a flat vector: its length,
+ * and a copy to (direction 0) or from (direction 1) a caller-owned device buffer -- the
+ * snapshots of the last P outer iterations' models.  Stream-ordered. */
+ng_status nnet_arena_size(nnet_t h, int64_t* count);
+ng_status nnet_copy_arena(nnet_t h, float* dev, int32_t direction);
+/* W_l = sum_p weights[l P + p] W_l^(p): models is a HOST array of P <= 32
+ * device arena pointers (snapshots), weights host float[L x P].  Stream-ordered. */
+ng_status nnet_set_combination(nnet_t h, const float* const* models, int32_t P, const float* weights);
+/* After nnet_forward_backward: grad[l P + p] = <X_l^T Y_l, W_l^(p)>_F, the derivative of the
+ * minibatch objective w.r.t. the combination weight w[l][p] (chain rule through
+ * W_l = sum_p w[l][p] W_l^(p)); host double[L x P].  Synchronises.  The L-BFGS search over
+ * the weights is host logic (driver.combine_models). */
+ng_status nnet_combination_grad(nnet_t h, const float* const* models, int32_t P, double* grad);
+
 /* 1-byte compression of n frames (R36): per column lo = min, step = (max - min)/255 (FP64),
  * q = clamp(round_half_even((x - lo)/step), 0, 255).  All pointers device; x is n x dim
  * (ld ldx), q n x dim (ld ldq), lo/step double[dim].  Stream-ordered on `stream`. */

@@ -98,6 +98,10 @@ SIGNATURES = {
     "nnet_forward_backward_ex": (c_int32, [c_void_p, ctypes.POINTER(NnetInput), c_int32, ctypes.POINTER(c_double)]),
     "ng_compress_frames": (c_int32, [c_int32, c_int32, c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
                                      c_void_p]),
+    "nnet_arena_size": (c_int32, [c_void_p, ctypes.POINTER(c_int64)]),
+    "nnet_copy_arena": (c_int32, [c_void_p, c_void_p, c_int32]),
+    "nnet_set_combination": (c_int32, [c_void_p, ctypes.POINTER(c_void_p), c_int32, ctypes.POINTER(c_float)]),
+    "nnet_combination_grad": (c_int32, [c_void_p, ctypes.POINTER(c_void_p), c_int32, ctypes.POINTER(c_double)]),
     "nnet_select_best": (c_int32, [c_void_p, c_double, ctypes.POINTER(c_int32)]),
     "nnet_average_local": (c_int32, [ctypes.POINTER(c_void_p), c_int32]),
     "ngsimple_create": (c_int32, [c_int32, c_int32, c_float, c_void_p, ctypes.POINTER(c_void_p)]),

@@ -269,6 +269,37 @@ class Nnet:
     def average(self, mode: int = 0) -> None:
         check(lib.nnet_average(self._h, int(mode)))
 
+    def arena_size(self) -> int:
+        c = ctypes.c_int64()
+        check(lib.nnet_arena_size(self._h, ctypes.byref(c)))
+        return c.value
+
+    def snapshot(self) -> torch.Tensor:
+        """A device copy of the parameter arena (a model of one outer iteration, C.4)."""
+        t = torch.empty(self.arena_size(), dtype=torch.float32, device="cuda")
+        check(lib.nnet_copy_arena(self._h, _ptr(t), 0))
+        return t
+
+    def load_snapshot(self, t: torch.Tensor) -> None:
+        check(lib.nnet_copy_arena(self._h, _ptr(t), 1))
+
+    @staticmethod
+    def _models(models):
+        return (ctypes.c_void_p * len(models))(*[m.data_ptr() for m in models])
+
+    def set_combination(self, models, weights: np.ndarray) -> None:
+        """W_l = sum_p weights[l, p] W_l^(p) (nnet_set_combination)."""
+        w = np.ascontiguousarray(weights, dtype=np.float32)
+        check(lib.nnet_set_combination(self._h, self._models(models), len(models),
+                                       w.ctypes.data_as(ctypes.POINTER(ctypes.c_float))))
+
+    def combination_grad(self, models) -> np.ndarray:
+        """d objective / d weights[l, p] of the last forward_backward (nnet_combination_grad)."""
+        g = np.zeros((self.num_layers, len(models)), dtype=np.float64)
+        check(lib.nnet_combination_grad(self._h, self._models(models), len(models),
+                                        g.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return g
+
     def select_best(self, objective: float) -> int:
         """Best-of-n instead of the average after a random initialisation."""
         w = ctypes.c_int32()

@@ -64,6 +64,8 @@ struct nnet_ctx {
   float* gatherbuf = nullptr;   // nranks x shard: averaged shards (all-gather target)
   double* objbuf = nullptr;     // nranks: all-gathered objectives (nnet_select_best)
   float* localsum = nullptr;    // nnet_average_local: the averaged arena
+  float* gradbuf = nullptr;     // arena-sized: X_l^T Y_l of every layer (model combination)
+  double* cgpart = nullptr;     // L x P: combination gradient
   size_t shard = 0;
 };
 
@@ -474,6 +476,36 @@ tree_avg_kernel(int nr, size_t count, size_t stride, const float* __restrict__ r
   }
 }
 
+// Generalised model combination (C.4): W_l = sum_p w[l][p] W_l^(p) over the
+// arena range of layer l (blockIdx.y), and grad[l][p] = <G_l, W_l^(p)> with G_l = X_l^T Y_l
+// (one CTA per (l, p), fixed-order reduction).
+constexpr int kCombMax = 32;
+struct CombineArgs {
+  const float* model[kCombMax];
+  float w[16 * kCombMax];          // L x P
+  int64_t off[17];                 // layer ranges in the arena
+  int P;
+};
+__global__ void __launch_bounds__(256) combine_kernel(const __grid_constant__ CombineArgs a, float* __restrict__ out) {
+  const int l = blockIdx.y;
+  for (int64_t i = a.off[l] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.off[l + 1];
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int p = 0; p < a.P; ++p) acc = fmaf(a.w[l * kCombMax + p], a.model[p][i], acc);
+    out[i] = acc;
+  }
+}
+__global__ void __launch_bounds__(256) combine_grad_kernel(const __grid_constant__ CombineArgs a,
+                                                           const float* __restrict__ G, double* __restrict__ grad) {
+  __shared__ double sc[32];
+  const int l = blockIdx.y, p = blockIdx.x;
+  double acc = 0.0;
+  for (int64_t i = a.off[l] + threadIdx.x; i < a.off[l + 1]; i += blockDim.x)
+    acc = fma((double)G[i], (double)a.model[p][i], acc);
+  acc = block_sum(acc, sc);
+  if (threadIdx.x == 0) grad[l * kCombMax + p] = acc;
+}
+
 static ng_status launch_tree_avg(cudaStream_t st, int nr, size_t count, size_t stride, const float* recv, float* out) {
   if (count == 0) return NG_OK;
   const int blocks = (int)std::min<size_t>(4 * 148, (count + 255) / 256);
@@ -512,6 +544,8 @@ static void nnet_free(nnet_ctx* h) {
   if (h->gatherbuf) cudaFree(h->gatherbuf);
   if (h->objbuf) cudaFree(h->objbuf);
   if (h->localsum) cudaFree(h->localsum);
+  if (h->gradbuf) cudaFree(h->gradbuf);
+  if (h->cgpart) cudaFree(h->cgpart);
   if (h->comm) ncclCommDestroy(h->comm);
   if (h->gpart) cudaFree(h->gpart);
   delete h;
@@ -1027,6 +1061,78 @@ ng_status nnet_average_local(nnet_t* nets, int32_t n) {
   if (s != NG_OK) return s;
   NG_CUDA_TRY(cudaStreamSynchronize(st));
   return NG_OK;
+}
+
+ng_status nnet_arena_size(nnet_t h, int64_t* count) {
+  NG_REQUIRE(h && count, NG_EINVAL, "NULL argument");
+  *count = (int64_t)h->arena_count;
+  return NG_OK;
+}
+
+ng_status nnet_copy_arena(nnet_t h, float* dev, int32_t direction) {
+  NG_REQUIRE(h && dev, NG_EINVAL, "NULL argument");
+  NG_TRY(nnet_join(h));
+  const size_t bytes = sizeof(float) * h->arena_count;
+  NG_CUDA_TRY(cudaMemcpyAsync(direction ? h->arena : dev, direction ? dev : h->arena, bytes, cudaMemcpyDeviceToDevice,
+                              h->st));
+  return NG_OK;
+}
+
+static ng_status comb_args(nnet_ctx* h, const float* const* models, int P, const float* w, CombineArgs* a) {
+  NG_REQUIRE(models != nullptr && P >= 1 && P <= kCombMax, NG_EINVAL, "1 <= P <= 32 models");
+  std::memset(a, 0, sizeof(*a));
+  a->P = P;
+  for (int p = 0; p < P; ++p) { NG_REQUIRE(models[p] != nullptr, NG_EINVAL, "NULL model"); a->model[p] = models[p]; }
+  if (w)
+    for (int l = 0; l < h->L; ++l)
+      for (int p = 0; p < P; ++p) a->w[l * kCombMax + p] = w[l * P + p];
+  for (int l = 0; l < h->L; ++l) a->off[l] = (int64_t)h->off[l];
+  a->off[h->L] = (int64_t)h->arena_count;
+  return NG_OK;
+}
+
+ng_status nnet_set_combination(nnet_t h, const float* const* models, int32_t P, const float* weights) {
+  NG_REQUIRE(h && weights, NG_EINVAL, "NULL argument");
+  CombineArgs a;
+  NG_TRY(comb_args(h, models, P, weights, &a));
+  NG_TRY(nnet_join(h));
+  combine_kernel<<<dim3(std::min<int64_t>(1024, ceil_div(h->arena_count, 256)), h->L), 256, 0, h->st>>>(a, h->arena);
+  return check_launch("combine_kernel");
+}
+
+ng_status nnet_combination_grad(nnet_t h, const float* const* models, int32_t P, double* grad) {
+  NG_REQUIRE(h && grad, NG_EINVAL, "NULL argument");
+  NG_REQUIRE(h->have_fb, NG_ESTATE, "nnet_combination_grad before nnet_forward_backward");
+  CombineArgs a;
+  NG_TRY(comb_args(h, models, P, nullptr, &a));
+  cudaStream_t st = h->st;
+  if (!h->gradbuf) {
+    NG_TRY(nalloc(&h->gradbuf, h->arena_count));
+    NG_TRY(nalloc(&h->cgpart, (size_t)16 * kCombMax));
+    NG_CUDA_TRY(cudaMemsetAsync(h->gradbuf, 0, sizeof(float) * h->arena_count, st));
+  }
+  const int n = h->n_last;
+  // G_l = X_l^T Y_l (the gradient of the objective w.r.t. W_l) for every layer
+  for (int l = 0; l < h->L; ++l) {
+    float* Gl = h->gradbuf + h->off[l];
+    if (h->cfg.precision != NG_FP32_SIMT) {
+      TcEpilogue e;
+      e.kind = TC_EPI_STORE; e.C = Gl; e.ldc = h->ldp[l];
+      NG_TRY(tc_gemm_tf32(st, h->rows[l], h->cols[l], n, h->X[l], h->ldr[l], false, h->Y[l], h->ldp[l], false, e, 128,
+                          1, nullptr, h->cfg.precision == NG_FP32));
+    } else {
+      NG_TRY((gemm_simt<float, false, false>(st, h->rows[l], h->cols[l], n, h->X[l], h->ldr[l], h->Y[l], h->ldp[l],
+                                             EpiStore<float>{Gl, h->ldp[l], 1.f})));
+    }
+  }
+  combine_grad_kernel<<<dim3(P, h->L), 256, 0, st>>>(a, h->gradbuf, h->cgpart);
+  NG_TRY(check_launch("combine_grad_kernel"));
+  std::vector<double> g((size_t)16 * kCombMax);
+  NG_CUDA_TRY(cudaMemcpyAsync(g.data(), h->cgpart, sizeof(double) * g.size(), cudaMemcpyDeviceToHost, st));
+  NG_CUDA_TRY(cudaStreamSynchronize(st));
+  for (int l = 0; l < h->L; ++l)
+    for (int p = 0; p < P; ++p) grad[l * P + p] = g[l * kCombMax + p];
+  return read_eflags(h, "nnet_combination_grad");
 }
 
 ng_status ng_compress_frames(int32_t n, int32_t dim, const float* x, int64_t ldx, uint8_t* q, int64_t ldq, double* lo,

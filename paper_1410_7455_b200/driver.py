@@ -117,3 +117,79 @@ def block_randomize(num_examples: int, n_jobs: int, k_samples: int = K_SAMPLES, 
         bounds.append(bounds[-1] + base + (1 if q < extra else 0))
     chunks = [perm[bounds[q]:bounds[q + 1]].astype(np.int32) for q in range(nb)]
     return [[chunks[b * n_jobs + n] for b in range(m)] for n in range(n_jobs)]
+
+
+COMBINE_REG = 1e-10   # "a very tiny regularizer" on the combination weights
+
+
+def combination_objective(net, models, weights, batches):
+    """Objective sum_i log p(y_i|x_i) of the combined model over the batches (device work:
+    nnet_set_combination, nnet_forward_backward, nnet_combination_grad) minus the tiny
+    regulariser, and its gradient w.r.t. the weights (host arrays)."""
+    import numpy as np
+    net.set_combination(models, weights)
+    obj = 0.0
+    grad = np.zeros_like(weights, dtype=np.float64)
+    for frames, labels in batches:
+        obj += net.forward_backward(frames, labels, objective=True)
+        grad += net.combination_grad(models)
+    return obj - COMBINE_REG * float(np.sum(weights * weights)), grad - 2.0 * COMBINE_REG * weights
+
+
+def combine_models(net, models, batches, iters: int = 20, history: int = 10):
+    """Generalised model combination (C.4): per-layer weights over the last P
+    models maximising the objective on `batches` (device tensors), by L-BFGS (P:1568;
+    two-loop recursion, backtracking Armijo line search; reading R37: no Fisher
+    preconditioning) from the best of the P + 1 starting points (each model, the average,
+    P:1571-1573).  Leaves the net set to the result; returns (weights, objective)."""
+    import numpy as np
+    L, P = net.num_layers, len(models)
+    cands = []
+    for p in range(P):
+        w = np.zeros((L, P))
+        w[:, p] = 1.0
+        cands.append(w)
+    cands.append(np.full((L, P), 1.0 / P))
+    evals = [combination_objective(net, models, w, batches) for w in cands]
+    best = int(np.argmax([e[0] for e in evals]))
+    w, (f, g) = cands[best], evals[best]
+    s_hist, y_hist = [], []
+    for _ in range(iters):
+        # ascent direction from the two-loop recursion on -f
+        q = -g.ravel().copy()
+        alphas = []
+        for s_, y_ in reversed(list(zip(s_hist, y_hist))):
+            a = float(s_ @ q) / float(y_ @ s_)
+            alphas.append(a)
+            q -= a * y_
+        if s_hist:
+            q *= float(s_hist[-1] @ y_hist[-1]) / float(y_hist[-1] @ y_hist[-1])
+        for (s_, y_), a in zip(zip(s_hist, y_hist), reversed(alphas)):
+            b = float(y_ @ q) / float(y_ @ s_)
+            q += (a - b) * s_
+        d = -q.reshape(w.shape)                     # ascent direction for f
+        slope = float(np.sum(g * d))
+        if slope <= 0.0:
+            d, slope = g.copy(), float(np.sum(g * g))
+        if slope <= 1e-12 * max(1.0, abs(f)):
+            break
+        step, ok = 1.0, False
+        for _ls in range(20):
+            wn = w + step * d
+            fn, gn = combination_objective(net, models, wn, batches)
+            if fn >= f + 1e-4 * step * slope:
+                ok = True
+                break
+            step *= 0.5
+        if not ok:
+            break
+        s_vec, y_vec = (wn - w).ravel(), -(gn - g).ravel()
+        if float(s_vec @ y_vec) > 1e-20:
+            s_hist.append(s_vec)
+            y_hist.append(y_vec)
+            if len(s_hist) > history:
+                s_hist.pop(0)
+                y_hist.pop(0)
+        w, f, g = wn, fn, gn
+    net.set_combination(models, w)
+    return w, f
