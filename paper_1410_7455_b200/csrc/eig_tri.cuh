@@ -187,7 +187,9 @@ __device__ __forceinline__ void tri_reduce_reg(const TriPlan& P, double* __restr
   for (int k = 0; k + 2 < n; ++k) {
     const int cur = k & 1, prv = cur ^ 1;
     const double* v = Q + k * ldq;
-    if (rwarp) {   // warp-uniform: the row-group shuffles need every lane of the warp
+    // warp-uniform: the row-group shuffles need every lane of the warp; warps whose rows
+    // are all above the trailing block (<= k) are finished and skip the pass
+    if (rwarp && 4 * (warp - 1) + 3 >= k + 1) {
       // column vectors streamed from shared memory two entries at a time (holding them
       // would need 60 more registers than a 1024-thread CTA allows)
       const double2* v2 = reinterpret_cast<const double2*>(v + j0);
