@@ -26,7 +26,6 @@ namespace ng {
 constexpr int kSimpleMaxJobs = 16;
 constexpr int kGramTile = 32;     // 32 x 32 output tile, 256 threads (4 outputs each)
 constexpr int kGramK = 32;        // k-chunk staged in shared memory
-constexpr int kSolveThreads = 128;
 
 struct SimpleJob {
   float* X;         // n x D, ld (in place: X -> X_hat)
@@ -96,14 +95,19 @@ __global__ void __launch_bounds__(256) simple_gram_kernel(const __grid_constant_
 }
 
 // beta, A = beta I + G/(n-1) and its Cholesky factor A = L L^T (lower, in place, row-major),
-// one CTA per job; right-looking, one column per step (the trailing update of the lower
-// triangle is spread over the CTA).  tr X^T X = tr G.
+// one CTA per job, right-looking and blocked by kCholB columns: the diagonal block is
+// factored in shared memory, the panel below it solved against it (a thread per row), then
+// the whole panel (<= 512 x kCholB doubles) is staged in shared memory for the trailing
+// update A_22 -= P P^T of the lower triangle (every element a kCholB-long dot product).
+constexpr int kCholB = 32;
 __global__ void __launch_bounds__(1024) simple_chol_kernel(const __grid_constant__ SimpleJobs jb) {
   const SimpleJob& J = jb.j[blockIdx.x];
   const int m = J.m, tid = threadIdx.x, nt = blockDim.x;
   double* G = J.G;
+  extern __shared__ __align__(16) double chs[];
+  double* Lkk = chs;                      // kCholB x (kCholB + 1)
+  double* P = chs + kCholB * (kCholB + 1);  // m x (kCholB + 1): the current panel
   __shared__ double red[32];
-  __shared__ double piv;
   double tr = 0.0;
   for (int i = tid; i < m; i += nt) tr += G[(int64_t)i * m + i];
   tr = block_sum(tr, red);
@@ -115,60 +119,141 @@ __global__ void __launch_bounds__(1024) simple_chol_kernel(const __grid_constant
   }
   if (tid == 0) { J.stats[0] = tr; J.stats[1] = beta; }
   __syncthreads();
-  for (int k = 0; k < m; ++k) {
-    if (tid == 0) {
-      const double d = G[(int64_t)k * m + k];
-      if (!(d > 0.0)) atomicOr(reinterpret_cast<unsigned*>(J.flags), kErrNotPD);
-      piv = sqrt(fmax(d, 1e-300));
-      G[(int64_t)k * m + k] = piv;
+  constexpr int LD = kCholB + 1;
+  for (int k0 = 0; k0 < m; k0 += kCholB) {
+    const int bk = min(kCholB, m - k0);
+    // (a) the diagonal block, unblocked in shared memory
+    for (int idx = tid; idx < bk * bk; idx += nt) {
+      const int i = idx / bk, j = idx % bk;
+      Lkk[i * LD + j] = (j <= i) ? G[(int64_t)(k0 + i) * m + k0 + j] : 0.0;
     }
     __syncthreads();
-    const double inv = 1.0 / piv;
-    for (int i = k + 1 + tid; i < m; i += nt) G[(int64_t)i * m + k] *= inv;
+    for (int k = 0; k < bk; ++k) {
+      if (tid == 0) {
+        const double d = Lkk[k * LD + k];
+        if (!(d > 0.0)) atomicOr(reinterpret_cast<unsigned*>(J.flags), kErrNotPD);
+        Lkk[k * LD + k] = sqrt(fmax(d, 1e-300));
+      }
+      __syncthreads();
+      const double inv = 1.0 / Lkk[k * LD + k];
+      for (int i = k + 1 + tid; i < bk; i += nt) Lkk[i * LD + k] *= inv;
+      __syncthreads();
+      const int r = bk - k - 1;
+      for (int idx = tid; idx < r * r; idx += nt) {
+        const int i = k + 1 + idx / r, j = k + 1 + idx % r;
+        if (j <= i) Lkk[i * LD + j] -= Lkk[i * LD + k] * Lkk[j * LD + k];
+      }
+      __syncthreads();
+    }
+    for (int idx = tid; idx < bk * bk; idx += nt) {
+      const int i = idx / bk, j = idx % bk;
+      if (j <= i) G[(int64_t)(k0 + i) * m + k0 + j] = Lkk[i * LD + j];
+    }
+    // (b) the panel below: row r solves x L_kk^T = a (a thread per row, x kept in P)
+    const int rows = m - k0 - bk;
+    for (int r = tid; r < rows; r += nt) {
+      const int gi = k0 + bk + r;
+      double* x = P + r * LD;
+      for (int j = 0; j < bk; ++j) {
+        double s2 = G[(int64_t)gi * m + k0 + j];
+        for (int t = 0; t < j; ++t) s2 = fma(-x[t], Lkk[j * LD + t], s2);
+        x[j] = s2 / Lkk[j * LD + j];
+      }
+      for (int j = 0; j < bk; ++j) G[(int64_t)gi * m + k0 + j] = x[j];
+    }
     __syncthreads();
-    const int r = m - k - 1;
-    for (int idx = tid; idx < r * r; idx += nt) {
-      const int i = k + 1 + idx / r, j = k + 1 + idx % r;
-      if (j <= i) G[(int64_t)i * m + j] -= G[(int64_t)i * m + k] * G[(int64_t)j * m + k];
+    // (c) trailing update of the lower triangle: A_ij -= sum_t P_it P_jt
+    for (int idx = tid; idx < rows * rows; idx += nt) {
+      const int i = idx / rows, j = idx % rows;
+      if (j > i) continue;
+      double acc = 0.0;
+      for (int t = 0; t < bk; ++t) acc = fma(P[i * LD + t], P[j * LD + t], acc);
+      G[(int64_t)(k0 + bk + i) * m + k0 + bk + j] -= acc;
     }
     __syncthreads();
   }
 }
 
-// One thread per right-hand side b (a row of X in the column space, a column in the row
-// space): L y = b, then L^T q = y, q -> Y (element (i, r) at Y[i * rhs + r]).
-__global__ void __launch_bounds__(kSolveThreads) simple_solve_kernel(const __grid_constant__ SimpleJobs jb) {
+// kSolveCols right-hand sides per CTA (a row of X in the column space, a column in the row
+// space), their vectors in shared memory; L y = b then L^T q = y, eight rows (forward) or
+// eight columns (backward) of L staged in shared memory at a time (coalesced, one L2 round
+// trip per eight steps), every dot product split over kSolveSplit lanes (3-level shuffle).
+// q -> Y (element (i, r) at Y[i * rhs + r]).
+constexpr int kSolveCols = 32, kSolveSplit = 8, kSolveBlk = 8;
+__global__ void __launch_bounds__(kSolveCols * kSolveSplit) simple_solve_kernel(const __grid_constant__ SimpleJobs jb) {
   const SimpleJob& J = jb.j[blockIdx.y];
-  const int r = blockIdx.x * kSolveThreads + threadIdx.x;
-  if (r >= J.rhs) return;
-  const int m = J.m, rhs = J.rhs;
+  const int m = J.m, rhs = J.rhs, tid = threadIdx.x, nt = blockDim.x;
+  const int c = tid / kSolveSplit, g = tid % kSolveSplit;
+  if ((int)(blockIdx.x * kSolveCols) >= rhs) return;   // uniform per CTA
+  // y of right-hand side c at ys[c * ldy + k] (ldy = m + 1: the eight lanes of a group read
+  // consecutive k, the four groups of a warp land on different banks)
+  const int ldy = m + 1;
+  extern __shared__ __align__(16) double ys[];
+  double* Lb = ys + (size_t)kSolveCols * ldy;       // kSolveBlk x m: rows (forward) / columns (backward) of L
   const double* L = J.G;
-  double* y = J.Y + r;
-  for (int i = 0; i < m; ++i) {
-    const double b = J.col ? (double)J.X[(int64_t)r * J.ld + i] : (double)J.X[(int64_t)i * J.ld + r];
-    const double* Li = L + (int64_t)i * m;
-    double s0 = b, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int k = 0;
-    for (; k + 4 <= i; k += 4) {
-      s0 = fma(-Li[k], y[(int64_t)k * rhs], s0);
-      s1 = fma(-Li[k + 1], y[(int64_t)(k + 1) * rhs], s1);
-      s2 = fma(-Li[k + 2], y[(int64_t)(k + 2) * rhs], s2);
-      s3 = fma(-Li[k + 3], y[(int64_t)(k + 3) * rhs], s3);
-    }
-    for (; k < i; ++k) s0 = fma(-Li[k], y[(int64_t)k * rhs], s0);
-    y[(int64_t)i * rhs] = ((s0 + s1) + (s2 + s3)) / Li[i];
+  for (int idx = tid; idx < m * kSolveCols; idx += nt) {
+    const int i = idx / kSolveCols, cc = idx % kSolveCols, rr = blockIdx.x * kSolveCols + cc;
+    double b = 0.0;
+    if (rr < rhs) b = J.col ? (double)J.X[(int64_t)rr * J.ld + i] : (double)J.X[(int64_t)i * J.ld + rr];
+    ys[cc * ldy + i] = b;
   }
-  for (int i = m - 1; i >= 0; --i) {
-    double s0 = y[(int64_t)i * rhs], s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int k = i + 1;
-    for (; k + 4 <= m; k += 4) {
-      s0 = fma(-L[(int64_t)k * m + i], y[(int64_t)k * rhs], s0);
-      s1 = fma(-L[(int64_t)(k + 1) * m + i], y[(int64_t)(k + 1) * rhs], s1);
-      s2 = fma(-L[(int64_t)(k + 2) * m + i], y[(int64_t)(k + 2) * rhs], s2);
-      s3 = fma(-L[(int64_t)(k + 3) * m + i], y[(int64_t)(k + 3) * rhs], s3);
+  double* y = ys + (size_t)c * ldy;
+  for (int i0 = 0; i0 < m; i0 += kSolveBlk) {       // forward: y_i = (b_i - sum_{k<i} L_ik y_k) / L_ii
+    const int bi = min(kSolveBlk, m - i0);
+    __syncthreads();
+    for (int idx = tid; idx < bi * (i0 + bi); idx += nt) {
+      const int r = idx / (i0 + bi), k = idx % (i0 + bi);
+      Lb[r * m + k] = L[(int64_t)(i0 + r) * m + k];
     }
-    for (; k < m; ++k) s0 = fma(-L[(int64_t)k * m + i], y[(int64_t)k * rhs], s0);
-    y[(int64_t)i * rhs] = ((s0 + s1) + (s2 + s3)) / L[(int64_t)i * m + i];
+    __syncthreads();
+    for (int ii = 0; ii < bi; ++ii) {
+      const int i = i0 + ii;
+      const double* Li = Lb + ii * m;
+      double s0 = 0.0, s1 = 0.0;
+      int k = g;
+      for (; k + kSolveSplit < i; k += 2 * kSolveSplit) {
+        s0 = fma(Li[k], y[k], s0);
+        s1 = fma(Li[k + kSolveSplit], y[k + kSolveSplit], s1);
+      }
+      if (k < i) s0 = fma(Li[k], y[k], s0);
+      double s = s0 + s1;
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      s += __shfl_xor_sync(0xffffffffu, s, 4);
+      if (g == 0) y[i] = (y[i] - s) / Li[i];
+      __syncwarp();
+    }
+  }
+  for (int i1 = m; i1 > 0; i1 -= kSolveBlk) {       // backward: q_i = (y_i - sum_{k>i} L_ki q_k) / L_ii
+    const int i0 = max(0, i1 - kSolveBlk), bi = i1 - i0;
+    __syncthreads();
+    for (int idx = tid; idx < (m - i0) * bi; idx += nt) {   // global reads: 8 consecutive columns per row
+      const int k = i0 + idx / bi, j = idx % bi;
+      Lb[j * m + k] = L[(int64_t)k * m + i0 + j];
+    }
+    __syncthreads();
+    for (int ii = bi - 1; ii >= 0; --ii) {
+      const int i = i0 + ii;
+      const double* Lc = Lb + ii * m;                 // column i of L, rows k
+      double s0 = 0.0, s1 = 0.0;
+      int k = i + 1 + g;
+      for (; k + kSolveSplit < m; k += 2 * kSolveSplit) {
+        s0 = fma(Lc[k], y[k], s0);
+        s1 = fma(Lc[k + kSolveSplit], y[k + kSolveSplit], s1);
+      }
+      if (k < m) s0 = fma(Lc[k], y[k], s0);
+      double s = s0 + s1;
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      s += __shfl_xor_sync(0xffffffffu, s, 4);
+      if (g == 0) y[i] = (y[i] - s) / Lc[i];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < m * kSolveCols; idx += nt) {
+    const int i = idx / kSolveCols, cc = idx % kSolveCols, rr = blockIdx.x * kSolveCols + cc;
+    if (rr < rhs) J.Y[(int64_t)i * rhs + rr] = ys[cc * ldy + i];
   }
 }
 
@@ -306,9 +391,21 @@ ng_status ngsimple_precondition_group_impl(const SimpleCall* calls, int count) {
     if (cnt == 0) continue;
     simple_gram_kernel<<<dim3(max_tiles, cnt), 256, 0, st>>>(jb);
     NG_TRY(check_launch("simple_gram_kernel"));
-    simple_chol_kernel<<<cnt, 1024, 0, st>>>(jb);
+    int max_m = 1;
+    for (int q = 0; q < cnt; ++q) max_m = std::max(max_m, jb.j[q].m);
+    const size_t chol_smem = sizeof(double) * ((size_t)kCholB * (kCholB + 1) + (size_t)max_m * (kCholB + 1));
+    const size_t solve_smem = sizeof(double) * ((size_t)kSolveCols * (max_m + 1) + (size_t)max_m * kSolveBlk);
+    static bool attr = false;
+    if (!attr) {
+      NG_CUDA_TRY(cudaFuncSetAttribute(simple_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      NG_CUDA_TRY(cudaFuncSetAttribute(simple_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    NG_REQUIRE(chol_smem <= 200u * 1024u && solve_smem <= 200u * 1024u, NG_ESHAPE,
+               "ngsimple: min(n, dim) too large for the shared-memory panels (<= 740)");
+    simple_chol_kernel<<<cnt, 1024, chol_smem, st>>>(jb);
     NG_TRY(check_launch("simple_chol_kernel"));
-    simple_solve_kernel<<<dim3(ceil_div(max_rhs, kSolveThreads), cnt), kSolveThreads, 0, st>>>(jb);
+    simple_solve_kernel<<<dim3(ceil_div(max_rhs, kSolveCols), cnt), kSolveCols * kSolveSplit, solve_smem, st>>>(jb);
     NG_TRY(check_launch("simple_solve_kernel"));
     simple_rows_kernel<<<dim3(max_n, cnt), 256, 0, st>>>(jb);
     NG_TRY(check_launch("simple_rows_kernel"));
