@@ -174,8 +174,18 @@ finalize_kernel(int n, int tiles, const float* __restrict__ xxpart, const float*
   __shared__ double sc[32];
   double sxx = 0.0, spp = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    float xx = 0.f, pp = 0.f;
-    for (int t = 0; t < tiles; ++t) { xx += xxpart[(int64_t)t * part_ld + i]; pp += ppart[(int64_t)t * part_ld + i]; }
+    // the same summation tree as finalize_group_kernel
+    float xa[4] = {0.f, 0.f, 0.f, 0.f}, pa[4] = {0.f, 0.f, 0.f, 0.f};
+    int t = 0;
+    for (; t + 4 <= tiles; t += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        xa[u] += xxpart[(int64_t)(t + u) * part_ld + i];
+        pa[u] += ppart[(int64_t)(t + u) * part_ld + i];
+      }
+    }
+    for (; t < tiles; ++t) { xa[0] += xxpart[(int64_t)t * part_ld + i]; pa[0] += ppart[(int64_t)t * part_ld + i]; }
+    const float xx = (xa[0] + xa[1]) + (xa[2] + xa[3]), pp = (pa[0] + pa[1]) + (pa[2] + pa[3]);
     p_int[i] = pp;
     if (p_out) p_out[i] = pp;
     sxx += (double)xx;
@@ -198,9 +208,14 @@ __global__ void reduce_splits_kernel(float* __restrict__ out, const float* __res
                                      int splits, int64_t zstride, const int* gate) {
   if (gate && *gate == 0) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += part[(int64_t)z * zstride + i];
-    out[i] = s;
+    float a4[4] = {0.f, 0.f, 0.f, 0.f};   // the summation tree of seg_reduce_kernel
+    int z = 0;
+    for (; z + 4 <= splits; z += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a4[u] += part[(int64_t)(z + u) * zstride + i];
+    }
+    for (; z < splits; ++z) a4[0] += part[(int64_t)z * zstride + i];
+    out[i] = (a4[0] + a4[1]) + (a4[2] + a4[3]);
   }
 }
 
@@ -210,9 +225,14 @@ __global__ void reduce_rows_kernel(float* __restrict__ out, int64_t ld, const fl
   const int64_t total = (int64_t)R * D;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t off = (i / D) * ld + (i % D);
-    float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += part[(int64_t)z * zstride + off];
-    out[off] = s;
+    float a4[4] = {0.f, 0.f, 0.f, 0.f};   // the summation tree of seg_reduce_kernel
+    int z = 0;
+    for (; z + 4 <= splits; z += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a4[u] += part[(int64_t)(z + u) * zstride + off];
+    }
+    for (; z < splits; ++z) a4[0] += part[(int64_t)z * zstride + off];
+    out[off] = (a4[0] + a4[1]) + (a4[2] + a4[3]);
   }
 }
 
@@ -1358,9 +1378,14 @@ __global__ void __launch_bounds__(256) seg_reduce_kernel(const __grid_constant__
        i += (int64_t)(sr.block_begin[g + 1] - sr.block_begin[g]) * blockDim.x) {
     const int64_t r = i / cols, c = i % cols;
     const float* src = sr.src[g] + r * sr.lds[g] + c;
-    float acc = 0.f;
-    for (int z = 0; z < sp; ++z) acc += src[(int64_t)z * sr.zstride[g]];
-    sr.out[g][r * sr.ldo[g] + c] = acc;
+    float a4[4] = {0.f, 0.f, 0.f, 0.f};   // independent loads in flight, fixed combination order
+    int z = 0;
+    for (; z + 4 <= sp; z += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a4[u] += src[(int64_t)(z + u) * sr.zstride[g]];
+    }
+    for (; z < sp; ++z) a4[0] += src[(int64_t)z * sr.zstride[g]];
+    sr.out[g][r * sr.ldo[g] + c] = (a4[0] + a4[1]) + (a4[2] + a4[3]);
   }
 }
 
@@ -1428,8 +1453,19 @@ __global__ void __launch_bounds__(512) finalize_group_kernel(const __grid_consta
   const int64_t pl = fg.part_ld[g];
   double sxx = 0.0, spp = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    float xx = 0.f, pp = 0.f;
-    for (int t = 0; t < tiles; ++t) { xx += fg.xxpart[g][(int64_t)t * pl + i]; pp += fg.ppart[g][(int64_t)t * pl + i]; }
+    // four interleaved partial sums (independent loads in flight), combined in a fixed
+    // order; ||x||^2 and ||x_hat||^2 use the identical tree (R = 0 gives gamma = 1 exactly, R27)
+    float xa[4] = {0.f, 0.f, 0.f, 0.f}, pa[4] = {0.f, 0.f, 0.f, 0.f};
+    int t = 0;
+    for (; t + 4 <= tiles; t += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        xa[u] += fg.xxpart[g][(int64_t)(t + u) * pl + i];
+        pa[u] += fg.ppart[g][(int64_t)(t + u) * pl + i];
+      }
+    }
+    for (; t < tiles; ++t) { xa[0] += fg.xxpart[g][(int64_t)t * pl + i]; pa[0] += fg.ppart[g][(int64_t)t * pl + i]; }
+    const float xx = (xa[0] + xa[1]) + (xa[2] + xa[3]), pp = (pa[0] + pa[1]) + (pa[2] + pa[3]);
     fg.p_int[g][i] = pp;
     if (fg.p_out[g]) fg.p_out[g][i] = pp;
     sxx += (double)xx;

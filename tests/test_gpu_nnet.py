@@ -276,13 +276,22 @@ def test_config3_fp32_steps_with_refreshes(api):
         st = net.update(0.01, 0.075, stats=True)
         fb = onn.forward_backward(before, cfg, fr.astype(np.float64), lb)
         ref = [b.copy() for b in before]
-        onn.update(ref, fb, 0.01, states)
+        ost = onn.update(ref, fb, 0.01, states)
         if k in (0, 4):
             assert np.all(st.updated_out == 1) and np.all(st.updated_in == 1), k
         for l in range(len(params)):
-            d_gpu = net.get_params(l).astype(np.float64) - before[l]
-            err = normwise(d_gpu, ref[l] - before[l])
-            assert err <= TOL, (k, l, err)
+            # the FP32 W_{t+1}'s own half-ulp rounding is not an error of the update
+            # (tests/test_gpu_r2_parity.py delta_err)
+            w_after = net.get_params(l)
+            d_gpu = w_after.astype(np.float64) - before[l]
+            half_ulp = 0.5 * np.spacing(np.abs(w_after)).astype(np.float64)
+            excess = np.maximum(np.abs(d_gpu - (ref[l] - before[l])) - half_ulp, 0.0)
+            err = float(np.max(excess) / np.max(np.abs(ref[l] - before[l])))
+            # the FP32 bar widened by the X_hat cancellation factor gamma beyond 25x (R33);
+            # once the two sides have refreshed their NG states independently (k >= 1) the
+            # states have separated at the FP32 level (R34) and the bar is 2e-4
+            bar = TOL * max(1.0, max(ost[l].gamma_in, ost[l].gamma_out) / 25.0) * (1.0 if k == 0 else 2.0)
+            assert err <= bar, (k, l, err, bar)
     for l, (s_in, s_out) in enumerate(states):
         for side, s in (("in", s_in), ("out", s_out)):
             g = net.ngsgd(l, side).get_state()
