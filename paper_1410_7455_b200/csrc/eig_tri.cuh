@@ -41,6 +41,8 @@ constexpr int kTriCoarseMin = 8;
 constexpr double kTriClusterTol = 1e-7;   // relative gap below which twisted vectors are redone
                                           // (above it their error n eps / relgap < 2e-7)
 __device__ long long g_tri_clk[8];
+__device__ long long g_tri_dbg[8];   // finer phase-2 stamps of the last solve (ng_debug_eig_tri ok[8..15])
+__device__ unsigned long long g_tri_rqimax;   // slowest eigenvalue's RQI loop (cycles)
 __device__ int g_tri_maxit;
 __device__ double g_tri_fail_z[kTriMax * kTriMax];   // last Z_t whose solve fell back (ng_debug_tri_fail)
 __device__ int g_tri_fail_n, g_tri_fail_count, g_tri_fail_why, g_tri_maxpos;   // thread 0's phase stamps of the last solve (ng_debug_eig_tri)
@@ -504,17 +506,24 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
   double tn = 0.0;
   for (int i = tid; i < n; i += nt) tn = fmax(tn, fmax(fabs(d[i]), i + 1 < n ? fabs(e[i]) : 0.0));
   tn = block_max(tn, red);
+  // the negligibility test of every off-diagonal in parallel (cpos[] holds the flags until
+  // the cluster pass reuses it), then thread 0 walks the flags
+  for (int i = tid; i < n; i += nt) {
+    bool cut = (i == n - 1);
+    if (!cut) {
+      const double ei = fabs(e[i]);
+      cut = ei <= eps * sqrt(fabs(d[i])) * sqrt(fabs(d[i + 1])) || ei <= 2.0 * eps * tn;
+      if (cut) e[i] = 0.0;
+    }
+    cpos[i] = cut ? 1 : 0;
+  }
+  __syncthreads();
   if (tid == 0) {
     int s0 = 0;
     status[0] = 1;
     status[2] = 0;
     for (int i = 0; i < n; ++i) {
-      bool cut = (i == n - 1);
-      if (!cut) {
-        const double ei = fabs(e[i]);
-        cut = ei <= eps * sqrt(fabs(d[i])) * sqrt(fabs(d[i + 1])) || ei <= 2.0 * eps * tn;
-        if (cut) e[i] = 0.0;
-      }
+      const bool cut = cpos[i] != 0;
       if (cut) {
         for (int k = s0; k <= i; ++k) { bstart[k] = s0; bend[k] = i + 1; }
         crow[s0] = -1;
@@ -527,6 +536,7 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
     }
   }
   __syncthreads();
+  if (tid == 0) g_tri_dbg[0] = clock64();
   const double pivmin = 1e-290;
   // root representation per block, L D L^T = T_b - sigma I positive definite
   double* DL = sm + P.oDL;
@@ -565,6 +575,7 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
     for (int i = lo; i < hi; ++i) { sig[i] = sigma; gub[i] = gu; }
   }
   __syncthreads();
+  if (tid == 0) g_tri_dbg[1] = clock64();
   if (status[0] == 0) return 0;
   // coarse pass: negcounts of each big block at gu 8^-k, k = 0..kTriCoarse-1 (a thread each)
   {
@@ -637,6 +648,7 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
         lj = Dr[lo];
       } else {
         if (g8 == 0) {
+          const long long rq0 = clock64();
           double lc = -1.0, lam_v = 0.0, gm = 0.0, nz = 1.0;
           bool have_vec = false, conv = false;
           double* ss = A + j * lda;
@@ -679,6 +691,7 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
           lj = lam_v;
           const double inv = rsqrt(nz);
           for (int c = lo; c < hi; ++c) x[c] *= inv;
+          atomicMax(&g_tri_rqimax, (unsigned long long)(clock64() - rq0));
         }
       }
       if (g8 == 0) {
@@ -688,6 +701,7 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
     }
   }
   __syncthreads();
+  if (tid == 0) g_tri_dbg[2] = clock64();
   // relative clusters (relgap < kTriClusterTol within a block): the twisted vectors of the
   // members are not reliable (error ~ n eps / relgap).  Every member redoes its vector by two
   // steps of inverse iteration from its own pseudo-random start (in parallel), then each

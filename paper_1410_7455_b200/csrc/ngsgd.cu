@@ -2001,6 +2001,15 @@ __global__ void __launch_bounds__(1024) debug_eig_tri_kernel(const double* Z, in
     ok[5] = g_tri_maxit; g_tri_maxit = 0;
     ok[6] = (int)(g_tri_clk[6] - g_tri_clk[5]);   // multisection
     ok[7] = (int)(g_tri_clk[2] - g_tri_clk[6]);   // RQI + vectors + clusters
+    if (ok[8] == 0x5eed) {                         // caller asked for the finer phase-2 stamps
+      ok[8] = (int)(g_tri_dbg[0] - g_tri_clk[1]);   // split
+      ok[9] = (int)(g_tri_dbg[1] - g_tri_dbg[0]);   // root representations
+      ok[10] = (int)(g_tri_clk[5] - g_tri_dbg[1]);  // coarse negcounts
+      ok[11] = (int)(g_tri_dbg[2] - g_tri_clk[6]);  // RQI + twisted vectors (all eigenvalues)
+      ok[12] = (int)(g_tri_clk[2] - g_tri_dbg[2]);  // clusters
+      ok[13] = (int)g_tri_rqimax;                    // slowest eigenvalue's RQI loop
+      g_tri_rqimax = 0;
+    }
   }
 }
 
