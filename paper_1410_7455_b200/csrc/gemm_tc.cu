@@ -433,6 +433,162 @@ __global__ void __launch_bounds__(S3 ? 192 : 128) tc_gemm_tf32_grouped_kernel(co
                                 grp.nstages);
 }
 
+// Persistent grouped weight update C += (*scale) A B (TC_EPI_AXPY, both operands MN-major,
+// 128 x 128 tiles, TF32): one CTA per SM walks tiles blockIdx.x, +gridDim.x, ...  Warp 0
+// lane 0 streams every tile's k-blocks through one TMA ring, warp 1 lane 0 issues the MMAs
+// into one of TWO TMEM accumulators (256 columns), and warps 2..5 drain the other one (the
+// read-modify-write of the previous tile, its old C prefetched while the MMAs run), so the
+// epilogue of tile i overlaps the mainloop of tile i + 1.
+__global__ void __launch_bounds__(192) tc_axpy_persistent_kernel(const __grid_constant__ TcGroup grp, int tiles) {
+  constexpr int BN = 128;
+  constexpr uint32_t A_BYTES = kBM * kBK * 4, B_BYTES = BN * kBK * 4, STAGE = A_BYTES + B_BYTES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ __align__(8) uint64_t full_bar[kStages];
+  __shared__ __align__(8) uint64_t empty_bar[kStages];
+  __shared__ __align__(8) uint64_t acc_full[2];
+  __shared__ __align__(8) uint64_t acc_empty[2];
+  __shared__ uint32_t tmem_base_sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nstages = grp.nstages;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < nstages; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&acc_full[b], 1); mbar_init(&acc_empty[b], 128); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  pdl_trigger();
+  pdl_wait();
+
+  // tile -> (problem, m tile, n tile)
+  auto locate = [&](int t, int& g, int& m0, int& n0) {
+    g = 0;
+    while (g + 1 < grp.count && t >= grp.p[g + 1].tile_begin) ++g;
+    const TcProblem& P = grp.p[g];
+    const int local = t - P.tile_begin, nt = (P.N + BN - 1) / BN;
+    n0 = (local % nt) * BN;
+    m0 = (local / nt) * kBM;
+  };
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer: every k-block of every tile of this CTA
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int g, m0, n0;
+        locate(t, g, m0, n0);
+        const TcProblem& P = grp.p[g];
+        const int nkb = (P.K + kBK - 1) / kBK;
+        for (int i = 0; i < nkb; ++i) {
+          mbar_wait(&empty_bar[s], ph ^ 1u);
+          uint8_t* sa = smem + s * STAGE;
+          uint8_t* sb = sa + A_BYTES;
+          mbar_expect_tx(&full_bar[s], STAGE);
+          const int kc = i * kBK;
+#pragma unroll
+          for (int j = 0; j < kBM / 32; ++j) tma_load_2d(sa + j * 4096, &P.tmA, m0 + 32 * j, kc, &full_bar[s]);
+#pragma unroll
+          for (int j = 0; j < BN / 32; ++j) tma_load_2d(sb + j * 4096, &P.tmB, n0 + 32 * j, kc, &full_bar[s]);
+          if (++s == nstages) { s = 0; ph ^= 1u; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer, accumulators alternating between TMEM columns 0 and 128
+      constexpr uint32_t idesc = idesc_tf32(kBM, BN, true, true);
+      int s = 0, it = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        int g, m0, n0;
+        locate(t, g, m0, n0);
+        const int nkb = (grp.p[g].K + kBK - 1) / kBK;
+        const int b = it & 1;
+        mbar_wait(&acc_empty[b], ((it >> 1) & 1) ^ 1u);   // the epilogue has drained buffer b
+        tc_fence_after();
+        const uint32_t acc = tmem + (uint32_t)(b * BN);
+        for (int i = 0; i < nkb; ++i) {
+          mbar_wait(&full_bar[s], ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * STAGE), sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < kBK / 8; ++k)
+            mma_tf32(acc, desc_mnmajor(sa, k), desc_mnmajor(sb, k), idesc, (i > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&empty_bar[s]);
+          if (++s == nstages) { s = 0; ph ^= 1u; }
+        }
+        umma_commit(&acc_full[b]);
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 2..5 (TMEM lane quarter = warp % 4)
+    const int q4 = warp & 3;
+    int it = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      int g, m0, n0;
+      locate(t, g, m0, n0);
+      const TcProblem& P = grp.p[g];
+      const int b = it & 1;
+      const int row = m0 + q4 * 32 + lane;
+      float* crow = P.epi.C + (int64_t)row * P.epi.ldc;
+      const float scale = __ldg(P.epi.scale);
+      // the old C row segment does not depend on the MMAs: load it before waiting for them
+      const bool rowok = row < P.M;
+      const bool vec = rowok && (n0 + BN <= P.N) && ((reinterpret_cast<uintptr_t>(crow + n0) & 15) == 0);
+      float oldv[BN];
+      if (vec) {
+#pragma unroll
+        for (int j = 0; j < BN; j += 4) {
+          const float4 o = *reinterpret_cast<const float4*>(crow + n0 + j);
+          oldv[j] = o.x; oldv[j + 1] = o.y; oldv[j + 2] = o.z; oldv[j + 3] = o.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < BN; ++j) oldv[j] = (rowok && n0 + j < P.N) ? crow[n0 + j] : 0.f;
+      }
+      mbar_wait(&acc_full[b], (it >> 1) & 1);
+      tc_fence_after();
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        const int nb = n0 + c * 32;
+        float acc[32];
+        uint32_t v[16];
+        tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * BN + c * 32), v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = __uint_as_float(v[j]);
+        tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(b * BN + c * 32 + 16), v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[16 + j] = __uint_as_float(v[j]);
+        if (vec) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(crow + nb + 4 * j) = make_float4(
+                fmaf(scale, acc[4 * j], oldv[c * 32 + 4 * j]), fmaf(scale, acc[4 * j + 1], oldv[c * 32 + 4 * j + 1]),
+                fmaf(scale, acc[4 * j + 2], oldv[c * 32 + 4 * j + 2]), fmaf(scale, acc[4 * j + 3], oldv[c * 32 + 4 * j + 3]));
+        } else if (rowok) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (nb + j < P.N) crow[nb + j] = fmaf(scale, acc[j], oldv[c * 32 + j]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[b]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
 // ------------------------------------------------------------------ host side
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -662,6 +818,43 @@ ng_status grouped_dispatch(cudaStream_t st, const TcGroup& grp, int tiles, bool 
 #undef NG_GRP_M
 #undef NG_GRP_E
 #undef NG_GRP
+}
+
+ng_status tc_gemm_tf32_axpy_persistent(cudaStream_t st, const TcGroupDesc* desc, int count) {
+  NG_REQUIRE(count >= 1 && count <= kTcGroupMax, NG_EINVAL, "tc_gemm_tf32_axpy_persistent: bad problem count");
+  constexpr int BN = 128;
+  TcGroup grp;
+  std::memset(&grp, 0, sizeof(grp));
+  grp.count = count;
+  int tiles = 0;
+  for (int g = 0; g < count; ++g) {
+    const TcGroupDesc& d = desc[g];
+    NG_REQUIRE(d.M >= 1 && d.N >= 1 && d.K >= 1 && d.epi.kind == TC_EPI_AXPY, NG_EINVAL, "axpy problems only");
+    TcProblem& P = grp.p[g];
+    NG_TRY(make_tmap(&P.tmA, d.A, d.M, d.K, d.lda, 32, true));   // [K][M]
+    NG_TRY(make_tmap(&P.tmB, d.B, d.N, d.K, d.ldb, 32, true));   // [K][N]
+    P.M = d.M; P.N = d.N; P.K = d.K; P.kbps = ceil_div(d.K, kBK);
+    P.tile_begin = tiles;
+    P.epi = d.epi;
+    tiles += ceil_div(d.M, kBM) * ceil_div(d.N, BN);
+  }
+  grp.nstages = ring_stages(BN, false);
+  const size_t smem = ring_smem(BN, grp.nstages, false);
+  static bool attr = false;
+  if (!attr) {
+    NG_CUDA_TRY(cudaFuncSetAttribute(tc_axpy_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)ring_smem(BN, ring_stages(BN, false), false)));
+    attr = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  NG_CUDA_TRY(launch_pdl(tc_axpy_persistent_kernel, dim3(std::min(tiles, sms)), dim3(192), smem, st, grp, tiles));
+  return check_launch("tc_axpy_persistent_kernel");
 }
 
 // Fixed-order reduction of split-K partials: C[m][n] = sum_z part[z][m][n].

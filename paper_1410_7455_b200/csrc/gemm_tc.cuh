@@ -77,6 +77,11 @@ struct TcGroup {
 ng_status tc_gemm_tf32_grouped(cudaStream_t st, const TcGroupDesc* desc, int count, bool a_kmajor, bool b_kmajor,
                                int epi_kind, int bn, bool split3 = false);
 
+// The weight update of every layer, C_g += (*scale_g) A_g B_g (both operands MN-major, TF32):
+// a persistent kernel, one CTA per SM, two TMEM accumulators so the read-modify-write
+// epilogue of one tile overlaps the mainloop of the next.
+ng_status tc_gemm_tf32_axpy_persistent(cudaStream_t st, const TcGroupDesc* desc, int count);
+
 // Forward affine layer fused with the p-norm (G = 10): Z = Y W^T (both K-major,
 // Z row stride ldz) and Ynext = [pnorm(Z), 1, 0 ...] (row stride ldy >= N/10 + 1).  N must be
 // a multiple of 10.  80-column tiles (8 whole groups each).

@@ -16,11 +16,11 @@ frames, labels = spliced_frames(1410, 64 * N, num_classes=5000)
 f = torch.from_numpy(frames).cuda()
 y = torch.from_numpy(labels).cuda()
 net = api.Nnet(360, 4, 3000, 10, 5000, max_minibatch=N, precond=True, rank_in=20, rank_out=80,
-               precision=os.environ.get("NG_PREC", "tf32"), seed=1410)
+               precision=os.environ.get("NG_PREC", "tf32"), seed=1410, renorm=True)
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 40
 for k in range(20):
     net.forward_backward(f[(k % 64) * N:(k % 64 + 1) * N], y[(k % 64) * N:(k % 64 + 1) * N])
-    net.update(0.01 / 6, 0.075)
+    net.update(0.01 / 6 / 8, 0.075)
 torch.cuda.synchronize()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
 host = []
@@ -30,7 +30,7 @@ for k in range(20, 20 + steps):
     t0 = time.perf_counter()
     net.forward_backward(f[i * N:(i + 1) * N], y[i * N:(i + 1) * N])
     t1 = time.perf_counter()
-    net.update(0.01 / 6, 0.075)
+    net.update(0.01 / 6 / 8, 0.075)
     t2 = time.perf_counter()
     host.append((t1 - t0, t2 - t1))
 ev[steps].record()
