@@ -411,10 +411,12 @@ ng_status ng_debug_eig_tri(const double* z, int32_t n, double* lam, double* vt, 
  * call (both reset)}.  Synchronises the device. */
 ng_status ng_debug_tri_fail(double* z_host, int32_t* info_host);
 
-/* Device-clock (globaltimer, ns) start / end of the last refresh_kernel launches: out host
- * uint64[256*5] ring of {R | D << 16, start, end, eigensolve start, eigensolve end} (slot =
- * launch index mod 256; the eigensolve stamps are 0 outside the default solver), count =
- * launches so far.  Synchronises the device.  For tools/refresh_timeline.py. */
+/* Device-clock (globaltimer, ns) start / end of the last refresh CTAs: out host
+ * uint64[256*9] ring of {R | D << 16, start, end, eigensolve start, eigensolve end, then the
+ * eigensolver's phases in SM cycles: tridiagonalisation, split..multisection, RQI + vectors,
+ * clusters + check + back-transformation} (slot = refresh index mod 256; the eigensolver
+ * stamps are 0 outside the default solver), count = refreshes so far.  Synchronises the
+ * device.  For tools/refresh_timeline.py. */
 ng_status ng_debug_refresh_times(uint64_t* out, int32_t* count);
 
 #ifdef __cplusplus

@@ -455,7 +455,7 @@ __device__ __forceinline__ double tri_gemm_nt(const double* __restrict__ Am, con
 // Full solve.  On entry A (= sm + P.oA, ld P.lda) holds the symmetric matrix.  On success
 // (return 1): lam[i] (sm + P.olam, unordered) and eigenvector rows V = sm + P.oA (ld P.lda).
 // Returns 0 when the orthogonality check fails (the caller falls back to Jacobi).
-__device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
+__device__ int eig_tri(const TriPlan& P, double* __restrict__ sm, long long* stamps = nullptr) {
   const int n = P.n, lda = P.lda, tid = threadIdx.x, nt = blockDim.x;
   double* A = sm + P.oA;
   double* X = sm + P.oX;
@@ -500,7 +500,9 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
   }
   __syncthreads();
   if (tid == 0) g_tri_clk[0] = clock64();
+  if (tid == 0 && stamps) stamps[0] = clock64();
   tri_reduce_reg(P, sm);
+  if (tid == 0 && stamps) stamps[1] = clock64();
   if (tid == 0) g_tri_clk[1] = clock64();
   // ||T|| and the split
   double tn = 0.0;
@@ -640,6 +642,7 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
     }
     __syncthreads();
     if (tid == 0) g_tri_clk[6] = clock64();
+    if (tid == 0 && stamps) stamps[2] = clock64();
     if (j < n) {
       const int lo = bstart[j], hi = bend[j], nb = hi - lo, jj = j - lo;
       double* x = X + j * lda;
@@ -702,6 +705,7 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
   }
   __syncthreads();
   if (tid == 0) g_tri_dbg[2] = clock64();
+  if (tid == 0 && stamps) stamps[3] = clock64();
   // relative clusters (relgap < kTriClusterTol within a block): the twisted vectors of the
   // members are not reliable (error ~ n eps / relgap).  Every member redoes its vector by two
   // steps of inverse iteration from its own pseudo-random start (in parallel), then each
@@ -760,31 +764,35 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
       }
       __syncthreads();
       // MGS twice over cluster positions: at step p the member at position p-1 of every
-      // cluster is final (normalised); the members after it project it out
+      // cluster is final (normalised); the members after it project it out.  A warp per
+      // member (members j = warp, warp + 32, ...), lanes over the vector's entries.
+      const int lane = tid & 31, warp = tid >> 5, nwarp = nt >> 5;
       for (int rep = 0; rep < 2; ++rep) {
         for (int p = 0; p <= mx; ++p) {
-          if (tid < n && cpos[tid] != 0) {
-            const int j = tid, lo = bstart[j], hi = bend[j];
+          for (int j = warp; j < n; j += nwarp) {
+            if (cpos[j] == 0) continue;   // warp-uniform
+            const int lo = bstart[j], hi = bend[j];
             const int pj = cpos[j] < 0 ? 0 : cpos[j];
+            if (pj != p) continue;
             double* y = X + j * lda;
-            if (pj == p) {
-              double nr = 0.0;
-              for (int i = lo; i < hi; ++i) nr = fma(y[i], y[i], nr);
-              const double inr = nr > 0.0 ? rsqrt(nr) : 0.0;
-              for (int i = lo; i < hi; ++i) y[i] *= inr;
-            }
+            double nr = 0.0;
+            for (int i = lo + lane; i < hi; i += 32) nr = fma(y[i], y[i], nr);
+            nr = warp_sum(nr);
+            const double inr = nr > 0.0 ? rsqrt(nr) : 0.0;
+            for (int i = lo + lane; i < hi; i += 32) y[i] *= inr;
           }
           __syncthreads();
-          if (tid < n && cpos[tid] != 0) {
-            const int j = tid, lo = bstart[j], hi = bend[j];
+          for (int j = warp; j < n; j += nwarp) {
+            if (cpos[j] == 0) continue;
+            const int lo = bstart[j], hi = bend[j];
             const int pj = cpos[j] < 0 ? 0 : cpos[j];
-            if (pj > p) {
-              const double* xq = X + (j - (pj - p)) * lda;   // the member at position p
-              double* y = X + j * lda;
-              double dt = 0.0;
-              for (int i = lo; i < hi; ++i) dt = fma(xq[i], y[i], dt);
-              for (int i = lo; i < hi; ++i) y[i] = fma(-dt, xq[i], y[i]);
-            }
+            if (pj <= p) continue;
+            const double* xq = X + (j - (pj - p)) * lda;   // the member at position p
+            double* y = X + j * lda;
+            double dt = 0.0;
+            for (int i = lo + lane; i < hi; i += 32) dt = fma(xq[i], y[i], dt);
+            dt = warp_sum(dt);
+            for (int i = lo + lane; i < hi; i += 32) y[i] = fma(-dt, xq[i], y[i]);
           }
           __syncthreads();
         }
@@ -792,6 +800,7 @@ __device__ int eig_tri(const TriPlan& P, double* __restrict__ sm) {
     }
   }
   if (tid == 0) g_tri_clk[2] = clock64();
+  if (tid == 0 && stamps) stamps[4] = clock64();
   if (status[0] == 0) return 0;
   // safety net: orthogonality of the eigenvectors of T
   const double dev = tri_gemm_nt(X, X, n, lda, nullptr, 0, true, red);

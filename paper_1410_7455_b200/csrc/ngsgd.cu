@@ -381,7 +381,7 @@ __device__ void refresh_vrank(const RefreshSmem& P, uint32_t rank, double* sm, f
   cl_sync();   // (2) rank 0's shared memory is no longer read
 }
 
-__device__ unsigned long long g_ref_t[256][5];   // refresh timing (ng_debug_refresh_times): R, start, end ns
+__device__ unsigned long long g_ref_t[256][9];   // refresh timing (ng_debug_refresh_times): R, start, end ns, eig, phase cycles
 __device__ unsigned int g_ref_n;
 
 template <int MODE>
@@ -390,6 +390,7 @@ __device__ __forceinline__ void refresh_body(int R, int D, int N, double eta, do
                                              const double* __restrict__ sums, float* __restrict__ Amat,
                                              float* __restrict__ svec, int* __restrict__ flags, int dbg_mask) {
   extern __shared__ __align__(16) unsigned char ng_smem[];
+  __shared__ long long eig_st[8];   // eigensolver phase stamps (thread 0)
   double* sm = reinterpret_cast<double*>(ng_smem);
   unsigned long long t_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
@@ -477,7 +478,7 @@ __device__ __forceinline__ void refresh_body(int R, int D, int N, double eta, do
   if (MODE == REFRESH_TRI) {
     const TriPlan tp = tri_plan(R);
     double* tb = sm + P.o_ring;
-    if (eig_tri(tp, tb)) {
+    if (eig_tri(tp, tb, eig_st)) {
       for (int i = tid; i < R; i += nt) lam[i] = tb[tp.olam + i];
       sweeps = 0;
       V = tb + tp.oA;
@@ -610,6 +611,12 @@ __device__ __forceinline__ void refresh_body(int R, int D, int N, double eta, do
     g_ref_t[slot][2] = t_end;
     g_ref_t[slot][3] = t_eig0;
     g_ref_t[slot][4] = t_eig1;
+    if (MODE == REFRESH_TRI) {   // cycles: tridiagonalisation, split..multisection, RQI + vectors, clusters + check + back
+      g_ref_t[slot][5] = (unsigned long long)(eig_st[1] - eig_st[0]);
+      g_ref_t[slot][6] = (unsigned long long)(eig_st[2] - eig_st[1]);
+      g_ref_t[slot][7] = (unsigned long long)(eig_st[3] - eig_st[2]);
+      g_ref_t[slot][8] = (unsigned long long)(eig_st[4] - eig_st[3]);
+    }
   }
 }
 
@@ -931,7 +938,7 @@ static ng_status set_kernel_attrs() {
                                    (int)refresh_plan(kDCMax, REFRESH_DC).total_bytes));
   NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<REFRESH_TRI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)refresh_plan(kTriMax, REFRESH_TRI).total_bytes));
-  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   NG_CUDA_TRY(cudaFuncSetAttribute(reorth_check_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)reorth_smem_bytes(kMaxRank)));
   NG_CUDA_TRY(cudaFuncSetAttribute(reorth_trsm_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1548,7 +1555,7 @@ static ng_status launch_refresh_group(NgCall* calls, const std::vector<int>& grp
     ProfScope pe(NG_PROF_NG_EIG, ss, flops, (double)G);
     // NG_TUNE_REFRESH_SMEM_KB pads the refresh CTA's shared memory so that no main-stream
     // CTA can share its SM (measurement knob)
-    static const size_t pad = (size_t)std::max(0, tune_int("NG_TUNE_REFRESH_SMEM_KB", 0)) * 1024;
+    static const size_t pad = (size_t)std::min(200, std::max(0, tune_int("NG_TUNE_REFRESH_SMEM_KB", 0))) * 1024;
     const size_t rsm = std::max(refresh_plan(maxR, REFRESH_TRI).total_bytes, pad);
     refresh_group_kernel<<<G, 1024, rsm, ss>>>(rg);
     NG_TRY(check_launch("refresh_group_kernel"));
@@ -2018,7 +2025,7 @@ ng_status ng_debug_refresh_times(uint64_t* out, int32_t* count) {
   NG_CUDA_TRY(cudaDeviceSynchronize());
   unsigned int n = 0;
   NG_CUDA_TRY(cudaMemcpyFromSymbol(&n, g_ref_n, sizeof(n)));
-  NG_CUDA_TRY(cudaMemcpyFromSymbol(out, g_ref_t, sizeof(unsigned long long) * 256 * 5));
+  NG_CUDA_TRY(cudaMemcpyFromSymbol(out, g_ref_t, sizeof(unsigned long long) * 256 * 9));
   *count = (int32_t)n;
   return NG_OK;
 }

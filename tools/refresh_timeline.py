@@ -22,7 +22,7 @@ f = torch.from_numpy(frames).cuda()
 y = torch.from_numpy(labels).cuda()
 net = api.Nnet(360, 4, 3000, 10, 5000, max_minibatch=N, precond=True, rank_in=20, rank_out=80,
                precision=os.environ.get("NG_PREC", "tf32"), seed=1410, renorm=True)
-buf = np.zeros(256 * 5, dtype=np.uint64)
+buf = np.zeros(256 * 9, dtype=np.uint64)
 cnt = np.zeros(1, dtype=np.int32)
 seen = 0
 for k in range(steps):
@@ -33,9 +33,10 @@ for k in range(steps):
         _lib.check(_lib.lib.ng_debug_refresh_times(buf.ctypes.data_as(ctypes.c_void_p), cnt.ctypes.data_as(ctypes.c_void_p)))
         c = int(cnt[0])
         if c > seen:
-            rows = [buf[(s % 256) * 5:(s % 256) * 5 + 5] for s in range(seen, c)]
+            rows = [buf[(s % 256) * 9:(s % 256) * 9 + 9] for s in range(seen, c)]
             t0 = min(int(r[1]) for r in rows)
             print(f"step {k}: " + "  ".join(f"R{int(r[0]) & 0xffff}D{int(r[0]) >> 16}:{(int(r[1]) - t0) / 1e3:.0f}-{(int(r[2]) - t0) / 1e3:.0f}us"
-                                           f"(eig {(int(r[4]) - int(r[3])) / 1e3:.0f})"
+                                           f"(eig {(int(r[4]) - int(r[3])) / 1e3:.0f}: tri {int(r[5]) / 1965:.0f} "
+                                           f"msect {int(r[6]) / 1965:.0f} rqi {int(r[7]) / 1965:.0f} rest {int(r[8]) / 1965:.0f})"
                                            for r in sorted(rows, key=lambda r: int(r[1]))))
             seen = c
