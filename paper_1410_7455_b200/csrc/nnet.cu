@@ -28,7 +28,7 @@
 using namespace ng;
 
 constexpr int kMaxRowWidth = 50000;   // widest activation row staged in shared memory
-constexpr int kBwdSplits = 6;
+constexpr int kBwdSplits = 8;
 constexpr int kMaxRanks = 64;      // nnet_average: jobs per communicator   // split-K of the TF32 backward-data GEMM (K = 3000..5000)
 
 struct nnet_ctx {
