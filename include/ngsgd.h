@@ -377,26 +377,10 @@ ng_status ng_debug_gemm_tc(int32_t M, int32_t N, int32_t K, const float* A, int6
                            const float* B, int64_t ldb, int32_t b_kmajor, float* C, int64_t ldc,
                            int32_t bn, int32_t splits, int32_t split3, void* cuda_stream);
 
-/* Eigensolver round timing, accumulated over every refresh since the last call and reset
- * by it (SM clock cycles; only recorded while NG_PROFILE_JACOBI_MASK has bit 64 set):
- *   out[0] rounds timed, out[1] angle thread: round start -> inputs loaded,
- *   out[2] inputs -> rotation computed, out[3] rotation -> hand-off issued,
- *   out[4] block thread: round start -> inputs loaded, out[5] inputs -> stores issued,
- *   out[6] round start -> barrier passed (thread 0), out[7] reserved;
- * divide-and-conquer solver (always recorded): out[8] Householder, out[9] D&C, out[10]
- * back-transformation cycles, out[11] solves, out[12 + l] merge level l (width 2^l).
- * out: host array of 24.  Synchronises the device. */
-ng_status ng_debug_eig_clocks(uint64_t* out);
-
-/* The refresh's dense symmetric eigensolver (Householder + divide and conquer, FP64, one
- * CTA; eqn:zt:eig) on its own, for unit tests: z device double[n*n] (row
- * major, symmetric), lam device double[n] (ascending), vt device double[n*n] (row i = the
- * unit eigenvector of lam[i]).  n in [1, 80]; asynchronous on `stream`. */
-ng_status ng_debug_eig_dc(const double* z, int32_t n, double* lam, double* vt, void* stream);
-
 /* The refresh's default eigensolver (Householder + relatively robust representation +
  * twisted-factorisation eigenvectors, FP64, one CTA; eqn:zt:eig) on its own,
- * for unit tests: same arguments as ng_debug_eig_dc except that lam / vt come out UNORDERED
+ * for unit tests: z device double[n*n] (row major, symmetric), lam device double[n], vt device
+ * double[n*n]; lam / vt come out UNORDERED
  * (vt row i = unit eigenvector of lam[i]); ok device int[4]: ok[0] = 1 when the solve passed
  * its orthogonality check (0 = the refresh would fall back to Jacobi; lam / vt undefined),
  * ok[1] = cycles spent (clock64, whole solve), ok[2..5] = cycles of the phases

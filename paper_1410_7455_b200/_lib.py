@@ -108,8 +108,6 @@ SIGNATURES = {
     "ngsimple_destroy": (c_int32, [c_void_p]),
     "ngsimple_precondition": (c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_void_p, c_void_p]),
     "ngsimple_read_flags": (c_int32, [c_void_p]),
-    "ng_debug_eig_clocks": (c_int32, [ctypes.POINTER(ctypes.c_uint64)]),
-    "ng_debug_eig_dc": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     "ng_debug_eig_tri": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ng_debug_tri_fail": (c_int32, [c_void_p, c_void_p]),
     "ng_debug_refresh_times": (c_int32, [c_void_p, c_void_p]),

@@ -359,463 +359,4 @@ __device__ __forceinline__ int jacobi_eig_smem(T* __restrict__ A, int lda, T* __
   return sweep;
 }
 
-// ---------------------------------------------------------------------------------------
-// Permuted ping-pong variant (double, n <= kJacobiPPMax): the cyclic circle-method
-// Jacobi of jacobi_eig_smem with the data MOVED instead of the pairing: pair k of every
-// round is always storage slots (2k, 2k+1), and after each round every row / column goes
-// from slot s to slot sigma(s) (T[k] = slot 2k, B[k] = slot 2k+1; T[0] stays, the others
-// turn one place: T[k] -> T[k+1], T[m-1] -> B[m-1], B[k] -> B[k-1], B[0] -> T[1]) -- the
-// same round-robin tournament, so every pair still meets once per sweep.  Every thread's
-// read and write addresses are therefore fixed for the whole solve (no per-round index
-// arithmetic), and round g reads buffer g&1 and writes buffer (g+1)&1 (one block barrier
-// per round).  Z is stored by 2x2 blocks of slot pairs, upper block triangle only:
-// element (r, c), r/2 <= c/2, at (r/2) * ldp + 2c + (r&1); a block is 4 contiguous
-// doubles.  Eigenvector rows (Vt) live in slot order too and move with their slot.  The
-// rotations of round g+1 are computed during round g by m "angle" threads from the
-// round-g inputs and rotations (the entries they need are fixed linear combinations).
-// The rotation rule, angle formula and stopping rule are those of jacobi_eig_smem.
-// An odd n is padded with a zero row / column (it never rotates).
-// ---------------------------------------------------------------------------------------
-constexpr int kJacobiPPMax = 80;
-
-__host__ __device__ constexpr int pp_ldp(int npad) { return 2 * npad + 2; }   // 16 B odd multiple
-
-__device__ __forceinline__ int pp_sigma(int s, int m) {
-  if (m == 1 || s == 0) return s;
-  const int k = s >> 1;
-  if ((s & 1) == 0) return (k < m - 1) ? s + 2 : s + 1;
-  return (k > 0) ? s - 2 : 2;
-}
-
-__device__ __forceinline__ int pp_addr(int r, int c, int ldp) {
-  if ((r >> 1) > (c >> 1)) { const int t = r; r = c; c = t; }
-  return (r >> 1) * ldp + 2 * c + (r & 1);
-}
-
-struct JacobiPPBuf {
-  double* Z[2];    // m * ldp each (Z[0] holds the input)
-  double* V[2];    // npad * npad each (eigenvector rows by slot)
-  double2* cs;     // 2 x m rotations
-  int* nrot;       // 32 per-warp counters
-  float* offmax;   // 32 per-warp maxima
-};
-
-// shared-space accesses by 32-bit byte address (offsets are fixed per thread)
-__device__ __forceinline__ uint32_t sh_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ double2 lds_d2(uint32_t a) {
-  double2 v;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ double lds_d(uint32_t a) {
-  double v;
-  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ void sts_d(uint32_t a, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v)); }
-__device__ __forceinline__ void sts_d2(uint32_t a, double2 v) {
-  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y));
-}
-
-// ---- thread-block-cluster helpers (the V-split refresh, ngsgd.cu)
-__device__ __forceinline__ uint32_t cl_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t cl_map(uint32_t local_addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void cl_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void mb_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mb_arm(uint32_t bar, uint32_t bytes) {   // local arrive + expect_tx
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-// (default .release.cta semantics, as CUTLASS's cluster pipelines: a cluster-scope release
-// would put a MEMBAR.GPU on every round)
-__device__ __forceinline__ void mb_arrive_remote(uint32_t cluster_bar) {
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
-}
-__device__ __forceinline__ void mb_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAITC_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAITC_%=;\n\t}" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void st_async_d2(uint32_t cluster_addr, double2 v, uint32_t cluster_bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
-                   cluster_addr),
-               "d"(v.x), "d"(v.y), "r"(cluster_bar)
-               : "memory");
-}
-__device__ __forceinline__ void st_async_u32(uint32_t cluster_addr, uint32_t v, uint32_t cluster_bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];" ::"r"(cluster_addr),
-               "r"(v), "r"(cluster_bar)
-               : "memory");
-}
-__device__ __forceinline__ double ld_cluster_d(uint32_t cluster_addr) {
-  double v;
-  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(cluster_addr) : "memory");
-  return v;
-}
-__device__ __forceinline__ int ld_cluster_i(uint32_t cluster_addr) {
-  int v;
-  asm volatile("ld.shared::cluster.b32 %0, [%1];" : "=r"(v) : "r"(cluster_addr) : "memory");
-  return v;
-}
-
-// Rotation hand-off from the Z CTA (cluster rank 0) to the eigenvector CTAs (ranks
-// 1..nv): a ring of `ring` rounds; slot s holds the m rotations of one round plus a
-// command word (CONTINUE / STOP).  All addresses are local shared addresses of the
-// same-offset arrays (identical layout in every CTA of the cluster).
-// round timing (ng_debug_eig_clocks), recorded when dbg & 64
-__device__ unsigned long long g_eig_clk[8];
-
-struct PPCluster {
-  int nv, ring;
-  uint32_t cs_ring;    // V CTAs: ring x m double2
-  uint32_t cmd_ring;   // V CTAs: ring x u32
-  uint32_t full_bar;   // V CTAs: ring mbarriers (1 local arrive + m*16+4 tx bytes)
-  uint32_t empty_bar;  // Z CTA: ring mbarriers (nv remote arrives)
-};
-constexpr uint32_t kPPContinue = 1u, kPPStop = 2u;
-
-__device__ __forceinline__ void pp_push_cs(const PPCluster& cl, int m, int gn, int kk, double2 v) {
-  const int s = gn % cl.ring;
-  if (gn >= cl.ring) mb_wait(cl.empty_bar + 8u * s, (uint32_t)((gn / cl.ring) - 1) & 1u);
-  for (int r = 1; r <= cl.nv; ++r)
-    st_async_d2(cl_map(cl.cs_ring + 16u * (s * m + kk), r), v, cl_map(cl.full_bar + 8u * s, r));
-}
-__device__ __forceinline__ void pp_push_cmd(const PPCluster& cl, int gn, uint32_t cmd) {
-  const int s = gn % cl.ring;
-  for (int r = 1; r <= cl.nv; ++r) st_async_u32(cl_map(cl.cmd_ring + 4u * s, r), cmd, cl_map(cl.full_bar + 8u * s, r));
-}
-
-// Returns the sweep count; *fb = buffer index holding the result, *phantom = slot of the
-// padding row (-1 if n is even).  Thread roles: threads [0, m) own the diagonal blocks,
-// [m, m + m(m-1)/2) the off-diagonal blocks (no divergence between the two kinds inside
-// a warp), the last m threads compute the next round's rotations; eigenvector items are
-// spread over all threads.  Requires m(m+1)/2 <= blockDim - m.
-// VLOCAL = false: the eigenvector rows live in the cluster's V CTAs (jacobi_pp_vworker);
-// the angle threads push every round's rotations to them through `cl`.
-template <bool VLOCAL>
-__device__ __forceinline__ int jacobi_pp(JacobiPPBuf b, int n, int max_sweeps, double abs_floor, double rel_tol,
-                                         int* fb, int* phantom, int dbg, const PPCluster cl) {
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
-  const int npad = n + (n & 1), m = npad / 2, rounds = npad - 1, ldp = pp_ldp(npad);
-  const int noff = m * (m - 1) / 2;
-  const double tol2 = rel_tol * rel_tol, flo2 = abs_floor * abs_floor;
-  const float stop2 = (float)rel_tol;
-  if (VLOCAL)
-    for (int idx = tid; idx < npad * npad; idx += nt) {
-      const int i = idx / npad, j = idx - i * npad;
-      b.V[0][idx] = (i == j && i < n) ? 1.0 : 0.0;
-    }
-  const uint32_t zb = sh_addr(b.Z[0]), zd = sh_addr(b.Z[1]) - zb;
-  const uint32_t vb = VLOCAL ? sh_addr(b.V[0]) : 0u, vd = VLOCAL ? sh_addr(b.V[1]) - vb : 0u;
-  const uint32_t csb = sh_addr(b.cs);
-  // ---- block role: byte offsets within a Z buffer, fixed for the whole solve
-  const bool is_diag = tid < m;
-  const bool is_off = tid >= m && tid < m + noff;
-  int ka = 0, kb = 0;
-  if (is_diag) {
-    ka = kb = tid;
-  } else if (is_off) {
-    const int bb = tid - m;                // strictly upper block triangle, kb >= 1
-    kb = (int)((sqrtf(8.f * bb + 1.f) + 1.f) * 0.5f);
-    while (kb * (kb - 1) / 2 > bb) --kb;
-    while ((kb + 1) * kb / 2 <= bb) ++kb;
-    ka = bb - kb * (kb - 1) / 2;
-  }
-  uint32_t boff = 0, w00 = 0, w01 = 0, w10 = 0, w11 = 0, x00 = 0, x01 = 0, x10 = 0, x11 = 0;
-  uint32_t ca = csb + 16u * ka, cbk = csb + 16u * kb;
-  int dup = 0;
-  if (is_diag || is_off) {
-    boff = 8u * (ka * ldp + 4 * kb);
-    const int r0 = pp_sigma(2 * ka, m), r1 = pp_sigma(2 * ka + 1, m);
-    const int c0 = pp_sigma(2 * kb, m), c1 = pp_sigma(2 * kb + 1, m);
-    w00 = 8u * pp_addr(r0, c0, ldp);
-    w01 = 8u * pp_addr(r0, c1, ldp);
-    w10 = 8u * pp_addr(r1, c0, ldp);
-    w11 = 8u * pp_addr(r1, c1, ldp);
-    // an off-diagonal element landing inside a next-round diagonal block is stored twice
-    if ((r0 >> 1) == (c0 >> 1) && r0 != c0) { dup |= 1; x00 = 8u * pp_addr(c0, r0, ldp); }
-    if ((r0 >> 1) == (c1 >> 1) && r0 != c1) { dup |= 2; x01 = 8u * pp_addr(c1, r0, ldp); }
-    if ((r1 >> 1) == (c0 >> 1) && r1 != c0) { dup |= 4; x10 = 8u * pp_addr(c0, r1, ldp); }
-    if ((r1 >> 1) == (c1 >> 1) && r1 != c1) { dup |= 8; x11 = 8u * pp_addr(c1, r1, ldp); }
-  }
-  // ---- angle role: pair k of the next round from the slots that move into 2k, 2k+1
-  const int angle0 = nt - m;
-  const bool is_angle = tid >= angle0;
-  const int kk = tid - angle0;
-  uint32_t du = 0, dv = 0, mbo = 0, cu = 0, cv = 0;
-  int mtr = 0, iu = 0, iv = 0;
-  if (is_angle) {
-    int u = 0, v = 0;
-    for (int s2 = 0; s2 < npad; ++s2) {
-      const int t = pp_sigma(s2, m);
-      if (t == 2 * kk) u = s2;
-      if (t == 2 * kk + 1) v = s2;
-    }
-    const int pu = u >> 1, pv = v >> 1;
-    iu = u & 1; iv = v & 1;
-    du = 8u * (pu * ldp + 4 * pu);
-    dv = 8u * (pv * ldp + 4 * pv);
-    mtr = pu > pv;
-    mbo = 8u * (mtr ? pv * ldp + 4 * pu : pu * ldp + 4 * pv);
-    cu = 16u * pu;
-    cv = 16u * pv;
-  }
-  // ---- eigenvector items (pair k, double2 column j): rows 2k, 2k+1 -> sigma(2k), sigma(2k+1)
-  const int nv2 = npad / 2;
-  uint32_t vr[2], vw0[2], vw1[2], vcs[2];
-  int nvi = 0;
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int it = tid + i * nt;
-    vr[i] = vw0[i] = vw1[i] = vcs[i] = 0;
-    if (VLOCAL && it < m * nv2) {
-      const int k = it / nv2, j = it - k * nv2;
-      vcs[i] = 16u * k;
-      vr[i] = 8u * ((2 * k) * npad + 2 * j);
-      vw0[i] = 8u * (pp_sigma(2 * k, m) * npad + 2 * j);
-      vw1[i] = 8u * (pp_sigma(2 * k + 1, m) * npad + 2 * j);
-      nvi = i + 1;
-    }
-  }
-  const uint32_t vrow = 8u * npad;
-  int rot_cur = 0, rot_next = 0;
-  float off_cur = 0.f, off_next = 0.f;
-  auto angle = [&](double app, double aqq, double apq, int& rot, float& off) -> double2 {
-    double2 r;
-    r.x = 1.0;
-    r.y = 0.0;
-    const double apq2 = apq * apq, dd = fabs(app * aqq);
-    if (apq2 > tol2 * dd && apq2 > flo2) {
-      off = fmaxf(off, __fdividef((float)apq2, (float)dd));
-      const float th = __fdividef((float)(aqq - app), 2.f * (float)apq);
-      float tf;
-      if (!(fabsf(th) < 1e18f)) {
-        tf = __fdividef(0.5f, th);
-      } else {
-        const float r2 = fmaf(th, th, 1.f);
-        tf = copysignf(__fdividef(1.f, fabsf(th) + r2 * rsqrtf(r2)), th);
-      }
-      const double t = (double)tf;
-      const double x = t * t + 1.0;
-      const double c0 = (double)rsqrtf((float)x);
-      const double c = c0 * (1.5 - 0.5 * x * c0 * c0);
-      r.x = c;
-      r.y = t * c;
-      ++rot;
-    }
-    return r;
-  };
-  if (tid == 0) *phantom = (n & 1) ? n : -1;
-  __syncthreads();   // input Z[0] complete (caller), V[0] initialised
-  if (is_angle) {
-    const double* z = b.Z[0] + kk * ldp + 4 * kk;
-    const double2 r0 = angle(z[0], z[3], z[2], rot_cur, off_cur);
-    b.cs[kk] = r0;
-    if (!VLOCAL) {
-      pp_push_cs(cl, m, 0, kk, r0);
-      if (kk == 0) pp_push_cmd(cl, 0, kPPContinue);
-    }
-  }
-  __syncthreads();
-  int sweep = 0, g = 0;
-  const uint32_t csd = 16u * m;
-  const bool timing = (dbg & 64) != 0;
-  unsigned long long ck[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const bool t_angle = timing && is_angle && kk == 0, t_blk = timing && tid == m + 1, t_zero = timing && tid == 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    for (int round = 0; round < rounds; ++round, ++g) {
-      const bool odd = g & 1;
-      long long c0 = 0;
-      if (timing) c0 = clock64();
-      const uint32_t zc = zb + (odd ? zd : 0u), zn = zb + (odd ? 0u : zd);
-      const uint32_t vc = vb + (odd ? vd : 0u), vn = vb + (odd ? 0u : vd);
-      const uint32_t cc_ = odd ? csd : 0u;
-      if (is_off && !(dbg & 16)) {
-        const double2 r1 = lds_d2(ca + cc_), r2 = lds_d2(cbk + cc_);
-        const double2 u = lds_d2(zc + boff);          // (2ka, 2kb), (2ka+1, 2kb)
-        const double2 w = lds_d2(zc + boff + 16u);    // (2ka, 2kb+1), (2ka+1, 2kb+1)
-        const double c1 = r1.x, s1 = r1.y, c2 = r2.x, s2 = r2.y;
-        const double m00 = u.x, m10 = u.y, m01 = w.x, m11 = w.y;
-        long long c1t = 0;
-        if (t_blk) {
-          asm volatile("" ::"d"(m00), "d"(m11), "d"(c1), "d"(s2));
-          c1t = clock64();
-          ck[4] += c1t - c0;
-        }
-        const double t00 = c1 * m00 - s1 * m10, t01 = c1 * m01 - s1 * m11;
-        const double t10 = s1 * m00 + c1 * m10, t11 = s1 * m01 + c1 * m11;
-        const double r00 = c2 * t00 - s2 * t01, r01 = s2 * t00 + c2 * t01;
-        const double r10 = c2 * t10 - s2 * t11, r11 = s2 * t10 + c2 * t11;
-        sts_d(zn + w00, r00);
-        sts_d(zn + w01, r01);
-        sts_d(zn + w10, r10);
-        sts_d(zn + w11, r11);
-        if (t_blk) ck[5] += clock64() - c1t;
-        if (dup) {
-          if (dup & 1) sts_d(zn + x00, r00);
-          if (dup & 2) sts_d(zn + x01, r01);
-          if (dup & 4) sts_d(zn + x10, r10);
-          if (dup & 8) sts_d(zn + x11, r11);
-        }
-      } else if (is_diag && !(dbg & 16)) {
-        const double2 r1 = lds_d2(ca + cc_);
-        const double2 u = lds_d2(zc + boff);
-        const double2 w = lds_d2(zc + boff + 16u);
-        const double c1 = r1.x, s1 = r1.y;
-        const double a = u.x, bb = w.x, d = w.y;
-        const double cc = c1 * c1, ss = s1 * s1, csx = c1 * s1;
-        const double bn = (cc - ss) * bb + csx * (a - d);
-        sts_d(zn + w00, cc * a - 2.0 * csx * bb + ss * d);
-        sts_d(zn + w11, ss * a + 2.0 * csx * bb + cc * d);
-        sts_d(zn + w01, bn);
-        if (dup & 2) sts_d(zn + x01, bn);   // m == 1 only
-      }
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        if (i >= nvi) break;
-        const double2 r = lds_d2(csb + vcs[i] + cc_);
-        const double2 a = lds_d2(vc + vr[i]);
-        const double2 bq = lds_d2(vc + vr[i] + vrow);
-        double2 na, nb2;
-        na.x = r.x * a.x - r.y * bq.x; na.y = r.x * a.y - r.y * bq.y;
-        nb2.x = r.y * a.x + r.x * bq.x; nb2.y = r.y * a.y + r.x * bq.y;
-        sts_d2(vn + vw0[i], na);
-        sts_d2(vn + vw1[i], nb2);
-      }
-      if (is_angle) {
-        // new row (slot u) = x0 row(2pu) + x1 row(2pu+1), with R = [[c, -s], [s, c]]
-        const double2 rP = lds_d2(csb + cu + cc_), rQ = lds_d2(csb + cv + cc_);
-        const double xu0 = iu ? rP.y : rP.x, xu1 = iu ? rP.x : -rP.y;
-        const double xv0 = iv ? rQ.y : rQ.x, xv1 = iv ? rQ.x : -rQ.y;
-        const double2 zu0 = lds_d2(zc + du), zu1 = lds_d2(zc + du + 16u);
-        const double2 zv0 = lds_d2(zc + dv), zv1 = lds_d2(zc + dv + 16u);
-        const double2 zm0 = lds_d2(zc + mbo), zm1 = lds_d2(zc + mbo + 16u);
-        const double app = xu0 * xu0 * zu0.x + 2.0 * xu0 * xu1 * zu1.x + xu1 * xu1 * zu1.y;
-        const double aqq = xv0 * xv0 * zv0.x + 2.0 * xv0 * xv1 * zv1.x + xv1 * xv1 * zv1.y;
-        // M(i, j) = Z[2pu+i][2pv+j]: stored (i, j) at 2j+i, or transposed at 2i+j
-        const double m00 = zm0.x, m11 = zm1.y;
-        const double m10 = mtr ? zm1.x : zm0.y, m01 = mtr ? zm0.y : zm1.x;
-        const double apq = xu0 * (m00 * xv0 + m01 * xv1) + xu1 * (m10 * xv0 + m11 * xv1);
-        const bool wrap = round + 1 == rounds;
-        long long a1t = 0;
-        if (t_angle) {
-          asm volatile("" ::"d"(zu0.x), "d"(zv1.y), "d"(zm0.x), "d"(zm1.y), "d"(rP.x), "d"(rQ.y));
-          a1t = clock64();
-          ck[1] += a1t - c0;
-        }
-        double2 rn;
-        if (dbg & 32) {   // profiling: fixed rotation, no angle chain
-          rn.x = 0.8;
-          rn.y = 0.6;
-        } else {
-          rn = wrap ? angle(app, aqq, apq, rot_next, off_next) : angle(app, aqq, apq, rot_cur, off_cur);
-        }
-        long long a2t = 0;
-        if (t_angle) {
-          asm volatile("" ::"d"(rn.x), "d"(rn.y));
-          a2t = clock64();
-          ck[2] += a2t - a1t;
-        }
-        sts_d2(csb + (odd ? 0u : csd) + 16u * kk, rn);
-        if (!VLOCAL) {
-          pp_push_cs(cl, m, g + 1, kk, rn);
-          if (kk == 0 && !wrap) pp_push_cmd(cl, g + 1, kPPContinue);
-        }
-        if (t_angle) { ck[3] += clock64() - a2t; ck[0] += 1; }
-      }
-      if (tid == 0 && *phantom >= 0) *phantom = pp_sigma(*phantom, m);
-      __syncthreads();
-      if (t_zero) ck[6] += clock64() - c0;
-    }
-    int my_rot = warp_sum(rot_cur);
-    float my_off = warp_max(off_cur);
-    if (lane == 0) { b.nrot[warp] = my_rot; b.offmax[warp] = my_off; }
-    rot_cur = rot_next; off_cur = off_next; rot_next = 0; off_next = 0.f;
-    __syncthreads();
-    int rot = 0;
-    float om = 0.f;
-    for (int w = 0; w < nwarps; ++w) { rot += b.nrot[w]; om = fmaxf(om, b.offmax[w]); }
-    __syncthreads();
-    const bool stop = rot == 0 || om < stop2 || ((dbg & 4) && sweep + 1 >= 5) || sweep + 1 >= max_sweeps;
-    // the next round's rotations were already pushed; its command decides
-    if (!VLOCAL && is_angle && kk == 0) pp_push_cmd(cl, g, stop ? kPPStop : kPPContinue);
-    if (stop) { ++sweep; break; }
-  }
-  if (timing) {
-    if (t_angle) for (int i = 0; i < 4; ++i) atomicAdd(&g_eig_clk[i], ck[i]);
-    if (t_blk) { atomicAdd(&g_eig_clk[4], ck[4]); atomicAdd(&g_eig_clk[5], ck[5]); }
-    if (t_zero) atomicAdd(&g_eig_clk[6], ck[6]);
-  }
-  *fb = g & 1;
-  return sweep;
-}
-
-// The eigenvector side of the cluster solve (ranks 1..nv): columns [j0, j0 + w) of the
-// slot-ordered eigenvector rows, ping-pong V0/V1 (npad x w, row stride w), rotations of
-// round g from ring slot g % ring.  Returns the number of rounds applied (the final
-// buffer is rounds & 1).
-__device__ __forceinline__ int jacobi_pp_vworker(double* V0, double* V1, int n, int j0, int w,
-                                                 const double2* cs_ring, const uint32_t* cmd_ring, const PPCluster cl) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int npad = n + (n & 1), m = npad / 2;
-  const int nw2 = w / 2;
-  for (int idx = tid; idx < npad * w; idx += nt) {
-    const int i = idx / w, j = j0 + (idx - (idx / w) * w);
-    V0[idx] = (i == j && i < n) ? 1.0 : 0.0;
-  }
-  // items (pair k, double2 column j) -- one per thread (m * w / 2 <= blockDim)
-  const bool has = tid < m * nw2;
-  uint32_t vr = 0, vw0 = 0, vw1 = 0, kcs = 0;
-  if (has) {
-    const int k = tid / nw2, j = tid - k * nw2;
-    kcs = 16u * k;
-    vr = 8u * ((2 * k) * w + 2 * j);
-    vw0 = 8u * (pp_sigma(2 * k, m) * w + 2 * j);
-    vw1 = 8u * (pp_sigma(2 * k + 1, m) * w + 2 * j);
-  }
-  const uint32_t vb = sh_addr(V0), vd = sh_addr(V1) - vb, vrow = 8u * w;
-  const uint32_t csr = sh_addr(cs_ring);
-  const uint32_t tx = 16u * m + 4u;
-  __syncthreads();
-  int g = 0;
-  for (;; ++g) {
-    const int s = g % cl.ring;
-    mb_wait(cl.full_bar + 8u * s, (uint32_t)(g / cl.ring) & 1u);
-    if (cmd_ring[s] == kPPStop) break;
-    if (has) {
-      const bool odd = g & 1;
-      const uint32_t vc = vb + (odd ? vd : 0u), vn = vb + (odd ? 0u : vd);
-      const double2 r = lds_d2(csr + 16u * (s * m) + kcs);
-      const double2 a = lds_d2(vc + vr);
-      const double2 bq = lds_d2(vc + vr + vrow);
-      double2 na, nb2;
-      na.x = r.x * a.x - r.y * bq.x; na.y = r.x * a.y - r.y * bq.y;
-      nb2.x = r.y * a.x + r.x * bq.x; nb2.y = r.y * a.y + r.x * bq.y;
-      sts_d2(vn + vw0, na);
-      sts_d2(vn + vw1, nb2);
-    }
-    __syncthreads();
-    if (tid == 0) {
-      mb_arm(cl.full_bar + 8u * s, tx);                 // next use of this slot
-      mb_arrive_remote(cl_map(cl.empty_bar + 8u * s, 0));
-    }
-  }
-  return g;
-}
-
 }  // namespace ng

@@ -27,10 +27,36 @@
 // per-thread qd recurrences.  scratch/ prototypes: tools/tri_proto.py.
 #pragma once
 
-#include "eig_dc.cuh"   // frcp / fdiv / fsqrt (MUFU approximations + Newton steps)
 #include "ng_common.cuh"
 
 namespace ng {
+
+// FP64 reciprocal / divide / square root from the hardware approximations (MUFU.RCP64H,
+// MUFU.RSQ64H) plus Newton steps: ~1 ulp, a fraction of the latency of the IEEE-rounded
+// library sequences -- the secular iterations and the Householder step are chains of them.
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double fdiv(double a, double b) {
+  const double r = frcp(b);
+  const double q = a * r;
+  return fma(fma(-b, q, a), r, q);
+}
+__device__ __forceinline__ double fsqrt(double x) {   // x >= 0
+  if (!(x > 0.0)) return 0.0;
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-0.5 * x * y, y, 1.5);
+  y = y * fma(-0.5 * x * y, y, 1.5);
+  const double s = x * y;
+  return fma(0.5 * y, fma(-s, s, x), s);
+}
+
 
 constexpr int kTriMax = 80;
 constexpr int kTriChunks = 5;   // column chunks of the Householder pass

@@ -20,7 +20,6 @@
 #include <vector>
 
 #include "eig_jacobi.cuh"
-#include "eig_dc.cuh"
 #include "eig_tri.cuh"
 #include "eig_topr.cuh"
 #include "gemm_simt.cuh"
@@ -262,123 +261,47 @@ __global__ void copy_gated_kernel(int R, int D, float* __restrict__ dst, const f
 
 // Eigensolver variants of refresh_kernel:
 //   REFRESH_INPLACE  one CTA, in-place two-barrier Jacobi (any R <= kMaxRank)
-//   REFRESH_PP       one CTA, permuted ping-pong Jacobi with the eigenvectors (R <= 80)
-//   REFRESH_CLUSTER  thread-block cluster: rank 0 runs the permuted Jacobi on Z, ranks
-//                    1..nv keep column slices of the eigenvectors and apply each round's
-//                    rotations as they arrive (DSMEM ring, eig_jacobi.cuh); the shared-
-//                    memory traffic of the eigenvector update leaves the Z CTA (R <= 80)
-//   REFRESH_DC       one CTA, Householder + divide and conquer (eig_dc.cuh)
 //   REFRESH_TRI      one CTA, Householder + relatively robust representation + twisted
 //                    factorisation eigenvectors (eig_tri.cuh), falling back to the in-place
 //                    Jacobi when its orthogonality check fails (default, 2 <= R <= 80)
-enum RefreshMode : int { REFRESH_INPLACE = 0, REFRESH_PP = 1, REFRESH_CLUSTER = 2, REFRESH_DC = 3, REFRESH_TRI = 4 };
-constexpr int kPPRing = 16;
+// (Round-1/2 alternatives measured slower and removed -- a permuted ping-pong Jacobi, its
+// thread-block-cluster split and a divide-and-conquer solver.)
+enum RefreshMode : int { REFRESH_INPLACE = 0, REFRESH_TRI = 4 };
 
 // Shared-memory plan (offsets in doubles from the 16-byte aligned dynamic base).
 struct RefreshSmem {
-  int R, npad, m, ldp, LD, LDV, mp, mode, nv, w;
-  size_t o_bar, o_cmd, o_d, o_lam, o_share, o_z0, o_z1, o_v0, o_v1, o_cs, o_ring, o_int, total_bytes;
+  int R, npad, LD, LDV, mp, mode;
+  size_t o_d, o_lam, o_z0, o_v0, o_cs, o_ring, o_int, total_bytes;
 };
 __host__ __device__ inline RefreshSmem refresh_plan(int R, int mode) {
   RefreshSmem p;
   p.R = R;
   p.npad = R + (R & 1);
-  p.m = p.npad / 2;
-  p.ldp = pp_ldp(p.npad);
   p.LD = R + 1;
   p.LDV = (R + 3) / 4 * 4;
   p.mp = R / 2 + 1;
   p.mode = mode;
-  p.nv = 0;
-  p.w = 0;
-  if (mode == REFRESH_CLUSTER) {
-    const int items = p.m * p.npad / 2;                 // (pair, double2 column) items
-    p.nv = (items + 1023) / 1024;
-    const int w = (p.npad + p.nv - 1) / p.nv;
-    p.w = w + (w & 1);
-  }
   size_t o = 0;
-  p.o_bar = o;  o += kPPRing;                          // ring mbarriers (empty: rank 0, full: V ranks)
-  p.o_cmd = o;  o += kPPRing / 2;                      // ring command words (u32)
   p.o_d = o;    o += 5 * (size_t)R + 32;               // d, emh, dr, c, dn, red[32]
-  p.o_lam = o;  o += (size_t)p.npad + 2;               // eigenvalues (slot / index order)
-  p.o_share = o; o += (size_t)R;                       // A_t row factors (cluster)
+  p.o_lam = o;  o += (size_t)p.npad + 2;               // eigenvalues
   o = (o + 1) & ~(size_t)1;                            // 16-byte alignment
-  if (mode == REFRESH_DC) {   // eig_dc's plan; Z_t is built in its A region (ld R + 1)
-    const DCPlan dp = dc_plan(R);
-    p.o_ring = o;
-    p.o_z0 = o + dp.oA; p.o_z1 = p.o_z0;
-    p.o_v0 = o + dp.oV; p.o_v1 = p.o_v0;     // eigenvector rows come out here (ld R)
-    p.o_cs = o;
-    o += (dp.total + 15) / 8;
-  } else if (mode == REFRESH_TRI) {   // eig_tri's plan; Z_t in its A region (ld R + 1)
+  if (mode == REFRESH_TRI) {   // eig_tri's plan; Z_t in its A region (ld R + 1)
     const TriPlan tp = tri_plan(R);
     p.o_ring = o;
-    p.o_z0 = o + tp.oA; p.o_z1 = p.o_z0;
-    p.o_v0 = o + tp.oX; p.o_v1 = p.o_v0;   // Jacobi fallback: eigenvector rows (ld LDV)
+    p.o_z0 = o + tp.oA;
+    p.o_v0 = o + tp.oX;                    // Jacobi fallback: eigenvector rows (ld LDV)
     p.o_cs = o + tp.oQ;                    // Jacobi fallback: (c, s) scratch
     o += ((tp.total + 15) / 16) * 2;
-  } else if (mode == REFRESH_INPLACE) {
+  } else {
     p.o_z0 = o; o += ((size_t)R * p.LD + 1) & ~(size_t)1;
-    p.o_z1 = p.o_z0;
     p.o_v0 = o; o += (size_t)R * p.LDV;
-    p.o_v1 = p.o_v0;
     p.o_cs = o; o += 2 * (size_t)p.mp + 2;
     p.o_ring = o;
-  } else {
-    const size_t zsz = (size_t)p.m * p.ldp;
-    const size_t vsz = (size_t)p.npad * (mode == REFRESH_PP ? p.npad : p.w);
-    const size_t z_part = 2 * zsz + 4 * (size_t)p.m;                   // rank 0 (and PP)
-    const size_t v_part = (mode == REFRESH_PP) ? 2 * vsz : 2 * vsz + 2 * (size_t)kPPRing * p.m;
-    p.o_z0 = o; p.o_z1 = o + zsz; p.o_cs = o + 2 * zsz;
-    if (mode == REFRESH_PP) {
-      p.o_v0 = o + z_part; p.o_v1 = p.o_v0 + vsz; p.o_ring = p.o_v1 + vsz;
-      o += z_part + v_part;
-    } else {   // the V ranks reuse the Z region
-      p.o_v0 = o; p.o_v1 = o + vsz; p.o_ring = o + 2 * vsz;
-      o += (z_part > v_part ? z_part : v_part);
-    }
   }
   p.o_int = o;
   // ints: perm[npad], nrot[64 + 2 mp], iflag, phantom, fb, offmax[32] (float)
   p.total_bytes = sizeof(double) * o + sizeof(int) * ((size_t)p.npad + 64 + 2 * p.mp + 3 + 32) + 64;
   return p;
-}
-
-// V ranks of the cluster refresh: rotate the eigenvector slice, then write their columns
-// of A_t from the row factors / permutation rank 0 publishes.
-__device__ void refresh_vrank(const RefreshSmem& P, uint32_t rank, double* sm, float* __restrict__ Amat) {
-  const int R = P.R, tid = threadIdx.x, nt = blockDim.x;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + P.o_bar);
-  uint32_t* cmd = reinterpret_cast<uint32_t*>(sm + P.o_cmd);
-  PPCluster cl{P.nv, kPPRing, sh_addr(sm + P.o_ring), sh_addr(cmd), sh_addr(bars), sh_addr(bars)};
-  if (tid == 0) {
-    for (int s2 = 0; s2 < kPPRing; ++s2) mb_init(cl.full_bar + 8u * s2, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s2 = 0; s2 < kPPRing; ++s2) mb_arm(cl.full_bar + 8u * s2, 16u * P.m + 4u);
-  }
-  cl_sync();   // (0) every barrier of the cluster initialised
-  const int j0 = ((int)rank - 1) * P.w;
-  double* V0 = sm + P.o_v0;
-  double* V1 = sm + P.o_v1;
-  const int rounds = jacobi_pp_vworker(V0, V1, R, j0, P.w, reinterpret_cast<const double2*>(sm + P.o_ring), cmd, cl);
-  const double* Vf = (rounds & 1) ? V1 : V0;
-  cl_sync();   // (1) rank 0 published perm, row factors, E_t^{-1/2}
-  double* fr = sm + P.o_share;
-  double* emh = sm + P.o_d + R;
-  int* perm = reinterpret_cast<int*>(sm + P.o_int);
-  for (int i = tid; i < R; i += nt) {
-    fr[i] = ld_cluster_d(cl_map(sh_addr(fr + i), 0));
-    emh[i] = ld_cluster_d(cl_map(sh_addr(emh + i), 0));
-    perm[i] = ld_cluster_i(cl_map(sh_addr(perm + i), 0));
-  }
-  __syncthreads();
-  const int jn = min(R, j0 + P.w) - j0;
-  for (int idx = tid; idx < R * (jn > 0 ? jn : 0); idx += nt) {
-    const int r = idx / jn, jj = idx - r * jn, j = j0 + jj;
-    Amat[r * R + j] = (float)(fr[r] * Vf[perm[r] * P.w + jj] * emh[j]);
-  }
-  cl_sync();   // (2) rank 0's shared memory is no longer read
 }
 
 __device__ unsigned long long g_ref_t[256][9];   // refresh timing (ng_debug_refresh_times): R, start, end ns, eig, phase cycles
@@ -395,18 +318,6 @@ __device__ __forceinline__ void refresh_body(int R, int D, int N, double eta, do
   unsigned long long t_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   const RefreshSmem P = refresh_plan(R, MODE);
-  PPCluster cl{};
-  if constexpr (MODE == REFRESH_CLUSTER) {
-    const uint32_t rank = cl_rank();
-    if (rank != 0) { refresh_vrank(P, rank, sm, Amat); return; }
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + P.o_bar);
-    cl = PPCluster{P.nv, kPPRing, sh_addr(sm + P.o_ring), sh_addr(sm + P.o_cmd), sh_addr(bars), sh_addr(bars)};
-    if (threadIdx.x == 0) {
-      for (int s2 = 0; s2 < kPPRing; ++s2) mb_init(cl.empty_bar + 8u * s2, (uint32_t)P.nv);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    cl_sync();   // (0)
-  }
   double* d = sm + P.o_d;               // R   old d
   double* emh = d + R;                  // R   E_t^{-1/2}
   double* dr = emh + R;                 // R   d + rho
@@ -421,7 +332,6 @@ __device__ __forceinline__ void refresh_body(int R, int D, int N, double eta, do
   int* fbuf = phantom + 1;
   float* offmax = reinterpret_cast<float*>(fbuf + 1);  // 32 (per-warp max ratio)
   const int tid = threadIdx.x, nt = blockDim.x;
-  constexpr bool PPK = MODE == REFRESH_PP || MODE == REFRESH_CLUSTER;
 
   const double rho = dstate[0];
   for (int i = tid; i < R; i += nt) d[i] = dstate[1 + i];
@@ -450,19 +360,9 @@ __device__ __forceinline__ void refresh_body(int R, int D, int N, double eta, do
     return z;
   };
   double* Z = sm + P.o_z0;
-  if (PPK && MODE != REFRESH_DC) {
-    // slot-pair block layout, upper block triangle (eig_jacobi.cuh), zero padding row
-    const int np = P.npad;
-    for (int idx = tid; idx < np * np; idx += nt) {
-      const int i = idx / np, j = idx % np;
-      if ((i >> 1) > (j >> 1)) continue;
-      Z[(i >> 1) * P.ldp + 2 * j + (i & 1)] = (i < R && j < R) ? zval(i, j) : 0.0;
-    }
-  } else {
-    for (int idx = tid; idx < R * R; idx += nt) {
-      const int i = idx / R, j = idx % R;
-      Z[i * P.LD + j] = zval(i, j);
-    }
+  for (int idx = tid; idx < R * R; idx += nt) {
+    const int i = idx / R, j = idx % R;
+    Z[i * P.LD + j] = zval(i, j);
   }
   double zmax = 0.0;
   for (int i = tid; i < R; i += nt) zmax = fmax(zmax, fabs(zval(i, i)));
@@ -502,30 +402,7 @@ __device__ __forceinline__ void refresh_body(int R, int D, int N, double eta, do
     }
     nlam = R;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_eig1));
-  } else if (MODE == REFRESH_DC) {
-    // Householder + divide and conquer (eig_dc.cuh); the eigenvector rows overwrite Z
-    eig_dc(sm + P.o_ring, dc_plan(R), Z, P.LD, lam, sm + P.o_v0, R);
-    sweeps = 0;
-    V = sm + P.o_v0;
-    ldv = R;
-    nlam = R;
-  } else if (PPK) {
-    JacobiPPBuf jb{{sm + P.o_z0, sm + P.o_z1}, {sm + P.o_v0, sm + P.o_v1},
-                   reinterpret_cast<double2*>(sm + P.o_cs), nrot, offmax};
-    int fb_local = 0;
-    if (MODE == REFRESH_CLUSTER)
-      sweeps = jacobi_pp<false>(jb, R, 20, 1e-15 * zmax, 1e-7, &fb_local, phantom, dbg_mask, cl);
-    else
-      sweeps = jacobi_pp<true>(jb, R, 20, 1e-15 * zmax, 1e-7, &fb_local, phantom, dbg_mask, cl);
-    __syncthreads();
-    const double* Zf = fb_local ? jb.Z[1] : jb.Z[0];
-    const int ph = *phantom;
-    for (int s2 = tid; s2 < P.npad; s2 += nt)
-      lam[s2] = (s2 == ph) ? -INFINITY : Zf[(s2 >> 1) * P.ldp + 2 * s2 + (s2 & 1)];
-    V = fb_local ? jb.V[1] : jb.V[0];
-    ldv = P.npad;
-    nlam = P.npad;
-  } else if (MODE == REFRESH_INPLACE) {
+  } else {
     JacobiSmem<double> scr{sm + P.o_cs, sm + P.o_cs + P.mp, nrot, offmax};
     double* Vt = sm + P.o_v0;
     sweeps = jacobi_eig_smem<double>(Z, P.LD, Vt, P.LDV, R, scr, 20, 1e-15 * zmax, 1e-7, dbg_mask);
@@ -565,20 +442,10 @@ __device__ __forceinline__ void refresh_body(int R, int D, int N, double eta, do
   sdn = block_sum(sdn, red);
   const double beta_new = rho_new * (1.0 + alpha) + (alpha / D) * sdn;
   // A_t = (eta/N) E_{t+1}^{1/2} C^{-1/2} U^T E_t^{-1/2}
-  if (MODE == REFRESH_CLUSTER) {
-    // row factors for the V ranks, which hold U (eig_jacobi.cuh); they write A_t
-    double* fr = sm + P.o_share;
-    for (int r = tid; r < R; r += nt) {
-      const double en = 1.0 / (beta_new / dn[r] + 1.0);
-      fr[r] = (eta / N) * sqrt(en) / sqrt(c[r]);
-    }
-    cl_sync();   // (1) published
-  } else {
-    for (int idx = tid; idx < R * R; idx += nt) {
-      const int r = idx / R, j = idx % R;
-      const double en = 1.0 / (beta_new / dn[r] + 1.0);
-      Amat[idx] = (float)((eta / N) * sqrt(en) / sqrt(c[r]) * V[perm[r] * ldv + j] * emh[j]);
-    }
+  for (int idx = tid; idx < R * R; idx += nt) {
+    const int r = idx / R, j = idx % R;
+    const double en = 1.0 / (beta_new / dn[r] + 1.0);
+    Amat[idx] = (float)((eta / N) * sqrt(en) / sqrt(c[r]) * V[perm[r] * ldv + j] * emh[j]);
   }
   // row scale of B_t with the OLD d, rho
   for (int k = tid; k < R; k += nt) svec[k] = (float)((N * (1.0 - eta) / eta) * dr[k]);
@@ -601,7 +468,6 @@ __device__ __forceinline__ void refresh_body(int R, int D, int N, double eta, do
     flags[4] = sweeps;
     if (!isfinite(rho_new) || !isfinite(sdn)) atomicOr(reinterpret_cast<unsigned*>(flags + 3), kErrNonFinite);
   }
-  if (MODE == REFRESH_CLUSTER) cl_sync();   // (2) the V ranks are done with this CTA's shared memory
   if (tid == 0) {
     unsigned long long t_end;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
@@ -930,12 +796,6 @@ static ng_status set_kernel_attrs() {
   if (done) return NG_OK;
   NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<REFRESH_INPLACE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)refresh_plan(kMaxRank, REFRESH_INPLACE).total_bytes));
-  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<REFRESH_PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)refresh_plan(kJacobiPPMax, REFRESH_PP).total_bytes));
-  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<REFRESH_CLUSTER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)refresh_plan(kJacobiPPMax, REFRESH_CLUSTER).total_bytes));
-  NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<REFRESH_DC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)refresh_plan(kDCMax, REFRESH_DC).total_bytes));
   NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<REFRESH_TRI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)refresh_plan(kTriMax, REFRESH_TRI).total_bytes));
   NG_CUDA_TRY(cudaFuncSetAttribute(refresh_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -1152,40 +1012,15 @@ static ng_status launch_refresh_chain(ngsgd_ctx* h, int n, double eta, const dou
     // most updates (measured on the config-3 network).
     static const int dbg = getenv("NG_PROFILE_JACOBI_MASK") ? atoi(getenv("NG_PROFILE_JACOBI_MASK")) : 0;
     // Solver choice: Householder + RRR/twisted eigenvectors (eig_tri.cuh, Jacobi fallback
-    // inside) for 2 <= R <= kTriMax, the in-place Jacobi beyond.  NG_TUNE_EIG_MODE = 0..4
-    // forces one (comparisons only): 1/2 the permuted one-CTA / cluster Jacobi, 3 D&C.
+    // inside) for 2 <= R <= kTriMax, the in-place Jacobi beyond.  NG_TUNE_EIG_MODE = 0
+    // forces the Jacobi (comparisons only).
     static const int force = tune_int("NG_TUNE_EIG_MODE", -1);
     int mode = (R >= 2 && R <= kTriMax) ? REFRESH_TRI : REFRESH_INPLACE;
-    if (force >= 0 && (force == REFRESH_INPLACE || R <= kJacobiPPMax) && (force != REFRESH_CLUSTER || R >= 8) &&
-        (force != REFRESH_DC || (R >= 2 && R <= kDCMax)) && (force != REFRESH_TRI || (R >= 2 && R <= kTriMax)))
-      mode = force;
+    if (force == REFRESH_INPLACE) mode = force;
     const RefreshSmem plan = refresh_plan(R, mode);
-    if (mode == REFRESH_CLUSTER) {
-      cudaLaunchConfig_t lc;
-      std::memset(&lc, 0, sizeof(lc));
-      lc.gridDim = dim3(1 + plan.nv, 1, 1);
-      lc.blockDim = dim3(1024, 1, 1);
-      lc.dynamicSmemBytes = plan.total_bytes;
-      lc.stream = ss;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = 1 + plan.nv;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      lc.attrs = at;
-      lc.numAttrs = 1;
-      NG_CUDA_TRY(cudaLaunchKernelEx(&lc, refresh_kernel<REFRESH_CLUSTER>, R, D, n, eta, a_, e_,
-                                     (const float*)h->KL, h->dstate, trx, h->Amat, h->svec,
-                                     h->flags, dbg));
-    } else if (mode == REFRESH_TRI) {
+    if (mode == REFRESH_TRI) {
       refresh_kernel<REFRESH_TRI><<<1, 1024, plan.total_bytes, ss>>>(R, D, n, eta, a_, e_, h->KL, h->dstate,
                                                                      trx, h->Amat, h->svec, h->flags, dbg);
-    } else if (mode == REFRESH_DC) {
-      refresh_kernel<REFRESH_DC><<<1, 1024, plan.total_bytes, ss>>>(R, D, n, eta, a_, e_, h->KL, h->dstate,
-                                                                    trx, h->Amat, h->svec, h->flags, dbg);
-    } else if (mode == REFRESH_PP) {
-      refresh_kernel<REFRESH_PP><<<1, 1024, plan.total_bytes, ss>>>(R, D, n, eta, a_, e_, h->KL, h->dstate,
-                                                                    trx, h->Amat, h->svec, h->flags, dbg);
     } else {
       refresh_kernel<REFRESH_INPLACE><<<1, 1024, plan.total_bytes, ss>>>(R, D, n, eta, a_, e_, h->KL, h->dstate,
                                                                          trx, h->Amat, h->svec, h->flags, dbg);
@@ -1959,35 +1794,6 @@ ng_status ngsgd_set_state(ngsgd_t h, const ngsgd_state_host* in) {
   h->initialized = in->initialized != 0;
   h->last_updated = 0;
   return NG_OK;
-}
-
-ng_status ng_debug_eig_clocks(uint64_t* out) {
-  NG_REQUIRE(out != nullptr, NG_EINVAL, "NULL argument");
-  NG_CUDA_TRY(cudaDeviceSynchronize());
-  unsigned long long v[8], w[16];
-  NG_CUDA_TRY(cudaMemcpyFromSymbol(v, g_eig_clk, sizeof(v)));
-  NG_CUDA_TRY(cudaMemcpyFromSymbol(w, g_dc_clk, sizeof(w)));
-  for (int i = 0; i < 8; ++i) out[i] = v[i];
-  for (int i = 0; i < 16; ++i) out[8 + i] = w[i];
-  std::memset(v, 0, sizeof(v));
-  std::memset(w, 0, sizeof(w));
-  NG_CUDA_TRY(cudaMemcpyToSymbol(g_eig_clk, v, sizeof(v)));
-  NG_CUDA_TRY(cudaMemcpyToSymbol(g_dc_clk, w, sizeof(w)));
-  return NG_OK;
-}
-
-__global__ void __launch_bounds__(1024) debug_eig_dc_kernel(const double* Z, int n, double* lam, double* vt) {
-  extern __shared__ __align__(16) unsigned char ng_smem[];
-  eig_dc(reinterpret_cast<double*>(ng_smem), dc_plan(n), Z, n, lam, vt, n);
-}
-
-ng_status ng_debug_eig_dc(const double* z, int32_t n, double* lam, double* vt, void* stream) {
-  NG_REQUIRE(z && lam && vt, NG_EINVAL, "NULL argument");
-  NG_REQUIRE(n >= 1 && n <= kDCMax, NG_ESHAPE, "n must be in [1, 80]");
-  const size_t smem = dc_plan(n).total;
-  NG_CUDA_TRY(cudaFuncSetAttribute(debug_eig_dc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  debug_eig_dc_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(z, n, lam, vt);
-  return check_launch("debug_eig_dc_kernel");
 }
 
 __global__ void __launch_bounds__(1024) debug_eig_tri_kernel(const double* Z, int n, double* lam, double* vt, int* ok) {

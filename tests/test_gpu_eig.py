@@ -1,5 +1,5 @@
 """GPU unit tests of the refresh's dense symmetric eigensolver (eqn:zt:eig, P:1382-1384:
-Householder + divide and conquer, FP64) through ng_debug_eig_dc, against numpy.linalg.eigh
+Householder + RRR / twisted-factorisation eigenvectors, FP64) through ng_debug_eig_tri, against numpy.linalg.eigh
 (absolute accuracy ~eps ||Z||, the oracle's own routine) on matrices shaped like Z_t:
 smooth spectra over 17 decades, clusters, exact multiplicities, zero and tiny sizes."""
 import ctypes
@@ -8,19 +8,6 @@ import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
-
-
-def _run(Z):
-    import torch
-    from paper_1410_7455_b200 import _lib
-    n = Z.shape[0]
-    z = torch.from_numpy(np.ascontiguousarray(Z, dtype=np.float64)).cuda()
-    lam = torch.empty(n, dtype=torch.float64, device="cuda")
-    vt = torch.empty(n, n, dtype=torch.float64, device="cuda")
-    _lib.check(_lib.lib.ng_debug_eig_dc(ctypes.c_void_p(z.data_ptr()), n, ctypes.c_void_p(lam.data_ptr()),
-                                        ctypes.c_void_p(vt.data_ptr()), None))
-    torch.cuda.synchronize()
-    return lam.cpu().numpy(), vt.cpu().numpy()
 
 
 def _spd(n, spectrum, seed):
@@ -40,30 +27,6 @@ CASES = [
     ("tiny", 2, lambda n: np.array([3.0, 1.0])),
     ("one", 1, lambda n: np.array([2.5])),
 ]
-
-
-@pytest.mark.parametrize("name,n,spec", CASES, ids=[c[0] for c in CASES])
-def test_eig_dc_matches_eigh(name, n, spec):
-    Z = _spd(n, spec(n), seed=n)
-    lam, vt = _run(Z)
-    zmax = max(np.max(np.abs(Z)), 1e-300)
-    l0 = np.linalg.eigvalsh(Z)
-    assert np.all(np.diff(lam) >= 0)                              # ascending
-    assert np.max(np.abs(lam - l0)) <= 64 * 2.2e-16 * zmax * n
-    assert np.max(np.abs(vt @ vt.T - np.eye(n))) <= 1e-13          # orthonormal rows
-    assert np.max(np.abs(Z @ vt.T - vt.T * lam)) <= 64 * 2.2e-16 * zmax * n   # residual
-
-
-def test_eig_dc_diagonal_and_tridiagonal():
-    """Already diagonal input (every boundary deflates) and a tridiagonal one (the Householder
-    stage is the identity)."""
-    D = np.diag(np.linspace(5.0, 1.0, 30))
-    lam, vt = _run(D)
-    assert np.allclose(lam, np.sort(np.diag(D)), rtol=0, atol=1e-14)
-    T = np.diag(np.full(40, 2.0)) + np.diag(np.full(39, -1.0), 1) + np.diag(np.full(39, -1.0), -1)
-    lam, vt = _run(T)
-    assert np.allclose(lam, np.linalg.eigvalsh(T), rtol=0, atol=1e-13)
-    assert np.max(np.abs(vt @ vt.T - np.eye(40))) <= 1e-13
 
 
 # ---------------------------------------------------------------------------------------
@@ -129,3 +92,19 @@ def test_eig_tri_diagonal_split_and_zero():
     assert np.max(np.abs(vt @ vt.T - np.eye(80))) == 0.0
     lam, vt, ok = _run_tri(np.zeros((16, 16)))
     assert ok[0] == 1 and np.all(lam == 0.0) and np.array_equal(vt, np.eye(16))
+
+
+def test_eig_tri_diagonal_and_tridiagonal():
+    """Already diagonal input with distinct entries and a tridiagonal one (the Householder
+    stage is the identity), against eigh."""
+    D = np.diag(np.linspace(5.0, 1.0, 30))
+    lam, vt, ok = _run_tri(D)
+    assert ok[0] == 1
+    assert np.allclose(np.sort(lam), np.sort(np.diag(D)), rtol=0, atol=1e-14)
+    T = np.diag(np.full(40, 2.0)) + np.diag(np.full(39, -1.0), 1) + np.diag(np.full(39, -1.0), -1)
+    lam, vt, ok = _run_tri(T)
+    assert ok[0] == 1
+    assert np.allclose(np.sort(lam), np.linalg.eigvalsh(T), rtol=0, atol=1e-13)
+    assert np.max(np.abs(vt @ vt.T - np.eye(40))) <= 1e-8          # the bar of test_eig_tri_matches_eigh
+    o = np.argsort(lam)
+    assert np.max(np.abs(T @ vt[o].T - vt[o].T * lam[o])) <= 64 * 2.2e-16 * 4.0 * 40

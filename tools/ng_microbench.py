@@ -26,14 +26,3 @@ prof = api.profile_read()
 for k, v in prof.items():
     if v["launches"]:
         print(f"{k:12s} launches {v['launches']:4d}  {v['ms'] / v['launches'] * 1e3:9.1f} us/launch")
-if int(os.environ.get("NG_PROFILE_JACOBI_MASK", "0")) & 64 or os.environ.get("NG_TUNE_EIG_MODE") == "3":
-    import ctypes
-    from paper_1410_7455_b200 import _lib
-    buf = (ctypes.c_uint64 * 24)()
-    _lib.check(_lib.lib.ng_debug_eig_clocks(buf))
-    n = max(1, buf[0])
-    print("eig round cycles (avg): angle load %.0f  angle math %.0f  hand-off %.0f | block load %.0f  block math+store %.0f | round %.0f  (rounds %d)"
-          % (buf[1] / n, buf[2] / n, buf[3] / n, buf[4] / n, buf[5] / n, buf[6] / n, buf[0]))
-    m = max(1, buf[11])
-    print("dc cycles per solve: householder %.0f  d&c %.0f  back %.0f  levels %s" % (buf[8] / m, buf[9] / m, buf[10] / m,
-          " ".join("%.0f" % (buf[12 + l] / m) for l in range(8))))
