@@ -162,6 +162,123 @@ __device__ __forceinline__ double tr_rowsum(double x) {   // sum over the 8 lane
   return x;
 }
 
+// The last columns of the reduction, once the trailing block has at most g_tri_tail rows
+// (<= 32 RPL): ONE warp (warp 0) finishes it from shared memory with shuffles and __syncwarp
+// only -- the CTA-wide pass of tri_reduce_reg costs two 1024-thread barriers per column,
+// which is most of its time when the block is small.  Same dsytd2 'L' steps and outputs as
+// tri_reduce_reg: T (= the A region, ld lda) holds A after updates 0..k0-1 in rows / columns
+// >= k0 + 1 and reflector k0 is built; writes reflectors k0+1.., taus, d, e.  Lane L owns
+// rows g = k0 + 1 + L + 32 r.
+template <int RPL>
+__device__ __forceinline__ void tri_reduce_tail(const TriPlan& P, double* __restrict__ sm, int k0, int lane) {
+  const int n = P.n, lda = P.lda;
+  constexpr int ldq = kTriMax;
+  double* T = sm + P.oA;
+  double* Q = sm + P.oQ;
+  double* taus = sm + P.otau;
+  double* d = sm + P.od;
+  double* e = sm + P.oe;
+  double* wsm = sm + P.ow;
+  for (int k = k0; k + 2 < n; ++k) {
+    const double* v = Q + k * ldq;
+    const double tau = taus[k];
+    double p[RPL], vg[RPL], w[RPL];
+    double dot = 0.0;
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int g = k0 + 1 + lane + 32 * r;
+      const bool act = g >= k + 1 && g < n;
+      double a0 = 0.0, a1 = 0.0;
+      if (act) {
+        const double* Tg = T + g * lda;
+        for (int j = k + 1; j < n; j += 4) {
+          double tq[4], vq[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const bool in = j + q < n;
+            tq[q] = in ? Tg[j + q] : 0.0;
+            vq[q] = in ? v[j + q] : 0.0;
+          }
+          a0 = fma(tq[0], vq[0], a0);
+          a1 = fma(tq[1], vq[1], a1);
+          a0 = fma(tq[2], vq[2], a0);
+          a1 = fma(tq[3], vq[3], a1);
+        }
+      }
+      p[r] = a0 + a1;
+      vg[r] = act ? v[g] : 0.0;
+      dot = fma(p[r], vg[r], dot);
+    }
+    dot = warp_sum(dot);
+    const double hk = 0.5 * tau * dot;
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int g = k0 + 1 + lane + 32 * r;
+      w[r] = tau * fma(-hk, vg[r], p[r]);
+      if (g >= k + 1 && g < n) wsm[g] = w[r];
+    }
+    __syncwarp();
+    // A_22 -= v w^T + w v^T
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int g = k0 + 1 + lane + 32 * r;
+      if (g >= k + 1 && g < n) {
+        double* Tg = T + g * lda;
+        // chunks of 4: the loads of a chunk issue together (the stores may alias them)
+        for (int j = k + 1; j < n; j += 4) {
+          double tq[4], vq[4], wq[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const bool in = j + q < n;
+            tq[q] = in ? Tg[j + q] : 0.0;
+            vq[q] = in ? v[j + q] : 0.0;
+            wq[q] = in ? wsm[j + q] : 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (j + q < n) Tg[j + q] = fma(-vg[r], wq[q], fma(-w[r], vq[q], tq[q]));
+        }
+      }
+    }
+    __syncwarp();
+    const int c = k + 1;
+    if (c + 2 < n) {
+      // reflector of column c (rows c+1..n-1), as tri_reflect
+      const double alpha = T[(c + 1) * lda + c];
+      double s = 0.0, x[RPL];
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int g = k0 + 1 + lane + 32 * r;
+        x[r] = (g >= c + 2 && g < n) ? T[g * lda + c] : 0.0;
+        s = fma(x[r], x[r], s);
+      }
+      s = warp_sum(s);
+      double beta, scal, tc;
+      if (s == 0.0) {
+        beta = alpha; tc = 0.0; scal = 0.0;
+      } else {
+        beta = -copysign(fsqrt(fma(alpha, alpha, s)), alpha);
+        tc = fdiv(beta - alpha, beta);
+        scal = frcp(alpha - beta);
+      }
+      double* vo = Q + c * ldq;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const int g = k0 + 1 + lane + 32 * r;
+        if (g >= c + 2 && g < n) vo[g] = x[r] * scal;
+      }
+      if (lane == 0) { vo[c + 1] = 1.0; d[c] = T[c * lda + c]; e[c] = beta; taus[c] = tc; }
+    } else if (lane == 0) {
+      d[c] = T[c * lda + c];
+      e[c] = T[(n - 1) * lda + c];
+      d[n - 1] = T[(n - 1) * lda + n - 1];
+    }
+    __syncwarp();
+  }
+}
+constexpr int kTriTailRPL = 1;   // rows per lane of the one-warp tail
+__device__ int g_tri_tail = 32 * kTriTailRPL;   // tail size (rows); 0 = CTA-wide pass throughout (NG_TUNE_TRI_TAIL)
+
 // Step 1 (register-resident): A (n x n symmetric, ld lda, scaled, in shared memory) ->
 // d, e; the reflectors are kept, not accumulated: v_k in row k of the Q region (v_k[i] at
 // Q[k kTriMax + i], v_k[k+1] = 1, zero elsewhere up to kTriMax), tau_k at taus[k].  The
@@ -171,7 +288,7 @@ __device__ __forceinline__ double tr_rowsum(double x) {   // sum over the 8 lane
 // and forms p = A v_k, and the owner of column k+1 publishes it; then warp 0 (which holds
 // no rows) forms w_k = tau (p - (tau/2)(p.v) v), updates column k+1 by it and builds
 // reflector k+1.  Two barriers per column (LAPACK dsytd2 'L' order).
-__device__ __forceinline__ void tri_reduce_reg(const TriPlan& P, double* __restrict__ sm) {
+__device__ __noinline__ void tri_reduce_reg(const TriPlan& P, double* __restrict__ sm) {
   const int n = P.n, lda = P.lda, tid = threadIdx.x, nt = blockDim.x;
   constexpr int ldq = kTriMax;
   const int lane = tid & 31, warp = tid >> 5, ra = lane >> 3, cb = lane & 7;
@@ -198,9 +315,11 @@ __device__ __forceinline__ void tri_reduce_reg(const TriPlan& P, double* __restr
   for (int i = tid; i < n * ldq; i += nt) Q[i] = 0.0;
   for (int i = tid; i < 2 * ldq; i += nt) wb[i] = 0.0;
   const bool own = rwarp && row < n;
+  // columns k >= k0 (trailing block <= g_tri_tail rows) go to the one-warp tail
+  const int k0 = max(0, n - 1 - min(g_tri_tail, 32 * kTriTailRPL));
   double M[kTrCols];
 #pragma unroll
-  for (int g = 0; g < kTrCols; ++g) M[g] = (own && j0 + g < n) ? A[row * lda + j0 + g] : 0.0;
+  for (int g = 0; g < kTrCols; ++g) M[g] = (own && j0 + g < n && k0 > 0) ? A[row * lda + j0 + g] : 0.0;
   __syncthreads();
   if (warp == 0) {
     double col[3];
@@ -215,6 +334,26 @@ __device__ __forceinline__ void tri_reduce_reg(const TriPlan& P, double* __restr
   for (int k = 0; k + 2 < n; ++k) {
     const int cur = k & 1, prv = cur ^ 1;
     const double* v = Q + k * ldq;
+    if (k == k0) {
+      // hand over: apply update k0-1 and store rows / columns >= k0+1 back into the A region
+      // (at k0 = 0 it still holds the input), then warp 0 finishes alone
+      if (k0 > 0 && rwarp && 4 * (warp - 1) + 3 >= k + 1) {
+        const double vr = own ? Q[(k - 1) * ldq + row] : 0.0;
+        const double wr = own ? wb[prv * ldq + row] : 0.0;
+        const double* vp = Q + (k - 1) * ldq + j0;
+        const double* wp = wb + prv * ldq + j0;
+        double* Aw = sm + P.oA;
+#pragma unroll
+        for (int g = 0; g < kTrCols; ++g) {
+          const double x = fma(-vr, wp[g], fma(-wr, vp[g], M[g]));
+          if (own && row >= k + 1 && j0 + g >= k + 1 && j0 + g < n) Aw[row * lda + j0 + g] = x;
+        }
+      }
+      __syncthreads();
+      if (warp == 0) tri_reduce_tail<kTriTailRPL>(P, sm, k0, lane);
+      __syncthreads();
+      return;
+    }
     // warp-uniform: the row-group shuffles need every lane of the warp; warps whose rows
     // are all above the trailing block (<= k) are finished and skip the pass
     if (rwarp && 4 * (warp - 1) + 3 >= k + 1) {
@@ -481,7 +620,7 @@ __device__ __forceinline__ double tri_gemm_nt(const double* __restrict__ Am, con
 // Full solve.  On entry A (= sm + P.oA, ld P.lda) holds the symmetric matrix.  On success
 // (return 1): lam[i] (sm + P.olam, unordered) and eigenvector rows V = sm + P.oA (ld P.lda).
 // Returns 0 when the orthogonality check fails (the caller falls back to Jacobi).
-__device__ int eig_tri(const TriPlan& P, double* __restrict__ sm, long long* stamps = nullptr) {
+__device__ __noinline__ int eig_tri(const TriPlan& P, double* __restrict__ sm, long long* stamps = nullptr) {
   const int n = P.n, lda = P.lda, tid = threadIdx.x, nt = blockDim.x;
   double* A = sm + P.oA;
   double* X = sm + P.oX;

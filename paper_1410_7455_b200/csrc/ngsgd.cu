@@ -282,7 +282,7 @@ __host__ __device__ inline RefreshSmem refresh_plan(int R, int mode) {
   p.mp = R / 2 + 1;
   p.mode = mode;
   size_t o = 0;
-  p.o_d = o;    o += 5 * (size_t)R + 32;               // d, emh, dr, c, dn, red[32]
+  p.o_d = o;    o += 5 * (size_t)R + 40;               // d, emh, dr, c, dn, red[32], scalars[8]
   p.o_lam = o;  o += (size_t)p.npad + 2;               // eigenvalues
   o = (o + 1) & ~(size_t)1;                            // 16-byte alignment
   if (mode == REFRESH_TRI) {   // eig_tri's plan; Z_t in its A region (ld R + 1)
@@ -307,40 +307,58 @@ __host__ __device__ inline RefreshSmem refresh_plan(int R, int mode) {
 __device__ unsigned long long g_ref_t[256][9];   // refresh timing (ng_debug_refresh_times): R, start, end ns, eig, phase cycles
 __device__ unsigned int g_ref_n;
 
+// One state's refresh job (the grouped launch passes a table of them).
+struct RefreshJob {
+  int R, D, N, pad_;
+  double eta, alpha, eps;
+  const float* KL;
+  double* dstate;
+  const double* sums;
+  float* Amat;
+  float* svec;
+  int* flags;
+};
+
+// The refresh in three calls -- refresh_pre (Z_t), the eigensolver, refresh_post (everything
+// after it) -- with nothing but the job and a few shared-memory scalars carried across: the
+// eigensolver is a separate (non-inlined) function, and values live across a call cost it
+// registers (measured: its tridiagonalisation 182 -> 148 us in the grouped kernel).
+// Shared scalars after red[32]: [0] sum d, [1] max |z_ii|, [2] t_start, [3] t_eig0 (ns).
+__device__ __forceinline__ double refresh_zval(const RefreshJob& J, const double* emh, const double* dr, int i, int j) {
+  const int R = J.R;
+  const float* K = J.KL;
+  const float* L = J.KL + R * R;
+  const double a1 = J.eta * J.eta / ((double)J.N * J.N), a2 = (1.0 - J.eta) * (1.0 - J.eta);
+  const double a3 = J.eta * (1.0 - J.eta) / J.N;
+  const double ks = 0.5 * ((double)K[i * R + j] + (double)K[j * R + i]);
+  const double ls = 0.5 * ((double)L[i * R + j] + (double)L[j * R + i]);
+  double z = a1 * emh[i] * ks * emh[j] + a3 * emh[i] * ls * emh[j] * (dr[i] + dr[j]);
+  if (i == j) z += a2 * dr[i] * dr[i];
+  return z;
+}
+
 template <int MODE>
-__device__ __forceinline__ void refresh_body(int R, int D, int N, double eta, double alpha, double eps,
-                                             const float* __restrict__ KL, double* __restrict__ dstate,
-                                             const double* __restrict__ sums, float* __restrict__ Amat,
-                                             float* __restrict__ svec, int* __restrict__ flags, int dbg_mask) {
+__device__ __noinline__ void refresh_pre(const RefreshJob& J) {
   extern __shared__ __align__(16) unsigned char ng_smem[];
-  __shared__ long long eig_st[8];   // eigensolver phase stamps (thread 0)
   double* sm = reinterpret_cast<double*>(ng_smem);
   unsigned long long t_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  const int R = J.R;
   const RefreshSmem P = refresh_plan(R, MODE);
   double* d = sm + P.o_d;               // R   old d
   double* emh = d + R;                  // R   E_t^{-1/2}
   double* dr = emh + R;                 // R   d + rho
-  double* c = dr + R;                   // R   sorted eigenvalues
-  double* dn = c + R;                   // R   new d
-  double* red = dn + R;                 // 32 reduction scratch
-  double* lam = sm + P.o_lam;           // eigenvalues
-  int* perm = reinterpret_cast<int*>(sm + P.o_int);   // npad
-  int* nrot = perm + P.npad;            // 32 per-warp sweep counts, 32 spare, then 2*mp pair table
-  int* iflag = nrot + 64 + 2 * P.mp;    // floored
-  int* phantom = iflag + 1;
-  int* fbuf = phantom + 1;
-  float* offmax = reinterpret_cast<float*>(fbuf + 1);  // 32 (per-warp max ratio)
+  double* red = dr + 3 * R;             // 32 reduction scratch, then the scalars
+  int* iflag = reinterpret_cast<int*>(sm + P.o_int) + P.npad + 64 + 2 * P.mp;
   const int tid = threadIdx.x, nt = blockDim.x;
-
-  const double rho = dstate[0];
-  for (int i = tid; i < R; i += nt) d[i] = dstate[1 + i];
+  const double rho = J.dstate[0];
+  for (int i = tid; i < R; i += nt) d[i] = J.dstate[1 + i];
   __syncthreads();
   // beta_t (eqn:beta2) and e_tii (eqn:etii)
   double sd = 0.0;
   for (int i = tid; i < R; i += nt) sd += d[i];
   sd = block_sum(sd, red);
-  const double beta = rho * (1.0 + alpha) + (alpha / D) * sd;
+  const double beta = rho * (1.0 + J.alpha) + (J.alpha / J.D) * sd;
   for (int i = tid; i < R; i += nt) {
     const double e = 1.0 / (beta / d[i] + 1.0);
     emh[i] = 1.0 / sqrt(e);
@@ -349,79 +367,93 @@ __device__ __forceinline__ void refresh_body(int R, int D, int N, double eta, do
   if (tid == 0) *iflag = 0;
   __syncthreads();
   // Z_t by eqn:zt:compute, symmetrised
-  const float* K = KL;
-  const float* L = KL + R * R;
-  const double a1 = eta * eta / ((double)N * N), a2 = (1.0 - eta) * (1.0 - eta), a3 = eta * (1.0 - eta) / N;
-  auto zval = [&](int i, int j) -> double {
-    const double ks = 0.5 * ((double)K[i * R + j] + (double)K[j * R + i]);
-    const double ls = 0.5 * ((double)L[i * R + j] + (double)L[j * R + i]);
-    double z = a1 * emh[i] * ks * emh[j] + a3 * emh[i] * ls * emh[j] * (dr[i] + dr[j]);
-    if (i == j) z += a2 * dr[i] * dr[i];
-    return z;
-  };
   double* Z = sm + P.o_z0;
   for (int idx = tid; idx < R * R; idx += nt) {
     const int i = idx / R, j = idx % R;
-    Z[i * P.LD + j] = zval(i, j);
+    Z[i * P.LD + j] = refresh_zval(J, emh, dr, i, j);
   }
   double zmax = 0.0;
-  for (int i = tid; i < R; i += nt) zmax = fmax(zmax, fabs(zval(i, i)));
+  for (int i = tid; i < R; i += nt) zmax = fmax(zmax, fabs(refresh_zval(J, emh, dr, i, i)));
   zmax = block_max(zmax, red);   // (its barriers also complete Z)
-  // Z = U C U^T (eqn:zt:eig:repeat).  rel_tol 1e-7: rotations stop once every
-  // |z_pq| <= 1e-7 sqrt(z_pp z_qq) (eigenvector error ~1e-7 / relative gap, far below the
-  // FP32 storage of A_t and W_{t+1})
+  if (tid == 0) {
+    unsigned long long t_eig0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_eig0));
+    red[32] = sd;
+    red[33] = zmax;
+    reinterpret_cast<unsigned long long*>(red)[34] = t_start;
+    reinterpret_cast<unsigned long long*>(red)[35] = t_eig0;
+  }
+  __syncthreads();
+}
+
+// eig_ok: the default solver's result (REFRESH_TRI); 0 runs the in-place Jacobi on Z_t (the
+// fallback, and REFRESH_INPLACE's solver).  Z = U C U^T (eqn:zt:eig:repeat); Jacobi rel_tol
+// 1e-7: rotations stop once every |z_pq| <= 1e-7 sqrt(z_pp z_qq) (eigenvector error ~1e-7 /
+// relative gap, far below the FP32 storage of A_t and W_{t+1}).
+template <int MODE>
+__device__ __noinline__ void refresh_post(const RefreshJob& J, int dbg_mask, int eig_ok, const long long* eig_st) {
+  extern __shared__ __align__(16) unsigned char ng_smem[];
+  double* sm = reinterpret_cast<double*>(ng_smem);
+  const int R = J.R, D = J.D, N = J.N;
+  const double eta = J.eta, alpha = J.alpha, eps = J.eps;
+  const RefreshSmem P = refresh_plan(R, MODE);
+  double* d = sm + P.o_d;
+  double* emh = d + R;
+  double* dr = emh + R;
+  double* c = dr + R;                   // R   sorted eigenvalues
+  double* dn = c + R;                   // R   new d
+  double* red = dn + R;
+  double* lam = sm + P.o_lam;           // eigenvalues
+  int* perm = reinterpret_cast<int*>(sm + P.o_int);   // npad
+  int* nrot = perm + P.npad;            // 32 per-warp sweep counts, 32 spare, then 2*mp pair table
+  int* iflag = nrot + 64 + 2 * P.mp;    // floored
+  float* offmax = reinterpret_cast<float*>(iflag + 3);  // 32 (per-warp max ratio)
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const double rho = J.dstate[0];
+  const double sd = red[32], zmax = red[33];
+  double* Z = sm + P.o_z0;
   int sweeps;
-  const double* V = nullptr;   // eigenvector rows (index / slot order), row stride ldv
-  int ldv = 0, nlam;
-  unsigned long long t_eig0 = 0, t_eig1 = 0;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_eig0));
-  if (MODE == REFRESH_TRI) {
+  const double* V;   // eigenvector rows (index order), row stride ldv
+  int ldv;
+  if (MODE == REFRESH_TRI && eig_ok) {
     const TriPlan tp = tri_plan(R);
-    double* tb = sm + P.o_ring;
-    if (eig_tri(tp, tb, eig_st)) {
-      for (int i = tid; i < R; i += nt) lam[i] = tb[tp.olam + i];
-      sweeps = 0;
-      V = tb + tp.oA;
-      ldv = tp.lda;
-    } else {
+    const double* tb = sm + P.o_ring;
+    for (int i = tid; i < R; i += nt) lam[i] = tb[tp.olam + i];
+    sweeps = 0;
+    V = tb + tp.oA;
+    ldv = tp.lda;
+  } else {
+    if (MODE == REFRESH_TRI) {
       // fallback: Z_t again (the solve overwrote it), in-place cyclic Jacobi
       __syncthreads();
       for (int idx = tid; idx < R * R; idx += nt) {
         const int i = idx / R, j = idx % R;
-        Z[i * P.LD + j] = zval(i, j);
+        Z[i * P.LD + j] = refresh_zval(J, emh, dr, i, j);
         g_tri_fail_z[idx] = Z[i * P.LD + j];
       }
       if (tid == 0) { g_tri_fail_n = R; atomicAdd(&g_tri_fail_count, 1); }
       __syncthreads();
-      JacobiSmem<double> scr{sm + P.o_cs, sm + P.o_cs + P.mp, nrot, offmax};
-      sweeps = jacobi_eig_smem<double>(Z, P.LD, sm + P.o_v0, P.LDV, R, scr, 20, 1e-15 * zmax, 1e-7, dbg_mask);
-      if (sweeps == 0) sweeps = 1;   // flags[4] > 0 marks the fallback
-      for (int i = tid; i < R; i += nt) lam[i] = Z[i * P.LD + i];
-      V = sm + P.o_v0;
-      ldv = P.LDV;
     }
-    nlam = R;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_eig1));
-  } else {
     JacobiSmem<double> scr{sm + P.o_cs, sm + P.o_cs + P.mp, nrot, offmax};
-    double* Vt = sm + P.o_v0;
-    sweeps = jacobi_eig_smem<double>(Z, P.LD, Vt, P.LDV, R, scr, 20, 1e-15 * zmax, 1e-7, dbg_mask);
+    sweeps = jacobi_eig_smem<double>(Z, P.LD, sm + P.o_v0, P.LDV, R, scr, 20, 1e-15 * zmax, 1e-7, dbg_mask);
+    if (MODE == REFRESH_TRI && sweeps == 0) sweeps = 1;   // flags[4] > 0 marks the fallback
     for (int i = tid; i < R; i += nt) lam[i] = Z[i * P.LD + i];
-    V = Vt;
+    V = sm + P.o_v0;
     ldv = P.LDV;
-    nlam = R;
   }
+  unsigned long long t_eig1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_eig1));
   __syncthreads();
   // descending order
-  for (int i = tid; i < nlam; i += nt) {
+  for (int i = tid; i < R; i += nt) {
     const double li = lam[i];
     int r = 0;
-    for (int j = 0; j < nlam; ++j) { const double lj = lam[j]; r += (lj > li) || (lj == li && j < i); }
+    for (int j = 0; j < R; ++j) { const double lj = lam[j]; r += (lj > li) || (lj == li && j < i); }
     perm[r] = i;
   }
   __syncthreads();
   // floor C at (1-eta)^2 rho_t^2 (reading R13)
-  const double cf = a2 * rho * rho;
+  const double cf = (1.0 - eta) * (1.0 - eta) * rho * rho;
   for (int r = tid; r < R; r += nt) {
     double cr = lam[perm[r]];
     if (cr < cf) { cr = cf; atomicOr(iflag, 1); }
@@ -429,7 +461,7 @@ __device__ __forceinline__ void refresh_body(int R, int D, int N, double eta, do
   }
   __syncthreads();
   // rho'_{t+1} (eqn:rhodash2), D_{t+1} (eqn:dt1), rho_{t+1} (eqn:rhot1)
-  const double trX = sums[0];
+  const double trX = J.sums[0];
   double ssc = 0.0;
   for (int r = tid; r < R; r += nt) ssc += sqrt(c[r]);
   ssc = block_sum(ssc, red);
@@ -445,37 +477,37 @@ __device__ __forceinline__ void refresh_body(int R, int D, int N, double eta, do
   for (int idx = tid; idx < R * R; idx += nt) {
     const int r = idx / R, j = idx % R;
     const double en = 1.0 / (beta_new / dn[r] + 1.0);
-    Amat[idx] = (float)((eta / N) * sqrt(en) / sqrt(c[r]) * V[perm[r] * ldv + j] * emh[j]);
+    J.Amat[idx] = (float)((eta / N) * sqrt(en) / sqrt(c[r]) * V[perm[r] * ldv + j] * emh[j]);
   }
   // row scale of B_t with the OLD d, rho
-  for (int k = tid; k < R; k += nt) svec[k] = (float)((N * (1.0 - eta) / eta) * dr[k]);
+  for (int k = tid; k < R; k += nt) J.svec[k] = (float)((N * (1.0 - eta) / eta) * dr[k]);
   double cmax = 0.0, cmin = 1e300;
   for (int r = tid; r < R; r += nt) { cmax = fmax(cmax, c[r]); cmin = fmin(cmin, c[r]); }
   cmax = block_max(cmax, red);
   cmin = -block_max(-cmin, red);
   __syncthreads();
   // commit the new state
-  if (tid == 0) dstate[0] = rho_new;
+  if (tid == 0) J.dstate[0] = rho_new;
   for (int r = tid; r < R; r += nt) {
-    dstate[1 + r] = dn[r];
-    dstate[1 + R + r] = 1.0 / (beta_new / dn[r] + 1.0);
+    J.dstate[1 + r] = dn[r];
+    J.dstate[1 + R + r] = 1.0 / (beta_new / dn[r] + 1.0);
   }
   if (tid == 0) {
     const int fl = *iflag;
+    int* flags = J.flags;
     flags[0] = fl;
     flags[1] = (fl || cmax / cmin > 1e6) ? 1 : 0;     // B.3.1 trigger
     flags[2] = 0;
     flags[4] = sweeps;
     if (!isfinite(rho_new) || !isfinite(sdn)) atomicOr(reinterpret_cast<unsigned*>(flags + 3), kErrNonFinite);
-  }
-  if (tid == 0) {
     unsigned long long t_end;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
     const unsigned slot = atomicAdd(&g_ref_n, 1u) & 255u;
+    const unsigned long long* ts = reinterpret_cast<const unsigned long long*>(red);
     g_ref_t[slot][0] = (unsigned long long)R | ((unsigned long long)D << 16);
-    g_ref_t[slot][1] = t_start;
+    g_ref_t[slot][1] = ts[34];
     g_ref_t[slot][2] = t_end;
-    g_ref_t[slot][3] = t_eig0;
+    g_ref_t[slot][3] = ts[35];
     g_ref_t[slot][4] = t_eig1;
     if (MODE == REFRESH_TRI) {   // cycles: tridiagonalisation, split..multisection, RQI + vectors, clusters + check + back
       g_ref_t[slot][5] = (unsigned long long)(eig_st[1] - eig_st[0]);
@@ -487,35 +519,37 @@ __device__ __forceinline__ void refresh_body(int R, int D, int N, double eta, do
 }
 
 template <int MODE>
+__device__ __forceinline__ void refresh_body(const RefreshJob& J, int dbg_mask) {
+  extern __shared__ __align__(16) unsigned char ng_smem[];
+  __shared__ long long eig_st[8];   // eigensolver phase stamps (thread 0)
+  refresh_pre<MODE>(J);
+  int ok = 0;
+  if (MODE == REFRESH_TRI) {
+    double* sm = reinterpret_cast<double*>(ng_smem);
+    ok = eig_tri(tri_plan(J.R), sm + refresh_plan(J.R, MODE).o_ring, eig_st);
+  }
+  refresh_post<MODE>(J, dbg_mask, ok, eig_st);
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(1024)
 refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
                const float* __restrict__ KL, double* __restrict__ dstate,
                const double* __restrict__ sums, float* __restrict__ Amat,
                float* __restrict__ svec, int* __restrict__ flags, int dbg_mask) {
-  refresh_body<MODE>(R, D, N, eta, alpha, eps, KL, dstate, sums, Amat, svec, flags, dbg_mask);
+  const RefreshJob J{R, D, N, 0, eta, alpha, eps, KL, dstate, sums, Amat, svec, flags};
+  refresh_body<MODE>(J, dbg_mask);
 }
 
 // Grouped refresh: every updating state of a step in ONE launch, one CTA per state
 // (Householder + RRR eigensolver, 2 <= R <= kTriMax), on one side stream.
-struct RefreshJob {
-  int R, D, N, pad_;
-  double eta, alpha, eps;
-  const float* KL;
-  double* dstate;
-  const double* sums;
-  float* Amat;
-  float* svec;
-  int* flags;
-};
 constexpr int kRefreshGroupMax = 16;
 struct RefreshGroup {
   RefreshJob j[kRefreshGroupMax];
   int count, dbg;
 };
 __global__ void __launch_bounds__(1024) refresh_group_kernel(const __grid_constant__ RefreshGroup g) {
-  const RefreshJob& J = g.j[blockIdx.x];
-  refresh_body<REFRESH_TRI>(J.R, J.D, J.N, J.eta, J.alpha, J.eps, J.KL, J.dstate, J.sums, J.Amat, J.svec, J.flags,
-                            g.dbg);
+  refresh_body<REFRESH_TRI>(g.j[blockIdx.x], g.dbg);
 }
 
 // B_t = J_t + (N(1-eta)/eta)(D_t + rho_t I) W_t of every job (blockIdx.y), in J's buffer.
@@ -794,6 +828,10 @@ static ng_status dalloc(T** p, size_t count) {
 static ng_status set_kernel_attrs() {
   static bool done = false;
   if (done) return NG_OK;
+  {
+    const int tail = tune_int("NG_TUNE_TRI_TAIL", 32 * kTriTailRPL);   // one-warp tail of the tridiagonalisation
+    NG_CUDA_TRY(cudaMemcpyToSymbol(g_tri_tail, &tail, sizeof(tail)));
+  }
   NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<REFRESH_INPLACE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)refresh_plan(kMaxRank, REFRESH_INPLACE).total_bytes));
   NG_CUDA_TRY(cudaFuncSetAttribute(refresh_kernel<REFRESH_TRI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1857,6 +1895,7 @@ ng_status ng_debug_eig_tri(const double* z, int32_t n, double* lam, double* vt, 
   NG_REQUIRE(z && lam && vt && ok, NG_EINVAL, "NULL argument");
   NG_REQUIRE(n >= 1 && n <= kTriMax, NG_ESHAPE, "n must be in [1, 80]");
   const size_t smem = tri_plan(n).total + 16;
+  NG_TRY(set_kernel_attrs());   // (also the solver's tuning knobs)
   NG_CUDA_TRY(cudaFuncSetAttribute(debug_eig_tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   debug_eig_tri_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(z, n, lam, vt, ok);
   return check_launch("debug_eig_tri_kernel");
