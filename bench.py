@@ -226,6 +226,16 @@ def roofline_for(group: str, prof: dict, precision: str, peaks: dict):
     except Exception:
         pass
     is_gemm = group in ("fwd_gemm", "bwd_gemm", "upd_gemm")
+    if group == "ng_apply" and g["bytes"] == 0 and g["flops"] > 0:
+        # simple NG-SGD (--precond simple): FP64 Gram, Cholesky, triangular solves on CUDA cores
+        flops = g["flops"] / g["launches"]
+        achieved = flops / per_launch_s / 1e12
+        peak = FP64_SM_PEAK_GFLOPS * 148 / 1e3
+        return {"kernel": "ng_simple", "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None,
+                "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md); algorithmic "
+                               "Gram m(m+1)K + Cholesky m^3/3 + solves 2 m^2 rhs + rows 4nD per side",
+                "algorithmic_per_launch": flops, "launch_ms": per_launch_s * 1e3}
     if group == "ng_eig":
         # one CTA per state by design (FP64 eigensolve of the R x R matrix Z_t; all updating
         # states of a step in one grouped launch): peak = that many SMs' FP64 FMA rate (the

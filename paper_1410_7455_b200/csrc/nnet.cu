@@ -827,7 +827,14 @@ ng_status nnet_update(nnet_t h, float lr, float max_change_per_sample, nnet_upda
       sc.push_back(SimpleCall{h->sn_out[l], n, h->X[l], h->ldr[l], h->gam + 2 * l + 1, px});
       sc.push_back(SimpleCall{h->sn_in[l], n, h->Y[l], h->ldp[l], h->gam + 2 * l, py});
     }
-    ProfScope ps(NG_PROF_NG_APPLY, st, 0.0, 0.0);
+    // algorithmic FP64 work (A.3): Gram m(m+1) K, Cholesky m^3/3, the two
+    // triangular solves 2 m^2 rhs, the rows 4 n D (m = min side, rhs / K = the other side)
+    double flops = 0.0;
+    for (const SimpleCall& c : sc) {
+      const double D = c.h->dim, m = (c.n > c.h->dim) ? D : (double)c.n, o = (c.n > c.h->dim) ? (double)c.n : D;
+      flops += m * (m + 1.0) * o + m * m * m / 3.0 + 2.0 * m * m * o + 4.0 * c.n * D;
+    }
+    ProfScope ps(NG_PROF_NG_APPLY, st, flops, 0.0);
     NG_TRY(ngsimple_precondition_group_impl(sc.data(), (int)sc.size()));
   } else if (h->cfg.precond) {
     // all 2I preconditioning calls of the step as one group: one launch per

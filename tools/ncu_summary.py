@@ -10,7 +10,11 @@ SCALE = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "ns": 1e-3, "u
 
 
 def raw_rows(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """rep: an .ncu-rep, or the `ncu -i rep --page raw --csv` export of one (.csv)."""
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr, units = rows[0], rows[1]
     return [{h: (u, v) for h, u, v in zip(hdr, units, r)} for r in rows[2:]]
@@ -59,7 +63,8 @@ def launch_table(csv_path, steps, title, marker="input_kernel"):
         if hdr and len(r) == len(hdr):
             data.append(dict(zip(hdr, r)))
     idx = [i for i, d in enumerate(data) if d["Kernel Name"].startswith(marker)]
-    sub = data[idx[-steps]:]
+    sub = data[idx[-steps - 1]:idx[-1]]   # `steps` whole steps, ending at the last step's start (later
+                                          # launches -- bench.py's standalone preconditioner run -- excluded)
     agg = collections.defaultdict(lambda: [0, 0.0])
     for d in sub:
         name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("ng::<unnamed>::", "").replace("ng::", "")
