@@ -33,6 +33,7 @@ struct SimpleJob {
   int n, D, m, col; // col != 0: column space (m = D, right-hand sides = rows); else row space (m = n)
   double* G;        // m x m: Gram, then beta I + G/(n-1), then its lower Cholesky factor
   double* Y;        // m x rhs: the solves (element (i, r) at Y[i * rhs + r])
+  double* DI;       // ceil(m / kTsB) x kTsB x kTsB: inverses of the diagonal blocks of L
   double* rowpart;  // 2 x n: ||x_r||^2, ||x_hat_r||^2
   double* stats;    // [0] tr X^T X [1] beta [2] sum ||x||^2 [3] sum p
   float* gamma;     // 1
@@ -174,86 +175,145 @@ __global__ void __launch_bounds__(1024) simple_chol_kernel(const __grid_constant
   }
 }
 
-// kSolveCols right-hand sides per CTA (a row of X in the column space, a column in the row
-// space), their vectors in shared memory; L y = b then L^T q = y, eight rows (forward) or
-// eight columns (backward) of L staged in shared memory at a time (coalesced, one L2 round
-// trip per eight steps), every dot product split over kSolveSplit lanes (3-level shuffle).
-// q -> Y (element (i, r) at Y[i * rhs + r]).
-constexpr int kSolveCols = 32, kSolveSplit = 8, kSolveBlk = 8;
-__global__ void __launch_bounds__(kSolveCols * kSolveSplit) simple_solve_kernel(const __grid_constant__ SimpleJobs jb) {
+// The two triangular solves L y = b, L^T q = y as GEMMs (round 2; the substitution kernel
+// before it did one dot product per row and reached ~1% of the FP64 rate): L is cut into
+// kTsB-row blocks whose diagonal blocks are inverted once (simple_diaginv_kernel); then,
+// for a tile of kTsC right-hand sides per CTA,
+//   forward,  block b ascending:  T = y_b - L[b, <b] y[<b],      y_b = L_bb^{-1} T
+//   backward, block b descending: T = y_b - L[>b, b]^T q[>b],    q_b = L_bb^{-T} T
+// every product a register-tiled FP64 GEMM (4 x 4 outputs per thread, kTsK-deep chunks
+// staged in shared memory).  y and q live in Y (L2-resident); the tiles are independent.
+constexpr int kTsB = 64;    // row block (diagonal blocks inverted)
+constexpr int kTsC = 64;    // right-hand sides per CTA
+constexpr int kTsK = 8;     // k-chunk staged in shared memory
+
+// DI[b] = L_bb^{-1} (kTsB x kTsB row-major; zero above the diagonal and outside the block):
+// thread c forms column c by forward substitution on e_c.
+__global__ void __launch_bounds__(kTsB) simple_diaginv_kernel(const __grid_constant__ SimpleJobs jb) {
   const SimpleJob& J = jb.j[blockIdx.y];
-  const int m = J.m, rhs = J.rhs, tid = threadIdx.x, nt = blockDim.x;
-  const int c = tid / kSolveSplit, g = tid % kSolveSplit;
-  if ((int)(blockIdx.x * kSolveCols) >= rhs) return;   // uniform per CTA
-  // y of right-hand side c at ys[c * ldy + k] (ldy = m + 1: the eight lanes of a group read
-  // consecutive k, the four groups of a warp land on different banks)
-  const int ldy = m + 1;
-  extern __shared__ __align__(16) double ys[];
-  double* Lb = ys + (size_t)kSolveCols * ldy;       // kSolveBlk x m: rows (forward) / columns (backward) of L
-  const double* L = J.G;
-  for (int idx = tid; idx < m * kSolveCols; idx += nt) {
-    const int i = idx / kSolveCols, cc = idx % kSolveCols, rr = blockIdx.x * kSolveCols + cc;
-    double b = 0.0;
-    if (rr < rhs) b = J.col ? (double)J.X[(int64_t)rr * J.ld + i] : (double)J.X[(int64_t)i * J.ld + rr];
-    ys[cc * ldy + i] = b;
-  }
-  double* y = ys + (size_t)c * ldy;
-  for (int i0 = 0; i0 < m; i0 += kSolveBlk) {       // forward: y_i = (b_i - sum_{k<i} L_ik y_k) / L_ii
-    const int bi = min(kSolveBlk, m - i0);
-    __syncthreads();
-    for (int idx = tid; idx < bi * (i0 + bi); idx += nt) {
-      const int r = idx / (i0 + bi), k = idx % (i0 + bi);
-      Lb[r * m + k] = L[(int64_t)(i0 + r) * m + k];
-    }
-    __syncthreads();
-    for (int ii = 0; ii < bi; ++ii) {
-      const int i = i0 + ii;
-      const double* Li = Lb + ii * m;
-      double s0 = 0.0, s1 = 0.0;
-      int k = g;
-      for (; k + kSolveSplit < i; k += 2 * kSolveSplit) {
-        s0 = fma(Li[k], y[k], s0);
-        s1 = fma(Li[k + kSolveSplit], y[k + kSolveSplit], s1);
-      }
-      if (k < i) s0 = fma(Li[k], y[k], s0);
-      double s = s0 + s1;
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      s += __shfl_xor_sync(0xffffffffu, s, 4);
-      if (g == 0) y[i] = (y[i] - s) / Li[i];
-      __syncwarp();
-    }
-  }
-  for (int i1 = m; i1 > 0; i1 -= kSolveBlk) {       // backward: q_i = (y_i - sum_{k>i} L_ki q_k) / L_ii
-    const int i0 = max(0, i1 - kSolveBlk), bi = i1 - i0;
-    __syncthreads();
-    for (int idx = tid; idx < (m - i0) * bi; idx += nt) {   // global reads: 8 consecutive columns per row
-      const int k = i0 + idx / bi, j = idx % bi;
-      Lb[j * m + k] = L[(int64_t)k * m + i0 + j];
-    }
-    __syncthreads();
-    for (int ii = bi - 1; ii >= 0; --ii) {
-      const int i = i0 + ii;
-      const double* Lc = Lb + ii * m;                 // column i of L, rows k
-      double s0 = 0.0, s1 = 0.0;
-      int k = i + 1 + g;
-      for (; k + kSolveSplit < m; k += 2 * kSolveSplit) {
-        s0 = fma(Lc[k], y[k], s0);
-        s1 = fma(Lc[k + kSolveSplit], y[k + kSolveSplit], s1);
-      }
-      if (k < m) s0 = fma(Lc[k], y[k], s0);
-      double s = s0 + s1;
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      s += __shfl_xor_sync(0xffffffffu, s, 4);
-      if (g == 0) y[i] = (y[i] - s) / Lc[i];
-      __syncwarp();
-    }
+  const int m = J.m, b = blockIdx.x, i0 = b * kTsB;
+  if (i0 >= m) return;
+  const int bs = min(kTsB, m - i0), c = threadIdx.x;
+  extern __shared__ __align__(16) double dis[];   // L_bb, then the inverse (2 x kTsB x (kTsB + 1))
+  double (*Ls)[kTsB + 1] = reinterpret_cast<double (*)[kTsB + 1]>(dis);
+  double (*xs)[kTsB + 1] = reinterpret_cast<double (*)[kTsB + 1]>(dis + kTsB * (kTsB + 1));
+  for (int idx = c; idx < kTsB * kTsB; idx += kTsB) {
+    const int i = idx / kTsB, j = idx % kTsB;
+    Ls[i][j] = (i < bs && j <= i) ? J.G[(int64_t)(i0 + i) * m + i0 + j] : 0.0;
   }
   __syncthreads();
-  for (int idx = tid; idx < m * kSolveCols; idx += nt) {
-    const int i = idx / kSolveCols, cc = idx % kSolveCols, rr = blockIdx.x * kSolveCols + cc;
-    if (rr < rhs) J.Y[(int64_t)i * rhs + rr] = ys[cc * ldy + i];
+  for (int i = 0; i < kTsB; ++i) {
+    double x = 0.0;
+    if (i < bs && i >= c) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int k = c; k < i; ++k) s = fma(-Ls[i][k], xs[k][c], s);
+      x = s / Ls[i][i];
+    }
+    xs[i][c] = x;
+  }
+  __syncthreads();
+  double* DI = J.DI + (size_t)b * kTsB * kTsB;
+  for (int idx = c; idx < kTsB * kTsB; idx += kTsB) DI[idx] = xs[idx / kTsB][idx % kTsB];
+}
+
+// acc += A B over one staged chunk: A as As[kk][row] (rows 4 tr .. 4 tr + 3), B rows at
+// B + kk * ldb (columns 4 tc .. 4 tc + 3), both 16-byte aligned.
+__device__ __forceinline__ void ts_chunk(const double (*As)[kTsB + 2], const double* B, int ldb, int tr, int tc,
+                                         double (&acc)[4][4]) {
+#pragma unroll
+  for (int kk = 0; kk < kTsK; ++kk) {
+    const double2 a01 = *reinterpret_cast<const double2*>(&As[kk][4 * tr]);
+    const double2 a23 = *reinterpret_cast<const double2*>(&As[kk][4 * tr + 2]);
+    const double2 b01 = *reinterpret_cast<const double2*>(B + kk * ldb + 4 * tc);
+    const double2 b23 = *reinterpret_cast<const double2*>(B + kk * ldb + 4 * tc + 2);
+    const double a[4] = {a01.x, a01.y, a23.x, a23.y}, bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], bv[j], acc[i][j]);
+  }
+}
+
+__global__ void __launch_bounds__(256) simple_trsm_kernel(const __grid_constant__ SimpleJobs jb) {
+  const SimpleJob& J = jb.j[blockIdx.y];
+  const int m = J.m, rhs = J.rhs, c0 = blockIdx.x * kTsC;
+  if (c0 >= rhs) return;   // uniform per CTA
+  const int tid = threadIdx.x, tr = tid >> 4, tc = tid & 15;
+  constexpr int LDS = kTsC + 2;   // 16-byte aligned rows
+  __shared__ __align__(16) double As[kTsK][kTsB + 2];
+  __shared__ __align__(16) double Bs[kTsK][LDS];
+  __shared__ __align__(16) double Ts[kTsB][LDS];
+  double* Y = J.Y;
+  const double* L = J.G;
+  const int nb = (m + kTsB - 1) / kTsB;
+  // b (this tile's right-hand sides) into Y, FP64
+  for (int idx = tid; idx < m * kTsC; idx += blockDim.x) {
+    int i, cc;
+    if (J.col) { cc = idx / m; i = idx - cc * m; } else { i = idx / kTsC; cc = idx - i * kTsC; }
+    const int c = c0 + cc;
+    if (c < rhs) Y[(int64_t)i * rhs + c] = J.col ? (double)J.X[(int64_t)c * J.ld + i] : (double)J.X[(int64_t)i * J.ld + c];
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {   // 0: L y = b, 1: L^T q = y
+    for (int s = 0; s < nb; ++s) {
+      const int b = pass == 0 ? s : nb - 1 - s;
+      const int i0 = b * kTsB, bs = min(kTsB, m - i0);
+      const int kb = pass == 0 ? 0 : i0 + bs, ke = pass == 0 ? i0 : m;
+      double acc[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+      for (int k0 = kb; k0 < ke; k0 += kTsK) {
+        for (int idx = tid; idx < kTsK * kTsB; idx += blockDim.x) {
+          int kk, r;
+          double v = 0.0;
+          if (pass == 0) {
+            r = idx / kTsK; kk = idx - r * kTsK;
+            if (r < bs && k0 + kk < ke) v = L[(int64_t)(i0 + r) * m + k0 + kk];
+          } else {
+            kk = idx / kTsB; r = idx - kk * kTsB;
+            if (r < bs && k0 + kk < ke) v = L[(int64_t)(k0 + kk) * m + i0 + r];
+          }
+          As[kk][r] = v;
+        }
+        for (int idx = tid; idx < kTsK * kTsC; idx += blockDim.x) {
+          const int kk = idx / kTsC, cc = idx - kk * kTsC, c = c0 + cc;
+          Bs[kk][cc] = (k0 + kk < ke && c < rhs) ? __ldcg(Y + (int64_t)(k0 + kk) * rhs + c) : 0.0;
+        }
+        __syncthreads();
+        ts_chunk(As, &Bs[0][0], LDS, tr, tc, acc);
+        __syncthreads();
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = 4 * tr + i, cc = 4 * tc + j, c = c0 + cc;
+          Ts[r][cc] = (r < bs && c < rhs) ? __ldcg(Y + (int64_t)(i0 + r) * rhs + c) - acc[i][j] : 0.0;
+          acc[i][j] = 0.0;
+        }
+      __syncthreads();
+      const double* DI = J.DI + (size_t)b * kTsB * kTsB;
+      for (int k0 = 0; k0 < kTsB; k0 += kTsK) {
+        for (int idx = tid; idx < kTsK * kTsB; idx += blockDim.x) {
+          int kk, r;
+          if (pass == 0) { r = idx / kTsK; kk = idx - r * kTsK; As[kk][r] = DI[r * kTsB + k0 + kk]; }
+          else { kk = idx / kTsB; r = idx - kk * kTsB; As[kk][r] = DI[(k0 + kk) * kTsB + r]; }
+        }
+        __syncthreads();
+        ts_chunk(As, &Ts[k0][0], LDS, tr, tc, acc);
+        __syncthreads();
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int r = 4 * tr + i, c = c0 + 4 * tc + j;
+          if (r < bs && c < rhs) Y[(int64_t)(i0 + r) * rhs + c] = acc[i][j];
+        }
+      __syncthreads();
+    }
   }
 }
 
@@ -324,6 +384,7 @@ void ngsimple_destroy_impl(ngsimple_ctx* h) {
   if (!h) return;
   if (h->G) cudaFree(h->G);
   if (h->Y) cudaFree(h->Y);
+  if (h->DI) cudaFree(h->DI);
   if (h->rowpart) cudaFree(h->rowpart);
   if (h->stats) cudaFree(h->stats);
   if (h->gamma) cudaFree(h->gamma);
@@ -345,6 +406,7 @@ ng_status ngsimple_create_impl(int dim, int max_rows, float alpha, cudaStream_t 
   const size_t m = (size_t)std::min(dim, max_rows);
   ng_status s = simple_alloc((void**)&h->G, sizeof(double) * m * m);
   if (s == NG_OK) s = simple_alloc((void**)&h->Y, sizeof(double) * (size_t)dim * max_rows);
+  if (s == NG_OK) s = simple_alloc((void**)&h->DI, sizeof(double) * (size_t)((m + kTsB - 1) / kTsB) * kTsB * kTsB);
   if (s == NG_OK) s = simple_alloc((void**)&h->rowpart, sizeof(double) * 2 * max_rows);
   if (s == NG_OK) s = simple_alloc((void**)&h->stats, sizeof(double) * 4);
   if (s == NG_OK) s = simple_alloc((void**)&h->gamma, sizeof(float));
@@ -379,7 +441,7 @@ ng_status ngsimple_precondition_group_impl(const SimpleCall* calls, int count) {
       J.col = c.n > h->dim ? 1 : 0;                       // strict N > D (reading R11)
       J.m = J.col ? h->dim : c.n;
       J.rhs = J.col ? c.n : h->dim;
-      J.G = h->G; J.Y = h->Y; J.rowpart = h->rowpart; J.stats = h->stats;
+      J.G = h->G; J.Y = h->Y; J.DI = h->DI; J.rowpart = h->rowpart; J.stats = h->stats;
       J.gamma = c.gamma_out ? c.gamma_out : h->gamma;
       J.p = c.p_out ? c.p_out : h->p;
       J.flags = h->flags; J.alpha = h->alpha;
@@ -394,19 +456,21 @@ ng_status ngsimple_precondition_group_impl(const SimpleCall* calls, int count) {
     int max_m = 1;
     for (int q = 0; q < cnt; ++q) max_m = std::max(max_m, jb.j[q].m);
     const size_t chol_smem = sizeof(double) * ((size_t)kCholB * (kCholB + 1) + (size_t)max_m * (kCholB + 1));
-    const size_t solve_smem = sizeof(double) * ((size_t)kSolveCols * (max_m + 1) + (size_t)max_m * kSolveBlk);
     static bool attr = false;
     if (!attr) {
       NG_CUDA_TRY(cudaFuncSetAttribute(simple_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      NG_CUDA_TRY(cudaFuncSetAttribute(simple_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      NG_CUDA_TRY(cudaFuncSetAttribute(simple_diaginv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(double) * 2 * kTsB * (kTsB + 1))));
       attr = true;
     }
-    NG_REQUIRE(chol_smem <= 200u * 1024u && solve_smem <= 200u * 1024u, NG_ESHAPE,
+    NG_REQUIRE(chol_smem <= 200u * 1024u, NG_ESHAPE,
                "ngsimple: min(n, dim) too large for the shared-memory panels (<= 740)");
     simple_chol_kernel<<<cnt, 1024, chol_smem, st>>>(jb);
     NG_TRY(check_launch("simple_chol_kernel"));
-    simple_solve_kernel<<<dim3(ceil_div(max_rhs, kSolveCols), cnt), kSolveCols * kSolveSplit, solve_smem, st>>>(jb);
-    NG_TRY(check_launch("simple_solve_kernel"));
+    simple_diaginv_kernel<<<dim3(ceil_div(max_m, kTsB), cnt), kTsB, sizeof(double) * 2 * kTsB * (kTsB + 1), st>>>(jb);
+    NG_TRY(check_launch("simple_diaginv_kernel"));
+    simple_trsm_kernel<<<dim3(ceil_div(max_rhs, kTsC), cnt), 256, 0, st>>>(jb);
+    NG_TRY(check_launch("simple_trsm_kernel"));
     simple_rows_kernel<<<dim3(max_n, cnt), 256, 0, st>>>(jb);
     NG_TRY(check_launch("simple_rows_kernel"));
     simple_gamma_kernel<<<cnt, 256, 0, st>>>(jb);

@@ -10,6 +10,7 @@ struct ngsimple_ctx {
   cudaStream_t st = nullptr;
   double* G = nullptr;        // min(dim, max_rows)^2: Gram / Cholesky factor
   double* Y = nullptr;        // dim x max_rows: solves
+  double* DI = nullptr;       // inverses of the diagonal blocks of the Cholesky factor
   double* rowpart = nullptr;  // 2 x max_rows
   double* stats = nullptr;    // [0] tr X^T X [1] beta [2] sum ||x||^2 [3] sum ||x_hat||^2
   float* gamma = nullptr;
