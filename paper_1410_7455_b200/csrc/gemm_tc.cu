@@ -193,8 +193,12 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
   constexpr bool RMW = EPI == TC_EPI_AXPY || EPI == TC_EPI_NGAPPLY;
   constexpr int CW = BN >= 32 ? 32 : 16;
   const int row = m0 + q4 * 32 + lane;
-  float* __restrict__ crow = epi.C + (EPI == TC_EPI_PARTIAL ? (int64_t)ztile * epi.zstride : 0) +
-                             (int64_t)row * epi.ldc;
+  float* __restrict__ cbase = epi.C + (EPI == TC_EPI_PARTIAL ? (int64_t)ztile * epi.zstride : 0);
+  float* __restrict__ crow = cbase + (int64_t)row * epi.ldc;
+  // coalesced (STORE / PARTIAL / PNORM) epilogue layout: lanes per row, rows per pass
+  constexpr int LPR = CW / 4, RPP = 32 / LPR, NP = 32 / RPP;
+  const int rr = lane / LPR, cc = (lane % LPR) * 4;
+  const int wrow0 = m0 + q4 * 32;
   float oldv[RMW ? BN : 1];
   if (RMW && epi_warp) {
 #pragma unroll
@@ -311,17 +315,38 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[c * 16 + j] = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
       }
-      if (row < M && nh < N) {
-        const bool full = nh + 80 <= N && ((reinterpret_cast<uintptr_t>(crow + nh) & 15) == 0);
-        if (full) {
+      // Z store, coalesced: 16-column chunks through a per-warp shared-memory transpose (the
+      // ring is idle), 4 lanes x 16 bytes per row, 8 rows per warp instruction
+      {
+        float* sc = reinterpret_cast<float*>(smem) + q4 * (32 * 17);
+        const int rr = lane >> 2, cc = (lane & 3) * 4;
 #pragma unroll
-          for (int j = 0; j < 80; j += 4)
-            *reinterpret_cast<float4*>(crow + nh + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-        } else {
+        for (int c = 0; c < 5; ++c) {
 #pragma unroll
-          for (int j = 0; j < 80; ++j)
-            if (nh + j < N) crow[nh + j] = acc[j];
+          for (int j = 0; j < 16; ++j) sc[lane * 17 + j] = acc[c * 16 + j];
+          __syncwarp();
+          const int gc = nh + c * 16 + cc;
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            const int lr = p * 8 + rr, r = m0 + q4 * 32 + lr;
+            const float* s4 = sc + lr * 17 + cc;
+            const float4 v = make_float4(s4[0], s4[1], s4[2], s4[3]);
+            if (r < M && gc < N) {
+              float* dst = cbase + (int64_t)r * epi.ldc + gc;
+              if (gc + 4 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                *reinterpret_cast<float4*>(dst) = v;
+              } else {
+                dst[0] = v.x;
+                if (gc + 1 < N) dst[1] = v.y;
+                if (gc + 2 < N) dst[2] = v.z;
+                if (gc + 3 < N) dst[3] = v.w;
+              }
+            }
+          }
+          __syncwarp();
         }
+      }
+      if (row < M && nh < N) {
         const int g0 = nh / 10;
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
@@ -337,7 +362,9 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
         }
       }
     }
-  } else {
+  } else if constexpr (RMW) {
+  // read-modify-write (AXPY, NGAPPLY): thread = row, old C already in registers (measured
+  // faster than the coalesced transpose below for these two)
   const float scale = (EPI == TC_EPI_AXPY) ? __ldg(epi.scale) : 0.f;
   float xx = 0.f, pp = 0.f;   // TC_EPI_NGAPPLY row partial sums over this tile's columns
 #pragma unroll
@@ -395,6 +422,46 @@ __device__ __forceinline__ void tc_tile(const CUtensorMap* tmA, const CUtensorMa
   if (EPI == TC_EPI_NGAPPLY && row < M) {
     epi.xx[(int64_t)ntile * epi.part_ld + row] = xx;
     epi.pp[(int64_t)ntile * epi.part_ld + row] = pp;
+  }
+  } else {
+  // STORE / PARTIAL, coalesced: each warp moves its 32 rows x CW columns from TMEM (thread =
+  // row) through a padded shared-memory transpose (the ring is idle once accum_bar fired) so
+  // a warp instruction covers whole 128-byte row segments (LPR lanes x 16 bytes per row)
+  // instead of 32 rows x 16 bytes.
+  float* sc = reinterpret_cast<float*>(smem) + q4 * (32 * 33);
+#pragma unroll 1
+  for (int c = 0; c < BN / CW; ++c) {
+    {
+      uint32_t v[16];
+      tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(c * CW), v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) sc[lane * 33 + j] = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
+      if (CW == 32) {
+        tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(c * CW + 16), v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sc[lane * 33 + 16 + j] = nkb > 0 ? __uint_as_float(v[j]) : 0.f;
+      }
+    }
+    __syncwarp();
+    const int gc = n0 + c * CW + cc;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const int lr = p * RPP + rr, r = wrow0 + lr;
+      const float* s4 = sc + lr * 33 + cc;
+      const float4 v = make_float4(s4[0], s4[1], s4[2], s4[3]);
+      if (r < M && gc < N) {
+        float* dst = cbase + (int64_t)r * epi.ldc + gc;
+        if (gc + 4 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+          *reinterpret_cast<float4*>(dst) = v;
+        } else {
+          dst[0] = v.x;
+          if (gc + 1 < N) dst[1] = v.y;
+          if (gc + 2 < N) dst[2] = v.z;
+          if (gc + 3 < N) dst[3] = v.w;
+        }
+      }
+    }
+    __syncwarp();
   }
   }   // EPI != TC_EPI_PNORM
   }   // epi_warp
