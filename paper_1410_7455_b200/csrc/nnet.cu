@@ -307,6 +307,19 @@ pnorm_back_kernel(const float* __restrict__ part, int splits, int n, int din, co
   float* ga = reinterpret_cast<float*>(nn_smem);
   const int r = blockIdx.x;
   const int64_t total = (int64_t)n * din;
+  // the row of Z (last phase) does not depend on g: its loads are issued first so their
+  // latency overlaps the split-K sum and the renormalisation backward
+  constexpr int kZP = 4;
+  const int dout = din * G;
+  const int c4 = dout >> 2;
+  const float* zr = Zp + (int64_t)r * ldx;
+  const bool zpre = (dout & 3) == 0 && (ldx & 3) == 0 && c4 <= kZP * (int)blockDim.x;
+  float4 zq[kZP];
+#pragma unroll
+  for (int q = 0; q < kZP; ++q) {
+    const int i = threadIdx.x + q * blockDim.x;
+    zq[q] = (zpre && i < c4) ? __ldg(reinterpret_cast<const float4*>(zr) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   if (rs != nullptr) {
     // renormalisation layer between: y = s a (R32).  g_a = s (g - y (y^T g) / D), then the
     // p-norm derivative divides by a = y / s (0 where a = 0).  g (the fixed-order sum of
@@ -378,10 +391,20 @@ pnorm_back_kernel(const float* __restrict__ part, int splits, int n, int din, co
     }
   }
   __syncthreads();
-  const int dout = din * G;
-  const float* zr = Zp + (int64_t)r * ldx;
   float* xr = Xp + (int64_t)r * ldx;
-  const int c4 = dout >> 2;
+  if (zpre) {
+#pragma unroll
+    for (int q = 0; q < kZP; ++q) {
+      const int i = threadIdx.x + q * blockDim.x;
+      if (i < c4) {
+        const float4 z = zq[q];
+        const int k = i << 2;
+        reinterpret_cast<float4*>(xr)[i] =
+            make_float4(ga[k / G] * z.x, ga[(k + 1) / G] * z.y, ga[(k + 2) / G] * z.z, ga[(k + 3) / G] * z.w);
+      }
+    }
+    return;
+  }
   for (int i = threadIdx.x; i < c4; i += blockDim.x) {
     const float4 z = __ldg(reinterpret_cast<const float4*>(zr) + i);
     const int k = i << 2;
