@@ -59,6 +59,12 @@ __device__ __forceinline__ double fsqrt(double x) {   // x >= 0
 
 
 constexpr int kTriMax = 80;
+// Threads of a CTA that runs eig_tri: 22 warps (the register-resident tridiagonalisation
+// needs 21: a serial warp + 20 warps of four rows each; the multisection 8n = 640 lanes).
+// Fewer than 1024 threads raise the per-thread register cap from 64 to 88, which removes
+// most of the solver's spills (local memory that misses L1 once the refresh's shared memory
+// takes most of the unified L1 / shared storage).
+constexpr int kTriThreads = 704;
 constexpr int kTriChunks = 5;   // column chunks of the Householder pass
 constexpr double kTriOrthTol = 1e-6;   // ~ the Jacobi solver's 1e-7 rotation threshold; W is FP32
 constexpr int kTriCoarse = 64;        // coarse negcount points per block (ratio 8 apart)
@@ -565,6 +571,116 @@ __device__ __forceinline__ int tri_twisted(const double* __restrict__ D, const d
   return neg;
 }
 
+// tri_twisted on TWO threads of one warp (role 0 = lane `base`, role 1 = lane `base + 1`,
+// both in `pmask`): the stationary top-down and the progressive bottom-up qd recurrences are
+// independent, so role 0 runs the top-down walk and role 1 the bottom-up one, meeting at
+// m = lo + (hi - 1 - lo) / 2.  Phase 1: role 0 does i < m (s_i kept in sc[i], L+_i in x[i]),
+// role 1 does i >= m (U-_i in sc[i], p_i parked in x[i]).  Phase 2 (after a __syncwarp):
+// role 0 does i >= m, reading p_i and forming gamma_i = s_i + p_i + lam before it writes L+_i
+// over it; role 1 does i < m, reading s_i before it writes U-_i.  Every recurrence value and
+// every gamma_i is the same arithmetic as tri_twisted; the twist r is the same argmin (ties:
+// the largest index).  The two halves of the vector walk (up from r, down from r) run on the
+// two roles as well; only the summation order of ||z||^2 differs from tri_twisted.  Both roles
+// return the same neg / gamma / ||z||^2.
+__device__ __forceinline__ int tri_twisted2(int role, unsigned pmask, int base, const double* __restrict__ D,
+                                            const double* __restrict__ L, const double* __restrict__ DL,
+                                            const double* __restrict__ DL2, int lo, int hi, double lam,
+                                            double pivmin, double* __restrict__ x, double* __restrict__ sc,
+                                            double* gamma_out, double* znorm2_out) {
+  const int m = lo + (hi - 1 - lo) / 2;
+  int neg = 0, r = hi - 1;
+  double gbest = 0.0, s = -lam, p = D[hi - 1] - lam;
+  if (role == 0) {
+    for (int i = lo; i < m; ++i) {
+      sc[i] = s;
+      double dp = D[i] + s;
+      if (fabs(dp) < pivmin) dp = -pivmin;
+      neg += dp < 0.0;
+      const double lp = fdiv(DL[i], dp);
+      x[i] = lp;
+      s = fma(lp * L[i], s, -lam);
+    }
+  } else {
+    x[hi - 1] = p;
+    for (int i = hi - 2; i >= m; --i) {
+      double dm = DL2[i] + p;
+      if (fabs(dm) < pivmin) dm = -pivmin;
+      const double rd = frcp(dm);
+      sc[i] = DL[i] * rd;
+      p = fma(p, D[i] * rd, -lam);
+      x[i] = p;
+    }
+  }
+  __syncwarp(pmask);
+  if (role == 0) {
+    bool first = true;
+    for (int i = m; i < hi - 1; ++i) {
+      const double g = s + x[i] + lam;
+      if (first || fabs(g) <= fabs(gbest)) { gbest = g; r = i; first = false; }
+      double dp = D[i] + s;
+      if (fabs(dp) < pivmin) dp = -pivmin;
+      neg += dp < 0.0;
+      const double lp = fdiv(DL[i], dp);
+      x[i] = lp;
+      s = fma(lp * L[i], s, -lam);
+    }
+    {
+      double dp = D[hi - 1] + s;
+      if (fabs(dp) < pivmin) dp = -pivmin;
+      neg += dp < 0.0;
+      const double g = s + x[hi - 1] + lam;
+      if (first || fabs(g) <= fabs(gbest)) { gbest = g; r = hi - 1; }
+    }
+  } else {
+    bool first = true;
+    for (int i = m - 1; i >= lo; --i) {
+      double dm = DL2[i] + p;
+      if (fabs(dm) < pivmin) dm = -pivmin;
+      const double rd = frcp(dm);
+      const double si = sc[i];
+      sc[i] = DL[i] * rd;
+      p = fma(p, D[i] * rd, -lam);
+      const double g = si + p + lam;
+      if (first || fabs(g) < fabs(gbest)) { gbest = g; r = i; first = false; }
+    }
+    if (first) r = -1;   // empty lower half
+  }
+  // combine: the upper half (role 0) wins ties
+  const double g0 = __shfl_sync(pmask, gbest, base), g1 = __shfl_sync(pmask, gbest, base + 1);
+  const int r0 = __shfl_sync(pmask, r, base), r1 = __shfl_sync(pmask, r, base + 1);
+  neg = __shfl_sync(pmask, neg, base);
+  if (r1 >= 0 && fabs(g1) < fabs(g0)) { gbest = g1; r = r1; } else { gbest = g0; r = r0; }
+  __syncwarp(pmask);   // x (L+, p_{hi-1}) and sc (U-) complete before the walks
+  double part = 0.0;
+  if (role == 0) {
+    double zn = 1.0, znn = 0.0;   // z_{i+1}, z_{i+2} on the upward walk
+    for (int i = r - 1; i >= lo; --i) {
+      double z = -x[i] * zn;
+      if (zn == 0.0 && i + 2 < hi) z = -fdiv(DL[i + 1], DL[i]) * znn;   // restart across a zero (dlar1v)
+      x[i] = z;
+      part = fma(z, z, part);
+      znn = zn;
+      zn = z;
+    }
+    x[r] = 1.0;
+  } else {
+    double zn = 1.0, znn = 0.0;
+    for (int i = r; i < hi - 1; ++i) {
+      double z = -sc[i] * zn;
+      if (zn == 0.0 && i > lo) z = -fdiv(DL[i - 1], DL[i]) * znn;
+      x[i + 1] = z;
+      part = fma(z, z, part);
+      znn = zn;
+      zn = z;
+    }
+  }
+  const double u0 = __shfl_sync(pmask, part, base), u1 = __shfl_sync(pmask, part, base + 1);
+  __syncwarp(pmask);
+  *gamma_out = gbest;
+  *znorm2_out = 1.0 + u0 + u1;
+  return neg;
+}
+
 // C[i][j] = sum_k A[i][k] B[j][k] (n x n, FP64, shared memory, ld ldx), 4 x 4 per thread with
 // rows i = ti + g a, columns j = tj + g b (g = ceil(n / 4)).  Returns max |C - I| over the
 // block when `dev_only` (C not written), else writes C.
@@ -745,12 +861,10 @@ __device__ __noinline__ int eig_tri(const TriPlan& P, double* __restrict__ sm, l
   if (tid == 0) g_tri_dbg[1] = clock64();
   if (status[0] == 0) return 0;
   // coarse pass: negcounts of each big block at gu 8^-k, k = 0..kTriCoarse-1 (a thread each)
-  {
-    const int b = tid / kTriCoarse, k = tid - b * kTriCoarse;
-    if (b < status[2]) {
-      const int lo = blo[b], hi = bend[lo];
-      ccnt[b * kTriCoarse + k] = (k == 0) ? (hi - lo) : tri_negcount(Dr, DL2, lo, hi, ldexp(gub[lo], -3 * k), pivmin);
-    }
+  for (int t = tid; t < status[2] * kTriCoarse; t += nt) {
+    const int b = t / kTriCoarse, k = t - b * kTriCoarse;
+    const int lo = blo[b], hi = bend[lo];
+    ccnt[b * kTriCoarse + k] = (k == 0) ? (hi - lo) : tri_negcount(Dr, DL2, lo, hi, ldexp(gub[lo], -3 * k), pivmin);
   }
   __syncthreads();
   if (tid == 0) g_tri_clk[5] = clock64();
@@ -803,23 +917,38 @@ __device__ __noinline__ int eig_tri(const TriPlan& P, double* __restrict__ sm, l
           if (f > 0) { a = xa; na = ca; }
           if (f < 8) { b = xb; nbc = cb; }
         }
+        if (g8 == 0) {   // the bracket, for the densely packed RQI threads below
+          sm[P.ov + j] = a;
+          sm[P.ov + n + j] = b;
+          sm[P.ov + 2 * n + j] = (double)(na * 256 + nbc);
+        }
       }
     }
     __syncthreads();
     if (tid == 0) g_tri_clk[6] = clock64();
     if (tid == 0 && stamps) stamps[2] = clock64();
-    if (j < n) {
-      const int lo = bstart[j], hi = bend[j], nb = hi - lo, jj = j - lo;
-      double* x = X + j * lda;
+    // RQI: TWO adjacent lanes per eigenvalue (tri_twisted2 splits each twisted factorisation
+    // between them), eigenvalues packed densely over the first 2n threads: the FP64 pipe
+    // issues a whole warp per instruction, so one active lane per 8-lane group (the
+    // multisection layout) wasted 7/8 of it on these long sequential chains.
+    if (tid < 2 * n) {
+      const int jr = tid >> 1, role = tid & 1;
+      const unsigned pmask = 3u << (tid & 31 & ~1);
+      const int pbase = tid & 31 & ~1;
+      const int lo = bstart[jr], hi = bend[jr], nb = hi - lo, jj = jr - lo;
+      double* x = X + jr * lda;
       double lj = 0.0;
       if (nb == 1) {
         lj = Dr[lo];
       } else {
-        if (g8 == 0) {
+        double a = sm[P.ov + jr], b = sm[P.ov + n + jr];
+        const int pk = (int)sm[P.ov + 2 * n + jr];
+        int na = pk >> 8, nbc = pk & 255;
+        {
           const long long rq0 = clock64();
           double lc = -1.0, lam_v = 0.0, gm = 0.0, nz = 1.0;
           bool have_vec = false, conv = false;
-          double* ss = A + j * lda;
+          double* ss = A + jr * lda;
           int it_used = 0, ntw = 0;
           for (int it = 0; it < 400 && !conv; ++it) {
             ++it_used;
@@ -832,7 +961,7 @@ __device__ __noinline__ int eig_tri(const TriPlan& P, double* __restrict__ sm, l
             else l = 0.5 * (a + b);
             int neg;
             if (rqi) {
-              neg = tri_twisted(Dr, Lr, DL, DL2, lo, hi, l, pivmin, x, ss, &gm, &nz);
+              neg = tri_twisted2(role, pmask, pbase, Dr, Lr, DL, DL2, lo, hi, l, pivmin, x, ss, &gm, &nz);
               have_vec = true;
               lam_v = l;
             } else {
@@ -850,21 +979,21 @@ __device__ __noinline__ int eig_tri(const TriPlan& P, double* __restrict__ sm, l
               conv = true;
             }
           }
-          atomicMax(&g_tri_maxit, 1000 * it_used + ntw);
+          if (role == 0) atomicMax(&g_tri_maxit, 1000 * it_used + ntw);
           if (!have_vec || !conv) {
             lam_v = have_vec ? lam_v : 0.5 * (a + b);
-            tri_twisted(Dr, Lr, DL, DL2, lo, hi, lam_v, pivmin, x, ss, &gm, &nz);
-            if (!conv) { atomicAnd(status, 0); g_tri_fail_why = 2; }
+            tri_twisted2(role, pmask, pbase, Dr, Lr, DL, DL2, lo, hi, lam_v, pivmin, x, ss, &gm, &nz);
+            if (!conv && role == 0) { atomicAnd(status, 0); g_tri_fail_why = 2; }
           }
           lj = lam_v;
           const double inv = rsqrt(nz);
-          for (int c = lo; c < hi; ++c) x[c] *= inv;
-          atomicMax(&g_tri_rqimax, (unsigned long long)(clock64() - rq0));
+          for (int c = lo + role; c < hi; c += 2) x[c] *= inv;
+          if (role == 0) atomicMax(&g_tri_rqimax, (unsigned long long)(clock64() - rq0));
         }
       }
-      if (g8 == 0) {
-        lam[j] = (lj + sig[lo]) * unscale;
-        sm[P.omu + j] = lj;
+      if (role == 0) {
+        lam[jr] = (lj + sig[lo]) * unscale;
+        sm[P.omu + jr] = lj;
       }
     }
   }

@@ -532,7 +532,7 @@ __device__ __forceinline__ void refresh_body(const RefreshJob& J, int dbg_mask) 
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(MODE == REFRESH_TRI ? kTriThreads : 1024, 1)
 refresh_kernel(int R, int D, int N, double eta, double alpha, double eps,
                const float* __restrict__ KL, double* __restrict__ dstate,
                const double* __restrict__ sums, float* __restrict__ Amat,
@@ -548,7 +548,7 @@ struct RefreshGroup {
   RefreshJob j[kRefreshGroupMax];
   int count, dbg;
 };
-__global__ void __launch_bounds__(1024) refresh_group_kernel(const __grid_constant__ RefreshGroup g) {
+__global__ void __launch_bounds__(kTriThreads, 1) refresh_group_kernel(const __grid_constant__ RefreshGroup g) {
   refresh_body<REFRESH_TRI>(g.j[blockIdx.x], g.dbg);
 }
 
@@ -1057,7 +1057,7 @@ static ng_status launch_refresh_chain(ngsgd_ctx* h, int n, double eta, const dou
     if (force == REFRESH_INPLACE) mode = force;
     const RefreshSmem plan = refresh_plan(R, mode);
     if (mode == REFRESH_TRI) {
-      refresh_kernel<REFRESH_TRI><<<1, 1024, plan.total_bytes, ss>>>(R, D, n, eta, a_, e_, h->KL, h->dstate,
+      refresh_kernel<REFRESH_TRI><<<1, kTriThreads, plan.total_bytes, ss>>>(R, D, n, eta, a_, e_, h->KL, h->dstate,
                                                                      trx, h->Amat, h->svec, h->flags, dbg);
     } else {
       refresh_kernel<REFRESH_INPLACE><<<1, 1024, plan.total_bytes, ss>>>(R, D, n, eta, a_, e_, h->KL, h->dstate,
@@ -1430,7 +1430,7 @@ static ng_status launch_refresh_group(NgCall* calls, const std::vector<int>& grp
     // CTA can share its SM (measurement knob)
     static const size_t pad = (size_t)std::min(200, std::max(0, tune_int("NG_TUNE_REFRESH_SMEM_KB", 0))) * 1024;
     const size_t rsm = std::max(refresh_plan(maxR, REFRESH_TRI).total_bytes, pad);
-    refresh_group_kernel<<<G, 1024, rsm, ss>>>(rg);
+    refresh_group_kernel<<<G, kTriThreads, rsm, ss>>>(rg);
     NG_TRY(check_launch("refresh_group_kernel"));
   }
   double flops = 0.0, bytes = 0.0;
@@ -1834,7 +1834,7 @@ ng_status ngsgd_set_state(ngsgd_t h, const ngsgd_state_host* in) {
   return NG_OK;
 }
 
-__global__ void __launch_bounds__(1024) debug_eig_tri_kernel(const double* Z, int n, double* lam, double* vt, int* ok) {
+__global__ void __launch_bounds__(kTriThreads, 1) debug_eig_tri_kernel(const double* Z, int n, double* lam, double* vt, int* ok) {
   extern __shared__ __align__(16) unsigned char ng_smem[];
   double* sm = reinterpret_cast<double*>(ng_smem);
   const TriPlan tp = tri_plan(n);
@@ -1897,7 +1897,7 @@ ng_status ng_debug_eig_tri(const double* z, int32_t n, double* lam, double* vt, 
   const size_t smem = tri_plan(n).total + 16;
   NG_TRY(set_kernel_attrs());   // (also the solver's tuning knobs)
   NG_CUDA_TRY(cudaFuncSetAttribute(debug_eig_tri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  debug_eig_tri_kernel<<<1, 1024, smem, (cudaStream_t)stream>>>(z, n, lam, vt, ok);
+  debug_eig_tri_kernel<<<1, kTriThreads, smem, (cudaStream_t)stream>>>(z, n, lam, vt, ok);
   return check_launch("debug_eig_tri_kernel");
 }
 
