@@ -61,9 +61,10 @@ __device__ __forceinline__ double fsqrt(double x) {   // x >= 0
 constexpr int kTriMax = 80;
 // Threads of a CTA that runs eig_tri: 22 warps (the register-resident tridiagonalisation
 // needs 21: a serial warp + 20 warps of four rows each; the multisection 8n = 640 lanes).
-// Fewer than 1024 threads raise the per-thread register cap from 64 to 88, which removes
-// most of the solver's spills (local memory that misses L1 once the refresh's shared memory
-// takes most of the unified L1 / shared storage).
+// Registers are handed out per 4 warps, so 21-24 warps allow 80 registers per thread against
+// 64 at 1024 threads, which removes most of the solver's spills (local memory that misses L1
+// once the refresh's shared memory takes most of the unified L1 / shared storage); 96
+// registers at 672 threads are refused at launch (24 x 32 x 96 > 65536).
 constexpr int kTriThreads = 704;
 constexpr int kTriChunks = 5;   // column chunks of the Householder pass
 constexpr double kTriOrthTol = 1e-6;   // ~ the Jacobi solver's 1e-7 rotation threshold; W is FP32

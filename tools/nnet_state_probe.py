@@ -9,7 +9,7 @@ prec = os.environ.get("NG_PREC", "tf32")
 N = 512
 frames, labels = spliced_frames(1410, 64 * N, num_classes=5000)
 f = torch.from_numpy(frames).cuda(); y = torch.from_numpy(labels).cuda()
-net = api.Nnet(360, 4, 3000, 10, 5000, max_minibatch=N, precond=True, rank_in=20, rank_out=80, precision=prec, seed=1410)
+net = api.Nnet(360, 4, 3000, 10, 5000, max_minibatch=N, precond=True, rank_in=20, rank_out=80, precision=prec, seed=1410, renorm=os.environ.get("NG_RENORM", "1") == "1")
 for k in range(int(sys.argv[1]) if len(sys.argv) > 1 else 30):
     i = k % 64
     net.forward_backward(f[i * N:(i + 1) * N], y[i * N:(i + 1) * N])
