@@ -911,7 +911,8 @@ ng_status ngsgd_create_impl(int dim, int max_rows, const ngsgd_config* cfg, cuda
   if (s == NG_OK && cudaMallocHost((void**)&h->h_scalar, 4 * sizeof(double)) != cudaSuccess) s = NG_ENOMEM;
   if (s == NG_OK && (cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, refresh_priority()) != cudaSuccess ||
                      cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-                     cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess)) {
+                     cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+                     cudaEventCreateWithFlags(&h->ev_ab, cudaEventDisableTiming) != cudaSuccess)) {
     set_error("ngsgd_create: stream/event creation failed");
     s = NG_ECUDA;
   }
@@ -942,6 +943,7 @@ void ngsgd_destroy_impl(ngsgd_ctx* h) {
   if (h->side) { cudaStreamSynchronize(h->side); cudaStreamDestroy(h->side); }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->ev_ab) cudaEventDestroy(h->ev_ab);
   delete h;
 }
 
@@ -1541,16 +1543,25 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
   }
   if (grp.empty()) return NG_OK;
   const int G = (int)grp.size();
+  // phase C keeps using the pre-refresh W_t of every state
+  std::vector<float*> Wold(G);
+  for (int g = 0; g < G; ++g) Wold[g] = calls[grp[g]].h->W[calls[grp[g]].h->cur];
+  // Phases A (H), B (J, K, L of the updating states), tr(X X^T) and the refresh launch for
+  // the states `sub` (call indices) on stream sx; ev_ab (optional) is recorded on sx once H,
+  // J and the trace are done, before the refresh chain is launched.
+  auto phases_ab = [&](const std::vector<int>& sub, cudaStream_t sx, cudaEvent_t ev_ab) -> ng_status {
+  const int S = (int)sub.size();
+  if (S == 0) return NG_OK;
   // ---- phase A: H = X W^T for every state (split-K partials), one launch
   {
     double flops = 0, bytes = 0;
     int64_t total_kt = 0;
-    for (int i : grp) total_kt += (int64_t)ceil_div(calls[i].n, 128) * ceil_div(calls[i].h->dim, 32);
+    for (int i : sub) total_kt += (int64_t)ceil_div(calls[i].n, 128) * ceil_div(calls[i].h->dim, 32);
     const int64_t target_kb = std::max<int64_t>(4, ceil_div(total_kt, 2 * 148));
-    std::vector<TcGroupDesc> d(G);
-    std::vector<int> sp(G);
-    for (int g = 0; g < G; ++g) {
-      NgCall& c = calls[grp[g]];
+    std::vector<TcGroupDesc> d(S);
+    std::vector<int> sp(S);
+    for (int g = 0; g < S; ++g) {
+      NgCall& c = calls[sub[g]];
       ngsgd_ctx* h = c.h;
       const int R = h->rank, D = h->dim;
       flops += 2.0 * c.n * R * D;
@@ -1562,28 +1573,28 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
       q.epi.kind = TC_EPI_PARTIAL; q.epi.C = h->Hpart; q.epi.ldc = R; q.epi.zstride = (int64_t)c.n * R;
       q.splits_used = &sp[g];
     }
-    ProfScope ps(NG_PROF_NG_PROJ, st, flops, bytes);
-    NG_TRY(tc_gemm_tf32_grouped(st, d.data(), G, true, true, TC_EPI_PARTIAL, 128, true));
+    ProfScope ps(NG_PROF_NG_PROJ, sx, flops, bytes);
+    NG_TRY(tc_gemm_tf32_grouped(sx, d.data(), S, true, true, TC_EPI_PARTIAL, 128, true));
     SegReduce sr;
     std::memset(&sr, 0, sizeof(sr));
-    sr.count = G;
-    for (int g = 0; g < G; ++g) {
-      NgCall& c = calls[grp[g]];
+    sr.count = S;
+    for (int g = 0; g < S; ++g) {
+      NgCall& c = calls[sub[g]];
       const int R = c.h->rank;
       sr.out[g] = c.h->H; sr.src[g] = c.h->Hpart; sr.ldo[g] = R; sr.lds[g] = R;
       sr.zstride[g] = (int64_t)c.n * R; sr.rows[g] = c.n; sr.cols[g] = R; sr.splits[g] = sp[g];
     }
-    NG_TRY(launch_seg_reduce(st, sr));
+    NG_TRY(launch_seg_reduce(sx, sr));
   }
   // ---- phase B (update states): J = H^T X (one launch), K = J J^T, L = W J^T (FP32)
   std::vector<int> ug;
-  for (int g = 0; g < G; ++g) if (upd[grp[g]]) ug.push_back(g);
+  for (int g = 0; g < S; ++g) if (upd[sub[g]]) ug.push_back(g);
   if (!ug.empty()) {
     double flops = 0, bytes = 0;
     std::vector<TcGroupDesc> d(ug.size());
     std::vector<int> sp(ug.size());
     for (size_t u = 0; u < ug.size(); ++u) {
-      NgCall& c = calls[grp[ug[u]]];
+      NgCall& c = calls[sub[ug[u]]];
       ngsgd_ctx* h = c.h;
       const int R = h->rank, D = h->dim;
       flops += 2.0 * c.n * R * D + 4.0 * (double)R * R * D;
@@ -1594,17 +1605,17 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
       q.epi.kind = TC_EPI_PARTIAL; q.epi.C = h->Hpart; q.epi.ldc = h->ldw; q.epi.zstride = (int64_t)R * h->ldw;
       q.splits_used = &sp[u];
     }
-    ProfScope ps(NG_PROF_NG_REFRESH, st, flops, bytes);
-    NG_TRY(tc_gemm_tf32_grouped(st, d.data(), (int)ug.size(), false, false, TC_EPI_PARTIAL, 128, true));
+    ProfScope ps(NG_PROF_NG_REFRESH, sx, flops, bytes);
+    NG_TRY(tc_gemm_tf32_grouped(sx, d.data(), (int)ug.size(), false, false, TC_EPI_PARTIAL, 128, true));
     SegReduce sr;
     std::memset(&sr, 0, sizeof(sr));
     sr.count = (int)ug.size();
     for (size_t u = 0; u < ug.size(); ++u) {
-      ngsgd_ctx* h = calls[grp[ug[u]]].h;
+      ngsgd_ctx* h = calls[sub[ug[u]]].h;
       sr.out[u] = h->J; sr.src[u] = h->Hpart; sr.ldo[u] = h->ldw; sr.lds[u] = h->ldw;
       sr.zstride[u] = (int64_t)h->rank * h->ldw; sr.rows[u] = h->rank; sr.cols[u] = h->dim; sr.splits[u] = sp[u];
     }
-    NG_TRY(launch_seg_reduce(st, sr));
+    NG_TRY(launch_seg_reduce(sx, sr));
     // K = J J^T and L = W J^T of every updating state: one grouped 3xTF32
     // tensor-core launch per 16 problems (FP32-grade: Z_t must equal Y_t Y_t^T for the
     // stored J to FP32 accuracy), split over D, then the fixed-order segmented reduction
@@ -1614,7 +1625,7 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
       const int nprob = 2 * (int)ug.size();
       const int want = std::max(1, std::min(kTcMaxSplits, ceil_div(2 * 148, nprob)));
       for (size_t u = 0; u < ug.size(); ++u) {
-        ngsgd_ctx* h = calls[grp[ug[u]]].h;
+        ngsgd_ctx* h = calls[sub[ug[u]]].h;
         const int R = h->rank, D = h->dim;
         for (int w = 0; w < 2; ++w) {
           TcGroupDesc q;
@@ -1630,44 +1641,72 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
       }
       for (size_t b = 0; b < d.size(); b += kTcGroupMax) {
         const int cnt = (int)std::min<size_t>(kTcGroupMax, d.size() - b);
-        NG_TRY(tc_gemm_tf32_grouped(st, d.data() + b, cnt, true, true, TC_EPI_PARTIAL, 128, true));
+        NG_TRY(tc_gemm_tf32_grouped(sx, d.data() + b, cnt, true, true, TC_EPI_PARTIAL, 128, true));
       }
       SegReduce kl;
       std::memset(&kl, 0, sizeof(kl));
       kl.count = 0;
       for (size_t u = 0; u < ug.size(); ++u) {
-        ngsgd_ctx* h = calls[grp[ug[u]]].h;
+        ngsgd_ctx* h = calls[sub[ug[u]]].h;
         const int R = h->rank;
         for (int w = 0; w < 2; ++w) {
-          if (kl.count == kSegMax) { NG_TRY(launch_seg_reduce(st, kl)); kl.count = 0; }
+          if (kl.count == kSegMax) { NG_TRY(launch_seg_reduce(sx, kl)); kl.count = 0; }
           const int k = kl.count++;
           kl.out[k] = h->KL + w * R * R; kl.src[k] = w ? h->Lpart : h->Kpart; kl.ldo[k] = R; kl.lds[k] = R;
           kl.zstride[k] = (int64_t)R * R; kl.rows[k] = R; kl.cols[k] = R; kl.splits[k] = spk[2 * u + w];
         }
       }
-      if (kl.count) NG_TRY(launch_seg_reduce(st, kl));
+      if (kl.count) NG_TRY(launch_seg_reduce(sx, kl));
     }
   }
   // ---- tr(X X^T) of the updating states, then their refresh chains start right away (they
   // need J, K, L and the trace only); phase C keeps using the pre-refresh W_t
-  std::vector<float*> Wold(G);
-  for (int g = 0; g < G; ++g) Wold[g] = calls[grp[g]].h->W[calls[grp[g]].h->cur];
   if (!ug.empty()) {
     TraceGroup tr;
     std::memset(&tr, 0, sizeof(tr));
     tr.count = (int)ug.size();
     for (size_t u = 0; u < ug.size(); ++u) {
-      NgCall& c = calls[grp[ug[u]]];
+      NgCall& c = calls[sub[ug[u]]];
       tr.x[u] = c.x; tr.ld[u] = c.ld; tr.n[u] = c.n; tr.D[u] = c.h->dim;
       tr.out[u] = c.h->sums + 2; tr.part[u] = c.h->trpart;
     }
     int nmax = 1;
     for (int u = 0; u < tr.count; ++u) nmax = std::max(nmax, tr.n[u]);
-    trace_part_kernel<<<dim3(nmax, tr.count), 128, 0, st>>>(tr);
+    trace_part_kernel<<<dim3(nmax, tr.count), 128, 0, sx>>>(tr);
     NG_TRY(check_launch("trace_part_kernel"));
-    trace_final_kernel<<<tr.count, 256, 0, st>>>(tr);
+    trace_final_kernel<<<tr.count, 256, 0, sx>>>(tr);
     NG_TRY(check_launch("trace_final_kernel"));
-    NG_TRY(launch_refresh_group(calls, grp, ug, st));
+    if (ev_ab) NG_CUDA_TRY(cudaEventRecord(ev_ab, sx));   // H, J, trace done: phase C may go
+    NG_TRY(launch_refresh_group(calls, sub, ug, sx));
+  }
+  if (ev_ab && ug.empty()) NG_CUDA_TRY(cudaEventRecord(ev_ab, sx));
+  return NG_OK;
+  };
+  // On an update step the state with the largest refresh (rank, then dimension) gets its
+  // phases A/B on its own side stream, concurrently with the other states' on the main
+  // stream, so its refresh chain -- the one the next step waits for -- starts as soon as its
+  // own J, K, L are formed instead of after everyone's (NG_TUNE_CRIT_FIRST=0: one group).
+  static const int crit_first = tune_int("NG_TUNE_CRIT_FIRST", 1);
+  int crit = -1, nupd = 0;
+  for (int g = 0; g < G; ++g) {
+    if (!upd[grp[g]]) continue;
+    ++nupd;
+    const ngsgd_ctx* h = calls[grp[g]].h;
+    if (crit < 0 || h->rank > calls[grp[crit]].h->rank ||
+        (h->rank == calls[grp[crit]].h->rank && h->dim > calls[grp[crit]].h->dim))
+      crit = g;
+  }
+  if (crit_first && nupd >= 2 && crit >= 0) {
+    ngsgd_ctx* hc = calls[grp[crit]].h;
+    NG_CUDA_TRY(cudaEventRecord(hc->ev_fork, st));
+    NG_CUDA_TRY(cudaStreamWaitEvent(hc->side, hc->ev_fork, 0));
+    NG_TRY(phases_ab(std::vector<int>{grp[crit]}, hc->side, hc->ev_ab));
+    std::vector<int> rest;
+    for (int g = 0; g < G; ++g) if (g != crit) rest.push_back(grp[g]);
+    NG_TRY(phases_ab(rest, st, nullptr));
+    NG_CUDA_TRY(cudaStreamWaitEvent(st, hc->ev_ab, 0));
+  } else {
+    NG_TRY(phases_ab(grp, st, nullptr));
   }
   // ---- phase C: X_hat = X - H W with fused row norms (one launch), finalize (one launch)
   {

@@ -43,6 +43,7 @@ struct ngsgd_ctx {
   // side stream for the refresh (Z_t eigensolve, W_{t+1}); joined before the next use
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_ab = nullptr;   // critical state's phases A/B done on its side stream (group path)
   bool pending = false;
 };
 
