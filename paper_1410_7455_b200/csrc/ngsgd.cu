@@ -1682,11 +1682,12 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
   if (ev_ab && ug.empty()) NG_CUDA_TRY(cudaEventRecord(ev_ab, sx));
   return NG_OK;
   };
-  // On an update step the state with the largest refresh (rank, then dimension) gets its
-  // phases A/B on its own side stream, concurrently with the other states' on the main
-  // stream, so its refresh chain -- the one the next step waits for -- starts as soon as its
-  // own J, K, L are formed instead of after everyone's (NG_TUNE_CRIT_FIRST=0: one group).
-  static const int crit_first = tune_int("NG_TUNE_CRIT_FIRST", 1);
+  // On an update step the states with the largest refreshes (every updating state of the
+  // largest rank; NG_TUNE_CRIT_FIRST=1: only the largest one, rank then dimension) get their
+  // phases A/B on a side stream, concurrently with the other states' on the main stream, so
+  // their refresh chains -- the ones the next step waits for -- start as soon as their own
+  // J, K, L are formed instead of after everyone's (NG_TUNE_CRIT_FIRST=0: one group).
+  static const int crit_first = tune_int("NG_TUNE_CRIT_FIRST", 2);
   int crit = -1, nupd = 0;
   for (int g = 0; g < G; ++g) {
     if (!upd[grp[g]]) continue;
@@ -1697,12 +1698,17 @@ ng_status ngsgd_precondition_group_impl(NgCall* calls, int count) {
       crit = g;
   }
   if (crit_first && nupd >= 2 && crit >= 0) {
-    ngsgd_ctx* hc = calls[grp[crit]].h;
+    std::vector<int> first, rest;
+    const int rmax = calls[grp[crit]].h->rank;
+    for (int g = 0; g < G; ++g) {
+      const bool side = crit_first == 2 ? (upd[grp[g]] && calls[grp[g]].h->rank == rmax) : g == crit;
+      (side ? first : rest).push_back(grp[g]);
+    }
+    if (rest.empty()) { first.assign(1, grp[crit]); rest.clear(); for (int g = 0; g < G; ++g) if (g != crit) rest.push_back(grp[g]); }
+    ngsgd_ctx* hc = calls[first[0]].h;
     NG_CUDA_TRY(cudaEventRecord(hc->ev_fork, st));
     NG_CUDA_TRY(cudaStreamWaitEvent(hc->side, hc->ev_fork, 0));
-    NG_TRY(phases_ab(std::vector<int>{grp[crit]}, hc->side, hc->ev_ab));
-    std::vector<int> rest;
-    for (int g = 0; g < G; ++g) if (g != crit) rest.push_back(grp[g]);
+    NG_TRY(phases_ab(first, hc->side, hc->ev_ab));
     NG_TRY(phases_ab(rest, st, nullptr));
     NG_CUDA_TRY(cudaStreamWaitEvent(st, hc->ev_ab, 0));
   } else {
